@@ -1,0 +1,431 @@
+"""Tree packing: MWU, ILP refinement, one-hop switch trees, weight split.
+TEST INFRASTRUCTURE ONLY (see oracle/__init__).
+
+Follows the paper step by step:
+
+* Sec. 3.2: "at each iteration we find the minimum weight spanning
+  tree given the current assignment.  We then increment the weight on this
+  chosen tree by an epsilon factor and update weights on the graph
+  correspondingly."  Step rule (R#4): Garg-Koenemann with bottleneck routing,
+  lengths l_e = delta / c_e kept as logs and normalised by their max before
+  each minimum-tree call (without normalisation the raw lengths
+  ~1e-34 lose the (1 - eps) guarantee).  Final uniform scaling to exact
+  feasibility; identical trees merged.
+* Sec. 3.2.1 (Eqs. 4-7): binary ILP over the MWU candidates, then
+  "iteratively relax the constraints (i.e. allowing w_i to take fractional
+  values) until c_hat is within a configured threshold (e.g., 5%) of c*"
+  (R#5, R#6: grid w in {0, 1/g, ..., 1} for g = 1, 2, 4, 8, 16; gap 0.05).
+* Sec. 3.3: AllReduce packs *undirected* spanning trees (a tree
+  of weight w consumes w on the link in both directions); the per-tree root is
+  the tree's centre (R#9).
+* Sec. 3.5: on a switch, m one-hop trees, each GPU root of 1/m.
+* Sec. 4.1: "split the buffer among all the spanning trees based on
+  their weights" -- 16-byte-grain prefix-floor split (R#11).
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+
+GRAIN = 16  # bytes; R#11
+
+
+# --------------------------------------------------------------------------
+# Minimum-weight arborescence (Chu-Liu / Edmonds), the MWU inner oracle
+# --------------------------------------------------------------------------
+def min_arborescence(n, r, lengths):
+    """Minimum-total-length arborescence rooted at r.
+
+    `lengths`: {(u, v): l}.  Ties: smallest (length, (u, v)) in-edge.
+    Returns a parent tuple (parent[r] = -1).  Plain recursive contraction."""
+    edges = [(u, v, w, (u, v)) for (u, v), w in lengths.items() if u != v]
+    chosen = _cle(n, r, edges)
+    parent = [-1] * n
+    for (u, v) in chosen:
+        parent[v] = u
+    return tuple(parent)
+
+
+def _cle(n, r, edges):
+    # 1. cheapest incoming edge per non-root vertex
+    inb = {}
+    for e in edges:
+        u, v, w, key = e
+        if v == r or u == v:
+            continue
+        if v not in inb or (w, key) < (inb[v][2], inb[v][3]):
+            inb[v] = e
+    for v in range(n):
+        if v != r and v not in inb:
+            raise ValueError(f"vertex {v} unreachable from root {r}")
+    # 2. cycles among the chosen edges
+    comp = [-1] * n
+    mark = [-1] * n
+    ncomp = 0
+    cyclic = False
+    for v in range(n):
+        x = v
+        while x != r and mark[x] == -1 and comp[x] == -1:
+            mark[x] = v
+            x = inb[x][0]
+        if x != r and mark[x] == v and comp[x] == -1:
+            # x lies on a new cycle
+            cyclic = True
+            y = x
+            while True:
+                comp[y] = ncomp
+                y = inb[y][0]
+                if y == x:
+                    break
+            ncomp += 1
+    if not cyclic:
+        return {inb[v][3] for v in range(n) if v != r}
+    for v in range(n):
+        if comp[v] == -1:
+            comp[v] = ncomp
+            ncomp += 1
+    # 3. contract and recurse; reduced cost w - w(inb[v])
+    new_edges = []
+    origin = {}
+    for e in edges:
+        u, v, w, key = e
+        cu, cv = comp[u], comp[v]
+        if cu == cv or v == r:
+            continue
+        ne = (cu, cv, w - inb[v][2], key)
+        new_edges.append(ne)
+        origin[key] = e
+    sub = _cle(ncomp, comp[r], new_edges)
+    # 4. expand: a vertex entered by a recursive choice keeps it; others keep inb
+    entered = {origin[k][1]: k for k in sub}
+    return {entered[v] if v in entered else inb[v][3] for v in range(n) if v != r}
+
+
+def min_spanning_tree(n, lengths):
+    """Kruskal over undirected {(u,v) u<v: l}; ties by (l, u, v).  Returns a
+    sorted tuple of (u, v) pairs."""
+    parent = list(range(n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    out = []
+    for (w, (u, v)) in sorted((w, e) for e, w in lengths.items()):
+        a, b = find(u), find(v)
+        if a != b:
+            parent[a] = b
+            out.append((u, v))
+    if len(out) != n - 1:
+        raise ValueError("graph is disconnected")
+    return tuple(sorted(out))
+
+
+def _logsumexp(xs):
+    m = max(xs)
+    return m + math.log(sum(math.exp(x - m) for x in xs))
+
+
+# --------------------------------------------------------------------------
+# MWU (Sec. 3.2)
+# --------------------------------------------------------------------------
+def _mwu(caps, tree_of, eps):
+    """Generic Garg-Koenemann loop over a capacity dict `caps`; `tree_of(lengths)`
+    returns a tree as a hashable object and its edge list.
+    Returns ({tree: weight}, c*) with weights scaled to exact feasibility."""
+    edges = sorted(caps)
+    mE = len(edges)
+    log_delta = math.log1p(eps) - (1.0 / eps) * math.log((1.0 + eps) * mE)
+    logl = {e: log_delta - math.log(caps[e]) for e in edges}
+    x = {}
+    tree_edges = {}
+    iters = 0
+    while True:
+        mx = max(logl.values())
+        lengths = {e: math.exp(logl[e] - mx) for e in edges}
+        T, Te = tree_of(lengths)
+        if _logsumexp([logl[e] for e in Te]) >= 0.0:   # sum_{e in T} l_e >= 1
+            break
+        cmin = min(caps[e] for e in Te)
+        x[T] = x.get(T, 0.0) + cmin
+        tree_edges[T] = Te
+        for e in Te:
+            logl[e] += math.log1p(eps * cmin / caps[e])
+        iters += 1
+        if iters > 10_000_000:
+            raise RuntimeError("MWU did not terminate")
+    load = {e: 0.0 for e in edges}
+    for T, w in x.items():
+        for e in tree_edges[T]:
+            load[e] += w
+    lam = max(load[e] / caps[e] for e in edges)
+    w = {T: v / lam for T, v in x.items()}
+    return w, tree_edges, sum(w.values()), iters
+
+
+def mwu_broadcast(g, r, eps=0.1):
+    """MWU packing of arborescences rooted at r on the directed graph.
+    Returns (weights {parent_tuple: w}, rate c*, iterations)."""
+    n, cap = g
+
+    def tree_of(lengths):
+        p = min_arborescence(n, r, lengths)
+        return p, [(u, v) for v, u in enumerate(p) if u >= 0]
+
+    w, _, rate, iters = _mwu(cap, tree_of, eps)
+    return w, rate, iters
+
+
+def mwu_allreduce(pairs, n, eps=0.1):
+    """MWU packing of undirected spanning trees: Kruskal inner
+    oracle, capacity per undirected link = per-direction capacity (R#9).
+    Returns (weights {edge_tuple: w}, rate c*, iterations)."""
+    def tree_of(lengths):
+        t = min_spanning_tree(n, lengths)
+        return t, list(t)
+
+    w, _, rate, iters = _mwu(pairs, tree_of, eps)
+    return w, rate, iters
+
+
+# --------------------------------------------------------------------------
+# Tree helpers
+# --------------------------------------------------------------------------
+def parent_depth(parent):
+    """Max hops root -> leaf of a parent tuple."""
+    best = 0
+    for v in range(len(parent)):
+        d, x = 0, v
+        while parent[x] >= 0:
+            x = parent[x]
+            d += 1
+        best = max(best, d)
+    return best
+
+
+def tree_centre(edges, n):
+    """Centre of an undirected tree: minimum eccentricity, ties -> lowest id
+    (R#9: "a chosen root vertex")."""
+    adj = {v: [] for v in range(n)}
+    for (u, v) in edges:
+        adj[u].append(v)
+        adj[v].append(u)
+
+    def ecc(s):
+        dist = {s: 0}
+        frontier = [s]
+        while frontier:
+            nxt = []
+            for u in frontier:
+                for w in adj[u]:
+                    if w not in dist:
+                        dist[w] = dist[u] + 1
+                        nxt.append(w)
+            frontier = nxt
+        return max(dist.values())
+
+    return min(range(n), key=lambda v: (ecc(v), v))
+
+
+def root_tree(edges, n, root):
+    """Orient an undirected tree away from `root`: parent tuple."""
+    adj = {v: [] for v in range(n)}
+    for (u, v) in edges:
+        adj[u].append(v)
+        adj[v].append(u)
+    parent = [None] * n
+    parent[root] = -1
+    stack = [root]
+    while stack:
+        u = stack.pop()
+        for w in adj[u]:
+            if parent[w] is None:
+                parent[w] = u
+                stack.append(w)
+    return tuple(parent)
+
+
+# --------------------------------------------------------------------------
+# ILP refinement (Sec. 3.2.1)
+# --------------------------------------------------------------------------
+def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_limit=500):
+    """Eqs. 4-7 with the relaxation grid (R#5).
+
+    `caps`: {edge: c_e}; `candidates`: list of (edge_list, depth, key) in a
+    fixed order.  For each g: maximise sum z_T s.t. sum_{T contains e} z_T <=
+    g c_e, z_T in {0..g}; tie-break fewest trees, then least total depth, then
+    (deterministic solver) whatever HiGHS returns.  Accept the first g with sum z / g >= (1 - gap) c*.
+    Returns (list of (candidate index, Fraction weight), g, accepted).
+    scipy.optimize.milp (HiGHS) is the library primitive; the lexicographic
+    tie-breaks are sequential MILPs."""
+    from scipy.optimize import milp, LinearConstraint, Bounds
+
+    edges = sorted(caps)
+    eidx = {e: i for i, e in enumerate(edges)}
+    k = len(candidates)
+    A = np.zeros((len(edges), k))
+    for j, (te, _, _) in enumerate(candidates):
+        for e in te:
+            A[eidx[e], j] += 1.0
+    cvec = np.array([caps[e] for e in edges], dtype=float)
+    depth = np.array([d for (_, d, _) in candidates], dtype=float)
+    best = None
+    for g in grids:
+        # variables: z (k, integer 0..g), y (k, binary) ; z_T <= g y_T
+        Z = np.hstack([A, np.zeros_like(A)])
+        link = np.hstack([np.eye(k), -g * np.eye(k)])
+        cons = [LinearConstraint(Z, -np.inf, g * cvec), LinearConstraint(link, -np.inf, 0.0)]
+        integ = np.ones(2 * k)
+        bnds = Bounds(np.zeros(2 * k), np.concatenate([np.full(k, g), np.ones(k)]))
+        ones_z = np.concatenate([np.ones(k), np.zeros(k)])
+        ones_y = np.concatenate([np.zeros(k), np.ones(k)])
+        dep_y = np.concatenate([np.zeros(k), depth])
+        r1 = milp(-ones_z, constraints=cons, integrality=integ, bounds=bnds)
+        zstar = round(-r1.fun)
+        x = r1.x
+        # tie-breaks (fewest trees, then least total depth) as sequential MILPs
+        # under a deterministic node limit; a limit-stopped stage keeps its
+        # best feasible point (the tie-break is a preference, not a pin).
+        cons.append(LinearConstraint(ones_z[None, :], zstar, zstar))
+        for obj in (ones_y, dep_y):
+            r = milp(obj, constraints=cons, integrality=integ, bounds=bnds,
+                     options={"node_limit": node_limit})
+            if r.x is None:
+                break
+            x = r.x
+            val = float(obj @ np.round(x))
+            cons.append(LinearConstraint(obj[None, :], -np.inf, val + 1e-6))
+        z = np.round(x[:k]).astype(int)
+        sol = [(j, Fraction(int(z[j]), g)) for j in range(k) if z[j] > 0]
+        best = (sol, g, zstar / g >= (1 - gap) * c_star - 1e-12)
+        if best[2]:
+            return best
+    return best
+
+
+# --------------------------------------------------------------------------
+# Plans
+# --------------------------------------------------------------------------
+def _order_trees(trees):
+    """Split order (R#11): weight descending, then lexicographic edge list."""
+    return sorted(trees, key=lambda t: (-t["weight"], sorted(t["edges"])))
+
+
+def plan_broadcast_graph(g, r, eps=0.1, gap=0.05):
+    """Broadcast plan on an explicit link graph: MWU then ILP (Secs. 3.2, 3.2.1).
+    Returns dict(trees=[{parent, root, weight(Fraction), edges, depth}], rate, c_star)."""
+    n, cap = g
+    if n == 1:
+        return dict(trees=[dict(parent=(-1,), root=0, weight=Fraction(1), edges=[], depth=0)],
+                    rate=Fraction(1), c_star=1.0)
+    w, c_star, _ = mwu_broadcast(g, r, eps)
+    cands = sorted(w)  # parent tuples, lexicographic
+    cand = [([(u, v) for v, u in enumerate(p) if u >= 0], parent_depth(p), p) for p in cands]
+    sol, gg, ok = ilp_refine(cap, cand, c_star, gap)
+    trees = []
+    for j, wt in sol:
+        p = cands[j]
+        trees.append(dict(parent=p, root=r, weight=wt, edges=cand[j][0], depth=cand[j][1]))
+    trees = _order_trees(trees)
+    return dict(trees=trees, rate=sum(t["weight"] for t in trees), c_star=c_star, grid=gg, accepted=ok)
+
+
+def plan_allreduce_graph(g, eps=0.1, gap=0.05):
+    """AllReduce plan on an explicit link graph: undirected MWU then ILP; each
+    tree rooted at its centre (Sec. 3.3)."""
+    from .graphs import undirected_pairs
+    n, cap = g
+    if n == 1:
+        return dict(trees=[dict(parent=(-1,), root=0, weight=Fraction(1), edges=[], depth=0)],
+                    rate=Fraction(1), c_star=1.0)
+    pairs = undirected_pairs(g)
+    w, c_star, _ = mwu_allreduce(pairs, n, eps)
+    cands = sorted(w)
+    cand = []
+    for t in cands:
+        root = tree_centre(t, n)
+        cand.append((list(t), parent_depth(root_tree(t, n, root)), t))
+    sol, gg, ok = ilp_refine(pairs, cand, c_star, gap)
+    trees = []
+    for j, wt in sol:
+        t = cands[j]
+        root = tree_centre(t, n)
+        trees.append(dict(parent=root_tree(t, n, root), root=root, weight=wt,
+                          edges=list(t), depth=cand[j][1]))
+    trees = _order_trees(trees)
+    return dict(trees=trees, rate=sum(t["weight"] for t in trees), c_star=c_star, grid=gg, accepted=ok)
+
+
+def plan_switch_allreduce(m):
+    """Sec. 3.5: "with m GPUs, each GPU acts as a root for 1/m of
+    the data chunks and each root is directly connected to (m - 1) leaf nodes,
+    resulting in m one-hop trees".  Tree j = star centred at j, weight 1/2 in
+    K_m link units (Nash-Williams optimum m/2, R#10).  Order: root rank."""
+    trees = []
+    for j in range(m):
+        parent = tuple(-1 if v == j else j for v in range(m))
+        trees.append(dict(parent=parent, root=j, weight=Fraction(1, 2),
+                          edges=[(min(j, v), max(j, v)) for v in range(m) if v != j], depth=1 if m > 1 else 0))
+    return dict(trees=trees, rate=Fraction(m, 2), c_star=m / 2)
+
+
+def plan_switch_broadcast(m, r, onehop=False):
+    """Switch Broadcast (R#10; the paper covers only AllReduce on a switch):
+    the m - 1 two-level trees r -> k -> (all others), weight 1 each (Edmonds
+    optimum m - 1 on K_m), ordered by k; or, for small buffers, the single
+    one-hop star r -> all."""
+    if m == 1:
+        return dict(trees=[dict(parent=(-1,), root=0, weight=Fraction(1), edges=[], depth=0)], rate=Fraction(1))
+    if onehop or m == 2:
+        parent = tuple(-1 if v == r else r for v in range(m))
+        return dict(trees=[dict(parent=parent, root=r, weight=Fraction(1),
+                                edges=[(r, v) for v in range(m) if v != r], depth=1)], rate=Fraction(1))
+    trees = []
+    for k in range(m):
+        if k == r:
+            continue
+        parent = tuple(-1 if v == r else (r if v == k else k) for v in range(m))
+        trees.append(dict(parent=parent, root=r, weight=Fraction(1),
+                          edges=[(p, v) for v, p in enumerate(parent) if p >= 0], depth=2))
+    return dict(trees=trees, rate=Fraction(m - 1))
+
+
+def split_bytes(S, weights):
+    """Weight-proportional split (R#11): G = floor(S/16) grains,
+    b_i = floor(G * sum_{j<i} w_j / sum w); tree i gets bytes
+    [16 b_i, 16 b_{i+1}); the last tree also gets the S mod 16 tail.
+    Returns a list of (lo, hi) byte ranges."""
+    ws = [Fraction(w) for w in weights]
+    W = sum(ws)
+    G = S // GRAIN
+    b = []
+    acc = Fraction(0)
+    for w in ws:
+        b.append(math.floor(G * acc / W))
+        acc += w
+    b.append(G)
+    out = [(GRAIN * b[i], GRAIN * b[i + 1]) for i in range(len(ws))]
+    lo, _ = out[-1]
+    out[-1] = (lo, S)
+    return out
+
+
+def link_load(plan, n, allreduce):
+    """Per-GPU max(egress, ingress) in units of S for a plan:
+    Broadcast edges carry S_i once; AllReduce edges carry S_i in each direction."""
+    egress = [Fraction(0)] * n
+    ingress = [Fraction(0)] * n
+    W = sum(t["weight"] for t in plan["trees"])
+    for t in plan["trees"]:
+        f = t["weight"] / W
+        for v, p in enumerate(t["parent"]):
+            if p < 0:
+                continue
+            egress[p] += f
+            ingress[v] += f
+            if allreduce:
+                egress[v] += f
+                ingress[p] += f
+    return max(max(egress), max(ingress))
