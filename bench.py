@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: tree-packed AllReduce (Blink, arXiv:1910.04940) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl blink|reference]
+
+Workload (BASELINE.json configs[2], "8xB200 NVSwitch one-hop-tree AllReduce"):
+AllReduce SUM of S = 256 MiB fp32 per rank over m = 8 ranks planned as m
+one-hop trees.  One step = one whole AllReduce (split, reduce to
+each tree root, broadcast back) = one launch of the tree executor.
+
+* N = 1 (default): the 8 ranks are virtual ranks on cuda:0 -- all 8 ranks'
+  buffers live in this GPU's HBM and one cooperative launch runs every rank's
+  channels (the same kernels/tables as the multi-GPU path; the fabric is HBM,
+  so the roofline is HBM bandwidth).
+* N > 1 (torchrun): one process per GPU, m = N real ranks over NVLink/NVSwitch
+  with symmetric registered buffers (CUDA IPC); handles exchanged over gloo.
+
+metric = algBW = S / t (GB/s, per-rank buffer bytes per collective time, the
+nccl-tests convention); busBW = algBW * 2(m-1)/m is reported alongside.
+Inputs: 8 x 256 MiB = 2 GiB per step, larger than the 126 MB L2 (no flush).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_M = 8
+DEFAULT_COUNT = 64 << 20           # 256 MiB fp32 per rank
+METRIC = "AllReduce/Broadcast algBW GB/s vs size, 2/4/8 B200, % NVLink peak vs NCCL"
+UNIT = "GB/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), hw=parts[5], hwt=parts[6],
+                                 swt=parts[7], pcap=parts[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        reasons = set()
+        for r in rows:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
+                            ("swt", "sw_thermal_slowdown"), ("pcap", "sw_power_cap")):
+                if r[k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows),
+                "sm_max_mhz": max(r["smax"] for r in rows), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def cpu_oracle_baseline(m, count, budget_s=10.0, max_s=30.0):
+    """The oracle (oracle/, plain numpy, single-threaded) on a bounded sample of
+    the same workload: AllReduce of `count` fp32 per rank over m one-hop trees,
+    repeated until ~budget_s of CPU time."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import synth
+    from oracle import collectives as OC
+    from oracle import packing as OP
+    plan = OP.plan_switch_allreduce(m)
+    sends = synth.inputs(3, m, count, "f32")
+    reps, t = 0, 0.0
+    while t < budget_s and reps < 100:
+        t0 = time.perf_counter()
+        OC.allreduce(plan, sends, "f32", "sum")
+        t += time.perf_counter() - t0
+        reps += 1
+        if t > max_s:
+            break
+    value = reps * count * 4 / t / 1e9
+    return {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{reps} x AllReduce of {count} fp32/rank over {m} one-hop trees "
+                      f"({count * 4 >> 20} MiB/rank), numpy single-thread, {t:.1f}s",
+            "host_cpus": os.cpu_count()}
+
+
+def traffic_from_profiles(workload):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(workload)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- blink arm
+def run_virtual(args):
+    import torch
+    import synth
+    import paper_1910_04940_b200 as B
+
+    m, count, dtype = args.ranks, args.count, "f32"
+    S = count * 4
+    comms = B.init_all([0] * m, cfg=B.config(timeout_s=60.0))
+    sends = [synth.device_input(3, r, count, dtype) for r in range(m)]
+    recvs = [torch.empty_like(s) for s in sends]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for r, c in enumerate(comms):
+            c.allreduce(sends[r], recvs[r], op="sum", stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = comms[0].stats()["launches"]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with Clocks(0) as clk:
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            starts[k].record(stream)
+            step()
+            ends[k].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = comms[0].stats()["launches"] - launches0
+    ms = t0.elapsed_time(t1) / args.steps
+    kern_ms = statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends))
+    algbw = S / (ms * 1e-3) / 1e9
+
+    # e2e: the same call with HOST buffers: pinned H2D of every rank's input,
+    # the collective, D2H of every rank's result -- all inside the timed region
+    hsend = [s.cpu().pin_memory() for s in sends]
+    hrecv = [torch.empty(count, dtype=torch.float32).pin_memory() for _ in range(m)]
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        for r in range(m):
+            sends[r].copy_(hsend[r], non_blocking=True)
+        step()
+        for r in range(m):
+            hrecv[r].copy_(recvs[r], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+
+    peaks, how = load_peaks()
+    workload = f"c3-onehop-allreduce-m{m}-virtual-1gpu-f32-{S >> 20}MiB"
+    alg_bytes = 2 * m * S        # HBM: read every rank's send once, write every rank's recv once
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    out = {
+        "metric": METRIC, "value": round(algbw, 3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded N(0,1)*1e-2 gradients, generated on device)",
+        "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
+                   "ranks_kind": "virtual (all on cuda:0)", "bytes_per_rank": S,
+                   "trees": m, "plan": "one-hop stars (P:440-442)",
+                   "bus_bw_gbs": round(algbw * 2 * (m - 1) / m, 3),
+                   "l2": "inputs 2 GiB/step > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(workload),
+                     "peak_source": f"{how} hbm_gbs",
+                     "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)},
+        "e2e": {"value": round(S / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": m * S, "d2h_bytes_per_step": m * S,
+                "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_oracle_baseline(m, min(count, 16 << 20))
+    for c in comms:
+        c.destroy()
+    return out
+
+
+def run_multiprocess(args):
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_1910_04940_b200 as B
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    ex = B.torch_exchange()
+    comm = B.init_multiprocess(world, rank, local, ex, cfg=B.config(timeout_s=60.0))
+    count = args.count
+    S = count * 4
+    send = synth.device_input(3, rank, count, "f32")
+    recv = torch.empty_like(send)
+    comm.register(send, S, ex)
+    comm.register(recv, S, ex)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        comm.allreduce(send, recv, op="sum", stream=stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = comm.stats()["launches"]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            comm.allreduce(send, recv, op="sum", stream=stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    tt = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    launches = comm.stats()["launches"] - launches0
+    algbw = S / (ms * 1e-3) / 1e9
+    # e2e through host buffers (pinned): H2D input, collective, D2H result
+    hsend = send.cpu().pin_memory()
+    hrecv = torch.empty(count, dtype=torch.float32).pin_memory()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    n_e2e = max(1, min(args.steps, 5))
+    for _ in range(n_e2e):
+        send.copy_(hsend, non_blocking=True)
+        comm.allreduce(send, recv, op="sum", stream=stream)
+        hrecv.copy_(recv, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    et = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64)
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    m = world
+    peak_nvl = 900.0
+    out = None
+    if rank == 0:
+        workload = f"c3-onehop-allreduce-m{m}-nvswitch-f32-{S >> 20}MiB"
+        out = {
+            "metric": METRIC, "value": round(algbw, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded N(0,1)*1e-2 gradients, generated on device)",
+            "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
+                       "ranks_kind": "one process per GPU", "bytes_per_rank": S,
+                       "bus_bw_gbs": round(algbw * 2 * (m - 1) / m, 3),
+                       "l2": "256 MiB/rank send+recv > L2"},
+            "roofline": {"bound": "nvlink", "achieved": round(algbw * 2 * (m - 1) / m, 2),
+                         "peak": peak_nvl, "unit": "GB/s",
+                         "frac": round(algbw * 2 * (m - 1) / m / peak_nvl, 4),
+                         "traffic": None, "peak_source": "nominal NVLink-5 per direction"},
+            "e2e": {"value": round(S / (float(et.item()) * 1e-3) / 1e9, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": S, "d2h_bytes_per_step": S},
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+    comm.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    return out
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle as the reference arm (no reference implementation exists):
+    rank 0 times oracle/ on a bounded sample of the same workload."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return None
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import synth
+    from oracle import collectives as OC
+    from oracle import packing as OP
+    m = args.ranks if int(os.environ.get("WORLD_SIZE", "1")) == 1 else int(os.environ["WORLD_SIZE"])
+    count = min(args.count, 4 << 20)
+    plan = OP.plan_switch_allreduce(m)
+    sends = synth.inputs(3, m, count, "f32")
+    for _ in range(args.warmup):
+        OC.allreduce(plan, sends, "f32", "sum")
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        OC.allreduce(plan, sends, "f32", "sum")
+    t = (time.perf_counter() - t0) / args.steps
+    v = count * 4 / t / 1e9
+    sample = f"AllReduce of {count} fp32/rank ({count * 4 >> 20} MiB) over {m} one-hop trees per step"
+    return {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "impl": "reference",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"c3-onehop-allreduce-m{m}-oracle-cpu-f32-{count * 4 >> 20}MiB",
+                       "collective": "allreduce", "ranks": m},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample, "host_cpus": os.cpu_count()},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="blink", choices=["blink", "reference"])
+    ap.add_argument("--ranks", type=int, default=DEFAULT_M, help="virtual ranks at N=1")
+    ap.add_argument("--count", type=int, default=DEFAULT_COUNT, help="fp32 elements per rank")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        out = run_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        out = run_multiprocess(args)
+    else:
+        out = run_virtual(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,194 @@
+/*
+ * blink.h -- C ABI of the B200-native Blink collectives library.
+ *
+ * Blink (Wang et al., arXiv:1910.04940) packs spanning trees over the link
+ * graph of the GPUs a job was allocated and runs Broadcast and AllReduce as
+ * chunked, pipelined transfers along those trees.  Citations "P:<line>" refer
+ * to PAPER.md (the paper's LaTeX) and name the section / equation.
+ *
+ *   - Problem statement: a graph G(V, E, c_e) of GPUs and links with
+ *     bandwidth-proportional capacities, a root r (Sec. 3.1,
+ *     Eqs. 1-3); the topology is probed over the allocated GPUs only.
+ *   - Broadcast: the buffer is split across the packed trees in proportion to
+ *     their weights, each piece is chunked and forwarded down its tree
+ *     (Sec. 4.1).
+ *   - AllReduce: per tree, reduce toward a chosen root, then broadcast the
+ *     result back down the same tree with the links reversed (P:395-398,
+ *     Sec. 3.3).  On a switch: m one-hop trees, GPU j roots 1/m of the
+ *     data (Sec. 3.5).
+ *   - The API shape follows NCCL's (the paper ships an "NCCL-compatible API",
+ *     P:113): stream-ordered, asynchronous, every rank makes the same
+ *     sequence of calls with the same count / dtype / op / root.
+ *
+ * Conventions for every entry point
+ *   - Every call returns blink_result_t; BLINK_SUCCESS == 0.  On failure the
+ *     comm's blink_last_error() names the offending argument / link / rank.
+ *   - Buffers (sendbuf / recvbuf) are DEVICE pointers on the comm's device,
+ *     owned by the caller, and must stay valid until the stream work of the
+ *     call completes.  In-place iff sendbuf == recvbuf.  count is in elements.
+ *   - Streams are cudaStream_t values passed as void* (NULL = legacy default
+ *     stream).  Calls only enqueue work; nothing blocks the host.
+ *   - The library owns its flag arrays, device tables, IPC mappings and plans;
+ *     blink_destroy() synchronises the device and frees them.
+ *   - One host thread per comm at a time.
+ */
+#ifndef BLINK_H_
+#define BLINK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Result codes; 0..5 mirror ncclResult_t. */
+typedef enum {
+  BLINK_SUCCESS = 0,
+  BLINK_ERR_CUDA = 1,             /* a CUDA runtime/driver call failed            */
+  BLINK_ERR_SYSTEM = 2,           /* host allocation / OS failure                 */
+  BLINK_ERR_INTERNAL = 3,         /* library bug                                  */
+  BLINK_ERR_INVALID_ARGUMENT = 4, /* NULL, bad count/dtype/op, root out of range  */
+  BLINK_ERR_INVALID_USAGE = 5,    /* call sequence or buffer contract violated    */
+  BLINK_ERR_TOPOLOGY = 8,         /* disconnected allocation, bad capacity, dangling
+                                     endpoint, missing reverse link for AllReduce */
+  BLINK_ERR_UNSUPPORTED = 9,      /* no peer access between ranks, too many ranks,
+                                     plan exceeds device-table limits             */
+  BLINK_ERR_TIMEOUT = 10          /* a per-chunk flag wait exceeded cfg.timeout_s;
+                                     reported by the NEXT call on that comm       */
+} blink_result_t;
+
+typedef enum { BLINK_FLOAT32 = 0, BLINK_BFLOAT16 = 1, BLINK_INT32 = 2 } blink_dtype_t;
+
+/* "all the reduction functions supported by NCCL (e.g. min, max, etc.)".
+ * SUM/PROD on floats accumulate in fp32 (bf16 widened exactly, rounded RNE once
+ * per tree node); int32 wraps modulo 2^32; MIN/MAX are exact (IEEE minNum /
+ * maxNum, -0 < +0). */
+typedef enum { BLINK_SUM = 0, BLINK_PROD = 1, BLINK_MIN = 2, BLINK_MAX = 3 } blink_redop_t;
+
+/* Link graph.  Nodes 0..nranks-1 are the ranks' GPUs, in rank order;
+ * further nodes may be SWITCH nodes.  Each link is directed src->dst with a
+ * positive bandwidth-proportional capacity; bidirectional != 0 adds the
+ * reverse edge with the same capacity.  Parallel links add up.  A graph in
+ * which every GPU is attached only to SWITCH nodes is planned with one-hop
+ * trees. */
+typedef enum { BLINK_NODE_GPU = 0, BLINK_NODE_SWITCH = 1 } blink_node_kind_t;
+typedef struct {
+  int src, dst;
+  double capacity;
+  int bidirectional;
+} blink_link_t;
+typedef struct {
+  int num_nodes;
+  const blink_node_kind_t* kinds; /* num_nodes entries; NULL = all GPU          */
+  int num_links;
+  const blink_link_t* links;
+} blink_graph_t;
+
+/* Configuration; pass NULL for defaults (see blink_config_default).
+ *   mwu_eps        MWU approximation parameter, default 0.1
+ *   ilp_gap        ILP relaxation threshold "(e.g., 5%)", default 0.05
+ *   chunk_bytes    0 = size-dependent static table (a8), else fixed chunk size
+ *   ctas           CTA budget per device launch; 0 = 2 x SM count
+ *   threads        threads per CTA (multiple of 32, <= 1024); 0 = 512
+ *   timeout_s      flag-wait bound; expiry aborts the launch and the next call
+ *                  returns BLINK_ERR_TIMEOUT; default 30
+ *   onehop_bcast_max_bytes  switch graphs: Broadcast below this size uses the
+ *                  single one-hop star, above it the m-1 two-level trees
+ *   staging_bytes  multi-process: size of the library-owned symmetric staging
+ *                  buffer used for unregistered user buffers; default 64 MiB */
+typedef struct {
+  double mwu_eps;
+  double ilp_gap;
+  size_t chunk_bytes;
+  int ctas;
+  int threads;
+  double timeout_s;
+  size_t onehop_bcast_max_bytes;
+  size_t staging_bytes;
+} blink_config_t;
+
+void blink_config_default(blink_config_t* cfg);
+
+typedef struct blink_comm* blink_comm_t;
+
+/* ---------------------------------------------------------------- control plane
+ * Host-only planning (no GPU needed): TreeGen for a graph plus the
+ * split and chunking of `count` elements.  Writes a JSON document
+ * {"coll","root","count","esize","rate":[num,den],"trees":[{"root","parent":[],
+ * "weight":[num,den],"depth","lo","hi","chunk","nchunks"}]} (lo/hi/chunk in
+ * elements).  *json_bytes is in/out: capacity in, required size (incl. NUL)
+ * out; BLINK_ERR_INVALID_ARGUMENT if the capacity is too small.
+ * graph == NULL means the NVSwitch model (all ranks behind one switch). */
+blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const blink_config_t* cfg,
+                               int is_allreduce, int root, size_t count, blink_dtype_t dtype,
+                               char* json, size_t* json_bytes);
+
+/* ---------------------------------------------------------------- init
+ * Single-process init of ndev ranks (like ncclCommInitAll).  devs[i] is rank
+ * i's CUDA device; devices may repeat, in which case the ranks sharing a
+ * device are "virtual ranks" whose buffers all live in that GPU's HBM and
+ * whose calls are batched into one launch (needed on a 1-GPU box).  Ranks on
+ * distinct devices need peer access (enabled here).  graph == NULL probes:
+ * all-pairs peer access => switch model, else BLINK_ERR_UNSUPPORTED. */
+blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
+                              const blink_graph_t* graph, const blink_config_t* cfg);
+
+/* Multi-process init (one GPU per process).  The handle exchange is the
+ * caller's: blink_export_handle() fills a blob (<= 512 bytes), the caller
+ * all-gathers the nranks blobs in rank order (e.g. torch.distributed over
+ * gloo) and passes them to blink_connect(), which maps the peers' flag arrays
+ * and staging buffers (CUDA IPC over NVLink) and builds the plans. */
+blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_device,
+                          const blink_graph_t* graph, const blink_config_t* cfg);
+blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_bytes);
+blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t blob_bytes);
+
+/* Symmetric buffer registration (multi-process zero-copy).  Collective: every
+ * rank registers its own buffer of the same size in the same order, exports a
+ * blob, all-gathers, and connects.  A registered buffer is used in place (the
+ * kernels read and write peers' copies directly); collectives on it must use
+ * the same byte offset into it on every rank.  Unregistered buffers go
+ * through the staging buffer (local copy in/out).  In single-process comms
+ * registration is unnecessary (pointers are exchanged at launch) and these
+ * calls are accepted no-ops. */
+blink_result_t blink_register_export(blink_comm_t comm, void* buf, size_t bytes, void* blob,
+                                     size_t* blob_bytes);
+blink_result_t blink_register_connect(blink_comm_t comm, void* buf, const void* all_blobs,
+                                      size_t blob_bytes);
+
+/* ---------------------------------------------------------------- collectives
+ * Broadcast `count` elements of root's sendbuf into every rank's recvbuf
+ * (P:477-478).  sendbuf is read on the root only (may be NULL elsewhere). */
+blink_result_t blink_broadcast(blink_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                               blink_dtype_t dtype, int root, void* stream);
+/* AllReduce of `count` elements.  Every rank's recvbuf
+ * receives the same result, computed along the packed trees in the fixed
+ * per-node operand order (ascending rank, R#12). */
+blink_result_t blink_allreduce(blink_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                               blink_dtype_t dtype, blink_redop_t op, void* stream);
+
+/* ---------------------------------------------------------------- introspection
+ * Same JSON as blink_plan_json, for the plan this comm would run, plus "ctas"
+ * (CTAs of this rank's launch). */
+blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, size_t count,
+                              blink_dtype_t dtype, char* json, size_t* json_bytes);
+/* Launch statistics of the most recent call that reached the device:
+ * kernels launched by it, CTAs, chunks. */
+typedef struct {
+  int64_t launches;      /* cumulative kernel launches by this comm's device batch */
+  int last_ctas;
+  int last_chunks;
+  int last_trees;
+} blink_stats_t;
+blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* stats);
+blink_result_t blink_comm_info(blink_comm_t comm, int* nranks, int* rank, int* device);
+
+blink_result_t blink_destroy(blink_comm_t comm);
+const char* blink_result_string(blink_result_t r);
+const char* blink_last_error(blink_comm_t comm); /* comm may be NULL: last global error */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLINK_H_ */

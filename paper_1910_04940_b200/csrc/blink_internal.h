@@ -1,0 +1,144 @@
+// Internal structures shared by the control plane (plan.cpp), the host
+// runtime (runtime.cpp) and the device executor (exec.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/blink.h"
+
+namespace blink {
+
+// ---------------------------------------------------------------- limits
+constexpr int kMaxRanks = 16;       // ranks per comm (one NVSwitch node; DGX-2 = 16)
+constexpr int kMaxTrees = 32;       // trees per plan
+constexpr int kMaxChunks = 512;     // chunks per tree per call
+constexpr int kGrain = 16;          // split grain in bytes (R#11) == one 128-bit vector
+
+// Flag region of one rank (uint64 words, monotonically increasing epochs,
+// never reset).  Producers write into the CONSUMER's region:
+//   entry[u]              rank u entered call `epoch` (its send is ready and
+//                         its recv may be overwritten)
+//   pflag[i][u][c]        child u's partial for tree i / chunk c is ready
+//                         (written by u into its parent's region)
+//   bflag[i][c]           the final value of tree i / chunk c has been
+//                         written into this rank's recv (written by parent)
+constexpr size_t kEntryWords = kMaxRanks;
+constexpr size_t kPflagWords = size_t(kMaxTrees) * kMaxRanks * kMaxChunks;
+constexpr size_t kBflagWords = size_t(kMaxTrees) * kMaxChunks;
+constexpr size_t kFlagWords = kEntryWords + kPflagWords + kBflagWords;
+constexpr size_t kFlagBytes = kFlagWords * sizeof(uint64_t);
+__host__ __device__ inline size_t entry_idx(int u) { return size_t(u); }
+__host__ __device__ inline size_t pflag_idx(int tree, int child, int chunk) {
+  return kEntryWords + (size_t(tree) * kMaxRanks + child) * kMaxChunks + chunk;
+}
+__host__ __device__ inline size_t bflag_idx(int tree, int chunk) {
+  return kEntryWords + kPflagWords + size_t(tree) * kMaxChunks + chunk;
+}
+
+enum Coll : int { kBroadcast = 0, kAllReduce = 1 };
+
+// ---------------------------------------------------------------- plans
+struct Tree {
+  int root = 0;
+  std::vector<int> parent;   // parent[root] = -1
+  int64_t wnum = 1;          // weight = wnum / wden (exact rational, P:390 grid)
+  int64_t wden = 1;
+  int depth = 0;
+};
+
+struct Plan {                // size-independent (TreeGen output)
+  int coll = kAllReduce;
+  int root = -1;             // broadcast root, -1 for AllReduce
+  int nranks = 0;
+  std::vector<Tree> trees;   // in split order (R#11)
+  int64_t rate_num = 0, rate_den = 1;
+  double c_star = 0.0;       // MWU rate (0 for closed forms)
+  int grid = 1;              // accepted relaxation level g
+  bool switch_model = false;
+};
+
+struct TreeRange {           // per call size
+  int64_t lo = 0, hi = 0;    // element range [lo, hi)
+  int64_t chunk = 0;         // elements per chunk
+  int nchunks = 0;
+};
+
+// Role of one CTA (a "channel" slice, a6).
+enum Role : int {
+  kRoleReduce = 0,  // AllReduce: combine own send + children, forward to parent
+                    // (or, at the root, write the result and push it down)
+  kRoleBcast = 1,   // forward a chunk down the tree (Broadcast, AllReduce phase 2)
+  kRoleExit = 2,    // only entry/exit bookkeeping for this rank
+};
+
+struct DevTask {             // one per CTA; 64 bytes
+  int16_t rank;              // acting rank v
+  int16_t tree;              // tree index i
+  int16_t role;
+  int16_t parent;            // -1 at the tree root
+  uint32_t children;         // bitmask of v's children in tree i
+  uint32_t leafmask;         // children that are leaves (their send is read directly)
+  int32_t cta_idx, cta_cnt;  // position among the CTAs of this (rank, tree, role)
+  int32_t exit_idx, exit_cnt;// position among the CTAs of rank v (exit wait split)
+  int32_t do_entry;          // this CTA publishes rank v's entry flag
+  int32_t pad0;
+  int64_t pad1[3];
+};
+static_assert(sizeof(DevTask) == 64, "DevTask layout");
+
+struct DevTree {             // 32 bytes; byte offsets into every rank's buffers
+  int64_t lo, hi, chunk;
+  int32_t nchunks;
+  int32_t root;
+};
+
+constexpr int kMaxArgRanks = kMaxRanks;
+struct LaunchArgs {
+  const DevTask* tasks;
+  const DevTree* trees;
+  int ntrees;
+  int nranks;
+  int coll;                  // Coll
+  int dtype;                 // blink_dtype_t
+  int op;                    // blink_redop_t
+  int exit_wait;             // 1 when ranks live in different launches
+  int bcast_root;            // Broadcast root rank
+  int pad;
+  uint64_t epoch;
+  uint64_t timeout_ns;
+  int* err;                  // host-mapped error word (0 = ok)
+  char* send[kMaxArgRanks];
+  char* recv[kMaxArgRanks];
+  uint64_t* flags[kMaxArgRanks];
+};
+
+// exec.cu
+cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,
+                        bool cooperative);
+cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream);
+int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll);
+
+// plan.cpp -------------------------------------------------------------
+struct Graph {
+  int n = 0;                       // GPU nodes (ranks)
+  bool switch_model = true;        // all GPUs behind a switch (or NULL graph)
+  std::vector<std::vector<double>> cap;  // cap[u][v], directed, GPU nodes only
+};
+
+// Parse/validate a user graph for nranks ranks.  Returns BLINK_SUCCESS or an
+// error with `err` describing the offending link/node.
+blink_result_t build_graph(const blink_graph_t* g, int nranks, Graph* out, std::string* err);
+blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_t& cfg, Plan* out,
+                         std::string* err);
+// Split (R#11) + chunking (a8).  ctas_for_tree: CTA count expected per tree channel.
+blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
+                         int ctas_hint, std::vector<TreeRange>* out, std::string* err);
+std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vector<TreeRange>& r,
+                         int ctas);
+int esize_of(blink_dtype_t d);
+
+}  // namespace blink

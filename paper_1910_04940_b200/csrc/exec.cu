@@ -1,0 +1,495 @@
+// Device executor for tree-packed Broadcast / AllReduce on sm_100a.
+//
+// One persistent, cooperative launch per device per collective.  Every CTA
+// owns one slice of a "channel" = (rank v, tree i, role) and walks that
+// tree's chunks c = cta_idx, cta_idx + cta_cnt, ... in increasing order, so
+// chunks of all trees and all hops are in flight at once (pipelining,
+// P:510-517; concurrency across trees with fair interleaving).
+//
+// Data movement is SM load/store over NVLink/NVSwitch peer mappings (or plain
+// HBM for virtual ranks sharing one GPU):
+//   REDUCE (a3)  pull the children's chunk (leaf child: its send buffer;
+//                internal child: the partial it left in its own recv
+//                buffer), combine with the own send chunk in ascending-rank
+//                order with fp32 accumulation (R#12, R#13), then
+//                  non-root: store the partial into the own recv buffer and
+//                           release the parent's pflag[i][v][c];
+//                  root:    store the result into the own recv and PUSH it
+//                           into every child's recv (a4), release bflag.
+//   BCAST  (a2/a4) wait bflag[i][c] (non-root), read the chunk from the own
+//                recv (root: send), push it into the children's recv,
+//                release their bflag[i][c].
+// Readiness (a5): 64-bit epoch flags in the consumer's memory, written with
+// st.release.sys after a CTA barrier + fence, polled with ld.acquire.sys by
+// one thread; data is read with ld.global.cg (L2, never a stale L1 line).
+// 128-bit vectors on the aligned body, scalar elements on tails / misaligned
+// buffers.  Timeouts (globaltimer) abort the launch and set a host-mapped
+// error word instead of hanging.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "blink_internal.h"
+
+namespace blink {
+namespace {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int ld_volatile_int(const int* p) {
+  return *reinterpret_cast<const volatile int*>(p);
+}
+
+// ------------------------------------------------------------------ arithmetic
+// R#12/R#13: fp32 accumulation, RNE, no FMA; int32 wraps; MIN/MAX minNum/maxNum
+// with -0 < +0.
+template <int OP>
+__device__ __forceinline__ float fop(float a, float b) {
+  if (OP == BLINK_SUM) return __fadd_rn(a, b);
+  if (OP == BLINK_PROD) return __fmul_rn(a, b);
+  if (OP == BLINK_MIN) {
+    float r = (a < b) ? a : b;
+    if (a == b) r = (__float_as_uint(a) & 0x80000000u) ? a : b;
+    if (a != a) r = b;
+    else if (b != b) r = a;
+    return r;
+  }
+  float r = (a > b) ? a : b;
+  if (a == b) r = (__float_as_uint(a) & 0x80000000u) ? b : a;
+  if (a != a) r = b;
+  else if (b != b) r = a;
+  return r;
+}
+template <int OP>
+__device__ __forceinline__ int iop(int a, int b) {
+  if (OP == BLINK_SUM) return int(unsigned(a) + unsigned(b));
+  if (OP == BLINK_PROD) return int(unsigned(a) * unsigned(b));
+  if (OP == BLINK_MIN) return a < b ? a : b;
+  return a > b ? a : b;
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t f2bf(float f) {  // RNE, NaN -> quiet NaN
+  uint32_t b = __float_as_uint(f);
+  if (f != f) return (b >> 16) | 0x40u;
+  return (b + 0x7fffu + ((b >> 16) & 1u)) >> 16;
+}
+
+template <int DT>
+struct Acc;
+template <>
+struct Acc<BLINK_FLOAT32> {
+  float v[4];
+};
+template <>
+struct Acc<BLINK_BFLOAT16> {
+  float v[8];
+};
+template <>
+struct Acc<BLINK_INT32> {
+  int v[4];
+};
+
+template <int DT>
+__device__ __forceinline__ void widen(Acc<DT>& a, const uint4& x);
+template <>
+__device__ __forceinline__ void widen<BLINK_FLOAT32>(Acc<BLINK_FLOAT32>& a, const uint4& x) {
+  a.v[0] = __uint_as_float(x.x);
+  a.v[1] = __uint_as_float(x.y);
+  a.v[2] = __uint_as_float(x.z);
+  a.v[3] = __uint_as_float(x.w);
+}
+template <>
+__device__ __forceinline__ void widen<BLINK_BFLOAT16>(Acc<BLINK_BFLOAT16>& a, const uint4& x) {
+  a.v[0] = bf_lo(x.x); a.v[1] = bf_hi(x.x);
+  a.v[2] = bf_lo(x.y); a.v[3] = bf_hi(x.y);
+  a.v[4] = bf_lo(x.z); a.v[5] = bf_hi(x.z);
+  a.v[6] = bf_lo(x.w); a.v[7] = bf_hi(x.w);
+}
+template <>
+__device__ __forceinline__ void widen<BLINK_INT32>(Acc<BLINK_INT32>& a, const uint4& x) {
+  a.v[0] = int(x.x);
+  a.v[1] = int(x.y);
+  a.v[2] = int(x.z);
+  a.v[3] = int(x.w);
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void combine(Acc<DT>& a, const uint4& x) {
+  Acc<DT> b;
+  widen<DT>(b, x);
+#pragma unroll
+  for (int k = 0; k < int(sizeof(a.v) / sizeof(a.v[0])); ++k) {
+    if constexpr (DT == BLINK_INT32)
+      a.v[k] = iop<OP>(a.v[k], b.v[k]);
+    else
+      a.v[k] = fop<OP>(a.v[k], b.v[k]);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ uint4 narrow(const Acc<DT>& a);
+template <>
+__device__ __forceinline__ uint4 narrow<BLINK_FLOAT32>(const Acc<BLINK_FLOAT32>& a) {
+  return make_uint4(__float_as_uint(a.v[0]), __float_as_uint(a.v[1]), __float_as_uint(a.v[2]),
+                    __float_as_uint(a.v[3]));
+}
+template <>
+__device__ __forceinline__ uint4 narrow<BLINK_BFLOAT16>(const Acc<BLINK_BFLOAT16>& a) {
+  return make_uint4(f2bf(a.v[0]) | (f2bf(a.v[1]) << 16), f2bf(a.v[2]) | (f2bf(a.v[3]) << 16),
+                    f2bf(a.v[4]) | (f2bf(a.v[5]) << 16), f2bf(a.v[6]) | (f2bf(a.v[7]) << 16));
+}
+template <>
+__device__ __forceinline__ uint4 narrow<BLINK_INT32>(const Acc<BLINK_INT32>& a) {
+  return make_uint4(unsigned(a.v[0]), unsigned(a.v[1]), unsigned(a.v[2]), unsigned(a.v[3]));
+}
+
+// Scalar element ops (tails, misaligned buffers).
+template <int DT, int OP>
+struct Scalar {
+  static constexpr int es = DT == BLINK_BFLOAT16 ? 2 : 4;
+  __device__ static float load_f(const char* p) {
+    if (DT == BLINK_BFLOAT16) return __uint_as_float(uint32_t(__ldcg((const unsigned short*)p)) << 16);
+    return __ldcg((const float*)p);
+  }
+  __device__ static void reduce(const char* const* srcs, int nsrc, char* const* dsts, int ndst,
+                                int64_t off) {
+    if constexpr (DT == BLINK_INT32) {
+      int acc = __ldcg((const int*)(srcs[0] + off));
+      for (int s = 1; s < nsrc; ++s) acc = iop<OP>(acc, __ldcg((const int*)(srcs[s] + off)));
+      for (int d = 0; d < ndst; ++d) __stcg((int*)(dsts[d] + off), acc);
+    } else {
+      float acc = load_f(srcs[0] + off);
+      for (int s = 1; s < nsrc; ++s) acc = fop<OP>(acc, load_f(srcs[s] + off));
+      if (DT == BLINK_BFLOAT16) {
+        unsigned short h = (unsigned short)f2bf(acc);
+        for (int d = 0; d < ndst; ++d) __stcg((unsigned short*)(dsts[d] + off), h);
+      } else {
+        for (int d = 0; d < ndst; ++d) __stcg((float*)(dsts[d] + off), acc);
+      }
+    }
+  }
+};
+
+// ------------------------------------------------------------------ chunk bodies
+constexpr int kU = 2;  // vectors per thread per step
+constexpr int kG = 4;  // sources loaded before combining (memory-level parallelism)
+
+// reduce bytes [b0, b1) of the chunk: dst_d[x] = combine_s src_s[x]
+template <int DT, int OP, bool VEC>
+__device__ __forceinline__ void reduce_range(const char* const* srcs, int nsrc, char* const* dsts,
+                                             int ndst, int64_t b0, int64_t b1) {
+  constexpr int es = Scalar<DT, OP>::es;
+  const int T = blockDim.x;
+  int64_t vb1 = b0;
+  if (VEC) {
+    const int64_t v0 = b0 >> 4, v1 = b1 >> 4;  // b0 is 16-byte aligned
+    int64_t j = v0 + threadIdx.x;
+    for (; j + (kU - 1) * T < v1; j += kU * T) {
+      Acc<DT> acc[kU];
+      for (int s0 = 0; s0 < nsrc; s0 += kG) {
+        uint4 x[kG][kU];
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+          if (s0 + g < nsrc) {
+            const uint4* p = reinterpret_cast<const uint4*>(srcs[s0 + g]);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) x[g][u] = __ldcg(p + j + u * T);
+          }
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+          if (s0 + g < nsrc) {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              if (s0 + g == 0)
+                widen<DT>(acc[u], x[g][u]);
+              else
+                combine<DT, OP>(acc[u], x[g][u]);
+            }
+          }
+      }
+      uint4 out[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) out[u] = narrow<DT>(acc[u]);
+      for (int d = 0; d < ndst; ++d) {
+        uint4* q = reinterpret_cast<uint4*>(dsts[d]);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) __stcg(q + j + u * T, out[u]);
+      }
+    }
+    for (; j < v1; j += T) {
+      Acc<DT> acc;
+      widen<DT>(acc, __ldcg(reinterpret_cast<const uint4*>(srcs[0]) + j));
+      for (int s = 1; s < nsrc; ++s)
+        combine<DT, OP>(acc, __ldcg(reinterpret_cast<const uint4*>(srcs[s]) + j));
+      uint4 o = narrow<DT>(acc);
+      for (int d = 0; d < ndst; ++d) __stcg(reinterpret_cast<uint4*>(dsts[d]) + j, o);
+    }
+    vb1 = v1 << 4;
+  }
+  for (int64_t off = vb1 + int64_t(threadIdx.x) * es; off < b1; off += int64_t(T) * es)
+    Scalar<DT, OP>::reduce(srcs, nsrc, dsts, ndst, off);
+}
+
+// copy bytes [b0, b1) from src to every dst
+template <bool VEC>
+__device__ __forceinline__ void copy_range(const char* src, char* const* dsts, int ndst, int64_t b0,
+                                           int64_t b1) {
+  const int T = blockDim.x;
+  int64_t vb1 = b0;
+  if (VEC) {
+    constexpr int U = 4;
+    const int64_t v0 = b0 >> 4, v1 = b1 >> 4;
+    const uint4* p = reinterpret_cast<const uint4*>(src);
+    int64_t j = v0 + threadIdx.x;
+    for (; j + (U - 1) * T < v1; j += U * T) {
+      uint4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = __ldcg(p + j + u * T);
+      for (int d = 0; d < ndst; ++d) {
+        uint4* q = reinterpret_cast<uint4*>(dsts[d]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) __stcg(q + j + u * T, x[u]);
+      }
+    }
+    for (; j < v1; j += T) {
+      uint4 x = __ldcg(p + j);
+      for (int d = 0; d < ndst; ++d) __stcg(reinterpret_cast<uint4*>(dsts[d]) + j, x);
+    }
+    vb1 = v1 << 4;
+  }
+  for (int64_t off = vb1 + threadIdx.x; off < b1; off += T) {
+    char c = __ldcg(src + off);
+    for (int d = 0; d < ndst; ++d) dsts[d][off] = c;
+  }
+}
+
+// ------------------------------------------------------------------ waits
+struct Ctl {
+  uint64_t epoch;
+  uint64_t timeout_ns;
+  int* err;
+};
+
+// Spin (one thread) until *p >= epoch.  Returns false on timeout / abort.
+__device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
+  if (ld_acquire_sys(p) >= c.epoch) return true;
+  uint64_t t0 = globaltimer();
+  for (int spin = 0;; ++spin) {
+    if (ld_acquire_sys(p) >= c.epoch) return true;
+    if ((spin & 255) == 255) {
+      if (ld_volatile_int(c.err) != 0) return false;
+      if (globaltimer() - t0 > c.timeout_ns) {
+        *reinterpret_cast<volatile int*>(c.err) = int(BLINK_ERR_TIMEOUT);  // host-mapped word
+        return false;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void signal(uint64_t* p, uint64_t epoch) { st_release_sys(p, epoch); }
+
+// ------------------------------------------------------------------ the kernel
+template <int DT, int OP, bool VEC>
+__global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
+  __shared__ const char* srcs[kMaxRanks + 1];
+  __shared__ char* dsts[kMaxRanks + 1];
+  __shared__ int s_nsrc, s_ndst, s_ok;
+  const DevTask t = a.tasks[blockIdx.x];
+  const int v = t.rank;
+  const Ctl ctl{a.epoch, a.timeout_ns, a.err};
+  uint64_t* myflags = a.flags[v];
+
+  // entry: my send is ready and my recv may be overwritten (epoch e)
+  if (t.do_entry && threadIdx.x == 0) {
+    fence_sys();
+    for (int u = 0; u < a.nranks; ++u)
+      if (u != v) signal(a.flags[u] + entry_idx(v), a.epoch);
+  }
+
+  if (t.role == kRoleReduce || t.role == kRoleBcast) {
+    const DevTree tr = a.trees[t.tree];
+    const bool is_root = t.parent < 0;
+    if (threadIdx.x == 0) {
+      int ns = 0, nd = 0;
+      bool ok = true;
+      if (t.role == kRoleReduce) {
+        const uint32_t ops = t.children | (1u << v);
+        for (int u = 0; u < a.nranks; ++u) {
+          if (!((ops >> u) & 1u)) continue;
+          srcs[ns++] = (u == v || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
+        }
+        dsts[nd++] = a.recv[v];
+        if (is_root)
+          for (int u = 0; u < a.nranks; ++u)
+            if ((t.children >> u) & 1u) dsts[nd++] = a.recv[u];
+        // leaf children: their send is ready once they entered
+        for (int u = 0; u < a.nranks && ok; ++u)
+          if ((t.leafmask >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
+      } else {
+        const bool src_root = (a.coll == kBroadcast) && is_root;
+        srcs[ns++] = src_root ? a.send[v] : a.recv[v];
+        if (src_root && a.send[v] != a.recv[v]) dsts[nd++] = a.recv[v];
+        for (int u = 0; u < a.nranks; ++u)
+          if ((t.children >> u) & 1u) dsts[nd++] = a.recv[u];
+        // Broadcast pushes into children's recv: they must have entered
+        if (a.coll == kBroadcast)
+          for (int u = 0; u < a.nranks && ok; ++u)
+            if ((t.children >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
+      }
+      s_nsrc = ns;
+      s_ndst = nd;
+      s_ok = ok;
+    }
+    __syncthreads();
+    bool alive = s_ok;
+    __syncthreads();  // everyone read s_ok before thread 0 may overwrite it
+    const bool need_bflag = (t.role == kRoleBcast) && !((a.coll == kBroadcast) && is_root);
+    for (int c = t.cta_idx; alive && c < tr.nchunks; c += t.cta_cnt) {
+      if (threadIdx.x == 0) {
+        bool ok = true;
+        if (t.role == kRoleReduce) {
+          const uint32_t internal = t.children & ~t.leafmask;
+          for (int u = 0; u < a.nranks && ok; ++u)
+            if ((internal >> u) & 1u) ok = wait_ge(myflags + pflag_idx(t.tree, u, c), ctl);
+        } else if (need_bflag) {
+          ok = wait_ge(myflags + bflag_idx(t.tree, c), ctl);
+        }
+        s_ok = ok;
+      }
+      __syncthreads();
+      alive = s_ok;
+      if (!alive) break;
+      const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
+      const int64_t b1 = min(tr.hi, b0 + tr.chunk);
+      if (t.role == kRoleReduce)
+        reduce_range<DT, OP, VEC>(srcs, s_nsrc, dsts, s_ndst, b0, b1);
+      else
+        copy_range<VEC>(srcs[0], dsts, s_ndst, b0, b1);
+      __syncthreads();  // every thread's stores of chunk c are issued
+      if (threadIdx.x == 0) {
+        fence_sys();
+        if (t.role == kRoleReduce && !is_root) {
+          signal(a.flags[t.parent] + pflag_idx(t.tree, v, c), a.epoch);
+        } else {
+          for (int u = 0; u < a.nranks; ++u)
+            if ((t.children >> u) & 1u) signal(a.flags[u] + bflag_idx(t.tree, c), a.epoch);
+        }
+      }
+    }
+  }
+
+  // exit: every final chunk of every tree not rooted here has arrived, which
+  // also means every peer finished reading this rank's buffers (causality).
+  if (a.exit_wait) {
+    __syncthreads();
+    int k = 0;
+    for (int i = 0; i < a.ntrees; ++i) {
+      const DevTree tr = a.trees[i];
+      if (tr.root == v) continue;
+      for (int c = 0; c < tr.nchunks; ++c, ++k) {
+        if (k % t.exit_cnt != t.exit_idx) continue;
+        if (((k / t.exit_cnt) % blockDim.x) != threadIdx.x) continue;
+        wait_ge(myflags + bflag_idx(i, c), ctl);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <bool VEC>
+__global__ void copy_kernel(char* dst, const char* src, int64_t bytes) {
+  const int64_t T = int64_t(gridDim.x) * blockDim.x;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t vb = 0;
+  if (VEC) {
+    const int64_t nv = bytes >> 4;
+    for (int64_t j = tid; j < nv; j += T)
+      __stcg(reinterpret_cast<uint4*>(dst) + j, __ldcg(reinterpret_cast<const uint4*>(src) + j));
+    vb = nv << 4;
+  }
+  for (int64_t j = vb + tid; j < bytes; j += T) dst[j] = src[j];
+}
+
+typedef void (*ExecFn)(const LaunchArgs);
+
+template <int DT, bool VEC>
+ExecFn pick_op(int op) {
+  switch (op) {
+    case BLINK_SUM: return exec_kernel<DT, BLINK_SUM, VEC>;
+    case BLINK_PROD: return exec_kernel<DT, BLINK_PROD, VEC>;
+    case BLINK_MIN: return exec_kernel<DT, BLINK_MIN, VEC>;
+    case BLINK_MAX: return exec_kernel<DT, BLINK_MAX, VEC>;
+  }
+  return nullptr;
+}
+
+ExecFn pick(int coll, int dtype, int op, bool vec) {
+  if (coll == kBroadcast) return vec ? exec_kernel<BLINK_FLOAT32, BLINK_SUM, true>
+                                     : exec_kernel<BLINK_FLOAT32, BLINK_SUM, false>;
+  switch (dtype) {
+    case BLINK_FLOAT32: return vec ? pick_op<BLINK_FLOAT32, true>(op) : pick_op<BLINK_FLOAT32, false>(op);
+    case BLINK_BFLOAT16: return vec ? pick_op<BLINK_BFLOAT16, true>(op) : pick_op<BLINK_BFLOAT16, false>(op);
+    case BLINK_INT32: return vec ? pick_op<BLINK_INT32, true>(op) : pick_op<BLINK_INT32, false>(op);
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,
+                        bool cooperative) {
+  ExecFn fn = pick(a.coll, a.dtype, a.op, vec);
+  if (!fn) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = cooperative ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll) {
+  ExecFn fn = pick(coll, dtype, op, vec);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, 0) != cudaSuccess) return 0;
+  return n;
+}
+
+cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0 || dst == src) return cudaSuccess;
+  bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t work = int64_t(bytes >> 4) / 512 + 1;
+  int grid = int(work < int64_t(sms) * 4 ? work : int64_t(sms) * 4);
+  if (vec)
+    copy_kernel<true><<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<char*>(dst), static_cast<const char*>(src), int64_t(bytes));
+  else
+    copy_kernel<false><<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<char*>(dst), static_cast<const char*>(src), int64_t(bytes));
+  return cudaGetLastError();
+}
+
+}  // namespace blink

@@ -1,0 +1,983 @@
+// Control plane: link graph, MWU tree packing, ILP tree-count minimisation,
+// one-hop switch trees, weight-proportional split and chunking.
+//
+//   Graph model ............ P:338 (Sec. 3.1)
+//   MWU packing ............ P:363-367 (Sec. 3.2), Garg-Koenemann step (R#4)
+//   ILP + relaxation ....... P:371-393 (Sec. 3.2.1, Eqs. 4-7; R#5, R#6)
+//   AllReduce trees ........ P:395-398 (Sec. 3.3): undirected packing,
+//                            per-tree root = centre (R#9)
+//   One-hop switch trees ... P:440-442 (Sec. 3.5); switch Broadcast (R#10)
+//   Split / chunking ....... P:477-478 (Sec. 4.1; R#11), P:510-517 (a8)
+//
+// This is host code only; it never touches a GPU.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <numeric>
+#include <set>
+#include <sstream>
+
+#include "blink_internal.h"
+
+namespace blink {
+
+int esize_of(blink_dtype_t d) {
+  switch (d) {
+    case BLINK_FLOAT32: return 4;
+    case BLINK_BFLOAT16: return 2;
+    case BLINK_INT32: return 4;
+  }
+  return 0;
+}
+
+// ============================================================== graph
+blink_result_t build_graph(const blink_graph_t* g, int nranks, Graph* out, std::string* err) {
+  out->n = nranks;
+  out->cap.assign(nranks, std::vector<double>(nranks, 0.0));
+  if (g == nullptr) {  // NVSwitch model: uniform K_m
+    out->switch_model = true;
+    return BLINK_SUCCESS;
+  }
+  if (g->num_nodes < nranks) {
+    *err = "graph has " + std::to_string(g->num_nodes) + " nodes but the comm has " +
+           std::to_string(nranks) + " ranks (nodes 0..nranks-1 must be the ranks' GPUs)";
+    return BLINK_ERR_TOPOLOGY;
+  }
+  if (g->num_links < 0 || (g->num_links > 0 && g->links == nullptr)) {
+    *err = "graph.links is NULL";
+    return BLINK_ERR_INVALID_ARGUMENT;
+  }
+  auto kind = [&](int v) { return g->kinds ? g->kinds[v] : BLINK_NODE_GPU; };
+  for (int v = 0; v < nranks; ++v)
+    if (kind(v) != BLINK_NODE_GPU) {
+      *err = "node " + std::to_string(v) + " is a rank but not a GPU node";
+      return BLINK_ERR_TOPOLOGY;
+    }
+  for (int v = nranks; v < g->num_nodes; ++v)
+    if (kind(v) == BLINK_NODE_GPU) {
+      *err = "GPU node " + std::to_string(v) + " is not one of the " + std::to_string(nranks) +
+             " ranks (pass the induced sub-allocation, P:320)";
+      return BLINK_ERR_TOPOLOGY;
+    }
+  bool any_switch = false;
+  std::vector<int> on_switch(nranks, 0);
+  for (int k = 0; k < g->num_links; ++k) {
+    const blink_link_t& L = g->links[k];
+    char buf[160];
+    if (L.src < 0 || L.src >= g->num_nodes || L.dst < 0 || L.dst >= g->num_nodes) {
+      snprintf(buf, sizeof buf, "link %d (%d->%d) has a dangling endpoint", k, L.src, L.dst);
+      *err = buf;
+      return BLINK_ERR_TOPOLOGY;
+    }
+    if (!(L.capacity > 0.0) || !std::isfinite(L.capacity)) {
+      snprintf(buf, sizeof buf, "link %d (%d->%d) has nonpositive capacity %g", k, L.src, L.dst,
+               L.capacity);
+      *err = buf;
+      return BLINK_ERR_TOPOLOGY;
+    }
+    if (L.src == L.dst) {
+      snprintf(buf, sizeof buf, "link %d is a self-loop on node %d", k, L.src);
+      *err = buf;
+      return BLINK_ERR_TOPOLOGY;
+    }
+    bool ss = kind(L.src) == BLINK_NODE_SWITCH, ds = kind(L.dst) == BLINK_NODE_SWITCH;
+    if (ss || ds) {
+      any_switch = true;
+      if (ss && ds) continue;  // switch fabric
+      on_switch[ss ? L.dst : L.src] = 1;
+      continue;
+    }
+    out->cap[L.src][L.dst] += L.capacity;
+    if (L.bidirectional) out->cap[L.dst][L.src] += L.capacity;
+  }
+  if (any_switch) {
+    for (int u = 0; u < nranks; ++u)
+      for (int v = 0; v < nranks; ++v)
+        if (out->cap[u][v] > 0) {
+          *err = "mixed switch + direct GPU links are not supported (GPU " + std::to_string(u) +
+                 "->" + std::to_string(v) + ")";
+          return BLINK_ERR_UNSUPPORTED;
+        }
+    for (int v = 0; v < nranks; ++v)
+      if (!on_switch[v] && nranks > 1) {
+        *err = "GPU " + std::to_string(v) + " is not attached to any switch (disconnected)";
+        return BLINK_ERR_TOPOLOGY;
+      }
+    out->switch_model = true;
+    return BLINK_SUCCESS;
+  }
+  out->switch_model = false;
+  // weak connectivity: report one disconnected partition
+  std::vector<int> seen(nranks, 0);
+  std::vector<int> st{0};
+  seen[0] = 1;
+  while (!st.empty()) {
+    int u = st.back();
+    st.pop_back();
+    for (int v = 0; v < nranks; ++v)
+      if (!seen[v] && (out->cap[u][v] > 0 || out->cap[v][u] > 0)) {
+        seen[v] = 1;
+        st.push_back(v);
+      }
+  }
+  std::string part;
+  for (int v = 0; v < nranks; ++v)
+    if (!seen[v]) part += (part.empty() ? "" : ",") + std::to_string(v);
+  if (!part.empty()) {
+    *err = "allocation is disconnected: GPUs {" + part + "} are unreachable from GPU 0";
+    return BLINK_ERR_TOPOLOGY;
+  }
+  return BLINK_SUCCESS;
+}
+
+// ============================================================== MWU inner oracles
+namespace {
+
+struct WEdge {
+  int u, v;
+  double w;
+  int key;  // lexicographic (src, dst) tie-break
+};
+
+// Chu-Liu / Edmonds minimum arborescence.  Returns, for every vertex, the key
+// of its chosen in-edge (-1 at the root).  Written as an explicit contraction
+// loop with a stack of levels that is unwound afterwards.
+std::vector<int> min_arborescence(int n, int root, const std::vector<WEdge>& edges0) {
+  struct Level {
+    int n, root;
+    std::vector<WEdge> edges;        // edges of this level (key = index into parent level's edges)
+    std::vector<int> best;           // chosen in-edge index per vertex
+    std::vector<int> comp;           // vertex -> contracted id
+  };
+  std::vector<Level> levels;
+  Level cur;
+  cur.n = n;
+  cur.root = root;
+  cur.edges = edges0;
+  // Work on indices: edge identity at level L is its position in levels[L].edges.
+  std::vector<std::vector<int>> origin;  // origin[L][j] = index of edge j of level L+1 in level L
+  while (true) {
+    const int N = cur.n;
+    cur.best.assign(N, -1);
+    for (int j = 0; j < int(cur.edges.size()); ++j) {
+      const WEdge& e = cur.edges[j];
+      if (e.v == cur.root || e.u == e.v) continue;
+      int b = cur.best[e.v];
+      if (b < 0 || e.w < cur.edges[b].w || (e.w == cur.edges[b].w && e.key < cur.edges[b].key))
+        cur.best[e.v] = j;
+    }
+    for (int v = 0; v < N; ++v)
+      if (v != cur.root && cur.best[v] < 0) return {};  // unreachable
+    // cycle search
+    cur.comp.assign(N, -1);
+    std::vector<int> mark(N, -1);
+    int nc = 0;
+    bool cyc = false;
+    for (int v = 0; v < N; ++v) {
+      int x = v;
+      while (x != cur.root && mark[x] < 0 && cur.comp[x] < 0) {
+        mark[x] = v;
+        x = cur.edges[cur.best[x]].u;
+      }
+      if (x != cur.root && mark[x] == v && cur.comp[x] < 0) {
+        cyc = true;
+        int y = x;
+        do {
+          cur.comp[y] = nc;
+          y = cur.edges[cur.best[y]].u;
+        } while (y != x);
+        ++nc;
+      }
+    }
+    if (!cyc) break;
+    for (int v = 0; v < N; ++v)
+      if (cur.comp[v] < 0) cur.comp[v] = nc++;
+    Level nxt;
+    nxt.n = nc;
+    nxt.root = cur.comp[cur.root];
+    std::vector<int> org;
+    for (int j = 0; j < int(cur.edges.size()); ++j) {
+      const WEdge& e = cur.edges[j];
+      int cu = cur.comp[e.u], cv = cur.comp[e.v];
+      if (cu == cv || e.v == cur.root) continue;
+      nxt.edges.push_back({cu, cv, e.w - cur.edges[cur.best[e.v]].w, e.key});
+      org.push_back(j);
+    }
+    levels.push_back(std::move(cur));
+    origin.push_back(std::move(org));
+    cur = std::move(nxt);
+  }
+  // Unwind: chosen edge indices at the deepest level, mapped upwards.
+  std::vector<int> chosen;  // edge indices at the current level
+  for (int v = 0; v < cur.n; ++v)
+    if (v != cur.root) chosen.push_back(cur.best[v]);
+  for (int L = int(levels.size()) - 1; L >= 0; --L) {
+    Level& lv = levels[L];
+    std::vector<int> in_of(lv.n, -1);  // vertex -> chosen in-edge (level L index)
+    for (int j : chosen) {
+      int jj = origin[L][j];
+      in_of[lv.edges[jj].v] = jj;
+    }
+    std::vector<int> up;
+    for (int v = 0; v < lv.n; ++v) {
+      if (v == lv.root) continue;
+      up.push_back(in_of[v] >= 0 ? in_of[v] : lv.best[v]);
+    }
+    chosen.swap(up);
+    cur = std::move(lv);
+  }
+  std::vector<int> parent(n, -1);
+  for (int j : chosen) parent[edges0[j].v] = edges0[j].u;
+  return parent;
+}
+
+// Kruskal over undirected pairs (u < v); ties (w, u, v).  Returns pair indices.
+std::vector<int> min_spanning_tree(int n, const std::vector<std::pair<int, int>>& pairs,
+                                   const std::vector<double>& w) {
+  std::vector<int> idx(pairs.size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) {
+    if (w[a] != w[b]) return w[a] < w[b];
+    return pairs[a] < pairs[b];
+  });
+  std::vector<int> uf(n);
+  std::iota(uf.begin(), uf.end(), 0);
+  std::function<int(int)> find = [&](int x) { return uf[x] == x ? x : uf[x] = find(uf[x]); };
+  std::vector<int> out;
+  for (int j : idx) {
+    int a = find(pairs[j].first), b = find(pairs[j].second);
+    if (a != b) {
+      uf[a] = b;
+      out.push_back(j);
+    }
+  }
+  if (int(out.size()) != n - 1) return {};
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+// Garg-Koenemann MWU (R#4) over `ne` resources with capacities `c`.  The
+// callback returns the resource list of the minimum-length tree under the
+// normalised lengths, or an empty list on failure.
+struct MwuResult {
+  std::map<std::vector<int>, double> x;  // tree (sorted resource list) -> weight
+  double rate = 0;
+  int iters = 0;
+};
+bool run_mwu(const std::vector<double>& c, double eps,
+             const std::function<std::vector<int>(const std::vector<double>&)>& tree_of,
+             MwuResult* out) {
+  const int ne = int(c.size());
+  const double log_delta = std::log1p(eps) - (1.0 / eps) * std::log((1.0 + eps) * ne);
+  std::vector<double> logl(ne);
+  for (int e = 0; e < ne; ++e) logl[e] = log_delta - std::log(c[e]);
+  std::vector<double> len(ne);
+  std::map<std::vector<int>, double> x;
+  int it = 0;
+  for (;; ++it) {
+    if (it > 5000000) return false;
+    double mx = *std::max_element(logl.begin(), logl.end());
+    for (int e = 0; e < ne; ++e) len[e] = std::exp(logl[e] - mx);
+    std::vector<int> T = tree_of(len);
+    if (T.empty()) return false;
+    // sum_{e in T} l_e >= 1 <=> logsumexp(logl[T]) >= 0
+    double m2 = -INFINITY;
+    for (int e : T) m2 = std::max(m2, logl[e]);
+    double s = 0;
+    for (int e : T) s += std::exp(logl[e] - m2);
+    if (m2 + std::log(s) >= 0.0) break;
+    double cmin = INFINITY;
+    for (int e : T) cmin = std::min(cmin, c[e]);
+    x[T] += cmin;
+    for (int e : T) logl[e] += std::log1p(eps * cmin / c[e]);
+  }
+  std::vector<double> load(ne, 0.0);
+  for (auto& kv : x)
+    for (int e : kv.first) load[e] += kv.second;
+  double lam = 0;
+  for (int e = 0; e < ne; ++e) lam = std::max(lam, load[e] / c[e]);
+  out->x.clear();
+  out->rate = 0;
+  for (auto& kv : x) {
+    out->x[kv.first] = kv.second / lam;
+    out->rate += kv.second / lam;
+  }
+  out->iters = it;
+  return true;
+}
+
+// ============================================================== ILP (Eqs. 4-7)
+// Branch and bound over candidate trees: maximise sum z, then fewest trees,
+// then least total depth; z_T in {0..g}; sum_{T contains e} z_T <= g c_e.
+struct IlpCand {
+  std::vector<int> res;  // resources used (each once)
+  int depth;
+  double x;              // MWU weight (search order / rounding seed)
+  int prio = 0;          // 1: exact/peeled integral candidate, tried first
+  int lovasz = 0;        // from the exact integral arborescence packing
+  int mult[5] = {0, 0, 0, 0, 0};  // peel multiplicity at grid 1, 2, 4, 8, 16
+};
+struct IlpSol {
+  std::vector<int> z;
+  int64_t sumz = -1;
+  int ntrees = 0;
+  int64_t sumdepth = 0;
+};
+
+// Branch and bound for Eqs. 4-7 on the relaxation grid g: maximise sum z,
+// then fewest trees, then least total depth; z_T in {0..g};
+// sum_{T contains e} z_T <= g c_e.  The incumbent is seeded with the rounded
+// MWU solution floor(g x_T) plus a greedy fill (always feasible); candidates
+// are searched heaviest-MWU-weight first; a node budget keeps it bounded and
+// deterministic.
+class Ilp {
+ public:
+  Ilp(const std::vector<IlpCand>& cand, const std::vector<double>& c, int g,
+      const std::function<int64_t(const std::vector<int64_t>&)>& cut_bound, int64_t node_limit)
+      : cand_(cand), g_(g), cut_bound_(cut_bound), node_limit_(node_limit) {
+    res_.resize(c.size());
+    for (size_t e = 0; e < c.size(); ++e) res_[e] = int64_t(std::floor(g * c[e] + 1e-9));
+    order_.resize(cand.size());
+    std::iota(order_.begin(), order_.end(), 0);
+    std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) {
+      if (cand[a].prio != cand[b].prio) return cand[a].prio > cand[b].prio;
+      if (cand[a].x != cand[b].x) return cand[a].x > cand[b].x;
+      return cand[a].depth < cand[b].depth;
+    });
+    z_.assign(cand.size(), 0);
+  }
+  IlpSol solve() {
+    seed();
+    dfs(0, 0, 0, 0);
+    return best_;
+  }
+
+ private:
+  void seed() {
+    std::vector<int64_t> res = res_;
+    std::vector<int> z(cand_.size(), 0);
+    for (int pass = 0; pass < 2; ++pass)
+      for (int j : order_) {
+        int64_t want = pass == 0 ? int64_t(std::floor(g_ * cand_[j].x + 1e-9)) : g_;
+        int64_t m = std::min<int64_t>(want, g_) - z[j];
+        for (int e : cand_[j].res) m = std::min(m, res[e]);
+        if (m <= 0) continue;
+        z[j] += int(m);
+        for (int e : cand_[j].res) res[e] -= m;
+      }
+    consider(z);
+  }
+  void consider(const std::vector<int>& z) {
+    int64_t sz = 0, sd = 0;
+    int nt = 0;
+    for (size_t j = 0; j < z.size(); ++j)
+      if (z[j] > 0) {
+        sz += z[j];
+        ++nt;
+        sd += cand_[j].depth;
+      }
+    if (better(sz, nt, sd)) {
+      best_.z = z;
+      best_.sumz = sz;
+      best_.ntrees = nt;
+      best_.sumdepth = sd;
+    }
+  }
+  int64_t cap_of(int j) const {
+    int64_t m = g_;
+    for (int e : cand_[j].res) m = std::min(m, res_[e]);
+    return std::max<int64_t>(m, 0);
+  }
+  int64_t upper(size_t k) const {
+    int64_t s = 0;
+    for (size_t t = k; t < order_.size(); ++t) s += cap_of(order_[t]);
+    return std::min(s, cut_bound_(res_));
+  }
+  bool better(int64_t sz, int nt, int64_t sd) const {
+    if (sz != best_.sumz) return sz > best_.sumz;
+    if (nt != best_.ntrees) return nt < best_.ntrees;
+    return sd < best_.sumdepth;
+  }
+  void dfs(size_t k, int64_t sz, int nt, int64_t sd) {
+    if (++nodes_ > node_limit_) return;
+    if (better(sz, nt, sd)) {
+      best_.z = z_;
+      best_.sumz = sz;
+      best_.ntrees = nt;
+      best_.sumdepth = sd;
+    }
+    if (k == order_.size()) return;
+    int64_t ub = upper(k);
+    if (sz + ub < best_.sumz) return;
+    if (sz + ub == best_.sumz || sz >= best_.sumz) {
+      // only a tie on sum z is reachable: it must use fewer trees or less depth
+      int64_t need = best_.sumz - sz;
+      int64_t more = need > 0 ? (need + g_ - 1) / g_ : 0;
+      if (sz + ub == best_.sumz && nt + more > best_.ntrees) return;
+      if (sz >= best_.sumz) return;  // adding trees can only worsen the tie-breaks
+    }
+    int j = order_[k];
+    int64_t cmax = cap_of(j);
+    for (int64_t zz = cmax; zz >= 0; --zz) {
+      if (zz > 0) {
+        for (int e : cand_[j].res) res_[e] -= zz;
+        z_[j] = int(zz);
+        dfs(k + 1, sz + zz, nt + 1, sd + cand_[j].depth);
+        z_[j] = 0;
+        for (int e : cand_[j].res) res_[e] += zz;
+      } else {
+        dfs(k + 1, sz, nt, sd);
+      }
+      if (nodes_ > node_limit_) return;
+    }
+  }
+  const std::vector<IlpCand>& cand_;
+  int g_;
+  std::function<int64_t(const std::vector<int64_t>&)> cut_bound_;
+  int64_t node_limit_;
+  int64_t nodes_ = 0;
+  std::vector<int64_t> res_;
+  std::vector<int> order_;
+  std::vector<int> z_;
+  IlpSol best_;
+};
+
+// Max flow (Edmonds-Karp) on a small dense integer capacity matrix.
+int64_t maxflow(std::vector<std::vector<int64_t>> c, int s, int t) {
+  const int n = int(c.size());
+  int64_t flow = 0;
+  while (true) {
+    std::vector<int> prev(n, -1);
+    prev[s] = s;
+    std::vector<int> q{s};
+    for (size_t h = 0; h < q.size() && prev[t] < 0; ++h)
+      for (int v = 0; v < n; ++v)
+        if (prev[v] < 0 && c[q[h]][v] > 0) {
+          prev[v] = q[h];
+          q.push_back(v);
+        }
+    if (prev[t] < 0) return flow;
+    int64_t b = INT64_MAX;
+    for (int v = t; v != s; v = prev[v]) b = std::min(b, c[prev[v]][v]);
+    for (int v = t; v != s; v = prev[v]) {
+      c[prev[v]][v] -= b;
+      c[v][prev[v]] += b;
+    }
+    flow += b;
+  }
+}
+
+// Integral arborescence packing by Lovasz's constructive proof of Edmonds'
+// theorem: with k = min_v lambda(r, v), grow each arborescence one
+// edge (u in S, v not in S) at a time, taking an edge only if the remaining
+// graph keeps lambda(r, v) >= k - t.  Edges are tried in BFS order (shallow
+// trees).  Used to enrich the ILP's candidate set (SURVEY 7 "hard parts" 8).
+std::vector<std::vector<int>> lovasz_packing(std::vector<std::vector<int64_t>> cap, int root) {
+  const int n = int(cap.size());
+  int64_t k = INT64_MAX;
+  for (int v = 0; v < n; ++v)
+    if (v != root) k = std::min(k, maxflow(cap, root, v));
+  std::vector<std::vector<int>> out;
+  for (int64_t t = 1; t <= k; ++t) {
+    std::vector<int> parent(n, -2), depth(n, 0);
+    parent[root] = -1;
+    int in_s = 1;
+    while (in_s < n) {
+      bool grown = false;
+      // candidate edges ordered by (depth of u, u, v)
+      std::vector<std::pair<int, std::pair<int, int>>> cand;
+      for (int u = 0; u < n; ++u)
+        if (parent[u] != -2)
+          for (int v = 0; v < n; ++v)
+            if (parent[v] == -2 && cap[u][v] > 0) cand.push_back({depth[u], {u, v}});
+      std::sort(cand.begin(), cand.end());
+      for (auto& ce : cand) {
+        int u = ce.second.first, v = ce.second.second;
+        cap[u][v] -= 1;
+        if (maxflow(cap, root, v) >= k - t) {
+          parent[v] = u;
+          depth[v] = depth[u] + 1;
+          ++in_s;
+          grown = true;
+          break;
+        }
+        cap[u][v] += 1;
+      }
+      if (!grown) return out;  // cannot happen for integral capacities (lemma)
+    }
+    out.push_back(parent);
+  }
+  return out;
+}
+
+// Greedy integral peeling of undirected spanning trees: Kruskal preferring
+// links with the largest RELATIVE residual capacity (balances single and
+// parallel links); candidates for the AllReduce ILP.
+std::vector<std::vector<int>> peel_spanning(int n, const std::vector<std::pair<int, int>>& pairs,
+                                            std::vector<int64_t> res) {
+  std::vector<std::vector<int>> out;
+  const std::vector<int64_t> cap0 = res;
+  while (true) {
+    std::vector<double> len(pairs.size());
+    for (size_t j = 0; j < pairs.size(); ++j)
+      len[j] = res[j] > 0 ? double(cap0[j]) / double(res[j]) : 1e30;
+    std::vector<int> t = min_spanning_tree(n, pairs, len);
+    if (t.empty()) break;
+    bool ok = true;
+    for (int j : t) ok = ok && res[j] > 0;
+    if (!ok) break;
+    for (int j : t) res[j] -= 1;
+    out.push_back(t);
+  }
+  return out;
+}
+
+int tree_depth(const std::vector<int>& parent) {
+  int best = 0;
+  for (size_t v = 0; v < parent.size(); ++v) {
+    int d = 0, x = int(v);
+    while (parent[x] >= 0 && d <= int(parent.size())) {
+      x = parent[x];
+      ++d;
+    }
+    best = std::max(best, d);
+  }
+  return best;
+}
+
+// Orient an undirected tree (edge list) away from `root`.
+std::vector<int> orient(int n, const std::vector<std::pair<int, int>>& edges, int root) {
+  std::vector<std::vector<int>> adj(n);
+  for (auto& e : edges) {
+    adj[e.first].push_back(e.second);
+    adj[e.second].push_back(e.first);
+  }
+  std::vector<int> parent(n, -2);
+  parent[root] = -1;
+  std::vector<int> st{root};
+  while (!st.empty()) {
+    int u = st.back();
+    st.pop_back();
+    for (int w : adj[u])
+      if (parent[w] == -2) {
+        parent[w] = u;
+        st.push_back(w);
+      }
+  }
+  return parent;
+}
+
+// Tree centre: minimum eccentricity, ties -> lowest rank (R#9).
+int centre(int n, const std::vector<std::pair<int, int>>& edges) {
+  int best = 0, bestecc = 1 << 30;
+  for (int s = 0; s < n; ++s) {
+    int e = tree_depth(orient(n, edges, s));
+    if (e < bestecc) {
+      bestecc = e;
+      best = s;
+    }
+  }
+  return best;
+}
+
+void sort_trees(std::vector<Tree>* trees, const std::vector<std::vector<std::pair<int, int>>>& keys) {
+  std::vector<int> idx(trees->size());
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+    const Tree &A = (*trees)[a], &B = (*trees)[b];
+    // weight descending: A.wnum/A.wden > B.wnum/B.wden
+    __int128 l = (__int128)A.wnum * B.wden, r = (__int128)B.wnum * A.wden;
+    if (l != r) return l > r;
+    return keys[a] < keys[b];
+  });
+  std::vector<Tree> out;
+  for (int i : idx) out.push_back((*trees)[i]);
+  trees->swap(out);
+}
+
+int64_t gcd64(int64_t a, int64_t b) { return b == 0 ? a : gcd64(b, a % b); }
+
+}  // namespace
+
+// ============================================================== plans
+blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_t& cfg, Plan* out,
+                         std::string* err) {
+  const int n = g.n;
+  *out = Plan();
+  out->coll = coll;
+  out->root = coll == kBroadcast ? root : -1;
+  out->nranks = n;
+  out->switch_model = g.switch_model;
+  if (n <= 0 || n > kMaxRanks) {
+    *err = "nranks must be in [1, " + std::to_string(kMaxRanks) + "]";
+    return BLINK_ERR_UNSUPPORTED;
+  }
+  if (coll == kBroadcast && (root < 0 || root >= n)) {
+    *err = "root " + std::to_string(root) + " out of range [0," + std::to_string(n) + ")";
+    return BLINK_ERR_INVALID_ARGUMENT;
+  }
+  if (n == 1) {
+    Tree t;
+    t.root = 0;
+    t.parent = {-1};
+    out->trees.push_back(t);
+    out->rate_num = 1;
+    return BLINK_SUCCESS;
+  }
+  if (g.switch_model) {
+    if (coll == kAllReduce) {
+      // m one-hop stars, star j rooted at j, weight 1/2 in K_m link units
+      for (int j = 0; j < n; ++j) {
+        Tree t;
+        t.root = j;
+        t.parent.assign(n, j);
+        t.parent[j] = -1;
+        t.wnum = 1;
+        t.wden = 2;
+        t.depth = 1;
+        out->trees.push_back(t);
+      }
+      out->rate_num = n % 2 == 0 ? n / 2 : n;
+      out->rate_den = n % 2 == 0 ? 1 : 2;
+      out->grid = 2;
+    } else {
+      // R#10: m-1 two-level trees r -> k -> others (Edmonds optimum m-1); the
+      // one-hop variant is selected per call size in size_plan.
+      for (int k = 0; k < n; ++k) {
+        if (k == root) continue;
+        Tree t;
+        t.root = root;
+        t.parent.assign(n, k);
+        t.parent[root] = -1;
+        t.parent[k] = root;
+        t.depth = n > 2 ? 2 : 1;
+        out->trees.push_back(t);
+      }
+      out->rate_num = n - 1;
+    }
+    return BLINK_SUCCESS;
+  }
+
+  // ---------------- explicit link graph: MWU then ILP
+  double cmin = INFINITY;
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      if (g.cap[u][v] > 0) cmin = std::min(cmin, g.cap[u][v]);
+  const double eps = cfg.mwu_eps > 0 ? cfg.mwu_eps : 0.1;
+  const double gap = cfg.ilp_gap > 0 ? cfg.ilp_gap : 0.05;
+
+  std::vector<IlpCand> cands;
+  std::vector<std::vector<int>> cand_parent;
+  std::vector<double> caps;
+  std::function<int64_t(const std::vector<int64_t>&)> cut;
+  double c_star = 0;
+  if (coll == kBroadcast) {
+    // resources = directed edges, capacities in units of the smallest link
+    std::vector<WEdge> edges;
+    for (int u = 0; u < n; ++u)
+      for (int v = 0; v < n; ++v)
+        if (g.cap[u][v] > 0) {
+          edges.push_back({u, v, 0.0, u * n + v});
+          caps.push_back(g.cap[u][v] / cmin);
+        }
+    // reachability from the root
+    std::vector<int> seen(n, 0);
+    std::vector<int> st{root};
+    seen[root] = 1;
+    while (!st.empty()) {
+      int u = st.back();
+      st.pop_back();
+      for (auto& e : edges)
+        if (e.u == u && !seen[e.v]) {
+          seen[e.v] = 1;
+          st.push_back(e.v);
+        }
+    }
+    for (int v = 0; v < n; ++v)
+      if (!seen[v]) {
+        *err = "GPU " + std::to_string(v) + " is unreachable from root " + std::to_string(root);
+        return BLINK_ERR_TOPOLOGY;
+      }
+    std::map<int, int> key_to_res;
+    for (size_t j = 0; j < edges.size(); ++j) key_to_res[edges[j].key] = int(j);
+    MwuResult mr;
+    auto tree_of = [&](const std::vector<double>& len) {
+      for (size_t j = 0; j < edges.size(); ++j) edges[j].w = len[j];
+      std::vector<int> par = min_arborescence(n, root, edges);
+      std::vector<int> res;
+      if (par.empty()) return res;
+      for (int v = 0; v < n; ++v)
+        if (par[v] >= 0) res.push_back(key_to_res[par[v] * n + v]);
+      std::sort(res.begin(), res.end());
+      return res;
+    };
+    if (!run_mwu(caps, eps, tree_of, &mr)) {
+      *err = "MWU failed to converge";
+      return BLINK_ERR_INTERNAL;
+    }
+    c_star = mr.rate;
+    for (auto& kv : mr.x) {
+      std::vector<int> par(n, -1);
+      for (int e : kv.first) par[edges[e].v] = edges[e].u;
+      cands.push_back({kv.first, tree_depth(par), kv.second});
+      cand_parent.push_back(par);
+    }
+    // exact integral candidates (Lovasz), weight 1 each
+    {
+      std::vector<std::vector<int64_t>> ic(n, std::vector<int64_t>(n, 0));
+      for (size_t j = 0; j < edges.size(); ++j)
+        ic[edges[j].u][edges[j].v] = int64_t(std::floor(caps[j] + 1e-9));
+      for (auto& par : lovasz_packing(ic, root)) {
+        std::vector<int> res;
+        for (int v = 0; v < n; ++v)
+          if (par[v] >= 0) res.push_back(key_to_res[par[v] * n + v]);
+        std::sort(res.begin(), res.end());
+        IlpCand c{res, tree_depth(par), 0.0};
+        c.lovasz = 1;
+        cands.push_back(c);
+        cand_parent.push_back(par);
+      }
+    }
+    // every arborescence enters each non-root vertex once: sum z <= min_v in-capacity
+    cut = [n, root, edges](const std::vector<int64_t>& res) {
+      int64_t b = INT64_MAX;
+      for (int v = 0; v < n; ++v) {
+        if (v == root) continue;
+        int64_t s = 0;
+        for (size_t j = 0; j < edges.size(); ++j)
+          if (edges[j].v == v) s += std::max<int64_t>(res[j], 0);
+        b = std::min(b, s);
+      }
+      return b;
+    };
+  } else {
+    // undirected pairs; every link needs its reverse
+    std::vector<std::pair<int, int>> pairs;
+    for (int u = 0; u < n; ++u)
+      for (int v = u + 1; v < n; ++v) {
+        bool f = g.cap[u][v] > 0, b = g.cap[v][u] > 0;
+        if (f != b) {
+          *err = "link " + std::to_string(f ? u : v) + "->" + std::to_string(f ? v : u) +
+                 " has no reverse edge (AllReduce needs bidirectional links, P:397)";
+          return BLINK_ERR_TOPOLOGY;
+        }
+        if (f) {
+          pairs.push_back({u, v});
+          caps.push_back(std::min(g.cap[u][v], g.cap[v][u]) / cmin);
+        }
+      }
+    MwuResult mr;
+    auto tree_of = [&](const std::vector<double>& len) { return min_spanning_tree(n, pairs, len); };
+    if (!run_mwu(caps, eps, tree_of, &mr)) {
+      *err = "MWU failed (graph disconnected?)";
+      return BLINK_ERR_TOPOLOGY;
+    }
+    c_star = mr.rate;
+    for (auto& kv : mr.x) {
+      std::vector<std::pair<int, int>> te;
+      for (int e : kv.first) te.push_back(pairs[e]);
+      int r = centre(n, te);
+      std::vector<int> par = orient(n, te, r);
+      cands.push_back({kv.first, tree_depth(par), kv.second});
+      cand_parent.push_back(par);
+    }
+    // greedy integral peelings at the grid scales (multiplicity / g each)
+    for (int gi = 0; gi < 4; ++gi) {
+      const int gg = 1 << gi;
+      std::vector<int64_t> res(caps.size());
+      for (size_t j = 0; j < caps.size(); ++j) res[j] = int64_t(std::floor(gg * caps[j] + 1e-9));
+      std::map<std::vector<int>, int> mult;
+      for (auto& t : peel_spanning(n, pairs, res)) mult[t]++;
+      for (auto& kv : mult) {
+        std::vector<std::pair<int, int>> te;
+        for (int e : kv.first) te.push_back(pairs[e]);
+        int r = centre(n, te);
+        std::vector<int> par = orient(n, te, r);
+        IlpCand c{kv.first, tree_depth(par), 0.0};
+        c.mult[gi] = kv.second;
+        cands.push_back(c);
+        cand_parent.push_back(par);
+      }
+    }
+    // every spanning tree uses n-1 links: sum z <= sum res / (n-1)
+    cut = [n](const std::vector<int64_t>& res) {
+      int64_t s = 0;
+      for (int64_t r : res) s += std::max<int64_t>(r, 0);
+      return s / (n - 1);
+    };
+  }
+  out->c_star = c_star;
+  {
+    std::map<std::vector<int>, int> seen;
+    std::vector<IlpCand> c2;
+    std::vector<std::vector<int>> p2;
+    for (size_t j = 0; j < cands.size(); ++j) {
+      auto it = seen.find(cands[j].res);
+      if (it != seen.end()) {
+        IlpCand& d = c2[it->second];
+        d.x = std::max(d.x, cands[j].x);
+        d.lovasz |= cands[j].lovasz;
+        for (int q = 0; q < 5; ++q) d.mult[q] += cands[j].mult[q];
+        continue;
+      }
+      seen[cands[j].res] = int(c2.size());
+      c2.push_back(cands[j]);
+      p2.push_back(cand_parent[j]);
+    }
+    cands.swap(c2);
+    cand_parent.swap(p2);
+  }
+
+  // ILP with the relaxation grid g = 1, 2, 4, 8, 16 (R#5)
+  IlpSol best;
+  int bestg = 1;
+  for (int gi = 0; gi < 5; ++gi) {
+    const int gg = 1 << gi;
+    // integral candidates first: the exact packing (Broadcast) or the peeling
+    // at this grid scale, seeded with their multiplicity
+    std::vector<IlpCand> cg = cands;
+    for (auto& c : cg) {
+      c.prio = (c.lovasz || c.mult[gi] > 0) ? 1 : 0;
+      if (c.lovasz) c.x = 1.0;
+      if (c.mult[gi] > 0) c.x = double(c.mult[gi]) / gg;
+    }
+    Ilp ilp(cg, caps, gg, cut, 200000);
+    IlpSol s = ilp.solve();
+    if (best.sumz < 0 || double(s.sumz) / gg > double(best.sumz) / bestg + 1e-12) {
+      best = s;
+      bestg = gg;
+    }
+    if (double(s.sumz) / gg >= (1.0 - gap) * c_star - 1e-12) {
+      best = s;
+      bestg = gg;
+      break;
+    }
+  }
+  std::vector<std::vector<std::pair<int, int>>> keys;
+  for (size_t j = 0; j < cands.size(); ++j) {
+    if (best.z.empty() || best.z[j] == 0) continue;
+    Tree t;
+    t.parent = cand_parent[j];
+    for (int v = 0; v < n; ++v)
+      if (t.parent[v] < 0) t.root = v;
+    int64_t gd = gcd64(best.z[j], bestg);
+    t.wnum = best.z[j] / gd;
+    t.wden = bestg / gd;
+    t.depth = cands[j].depth;
+    out->trees.push_back(t);
+    std::vector<std::pair<int, int>> k;
+    for (int v = 0; v < n; ++v)
+      if (t.parent[v] >= 0) {
+        if (coll == kBroadcast)
+          k.push_back({t.parent[v], v});
+        else
+          k.push_back({std::min(t.parent[v], v), std::max(t.parent[v], v)});
+      }
+    std::sort(k.begin(), k.end());
+    keys.push_back(k);
+  }
+  if (out->trees.empty()) {
+    *err = "ILP found no tree";
+    return BLINK_ERR_INTERNAL;
+  }
+  if (int(out->trees.size()) > kMaxTrees) {
+    *err = "plan needs " + std::to_string(out->trees.size()) + " trees (max " +
+           std::to_string(kMaxTrees) + ")";
+    return BLINK_ERR_UNSUPPORTED;
+  }
+  sort_trees(&out->trees, keys);
+  out->grid = bestg;
+  out->rate_num = best.sumz;
+  out->rate_den = bestg;
+  int64_t gd = gcd64(out->rate_num, out->rate_den);
+  out->rate_num /= gd;
+  out->rate_den /= gd;
+  return BLINK_SUCCESS;
+}
+
+// ============================================================== split + chunks
+blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
+                         int ctas_hint, std::vector<TreeRange>* out, std::string* err) {
+  out->clear();
+  const size_t S = count * size_t(esize);
+  const int k = int(p.trees.size());
+  // R#11: b_i = floor(G * sum_{j<i} w_j / W) with exact rationals
+  int64_t L = 1;
+  for (const Tree& t : p.trees) L = L / gcd64(L, t.wden) * t.wden;
+  std::vector<int64_t> wi(k);
+  int64_t W = 0;
+  for (int i = 0; i < k; ++i) {
+    wi[i] = p.trees[i].wnum * (L / p.trees[i].wden);
+    W += wi[i];
+  }
+  const int64_t G = int64_t(S / kGrain);
+  int64_t acc = 0;
+  std::vector<int64_t> b(k + 1);
+  for (int i = 0; i < k; ++i) {
+    b[i] = int64_t((__int128)G * acc / W);
+    acc += wi[i];
+  }
+  b[k] = G;
+  for (int i = 0; i < k; ++i) {
+    TreeRange r;
+    int64_t lo = b[i] * kGrain, hi = (i == k - 1) ? int64_t(S) : b[i + 1] * kGrain;
+    r.lo = lo / esize;
+    r.hi = hi / esize;
+    int64_t bytes = hi - lo;
+    // a8: static chunk table.  Aim for >= `per_cta` chunks per CTA of the
+    // channel (deeper trees pipeline better with more chunks: (c+h-1)/c,
+    // P:511-513), chunks >= 64 KiB unless the range is smaller, <= 4 MiB.
+    int64_t cb;
+    if (cfg.chunk_bytes > 0) {
+      cb = int64_t(cfg.chunk_bytes);
+    } else {
+      int per_cta = p.trees[i].depth >= 2 ? 4 : 1;
+      int64_t want = int64_t(std::max(1, ctas_hint)) * per_cta;
+      cb = (bytes + want - 1) / want;
+      cb = std::max<int64_t>(cb, 64 << 10);
+      cb = std::min<int64_t>(cb, 4 << 20);
+    }
+    cb = (cb + kGrain - 1) / kGrain * kGrain;
+    if (cb <= 0) cb = kGrain;
+    int64_t nch = bytes > 0 ? (bytes + cb - 1) / cb : 0;
+    if (nch > kMaxChunks) {
+      cb = ((bytes + kMaxChunks - 1) / kMaxChunks + kGrain - 1) / kGrain * kGrain;
+      nch = (bytes + cb - 1) / cb;
+    }
+    if (nch > kMaxChunks) {
+      *err = "too many chunks";
+      return BLINK_ERR_INTERNAL;
+    }
+    r.chunk = cb / esize;
+    r.nchunks = int(nch);
+    out->push_back(r);
+  }
+  return BLINK_SUCCESS;
+}
+
+std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vector<TreeRange>& r,
+                         int ctas) {
+  std::ostringstream o;
+  o << "{\"coll\":\"" << (p.coll == kAllReduce ? "allreduce" : "broadcast") << "\",\"root\":"
+    << p.root << ",\"nranks\":" << p.nranks << ",\"count\":" << count << ",\"esize\":" << esize
+    << ",\"switch\":" << (p.switch_model ? "true" : "false") << ",\"rate\":[" << p.rate_num << ","
+    << p.rate_den << "],\"c_star\":" << p.c_star << ",\"grid\":" << p.grid << ",\"ctas\":" << ctas
+    << ",\"trees\":[";
+  for (size_t i = 0; i < p.trees.size(); ++i) {
+    const Tree& t = p.trees[i];
+    o << (i ? "," : "") << "{\"root\":" << t.root << ",\"parent\":[";
+    for (size_t v = 0; v < t.parent.size(); ++v) o << (v ? "," : "") << t.parent[v];
+    o << "],\"weight\":[" << t.wnum << "," << t.wden << "],\"depth\":" << t.depth;
+    if (i < r.size())
+      o << ",\"lo\":" << r[i].lo << ",\"hi\":" << r[i].hi << ",\"chunk\":" << r[i].chunk
+        << ",\"nchunks\":" << r[i].nchunks;
+    o << "}";
+  }
+  o << "]}";
+  return o.str();
+}
+
+}  // namespace blink

@@ -1,0 +1,1091 @@
+// Host runtime + C ABI: communicators, flag memory, CUDA-IPC peer mappings,
+// symmetric registration, staging, CTA/channel assignment and launches.
+//
+// Two process models share one device executor (exec.cu):
+//   single-process (blink_init_all): all ranks' buffers are visible to one
+//     host thread.  Calls are batched until every rank of the comm set has
+//     called (implicit NCCL-style group); then one cooperative launch per
+//     device runs the channels of all ranks on that device.  Ranks may share
+//     a device ("virtual ranks": their HBM stands in for the peers' HBM).
+//   multi-process (blink_init + export/connect): one rank per process; peers'
+//     flags, staging and registered buffers are CUDA-IPC mappings over
+//     NVLink/NVSwitch; each call launches this rank's channels only, with an
+//     entry handshake and an exit wait.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unistd.h>
+#include <vector>
+
+#include "blink_internal.h"
+
+using namespace blink;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct SizedKey {
+  int coll, root, dtype;
+  size_t count;
+  uint64_t launch_mask;
+  bool operator<(const SizedKey& o) const {
+    if (coll != o.coll) return coll < o.coll;
+    if (root != o.root) return root < o.root;
+    if (dtype != o.dtype) return dtype < o.dtype;
+    if (count != o.count) return count < o.count;
+    return launch_mask < o.launch_mask;
+  }
+};
+
+struct Sized {
+  const Plan* plan = nullptr;
+  std::vector<TreeRange> ranges;
+  std::vector<DevTask> tasks;
+  DevTask* d_tasks = nullptr;
+  DevTree* d_trees = nullptr;
+  int ctas = 0;
+  int chunks = 0;
+};
+
+struct Reg {
+  char* buf = nullptr;
+  size_t bytes = 0;
+  char* peer[kMaxRanks] = {};
+};
+
+struct Clique;
+
+struct Pending {
+  bool posted = false;
+  const void* send = nullptr;
+  void* recv = nullptr;
+  cudaStream_t stream = nullptr;
+};
+
+}  // namespace
+
+struct blink_comm {
+  int nranks = 0, rank = 0, device = 0;
+  blink_config_t cfg{};
+  Graph graph;
+  bool multiprocess = false;
+  bool connected = false;
+  Clique* clique = nullptr;
+  uint64_t epoch = 0;  // multi-process
+  uint64_t* flags = nullptr;
+  uint64_t* peer_flags[kMaxRanks] = {};
+  int* err_host = nullptr;  // multi-process error word
+  int* err_dev = nullptr;
+  int sms = 148;
+  std::map<std::pair<int, int>, std::unique_ptr<Plan>> plans;  // (coll, root|variant)
+  std::map<SizedKey, Sized> sized;                             // multi-process launches
+  std::vector<Reg> regs;
+  std::map<std::string, char*> opened;  // peer IPC handle bytes -> mapped base
+  struct PendingReg {
+    void* buf;
+    size_t bytes;
+    size_t offset;
+  };
+  std::vector<PendingReg> pending_regs;
+  char* staging = nullptr;
+  size_t staging_bytes = 0;
+  char* peer_staging[kMaxRanks] = {};
+  std::string last_error;
+  blink_stats_t stats{};
+};
+
+namespace {
+
+struct Clique {
+  std::mutex mu;
+  int nranks = 0;
+  std::vector<blink_comm*> comms;
+  std::vector<int> devices;  // distinct devices
+  int alive = 0;
+  uint64_t epoch = 0;
+  // the batch being assembled
+  int nposted = 0;
+  int coll = -1, root = -1, dtype = -1, op = -1;
+  size_t count = 0;
+  std::vector<Pending> pending;
+  // per device state
+  std::map<int, int*> err_host, err_dev;
+  std::map<SizedKey, Sized> sized;
+  int64_t launches = 0;
+  bool sticky_error = false;
+};
+
+blink_result_t fail(blink_comm_t comm, blink_result_t r, const std::string& msg) {
+  g_last_error = msg;
+  if (comm) comm->last_error = msg;
+  if (getenv("BLINK_DEBUG")) fprintf(stderr, "[blink] error %d: %s\n", int(r), msg.c_str());
+  return r;
+}
+
+#define CUDA_TRY(comm, call)                                                          \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(comm, BLINK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+blink_config_t resolve_cfg(const blink_config_t* c) {
+  blink_config_t d;
+  blink_config_default(&d);
+  if (!c) return d;
+  blink_config_t r = *c;
+  if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
+  if (!(r.ilp_gap > 0 && r.ilp_gap < 1)) r.ilp_gap = d.ilp_gap;
+  if (r.threads <= 0) r.threads = d.threads;
+  if (r.threads > 512) r.threads = 512;
+  r.threads = (r.threads + 31) / 32 * 32;
+  if (!(r.timeout_s > 0)) r.timeout_s = d.timeout_s;
+  if (r.staging_bytes == 0) r.staging_bytes = d.staging_bytes;
+  r.staging_bytes = (r.staging_bytes + 4095) / 4096 * 4096;
+  return r;
+}
+
+// Plan cache: key (coll, root) with root = -1 for AllReduce, and root + 1000
+// for the one-hop Broadcast star variant on switches.
+blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, const Plan** out) {
+  int key_root = coll == kAllReduce ? -1 : root;
+  bool star = coll == kBroadcast && comm->graph.switch_model && comm->nranks > 2 &&
+              bytes <= comm->cfg.onehop_bcast_max_bytes;
+  if (star) key_root += 1000;
+  auto k = std::make_pair(coll, key_root);
+  auto it = comm->plans.find(k);
+  if (it != comm->plans.end()) {
+    *out = it->second.get();
+    return BLINK_SUCCESS;
+  }
+  auto p = std::make_unique<Plan>();
+  std::string err;
+  blink_result_t r;
+  if (star) {
+    p->coll = kBroadcast;
+    p->root = root;
+    p->nranks = comm->nranks;
+    p->switch_model = true;
+    Tree t;
+    t.root = root;
+    t.parent.assign(comm->nranks, root);
+    t.parent[root] = -1;
+    t.depth = 1;
+    p->trees.push_back(t);
+    p->rate_num = 1;
+    r = BLINK_SUCCESS;
+  } else {
+    r = make_plan(comm->graph, coll, root, comm->cfg, p.get(), &err);
+  }
+  if (r != BLINK_SUCCESS) return fail(comm, r, err);
+  if (getenv("BLINK_DEBUG")) {
+    std::vector<TreeRange> none;
+    fprintf(stderr, "[blink] plan %s\n", plan_to_json(*p, 0, 4, none, 0).c_str());
+  }
+  *out = p.get();
+  comm->plans[k] = std::move(p);
+  return BLINK_SUCCESS;
+}
+
+struct Channel {
+  int rank, tree, role, parent;
+  uint32_t children, leafmask;
+  double work;
+  int ctas = 1;
+};
+
+// CTA / channel assignment for the ranks in `launch_mask` (a6) and the device
+// tables of one launch.
+blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, int esize,
+                           uint64_t launch_mask, int budget, Sized* s) {
+  const int n = plan.nranks;
+  const int k = int(plan.trees.size());
+  std::vector<std::vector<uint32_t>> ch(k, std::vector<uint32_t>(n, 0));
+  for (int i = 0; i < k; ++i)
+    for (int v = 0; v < n; ++v)
+      if (plan.trees[i].parent[v] >= 0) ch[i][plan.trees[i].parent[v]] |= 1u << v;
+  // provisional byte shares (equal CTAs hint) to weigh channels
+  std::vector<TreeRange> r0;
+  std::string err;
+  blink_result_t rr = size_plan(plan, count, esize, comm->cfg, 1, &r0, &err);
+  if (rr != BLINK_SUCCESS) return fail(comm, rr, err);
+  std::vector<Channel> chans;
+  std::vector<int> rank_has(n, 0);
+  for (int v = 0; v < n; ++v) {
+    if (!((launch_mask >> v) & 1)) continue;
+    for (int i = 0; i < k; ++i) {
+      uint32_t c = ch[i][v];
+      if (!c) continue;
+      int nc = __builtin_popcount(c);
+      uint32_t leaf = 0;
+      for (int u = 0; u < n; ++u)
+        if (((c >> u) & 1u) && ch[i][u] == 0) leaf |= 1u << u;
+      double bytes = double(r0[i].hi - r0[i].lo) * esize + 1.0;
+      int par = plan.trees[i].parent[v];
+      if (plan.coll == kAllReduce) {
+        double wr = bytes * ((nc + 1) + (par < 0 ? nc + 1 : 1));
+        chans.push_back({v, i, kRoleReduce, par, c, leaf, wr});
+        if (par >= 0) chans.push_back({v, i, kRoleBcast, par, c, leaf, bytes * (1 + nc)});
+      } else {
+        chans.push_back({v, i, kRoleBcast, par, c, leaf, bytes * (1 + nc + (par < 0 ? 1 : 0))});
+      }
+      rank_has[v] = 1;
+    }
+  }
+  int nexit = 0;
+  for (int v = 0; v < n; ++v)
+    if (((launch_mask >> v) & 1) && !rank_has[v]) ++nexit;
+  int avail = budget - nexit;
+  if (int(chans.size()) > avail)
+    return fail(comm, BLINK_ERR_UNSUPPORTED,
+                "plan needs " + std::to_string(chans.size() + nexit) + " channels but only " +
+                    std::to_string(budget) + " CTAs can be co-resident");
+  double tot = 0;
+  for (auto& c : chans) tot += c.work;
+  int used = 0;
+  for (auto& c : chans) {
+    c.ctas = std::max(1, int(std::floor(avail * c.work / tot)));
+    used += c.ctas;
+  }
+  while (used > avail) {  // trim the largest
+    auto it = std::max_element(chans.begin(), chans.end(),
+                               [](const Channel& a, const Channel& b) { return a.ctas < b.ctas; });
+    --it->ctas;
+    --used;
+  }
+  // chunking with the CTA count of the busiest channel of each tree
+  std::vector<int> hint(k, 1);
+  for (auto& c : chans) hint[c.tree] = std::max(hint[c.tree], c.ctas);
+  s->ranges.clear();
+  for (int i = 0; i < k; ++i) {
+    std::vector<TreeRange> ri;
+    rr = size_plan(plan, count, esize, comm->cfg, hint[i], &ri, &err);
+    if (rr != BLINK_SUCCESS) return fail(comm, rr, err);
+    s->ranges.push_back(ri[i]);
+  }
+  for (auto& c : chans) c.ctas = std::max(1, std::min(c.ctas, s->ranges[c.tree].nchunks));
+  // tasks: grouped by rank so exit work is split across a rank's CTAs
+  s->tasks.clear();
+  s->chunks = 0;
+  for (auto& r : s->ranges) s->chunks += r.nchunks;
+  for (int v = 0; v < n; ++v) {
+    if (!((launch_mask >> v) & 1)) continue;
+    size_t first = s->tasks.size();
+    for (auto& c : chans) {
+      if (c.rank != v) continue;
+      for (int j = 0; j < c.ctas; ++j) {
+        DevTask t{};
+        t.rank = int16_t(v);
+        t.tree = int16_t(c.tree);
+        t.role = int16_t(c.role);
+        t.parent = int16_t(c.parent);
+        t.children = c.children;
+        t.leafmask = c.leafmask;
+        t.cta_idx = j;
+        t.cta_cnt = c.ctas;
+        s->tasks.push_back(t);
+      }
+    }
+    if (s->tasks.size() == first) {
+      DevTask t{};
+      t.rank = int16_t(v);
+      t.role = kRoleExit;
+      t.parent = -1;
+      t.cta_cnt = 1;
+      s->tasks.push_back(t);
+    }
+    int cnt = int(s->tasks.size() - first);
+    for (int j = 0; j < cnt; ++j) {
+      s->tasks[first + j].exit_idx = j;
+      s->tasks[first + j].exit_cnt = cnt;
+      s->tasks[first + j].do_entry = (j == 0);
+    }
+  }
+  s->ctas = int(s->tasks.size());
+  s->plan = &plan;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* s) {
+  DeviceGuard g(device);
+  std::vector<DevTree> trees(s->ranges.size());
+  for (size_t i = 0; i < s->ranges.size(); ++i) {
+    trees[i].lo = s->ranges[i].lo * esize;
+    trees[i].hi = s->ranges[i].hi * esize;
+    trees[i].chunk = s->ranges[i].chunk * esize;
+    trees[i].nchunks = s->ranges[i].nchunks;
+    trees[i].root = s->plan->trees[i].root;
+  }
+  // the last tree's hi may not be a multiple of esize*... it is count*esize
+  CUDA_TRY(comm, cudaMalloc(&s->d_tasks, sizeof(DevTask) * s->tasks.size()));
+  CUDA_TRY(comm, cudaMalloc(&s->d_trees, sizeof(DevTree) * std::max<size_t>(1, trees.size())));
+  CUDA_TRY(comm, cudaMemcpy(s->d_tasks, s->tasks.data(), sizeof(DevTask) * s->tasks.size(),
+                            cudaMemcpyHostToDevice));
+  if (!trees.empty())
+    CUDA_TRY(comm, cudaMemcpy(s->d_trees, trees.data(), sizeof(DevTree) * trees.size(),
+                              cudaMemcpyHostToDevice));
+  return BLINK_SUCCESS;
+}
+
+int co_resident_budget(blink_comm_t comm, int device, int dtype, int op, int coll) {
+  DeviceGuard g(device);
+  int per_sm = exec_max_ctas_per_sm(comm->cfg.threads, true, dtype, op, coll);
+  int per_sm2 = exec_max_ctas_per_sm(comm->cfg.threads, false, dtype, op, coll);
+  per_sm = std::min(per_sm, per_sm2);
+  if (per_sm <= 0) per_sm = 1;
+  int cap = per_sm * comm->sms;
+  if (comm->cfg.ctas > 0) cap = std::min(cap, comm->cfg.ctas);
+  return cap;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtype, int op,
+                             int root, int coll) {
+  if (!comm) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "comm is NULL");
+  if (esize_of(dtype) == 0)
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported dtype " + std::to_string(dtype));
+  if (coll == kAllReduce && (op < BLINK_SUM || op > BLINK_MAX))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported op " + std::to_string(op));
+  if (coll == kBroadcast && (root < 0 || root >= comm->nranks))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT,
+                "root " + std::to_string(root) + " out of range [0," + std::to_string(comm->nranks) + ")");
+  if (count > (size_t(1) << 40))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "count too large");
+  if (comm->multiprocess && !comm->connected)
+    return fail(comm, BLINK_ERR_INVALID_USAGE, "blink_connect has not been called");
+  return BLINK_SUCCESS;
+}
+
+// ---------------------------------------------------------------- single-process launch
+blink_result_t clique_launch(Clique* q) {
+  const int n = q->nranks;
+  const int es = esize_of(blink_dtype_t(q->dtype));
+  const size_t bytes = q->count * es;
+  q->epoch++;
+  blink_comm_t c0 = q->comms[0];
+  if (n == 1) {
+    DeviceGuard g(c0->device);
+    CUDA_TRY(c0, launch_copy(q->pending[0].recv, q->coll == kBroadcast ? q->pending[0].send
+                                                                       : q->pending[0].send,
+                             bytes, q->pending[0].stream));
+    q->launches++;
+    return BLINK_SUCCESS;
+  }
+  const Plan* plan = nullptr;
+  blink_result_t r = get_plan(c0, q->coll, q->root, bytes, &plan);
+  if (r != BLINK_SUCCESS) return r;
+  bool vec = true;
+  for (int v = 0; v < n; ++v) {
+    const Pending& p = q->pending[v];
+    if ((q->coll == kAllReduce || v == q->root) && !aligned16(p.send)) vec = false;
+    if (!aligned16(p.recv)) vec = false;
+  }
+  const bool all_one_launch = q->devices.size() == 1;
+  for (int dev : q->devices) {
+    uint64_t mask = 0;
+    for (int v = 0; v < n; ++v)
+      if (q->comms[v]->device == dev) mask |= uint64_t(1) << v;
+    blink_comm_t cd = nullptr;
+    for (int v = 0; v < n && !cd; ++v)
+      if ((mask >> v) & 1) cd = q->comms[v];
+    SizedKey key{q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count,
+                 mask | (uint64_t(plan->trees.size()) << 32) |
+                     (uint64_t(q->coll == kBroadcast && plan->trees.size() == 1) << 48)};
+    auto it = q->sized.find(key);
+    if (it == q->sized.end()) {
+      Sized s;
+      int budget = co_resident_budget(cd, dev, q->dtype, q->op, q->coll);
+      r = build_sized(cd, *plan, q->count, es, mask, budget, &s);
+      if (r != BLINK_SUCCESS) return r;
+      r = finalize_tables(cd, dev, es, &s);
+      if (r != BLINK_SUCCESS) return r;
+      it = q->sized.emplace(key, std::move(s)).first;
+    }
+    Sized& s = it->second;
+    LaunchArgs a{};
+    a.tasks = s.d_tasks;
+    a.trees = s.d_trees;
+    a.ntrees = int(plan->trees.size());
+    a.nranks = n;
+    a.coll = q->coll;
+    a.dtype = q->dtype;
+    a.op = q->op;
+    a.exit_wait = all_one_launch ? 0 : 1;
+    a.bcast_root = q->coll == kBroadcast ? q->root : -1;
+    a.epoch = q->epoch;
+    a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
+    a.err = q->err_dev[dev];
+    for (int v = 0; v < n; ++v) {
+      a.send[v] = const_cast<char*>(static_cast<const char*>(q->pending[v].send));
+      a.recv[v] = static_cast<char*>(q->pending[v].recv);
+      a.flags[v] = q->comms[v]->flags;
+    }
+    DeviceGuard g(dev);
+    // launch on the first rank's stream of this device after the others' streams
+    int lead = -1;
+    for (int v = 0; v < n; ++v)
+      if ((mask >> v) & 1) {
+        lead = v;
+        break;
+      }
+    cudaStream_t ls = q->pending[lead].stream;
+    std::vector<cudaEvent_t> evs;
+    for (int v = 0; v < n; ++v) {
+      if (!((mask >> v) & 1) || v == lead || q->pending[v].stream == ls) continue;
+      cudaEvent_t e;
+      CUDA_TRY(cd, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CUDA_TRY(cd, cudaEventRecord(e, q->pending[v].stream));
+      CUDA_TRY(cd, cudaStreamWaitEvent(ls, e, 0));
+      evs.push_back(e);
+    }
+    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, true);
+    if (le != cudaSuccess)
+      return fail(cd, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
+    q->launches++;
+    for (int v = 0; v < n; ++v) {
+      if (!((mask >> v) & 1)) continue;
+      q->comms[v]->stats.launches++;
+      q->comms[v]->stats.last_ctas = s.ctas;
+      q->comms[v]->stats.last_chunks = s.chunks;
+      q->comms[v]->stats.last_trees = int(plan->trees.size());
+    }
+    if (!evs.empty()) {
+      cudaEvent_t done;
+      CUDA_TRY(cd, cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      CUDA_TRY(cd, cudaEventRecord(done, ls));
+      for (int v = 0; v < n; ++v) {
+        if (!((mask >> v) & 1) || v == lead || q->pending[v].stream == ls) continue;
+        CUDA_TRY(cd, cudaStreamWaitEvent(q->pending[v].stream, done, 0));
+      }
+      cudaEventDestroy(done);
+      for (auto e : evs) cudaEventDestroy(e);
+    }
+  }
+  return BLINK_SUCCESS;
+}
+
+blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* recv, size_t count,
+                           blink_dtype_t dtype, int op, int root, void* stream) {
+  Clique* q = comm->clique;
+  std::lock_guard<std::mutex> lk(q->mu);
+  for (auto& kv : q->err_host)
+    if (*kv.second != 0) {
+      q->sticky_error = true;
+      return fail(comm, blink_result_t(*kv.second),
+                  "a previous launch aborted (flag wait timed out on device " +
+                      std::to_string(kv.first) + ")");
+    }
+  if (q->nposted == 0) {
+    q->coll = coll;
+    q->root = root;
+    q->dtype = dtype;
+    q->op = op;
+    q->count = count;
+  } else if (q->coll != coll || q->count != count || q->dtype != int(dtype) ||
+             (coll == kAllReduce && q->op != op) || (coll == kBroadcast && q->root != root)) {
+    return fail(comm, BLINK_ERR_INVALID_USAGE,
+                "rank " + std::to_string(comm->rank) +
+                    " called a different collective/count/dtype/op/root than the ranks already "
+                    "posted in this batch");
+  }
+  Pending& p = q->pending[comm->rank];
+  if (p.posted)
+    return fail(comm, BLINK_ERR_INVALID_USAGE,
+                "rank " + std::to_string(comm->rank) + " posted twice before all ranks called");
+  p.posted = true;
+  p.send = send;
+  p.recv = recv;
+  p.stream = static_cast<cudaStream_t>(stream);
+  if (++q->nposted < q->nranks) return BLINK_SUCCESS;
+  blink_result_t r = BLINK_SUCCESS;
+  if (count > 0) r = clique_launch(q);
+  for (auto& pp : q->pending) pp = Pending();
+  q->nposted = 0;
+  return r;
+}
+
+// ---------------------------------------------------------------- multi-process
+struct Blob {
+  char magic[8];
+  int32_t rank, nranks, device, pid;
+  char bus_id[32];
+  cudaIpcMemHandle_t flags_h;
+  cudaIpcMemHandle_t staging_h;
+  uint64_t staging_bytes;
+};
+struct RegBlob {
+  char magic[8];
+  int32_t rank, pad;
+  cudaIpcMemHandle_t h;
+  uint64_t offset, bytes;
+};
+
+blink_result_t open_handle(blink_comm_t comm, const cudaIpcMemHandle_t& h, char** out) {
+  std::string key(reinterpret_cast<const char*>(&h), sizeof h);
+  auto it = comm->opened.find(key);
+  if (it != comm->opened.end()) {
+    *out = it->second;
+    return BLINK_SUCCESS;
+  }
+  void* p = nullptr;
+  CUDA_TRY(comm, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  comm->opened[key] = static_cast<char*>(p);
+  *out = static_cast<char*>(p);
+  return BLINK_SUCCESS;
+}
+
+bool resolve(blink_comm_t comm, const void* ptr, size_t bytes, char* out[kMaxRanks]) {
+  const char* p = static_cast<const char*>(ptr);
+  for (const Reg& r : comm->regs) {
+    if (p >= r.buf && p + bytes <= r.buf + r.bytes) {
+      size_t off = size_t(p - r.buf);
+      for (int u = 0; u < comm->nranks; ++u) out[u] = r.peer[u] + off;
+      return true;
+    }
+  }
+  return false;
+}
+
+blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* recv[kMaxRanks],
+                      size_t count, blink_dtype_t dtype, int op, int root, cudaStream_t stream) {
+  const int n = comm->nranks;
+  const int es = esize_of(dtype);
+  const size_t bytes = count * es;
+  comm->epoch++;
+  const Plan* plan = nullptr;
+  blink_result_t r = get_plan(comm, coll, root, bytes, &plan);
+  if (r != BLINK_SUCCESS) return r;
+  uint64_t mask = uint64_t(1) << comm->rank;
+  SizedKey key{coll, coll == kBroadcast ? root : -1, int(dtype), count,
+               mask | (uint64_t(plan->trees.size()) << 32)};
+  auto it = comm->sized.find(key);
+  if (it == comm->sized.end()) {
+    Sized s;
+    int budget = co_resident_budget(comm, comm->device, dtype, op, coll);
+    r = build_sized(comm, *plan, count, es, mask, budget, &s);
+    if (r != BLINK_SUCCESS) return r;
+    r = finalize_tables(comm, comm->device, es, &s);
+    if (r != BLINK_SUCCESS) return r;
+    it = comm->sized.emplace(key, std::move(s)).first;
+  }
+  Sized& s = it->second;
+  bool vec = true;
+  for (int u = 0; u < n; ++u) {
+    if ((coll == kAllReduce || u == root) && !aligned16(send[u])) vec = false;
+    if (!aligned16(recv[u])) vec = false;
+  }
+  LaunchArgs a{};
+  a.tasks = s.d_tasks;
+  a.trees = s.d_trees;
+  a.ntrees = int(plan->trees.size());
+  a.nranks = n;
+  a.coll = coll;
+  a.dtype = dtype;
+  a.op = op;
+  a.exit_wait = 1;
+  a.bcast_root = coll == kBroadcast ? root : -1;
+  a.epoch = comm->epoch;
+  a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
+  a.err = comm->err_dev;
+  for (int u = 0; u < n; ++u) {
+    a.send[u] = send[u];
+    a.recv[u] = recv[u];
+    a.flags[u] = comm->peer_flags[u];
+  }
+  cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, true);
+  if (le != cudaSuccess)
+    return fail(comm, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
+  comm->stats.launches++;
+  comm->stats.last_ctas = s.ctas;
+  comm->stats.last_chunks = s.chunks;
+  comm->stats.last_trees = int(plan->trees.size());
+  return BLINK_SUCCESS;
+}
+
+blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, void* recvbuf,
+                             size_t count, blink_dtype_t dtype, int op, int root, void* stream_) {
+  if (*comm->err_host != 0)
+    return fail(comm, blink_result_t(*comm->err_host),
+                "a previous launch aborted (flag wait timed out)");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const int es = esize_of(dtype);
+  const size_t bytes = count * es;
+  DeviceGuard g(comm->device);
+  if (comm->nranks == 1) {
+    CUDA_TRY(comm, launch_copy(recvbuf, sendbuf, bytes, stream));
+    comm->stats.launches++;
+    return BLINK_SUCCESS;
+  }
+  char* sp[kMaxRanks] = {};
+  char* rp[kMaxRanks] = {};
+  const bool recv_ok = resolve(comm, recvbuf, bytes, rp);
+  if (coll == kBroadcast) {
+    // only the root reads a send buffer, its own: no registration needed
+    if (comm->rank == root) sp[root] = const_cast<char*>(static_cast<const char*>(sendbuf));
+    if (recv_ok) return mp_run(comm, coll, sp, rp, count, dtype, op, root, stream);
+  } else if (recv_ok && resolve(comm, sendbuf, bytes, sp)) {
+    // zero-copy: registered symmetric buffers (parents pull from leaves' send)
+    return mp_run(comm, coll, sp, rp, count, dtype, op, root, stream);
+  }
+  // staging path: in-place collective on the symmetric staging buffer, in pieces
+  const size_t piece_elems = comm->staging_bytes / es;
+  for (size_t off = 0; off < count; off += piece_elems) {
+    size_t cnt = std::min(piece_elems, count - off);
+    const char* s = static_cast<const char*>(sendbuf) + off * es;
+    char* d = static_cast<char*>(recvbuf) + off * es;
+    if (coll == kAllReduce || comm->rank == root)
+      CUDA_TRY(comm, launch_copy(comm->staging, s, cnt * es, stream));
+    char* st[kMaxRanks];
+    for (int u = 0; u < comm->nranks; ++u) st[u] = comm->peer_staging[u];
+    blink_result_t r = mp_run(comm, coll, st, st, cnt, dtype, op, root, stream);
+    if (r != BLINK_SUCCESS) return r;
+    CUDA_TRY(comm, launch_copy(d, comm->staging, cnt * es, stream));
+  }
+  return BLINK_SUCCESS;
+}
+
+}  // namespace
+
+// =============================================================== C ABI
+extern "C" {
+
+void blink_config_default(blink_config_t* c) {
+  if (!c) return;
+  c->mwu_eps = 0.1;
+  c->ilp_gap = 0.05;
+  c->chunk_bytes = 0;
+  c->ctas = 0;
+  c->threads = 256;
+  c->timeout_s = 30.0;
+  c->onehop_bcast_max_bytes = 256 << 10;
+  c->staging_bytes = 64 << 20;
+}
+
+const char* blink_result_string(blink_result_t r) {
+  switch (r) {
+    case BLINK_SUCCESS: return "success";
+    case BLINK_ERR_CUDA: return "CUDA error";
+    case BLINK_ERR_SYSTEM: return "system error";
+    case BLINK_ERR_INTERNAL: return "internal error";
+    case BLINK_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case BLINK_ERR_INVALID_USAGE: return "invalid usage";
+    case BLINK_ERR_TOPOLOGY: return "topology error";
+    case BLINK_ERR_UNSUPPORTED: return "unsupported";
+    case BLINK_ERR_TIMEOUT: return "timeout";
+  }
+  return "unknown";
+}
+
+const char* blink_last_error(blink_comm_t comm) {
+  return comm ? comm->last_error.c_str() : g_last_error.c_str();
+}
+
+blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const blink_config_t* cfg_in,
+                               int is_allreduce, int root, size_t count, blink_dtype_t dtype,
+                               char* json, size_t* json_bytes) {
+  if (!json_bytes) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "json_bytes is NULL");
+  if (nranks < 1 || nranks > kMaxRanks)
+    return fail(nullptr, BLINK_ERR_UNSUPPORTED, "nranks out of range");
+  int es = esize_of(dtype);
+  if (!es) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "bad dtype");
+  blink_config_t cfg = resolve_cfg(cfg_in);
+  Graph g;
+  std::string err;
+  blink_result_t r = build_graph(graph, nranks, &g, &err);
+  if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
+  Plan p;
+  r = make_plan(g, is_allreduce ? kAllReduce : kBroadcast, root, cfg, &p, &err);
+  if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
+  std::vector<TreeRange> ranges;
+  int hint = std::max(1, (cfg.ctas > 0 ? cfg.ctas : 296) / int(p.trees.size()));
+  r = size_plan(p, count, es, cfg, hint, &ranges, &err);
+  if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
+  std::string s = plan_to_json(p, count, es, ranges, 0);
+  size_t need = s.size() + 1;
+  size_t cap = *json_bytes;
+  *json_bytes = need;
+  if (!json || cap < need) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "json buffer too small");
+  memcpy(json, s.c_str(), need);
+  return BLINK_SUCCESS;
+}
+
+static blink_result_t alloc_comm_common(blink_comm_t c) {
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+  CUDA_TRY(c, cudaMalloc(&c->flags, kFlagBytes));
+  CUDA_TRY(c, cudaMemset(c->flags, 0, kFlagBytes));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
+                              const blink_graph_t* graph, const blink_config_t* cfg_in) {
+  if (!comms || !devs || ndev < 1)
+    return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "comms/devs NULL or ndev < 1");
+  if (ndev > kMaxRanks)
+    return fail(nullptr, BLINK_ERR_UNSUPPORTED,
+                "at most " + std::to_string(kMaxRanks) + " ranks per comm");
+  int ndevices = 0;
+  if (cudaGetDeviceCount(&ndevices) != cudaSuccess || ndevices == 0)
+    return fail(nullptr, BLINK_ERR_CUDA, "no CUDA device visible");
+  for (int i = 0; i < ndev; ++i)
+    if (devs[i] < 0 || devs[i] >= ndevices)
+      return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT,
+                  "devs[" + std::to_string(i) + "] = " + std::to_string(devs[i]) + " is not a device");
+  blink_config_t cfg = resolve_cfg(cfg_in);
+  Graph gr;
+  std::string err;
+  blink_result_t r = build_graph(graph, ndev, &gr, &err);
+  if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
+  // probe / peer access: distinct devices must reach each other
+  std::vector<int> distinct;
+  for (int i = 0; i < ndev; ++i)
+    if (std::find(distinct.begin(), distinct.end(), devs[i]) == distinct.end())
+      distinct.push_back(devs[i]);
+  for (int a : distinct)
+    for (int b : distinct) {
+      if (a == b) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a, b);
+      if (!can)
+        return fail(nullptr, BLINK_ERR_UNSUPPORTED,
+                    "no peer access from device " + std::to_string(a) + " to " + std::to_string(b));
+      DeviceGuard g(a);
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(nullptr, BLINK_ERR_CUDA, std::string("enable peer access: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  Clique* q = new Clique();
+  q->nranks = ndev;
+  q->devices = distinct;
+  q->pending.resize(ndev);
+  for (int i = 0; i < ndev; ++i) {
+    blink_comm_t c = new blink_comm();
+    c->nranks = ndev;
+    c->rank = i;
+    c->device = devs[i];
+    c->cfg = cfg;
+    c->graph = gr;
+    c->clique = q;
+    c->connected = true;
+    r = alloc_comm_common(c);
+    if (r != BLINK_SUCCESS) {
+      g_last_error = c->last_error;
+      return r;
+    }
+    q->comms.push_back(c);
+    comms[i] = c;
+  }
+  for (int d : distinct) {
+    DeviceGuard g(d);
+    int* h = nullptr;
+    int* dp = nullptr;
+    if (cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&dp, h, 0) != cudaSuccess)
+      return fail(nullptr, BLINK_ERR_CUDA, "mapped error word allocation failed");
+    *h = 0;
+    q->err_host[d] = h;
+    q->err_dev[d] = dp;
+  }
+  q->alive = ndev;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_device,
+                          const blink_graph_t* graph, const blink_config_t* cfg_in) {
+  if (!comm) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "comm is NULL");
+  if (nranks < 1 || nranks > kMaxRanks)
+    return fail(nullptr, BLINK_ERR_UNSUPPORTED, "nranks out of range [1,16]");
+  if (rank < 0 || rank >= nranks) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "rank out of range");
+  blink_comm_t c = new blink_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = cuda_device;
+  c->cfg = resolve_cfg(cfg_in);
+  c->multiprocess = true;
+  std::string err;
+  blink_result_t r = build_graph(graph, nranks, &c->graph, &err);
+  if (r != BLINK_SUCCESS) {
+    delete c;
+    return fail(nullptr, r, err);
+  }
+  r = alloc_comm_common(c);
+  if (r != BLINK_SUCCESS) {
+    g_last_error = c->last_error;
+    delete c;
+    return r;
+  }
+  DeviceGuard g(c->device);
+  CUDA_TRY(c, cudaMalloc(&c->staging, c->cfg.staging_bytes));
+  c->staging_bytes = c->cfg.staging_bytes;
+  CUDA_TRY(c, cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped));
+  CUDA_TRY(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
+  *c->err_host = 0;
+  *comm = c;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_bytes) {
+  if (!comm || !blob_bytes) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!comm->multiprocess) return fail(comm, BLINK_ERR_INVALID_USAGE, "not a multi-process comm");
+  size_t cap = *blob_bytes;
+  *blob_bytes = sizeof(Blob);
+  if (!blob || cap < sizeof(Blob)) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "blob too small");
+  Blob b{};
+  memcpy(b.magic, "BLINKv1", 8);
+  b.rank = comm->rank;
+  b.nranks = comm->nranks;
+  b.device = comm->device;
+  b.pid = int(getpid());
+  DeviceGuard g(comm->device);
+  CUDA_TRY(comm, cudaDeviceGetPCIBusId(b.bus_id, sizeof b.bus_id, comm->device));
+  CUDA_TRY(comm, cudaIpcGetMemHandle(&b.flags_h, comm->flags));
+  CUDA_TRY(comm, cudaIpcGetMemHandle(&b.staging_h, comm->staging));
+  b.staging_bytes = comm->staging_bytes;
+  memcpy(blob, &b, sizeof b);
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t blob_bytes) {
+  if (!comm || !all_blobs) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!comm->multiprocess) return fail(comm, BLINK_ERR_INVALID_USAGE, "not a multi-process comm");
+  if (blob_bytes < sizeof(Blob)) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "blob_bytes too small");
+  DeviceGuard g(comm->device);
+  const char* base = static_cast<const char*>(all_blobs);
+  for (int u = 0; u < comm->nranks; ++u) {
+    Blob b;
+    memcpy(&b, base + size_t(u) * blob_bytes, sizeof b);
+    if (memcmp(b.magic, "BLINKv1", 8) != 0 || b.rank != u || b.nranks != comm->nranks)
+      return fail(comm, BLINK_ERR_INVALID_USAGE,
+                  "blob " + std::to_string(u) + " is not rank " + std::to_string(u) + "'s handle");
+    if (b.staging_bytes != comm->staging_bytes)
+      return fail(comm, BLINK_ERR_INVALID_USAGE, "staging_bytes differs across ranks");
+    if (u == comm->rank) {
+      comm->peer_flags[u] = comm->flags;
+      comm->peer_staging[u] = comm->staging;
+      continue;
+    }
+    // probe: the peer GPU must be reachable (same GPU or peer access)
+    int pdev = -1;
+    if (cudaDeviceGetByPCIBusId(&pdev, b.bus_id) == cudaSuccess && pdev != comm->device) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, comm->device, pdev);
+      if (!can)
+        return fail(comm, BLINK_ERR_UNSUPPORTED,
+                    "no peer access to rank " + std::to_string(u) + " (" + b.bus_id + ")");
+    }
+    cudaGetLastError();
+    char* p = nullptr;
+    blink_result_t r = open_handle(comm, b.flags_h, &p);
+    if (r != BLINK_SUCCESS) return r;
+    comm->peer_flags[u] = reinterpret_cast<uint64_t*>(p);
+    r = open_handle(comm, b.staging_h, &p);
+    if (r != BLINK_SUCCESS) return r;
+    comm->peer_staging[u] = p;
+  }
+  Reg st;
+  st.buf = comm->staging;
+  st.bytes = comm->staging_bytes;
+  for (int u = 0; u < comm->nranks; ++u) st.peer[u] = comm->peer_staging[u];
+  comm->regs.push_back(st);
+  comm->connected = true;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_register_export(blink_comm_t comm, void* buf, size_t bytes, void* blob,
+                                     size_t* blob_bytes) {
+  if (!comm || !blob_bytes) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  size_t cap = *blob_bytes;
+  *blob_bytes = sizeof(RegBlob);
+  if (!comm->multiprocess) return BLINK_SUCCESS;
+  if (!blob || cap < sizeof(RegBlob)) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "blob too small");
+  if (!buf || bytes == 0) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "empty buffer");
+  DeviceGuard g(comm->device);
+  // allocation base of `buf` (IPC handles name whole allocations); the driver
+  // symbol is fetched through the runtime so the library never links libcuda.
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    CUDA_TRY(comm, cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &qr));
+    if (!fn) return fail(comm, BLINK_ERR_CUDA, "cuMemGetAddressRange entry point not found");
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  CUresult cr = get_range(&base, &size, reinterpret_cast<CUdeviceptr>(buf));
+  if (cr != CUDA_SUCCESS) return fail(comm, BLINK_ERR_CUDA, "cuMemGetAddressRange failed");
+  RegBlob rb{};
+  memcpy(rb.magic, "BLINKrg", 8);
+  rb.rank = comm->rank;
+  CUDA_TRY(comm, cudaIpcGetMemHandle(&rb.h, reinterpret_cast<void*>(base)));
+  rb.offset = uint64_t(reinterpret_cast<char*>(buf) - reinterpret_cast<char*>(base));
+  rb.bytes = bytes;
+  memcpy(blob, &rb, sizeof rb);
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_register_connect(blink_comm_t comm, void* buf, const void* all_blobs,
+                                      size_t blob_bytes) {
+  if (!comm) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL comm");
+  if (!comm->multiprocess) return BLINK_SUCCESS;
+  if (!all_blobs || blob_bytes < sizeof(RegBlob))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "bad blobs");
+  DeviceGuard g(comm->device);
+  Reg reg;
+  reg.buf = static_cast<char*>(buf);
+  const char* base = static_cast<const char*>(all_blobs);
+  for (int u = 0; u < comm->nranks; ++u) {
+    RegBlob rb;
+    memcpy(&rb, base + size_t(u) * blob_bytes, sizeof rb);
+    if (memcmp(rb.magic, "BLINKrg", 8) != 0 || rb.rank != u)
+      return fail(comm, BLINK_ERR_INVALID_USAGE, "registration blob " + std::to_string(u) + " is invalid");
+    if (u == 0) reg.bytes = rb.bytes;
+    if (rb.bytes != reg.bytes)
+      return fail(comm, BLINK_ERR_INVALID_USAGE, "registered sizes differ across ranks (symmetric registration)");
+    if (u == comm->rank) {
+      reg.peer[u] = reg.buf;
+      continue;
+    }
+    char* p = nullptr;
+    blink_result_t r = open_handle(comm, rb.h, &p);
+    if (r != BLINK_SUCCESS) return r;
+    reg.peer[u] = p + rb.offset;
+  }
+  comm->regs.push_back(reg);
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_broadcast(blink_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                               blink_dtype_t dtype, int root, void* stream) {
+  blink_result_t r = validate_call(comm, count, dtype, BLINK_SUM, root, kBroadcast);
+  if (r != BLINK_SUCCESS) return r;
+  if (count > 0 && (!recvbuf || (comm->rank == root && !sendbuf)))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (comm->multiprocess) {
+    if (count == 0) return BLINK_SUCCESS;
+    return mp_collective(comm, kBroadcast, sendbuf, recvbuf, count, dtype, BLINK_SUM, root, stream);
+  }
+  return clique_post(comm, kBroadcast, sendbuf, recvbuf, count, dtype, BLINK_SUM, root, stream);
+}
+
+blink_result_t blink_allreduce(blink_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                               blink_dtype_t dtype, blink_redop_t op, void* stream) {
+  blink_result_t r = validate_call(comm, count, dtype, op, 0, kAllReduce);
+  if (r != BLINK_SUCCESS) return r;
+  if (count > 0 && (!recvbuf || !sendbuf))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (comm->multiprocess) {
+    if (count == 0) return BLINK_SUCCESS;
+    return mp_collective(comm, kAllReduce, sendbuf, recvbuf, count, dtype, op, -1, stream);
+  }
+  return clique_post(comm, kAllReduce, sendbuf, recvbuf, count, dtype, op, -1, stream);
+}
+
+blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, size_t count,
+                              blink_dtype_t dtype, char* json, size_t* json_bytes) {
+  if (!comm || !json_bytes) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  int coll = is_allreduce ? kAllReduce : kBroadcast;
+  blink_result_t r = validate_call(comm, count, dtype, BLINK_SUM, root, coll);
+  if (r != BLINK_SUCCESS) return r;
+  const int es = esize_of(dtype);
+  const Plan* plan = nullptr;
+  r = get_plan(comm, coll, root, count * es, &plan);
+  if (r != BLINK_SUCCESS) return r;
+  // the launch this rank belongs to
+  uint64_t mask = 0;
+  if (comm->multiprocess) {
+    mask = uint64_t(1) << comm->rank;
+  } else {
+    for (int v = 0; v < comm->nranks; ++v)
+      if (comm->clique->comms[v]->device == comm->device) mask |= uint64_t(1) << v;
+  }
+  Sized s;
+  int budget = co_resident_budget(comm, comm->device, dtype, BLINK_SUM, coll);
+  r = build_sized(comm, *plan, count, es, mask, budget, &s);
+  if (r != BLINK_SUCCESS) return r;
+  std::string j = plan_to_json(*plan, count, es, s.ranges, s.ctas);
+  size_t need = j.size() + 1, cap = *json_bytes;
+  *json_bytes = need;
+  if (!json || cap < need) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "json buffer too small");
+  memcpy(json, j.c_str(), need);
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* st) {
+  if (!comm || !st) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  *st = comm->stats;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_comm_info(blink_comm_t comm, int* nranks, int* rank, int* device) {
+  if (!comm) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "NULL comm");
+  if (nranks) *nranks = comm->nranks;
+  if (rank) *rank = comm->rank;
+  if (device) *device = comm->device;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t blink_destroy(blink_comm_t comm) {
+  if (!comm) return BLINK_SUCCESS;
+  {
+    DeviceGuard g(comm->device);
+    cudaDeviceSynchronize();
+    if (comm->multiprocess) {
+      for (auto& kv : comm->sized) {
+        cudaFree(kv.second.d_tasks);
+        cudaFree(kv.second.d_trees);
+      }
+      for (auto& kv : comm->opened) cudaIpcCloseMemHandle(kv.second);
+      if (comm->staging) cudaFree(comm->staging);
+      if (comm->err_host) cudaFreeHost(comm->err_host);
+    }
+    if (comm->flags) cudaFree(comm->flags);
+  }
+  Clique* q = comm->clique;
+  if (q) {
+    bool last = false;
+    {
+      std::lock_guard<std::mutex> lk(q->mu);
+      last = --q->alive == 0;
+    }
+    if (last) {
+      for (auto& kv : q->sized) {
+        cudaFree(kv.second.d_tasks);
+        cudaFree(kv.second.d_trees);
+      }
+      for (auto& kv : q->err_host) cudaFreeHost(kv.second);
+      delete q;
+    }
+  }
+  delete comm;
+  return BLINK_SUCCESS;
+}
+
+}  // extern "C"

@@ -67,3 +67,18 @@ BUCKETS = {
     ("vgg16", "f32"): [4097000, 16781312, 102764544, 7079424, 7079936, 555328],
     ("vgg16", "bf16"): [4097000, 16781312, 102764544, 13569280, 1145408],
 }
+
+
+def device_input(config, rank, count, dtype, device="cuda"):
+    """Large seeded inputs generated on the device (torch's Philox generator):
+    same recipe (N(0,1)*1e-2 / its bf16 rounding / uniform int), used where
+    host generation would dominate (full-size parity samples and the bench).
+    Oracle comparisons copy the sampled inputs back to the host."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed(config, rank))
+    if dtype == "i32":
+        return torch.randint(-(1 << 20), (1 << 20) + 1, (count,), generator=g, device=device,
+                             dtype=torch.int32)
+    x = torch.randn(count, generator=g, device=device, dtype=torch.float32) * 1e-2
+    return x if dtype == "f32" else x.to(torch.bfloat16)

@@ -1,0 +1,170 @@
+"""CPU-only checks of the C-ABI library: it loads without a GPU, exports every
+symbol include/blink.h declares, and its host-only control plane
+(blink_plan_json) satisfies the oracle's invariants (feasibility, rate within
+the ILP gap of the Edmonds / Nash-Williams optimum, exact splits) -- no compute
+calls, no GPU."""
+import ctypes
+import os
+import re
+from fractions import Fraction
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "blink.h")
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_1910_04940_b200 import build
+    build.build()
+    import paper_1910_04940_b200 as B
+    return B
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(blink_[a-z_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_survey_boundary():
+    syms = declared_symbols()
+    for s in ("blink_init", "blink_init_all", "blink_export_handle", "blink_connect",
+              "blink_broadcast", "blink_allreduce", "blink_get_plan", "blink_destroy",
+              "blink_result_string", "blink_last_error", "blink_plan_json"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(B):
+    lib = ctypes.CDLL(B.LIB_PATH)
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+
+
+def test_result_strings_and_defaults(B):
+    lib = B._lib
+    assert lib.blink_result_string(0) == b"success"
+    assert lib.blink_result_string(10) == b"timeout"
+    c = B.config()
+    assert c.mwu_eps == 0.1 and c.ilp_gap == 0.05 and c.threads == 256
+
+
+def _oracle_plan(p):
+    return dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"],
+                            weight=Fraction(*t["weight"])) for t in p["trees"]])
+
+
+def _check_plan(p, g, allreduce):
+    from oracle import bounds, graphs
+    n, cap = g
+    W = sum(Fraction(*t["weight"]) for t in p["trees"])
+    assert Fraction(*p["rate"]) == W
+    if allreduce:
+        pairs = graphs.undirected_pairs(g)
+        load = {e: Fraction(0) for e in pairs}
+        for t in p["trees"]:
+            for v, u in enumerate(t["parent"]):
+                if u >= 0:
+                    load[(min(u, v), max(u, v))] += Fraction(*t["weight"])
+        assert all(load[e] <= pairs[e] for e in pairs)
+        opt = bounds.nash_williams_rate(pairs, n)
+    else:
+        load = {e: Fraction(0) for e in cap}
+        for t in p["trees"]:
+            assert t["parent"][p["root"]] == -1
+            for v, u in enumerate(t["parent"]):
+                if u >= 0:
+                    load[(u, v)] += Fraction(*t["weight"])
+        assert all(load[e] <= cap[e] for e in cap)
+        opt = bounds.edmonds_rate(g, p["root"])
+    # rate within the ILP gap of the true optimum (MWU is (1-eps)-optimal)
+    assert float(W) >= 0.95 * 0.9 * opt
+    # split: contiguous, 16-byte grains, covers [0, count)
+    es = p["esize"]
+    rngs = [(t["lo"], t["hi"]) for t in p["trees"]]
+    assert rngs[0][0] == 0 and rngs[-1][1] == p["count"]
+    for (a, b), (c, d) in zip(rngs, rngs[1:]):
+        assert b == c and (a * es) % 16 == 0
+    for t in p["trees"]:
+        if t["hi"] > t["lo"]:
+            assert t["nchunks"] == -(-(t["hi"] - t["lo"]) // t["chunk"])
+
+
+@pytest.mark.parametrize("root", range(8))
+def test_dgx1v_broadcast_plan_is_six_unit_trees(B, root):
+    from oracle import graphs
+    g = graphs.dgx1v()
+    p = B.plan_json(8, False, root, 1000 * 10**6 // 4, "f32", graph=B.Graph.from_pairs(8, g[1]))
+    assert len(p["trees"]) == 6 and p["rate"] == [6, 1]
+    assert all(t["weight"] == [1, 1] for t in p["trees"])
+    _check_plan(p, g, False)
+
+
+def test_dgx1_allreduce_plans(B):
+    from oracle import graphs
+    for g in (graphs.dgx1v(), graphs.dgx1p()):
+        p = B.plan_json(8, True, 0, (1 << 20) + 3, "f32", graph=B.Graph.from_pairs(8, g[1]))
+        _check_plan(p, g, True)
+        assert Fraction(*p["rate"]) >= Fraction(95, 100) * Fraction(p["c_star"]).limit_denominator(10**6) - Fraction(1, 10**5)
+
+
+def test_three_gpu_plans_match_the_oracle_exactly(B):
+    from oracle import graphs, packing
+    tri, _ = graphs.induced(graphs.dgx1p(), [0, 1, 3])
+    G = B.Graph.from_pairs(3, tri[1])
+    pb = B.plan_json(3, False, 0, 262144, "f32", graph=G)
+    ob = packing.plan_broadcast_graph(tri, 0)
+    assert {tuple(t["parent"]) for t in pb["trees"]} == {t["parent"] for t in ob["trees"]}
+    pa = B.plan_json(3, True, 0, 262144, "f32", graph=G)
+    oa = packing.plan_allreduce_graph(tri)
+    assert [tuple(t["parent"]) for t in pa["trees"]] == [t["parent"] for t in oa["trees"]]
+    assert [t["hi"] - t["lo"] for t in pa["trees"]] == [87380, 87380, 87384]
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 8, 16])
+def test_switch_plans_equal_oracle_closed_forms(B, m):
+    from oracle import collectives, packing
+    count = 1000 * m + 7
+    pa = B.plan_json(m, True, 0, count, "bf16")
+    oa = packing.plan_switch_allreduce(m)
+    assert [tuple(t["parent"]) for t in pa["trees"]] == [t["parent"] for t in oa["trees"]]
+    assert [(t["lo"], t["hi"]) for t in pa["trees"]] == collectives.tree_element_ranges(oa, count, "bf16")
+    if m > 2:
+        pb = B.plan_json(m, False, m - 1, count, "f32")
+        ob = packing.plan_switch_broadcast(m, m - 1)
+        assert [tuple(t["parent"]) for t in pb["trees"]] == [t["parent"] for t in ob["trees"]]
+
+
+@pytest.mark.parametrize("count", [0, 1, 3, 4, 5, 262144, 10**9 // 4 + 1])
+def test_split_matches_oracle_for_weighted_trees(B, count):
+    from oracle import collectives, graphs
+    g = graphs.dgx1v()
+    p = B.plan_json(8, True, 0, count, "f32", graph=B.Graph.from_pairs(8, g[1]))
+    got = [(t["lo"], t["hi"]) for t in p["trees"]]
+    assert got == collectives.tree_element_ranges(_oracle_plan(p), count, "f32")
+
+
+def test_topology_errors(B):
+    # dangling endpoint, nonpositive capacity, disconnected, missing reverse
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(3, False, 0, 16, graph=B.Graph(3, [(0, 1, 1, 1), (1, 9, 1, 1)]))
+    assert e.value.code == 8 and "dangling" in str(e.value)
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(2, False, 0, 16, graph=B.Graph(2, [(0, 1, 0.0, 1)]))
+    assert e.value.code == 8 and "capacity" in str(e.value)
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(4, False, 0, 16, graph=B.Graph(4, [(0, 1, 1, 1), (2, 3, 1, 1)]))
+    assert e.value.code == 8 and "{2,3}" in str(e.value)
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(3, True, 0, 16, graph=B.Graph(3, [(0, 1, 1, 1), (1, 2, 1, 0), (2, 0, 1, 1)]))
+    assert e.value.code == 8 and "reverse" in str(e.value)
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(3, False, 5, 16)
+    assert e.value.code == 4
+
+
+def test_switch_graph_with_switch_node(B):
+    # 4 GPUs on one SWITCH node (node 4): one-hop trees
+    G = B.Graph(4, [(v, 4, 6.0, 1) for v in range(4)], switches=1)
+    p = B.plan_json(4, True, 0, 4096, "f32", graph=G)
+    assert p["switch"] and len(p["trees"]) == 4 and p["rate"] == [2, 1]

@@ -1,0 +1,338 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+All ranks are virtual ranks on cuda:0 (the GPU box has one B200): their
+buffers live in one HBM and one cooperative launch runs every rank's channels,
+exactly the kernels and tables the multi-GPU path runs (DESIGN.md
+"Virtual ranks").  Expected values come only from oracle/ on the same seeded
+inputs:
+  * Broadcast: bitwise copy of the root's send (definition).
+  * AllReduce on one-hop / unique plans: bit-exact vs the oracle's OWN plan.
+  * AllReduce on other multi-level plans: the library's plan is first checked
+    against the oracle's invariants (tests/test_capi_cpu.py), then the GPU
+    result must be bit-exact vs the oracle's tree-order evaluation of that
+    plan and within rtol * sum|x| of the naive-order sum (R#20).
+  * int32 and MIN/MAX: exact vs the oracle under any plan.
+Receive buffers start as 0xFF sentinels so unwritten bytes show up.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import collectives as OC
+from oracle import graphs as OG
+from oracle import packing as OP
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}
+NP_VIEW = {"f32": np.float32, "bf16": np.int16, "i32": np.int32}
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1910_04940_b200 as B
+    return B
+
+
+def to_dev(arr, dtype):
+    a = np.ascontiguousarray(arr)
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def to_host(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def sentinel(count, dtype, offset=0):
+    es = OC.ESIZE[dtype]
+    raw = torch.full((count * es + offset + 16,), 0xFF, dtype=torch.uint8, device="cuda")
+    return raw[offset:offset + count * es].view(TORCH_DT[dtype]) if offset % es == 0 else raw
+
+
+def oracle_plan_from_json(p):
+    from fractions import Fraction
+    return dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"],
+                            weight=Fraction(*t["weight"])) for t in p["trees"]])
+
+
+def run_allreduce(B, comms, sends, dtype, op, inplace=False):
+    m = len(comms)
+    count = len(sends[0])
+    dsend = [to_dev(s, dtype) for s in sends]
+    drecv = dsend if inplace else [sentinel(count, dtype) for _ in range(m)]
+    for r, c in enumerate(comms):
+        c.allreduce(dsend[r], drecv[r], op=op, count=count, dtype=dtype)
+    torch.cuda.synchronize()
+    return [to_host(x, dtype) for x in drecv]
+
+
+def bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint16) if a.dtype.itemsize == 2 else a.view(np.uint32)
+
+
+def assert_bitwise(got, want):
+    gb, wb = bits(got), bits(want)
+    bad = np.nonzero(gb != wb)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:5]}: got {got[bad[:5]]} want {want[bad[:5]]}"
+
+
+def make_comms(B, m, graph=None, **cfg):
+    cfg.setdefault("timeout_s", 20.0)
+    return B.init_all([0] * m, graph=graph, cfg=B.config(**cfg))
+
+
+# ----------------------------------------------------------------- config 3/4: switch one-hop
+@pytest.mark.parametrize("m", [2, 3, 5, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+@pytest.mark.parametrize("op", ["sum", "min", "max", "prod"])
+def test_onehop_allreduce_bitexact(B, m, dtype, op):
+    count = 2048 * m + 13          # several tiles + a ragged, sub-16-byte tail
+    sends = synth.inputs(30 + m, m, count, dtype)
+    if op == "prod" and dtype == "i32":
+        sends = [(s % 5 - 2).astype(np.int32) for s in sends]
+    comms = make_comms(B, m, chunk_bytes=4096)
+    got = run_allreduce(B, comms, sends, dtype, op)
+    want = OC.allreduce(OP.plan_switch_allreduce(m), sends, dtype, op)
+    for g in got:
+        assert_bitwise(g, want)
+    # one-hop tree order = naive left-to-right order (R#12)
+    assert_bitwise(want, OC.naive_reduce(sends, dtype, op))
+    for c in comms:
+        c.destroy()
+
+
+def test_onehop_edge_values_f32(B):
+    m, count = 6, 4099
+    sends = [synth.edge_case_f32(4, r, count) for r in range(m)]
+    comms = make_comms(B, m)
+    for op in ("sum", "min", "max"):
+        got = run_allreduce(B, comms, sends, "f32", op)
+        want = OC.allreduce(OP.plan_switch_allreduce(m), sends, "f32", op)
+        for g in got:
+            assert_bitwise(g, want)
+
+
+@pytest.mark.parametrize("count", [0, 1, 2, 3, 4, 5, 7, 8, 9, 31, 33, 1000])
+def test_tiny_and_ragged_counts(B, count):
+    m = 8
+    comms = make_comms(B, m)
+    for dtype in ("f32", "bf16"):
+        sends = synth.inputs(50, m, count, dtype)
+        got = run_allreduce(B, comms, sends, dtype, "sum")
+        if count:
+            want = OC.allreduce(OP.plan_switch_allreduce(m), sends, dtype, "sum")
+            for g in got:
+                assert_bitwise(g, want)
+
+
+def test_inplace_and_misaligned(B):
+    m, count = 4, 10007
+    comms = make_comms(B, m)
+    sends = synth.inputs(60, m, count, "f32")
+    got = run_allreduce(B, comms, sends, "f32", "sum", inplace=True)
+    want = OC.allreduce(OP.plan_switch_allreduce(m), sends, "f32", "sum")
+    for g in got:
+        assert_bitwise(g, want)
+    # misaligned (4-byte offset) views -> scalar path
+    dsend, drecv = [], []
+    for s in sends:
+        buf = torch.empty(count + 1, dtype=torch.float32, device="cuda")
+        buf[1:] = torch.from_numpy(s).cuda()
+        dsend.append(buf[1:])
+        r = torch.full((count + 3,), float("nan"), device="cuda")
+        drecv.append(r[3:])
+    for r, c in enumerate(comms):
+        c.allreduce(dsend[r], drecv[r], op="sum")
+    torch.cuda.synchronize()
+    for x in drecv:
+        assert_bitwise(x.cpu().numpy(), want)
+
+
+def test_single_rank_is_a_copy(B):
+    comms = make_comms(B, 1)
+    s = synth.inputs(70, 1, 12345, "bf16")
+    got = run_allreduce(B, comms, s, "bf16", "sum")
+    assert_bitwise(got[0], s[0])
+
+
+# ----------------------------------------------------------------- config 1: paper's 3-GPU example
+def triangle():
+    tri, _ = OG.induced(OG.dgx1p(), [0, 1, 3])
+    return tri
+
+
+def test_config1_three_gpu_allreduce_and_broadcast(B):
+    tri = triangle()
+    comms = make_comms(B, 3, graph=B.Graph.from_pairs(3, tri[1]))
+    count = 262144                    # 1 MiB fp32 (BASELINE configs[0])
+    sends = synth.inputs(1, 3, count, "f32")
+    got = run_allreduce(B, comms, sends, "f32", "sum")
+    # the oracle's own plan (unique LP optimum: three 1/2-weight paths)
+    want = OC.allreduce(OP.plan_allreduce_graph(tri), sends, "f32", "sum")
+    for g in got:
+        assert_bitwise(g, want)
+    isends = synth.inputs(1, 3, count, "i32")
+    got = run_allreduce(B, comms, isends, "i32", "sum")
+    iwant = OC.naive_reduce(isends, "i32", "sum")
+    for g in got:
+        assert_bitwise(g, iwant)
+    # Broadcast from GPU 0 along the two chains
+    dsend = to_dev(sends[0], "f32")
+    recvs = [sentinel(count, "f32") for _ in range(3)]
+    for r, c in enumerate(comms):
+        c.broadcast(dsend if r == 0 else None, recvs[r], root=0, count=count, dtype="f32")
+    torch.cuda.synchronize()
+    for x in recvs:
+        assert_bitwise(x.cpu().numpy(), sends[0])
+    assert comms[0].plan(False, 0, count)["rate"] == [2, 1]
+
+
+# ----------------------------------------------------------------- config 2: emulated DGX-1V
+@pytest.mark.parametrize("root", [0, 3, 7])
+@pytest.mark.parametrize("count", [1, 257, 1 << 20, (1 << 22) + 5])
+def test_config2_dgx1v_broadcast(B, root, count):
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]))
+    dtype = "f32"
+    send = synth.rank_input(2, root, count, dtype)
+    dsend = to_dev(send, dtype)
+    recvs = [sentinel(count, dtype) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.broadcast(dsend if r == root else None, recvs[r], root=root, count=count, dtype=dtype)
+    torch.cuda.synchronize()
+    for x in recvs:
+        assert_bitwise(x.cpu().numpy(), send)
+    p = comms[0].plan(False, root, count)
+    assert len(p["trees"]) == 6
+    assert comms[0].stats()["last_trees"] == 6
+
+
+def test_config2_dgx1v_broadcast_bf16_inplace(B):
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]))
+    count = 300001
+    send = synth.rank_input(2, 5, count, "bf16")
+    bufs = [to_dev(send, "bf16") if r == 5 else sentinel(count, "bf16") for r in range(8)]
+    for r, c in enumerate(comms):
+        c.broadcast(bufs[r], bufs[r], root=5)
+    torch.cuda.synchronize()
+    for x in bufs:
+        assert_bitwise(to_host(x, "bf16"), send)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_dgx1v_allreduce_multilevel_tree_order(B, dtype):
+    g = OG.dgx1v()
+    G = B.Graph.from_pairs(8, g[1])
+    comms = make_comms(B, 8, graph=G, chunk_bytes=16384)
+    count = 200003
+    sends = synth.inputs(21, 8, count, dtype)
+    got = run_allreduce(B, comms, sends, dtype, "sum")
+    plan = oracle_plan_from_json(comms[0].plan(True, 0, count, dtype))
+    assert max(t["parent"].count(-1) for t in plan["trees"]) == 1
+    want = OC.allreduce(plan, sends, dtype, "sum")
+    for x in got:
+        assert_bitwise(x, want)
+    # tolerance vs the naive-order sum (north_star): |gpu - naive| <= rtol * sum|x|
+    rtol = 1e-5 if dtype == "f32" else 1e-2
+    w = OC.bf16_to_f32(want) if dtype == "bf16" else want
+    naive = OC.naive_reduce(sends, dtype, "sum")
+    nv = OC.bf16_to_f32(naive) if dtype == "bf16" else naive
+    absum = sum(np.abs(OC.bf16_to_f32(s) if dtype == "bf16" else s).astype(np.float64) for s in sends)
+    assert np.all(np.abs(w.astype(np.float64) - nv) <= rtol * absum + 1e-30)
+
+
+def test_dgx1v_allreduce_int_exact_and_fragments(B):
+    g = OG.dgx1v()
+    # fragmented allocations (config 4 secondary): induced sub-graphs
+    for nodes in ([0, 1, 4], [0, 1, 3, 4, 5, 7], [2, 3, 6, 7], [1, 4, 5, 6], list(range(8))):
+        sub, _ = OG.induced(g, nodes)
+        m = len(nodes)
+        comms = make_comms(B, m, graph=B.Graph.from_pairs(m, sub[1]), chunk_bytes=8192)
+        count = 50021
+        sends = synth.inputs(4, m, count, "i32")
+        got = run_allreduce(B, comms, sends, "i32", "sum")
+        want = OC.naive_reduce(sends, "i32", "sum")
+        for x in got:
+            assert_bitwise(x, want)
+        mx = run_allreduce(B, comms, synth.inputs(5, m, count, "f32"), "f32", "max")
+        wmx = OC.naive_reduce(synth.inputs(5, m, count, "f32"), "f32", "max")
+        for x in mx:
+            assert_bitwise(x, wmx)
+        for c in comms:
+            c.destroy()
+
+
+def test_switch_broadcast_both_variants(B):
+    m = 8
+    for count, dtype in ((1000, "f32"), (3 * (1 << 20) + 1, "bf16")):   # star / two-level trees
+        comms = make_comms(B, m)
+        for root in (0, 6):
+            send = synth.rank_input(9, root, count, dtype)
+            dsend = to_dev(send, dtype)
+            recvs = [sentinel(count, dtype) for _ in range(m)]
+            for r, c in enumerate(comms):
+                c.broadcast(dsend if r == root else None, recvs[r], root=root, count=count, dtype=dtype)
+            torch.cuda.synchronize()
+            for x in recvs:
+                assert_bitwise(to_host(x, dtype), send)
+
+
+def test_back_to_back_calls_and_epochs(B):
+    # many calls without host sync: flags are epoch-monotonic, never reset
+    m, count = 8, 65537
+    comms = make_comms(B, m, chunk_bytes=8192)
+    sends = synth.inputs(80, m, count, "f32")
+    dsend = [to_dev(s, "f32") for s in sends]
+    outs = [[torch.empty_like(d) for d in dsend] for _ in range(6)]
+    for k in range(6):
+        for r, c in enumerate(comms):
+            c.allreduce(dsend[r], outs[k][r], op="sum")
+    torch.cuda.synchronize()
+    want = OC.naive_reduce(sends, "f32", "sum")
+    for k in range(6):
+        for x in outs[k]:
+            assert_bitwise(x.cpu().numpy(), want)
+
+
+def test_errors(B):
+    comms = make_comms(B, 2)
+    x = torch.zeros(16, device="cuda")
+    with pytest.raises(B.BlinkError) as e:
+        comms[0].broadcast(x, x, root=7)
+    assert e.value.code == 4
+    comms[0].allreduce(x, x, op="sum")
+    with pytest.raises(B.BlinkError) as e:          # rank 1 disagrees on count
+        comms[1].allreduce(x[:8], x[:8], op="sum")
+    assert e.value.code == 5
+
+
+# ----------------------------------------------------------------- full size, bench launch config
+def test_fullsize_config3_sampled(B):
+    """BASELINE config 3 at the bench size: 8 ranks x 256 MiB fp32, the exact
+    launch configuration bench.py times; 65536 sampled outputs checked against
+    the oracle's naive-order (= one-hop tree-order) sum."""
+    import bench
+    m, count = 8, bench.DEFAULT_COUNT
+    comms = make_comms(B, m)
+    sends = [synth.device_input(3, r, count, "f32") for r in range(m)]
+    recvs = [torch.empty_like(s) for s in sends]
+    for r, c in enumerate(comms):
+        c.allreduce(sends[r], recvs[r], op="sum")
+    torch.cuda.synchronize()
+    idx = torch.from_numpy(np.random.default_rng(0).integers(0, count, 65536)).cuda()
+    cols = [s[idx].cpu().numpy() for s in sends]
+    want = OC.naive_reduce(cols, "f32", "sum")
+    for r in range(m):
+        assert_bitwise(recvs[r][idx].cpu().numpy(), want)
+    # the last element and a tail window
+    tail = [s[-37:].cpu().numpy() for s in sends]
+    assert_bitwise(recvs[0][-37:].cpu().numpy(), OC.naive_reduce(tail, "f32", "sum"))
