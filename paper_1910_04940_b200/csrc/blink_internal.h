@@ -107,7 +107,7 @@ struct LaunchArgs {
   int op;                    // blink_redop_t
   int exit_wait;             // 1 when ranks live in different launches
   int bcast_root;            // Broadcast root rank
-  int pad;
+  int use_tma;               // stage aligned bodies through TMA bulk copies
   uint64_t epoch;
   uint64_t timeout_ns;
   int* err;                  // host-mapped error word (0 = ok)

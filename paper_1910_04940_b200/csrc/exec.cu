@@ -277,6 +277,141 @@ __device__ __forceinline__ void copy_range(const char* src, char* const* dsts, i
   }
 }
 
+// ------------------------------------------------------------------ TMA staging
+// Bulk asynchronous copies (cp.async.bulk, the 1-D TMA path) move tiles of
+// every source into a shared-memory ring; an mbarrier per stage counts the
+// arriving bytes.  Bytes in flight are set by the ring size, not by registers.
+constexpr int kSmemBytes = 96 * 1024;  // dynamic smem per CTA (2 CTAs / SM)
+constexpr int kMaxStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+
+struct Ring {
+  char* buf;        // kSmemBytes
+  uint64_t* full;   // kMaxStages mbarriers
+  int stages;       // stages in use
+  int tile;         // bytes per source per stage
+  uint32_t it;      // tiles consumed so far (phase tracking)
+};
+
+// Reduce the 16-byte-aligned body [b0, b0 + body) with TMA-staged sources and
+// 128-bit LSU stores to every destination.
+template <int DT, int OP>
+__device__ __forceinline__ void reduce_body_tma(const char* const* srcs, int nsrc, char* const* dsts,
+                                                int ndst, int64_t b0, int64_t body, Ring& R) {
+  const int T = blockDim.x;
+  const int ntiles = int((body + R.tile - 1) / R.tile);
+  auto issue = [&](int t) {
+    const uint32_t g = R.it + t;
+    const int s = int(g % uint32_t(R.stages));
+    const int64_t off = int64_t(t) * R.tile;
+    const uint32_t tb = uint32_t(min(int64_t(R.tile), body - off));
+    mbar_expect_tx(&R.full[s], tb * uint32_t(nsrc));
+    char* st = R.buf + size_t(s) * R.tile * nsrc;
+    for (int k = 0; k < nsrc; ++k) tma_load(st + size_t(k) * R.tile, srcs[k] + b0 + off, tb, &R.full[s]);
+  };
+  if (threadIdx.x == 0) {
+    fence_proxy_async();
+    for (int t = 0; t < min(R.stages, ntiles); ++t) issue(t);
+  }
+  for (int t = 0; t < ntiles; ++t) {
+    const uint32_t g = R.it + t;
+    const int s = int(g % uint32_t(R.stages));
+    mbar_wait(&R.full[s], (g / uint32_t(R.stages)) & 1u);
+    const int64_t off = int64_t(t) * R.tile;
+    const int vecs = int(min(int64_t(R.tile), body - off) >> 4);
+    const uint4* st = reinterpret_cast<const uint4*>(R.buf + size_t(s) * R.tile * nsrc);
+    const int vstride = R.tile >> 4;
+    for (int v = threadIdx.x; v < vecs; v += T) {
+      Acc<DT> acc;
+      widen<DT>(acc, st[v]);
+      for (int k = 1; k < nsrc; ++k) combine<DT, OP>(acc, st[k * vstride + v]);
+      const uint4 o = narrow<DT>(acc);
+      const int64_t gb = b0 + off + int64_t(v) * 16;
+      for (int d = 0; d < ndst; ++d) __stcg(reinterpret_cast<uint4*>(dsts[d] + gb), o);
+    }
+    __syncthreads();  // stage s fully read
+    if (threadIdx.x == 0 && t + R.stages < ntiles) issue(t + R.stages);
+  }
+  R.it += ntiles;
+}
+
+// Copy the 16-byte-aligned body [b0, b0 + body) from src to every dst with TMA
+// loads into the ring and TMA bulk stores out of it (one thread drives it).
+__device__ __forceinline__ void copy_body_tma(const char* src, char* const* dsts, int ndst, int64_t b0,
+                                              int64_t body, Ring& R) {
+  if (threadIdx.x != 0) return;
+  const int ntiles = int((body + R.tile - 1) / R.tile);
+  auto issue = [&](int t) {
+    const uint32_t g = R.it + t;
+    const int s = int(g % uint32_t(R.stages));
+    const int64_t off = int64_t(t) * R.tile;
+    const uint32_t tb = uint32_t(min(int64_t(R.tile), body - off));
+    mbar_expect_tx(&R.full[s], tb);
+    tma_load(R.buf + size_t(s) * R.tile, src + b0 + off, tb, &R.full[s]);
+  };
+  fence_proxy_async();
+  for (int t = 0; t < min(R.stages, ntiles); ++t) issue(t);
+  for (int t = 0; t < ntiles; ++t) {
+    const uint32_t g = R.it + t;
+    const int s = int(g % uint32_t(R.stages));
+    mbar_wait(&R.full[s], (g / uint32_t(R.stages)) & 1u);
+    const int64_t off = int64_t(t) * R.tile;
+    const uint32_t tb = uint32_t(min(int64_t(R.tile), body - off));
+    for (int d = 0; d < ndst; ++d) tma_store(dsts[d] + b0 + off, R.buf + size_t(s) * R.tile, tb);
+    tma_commit();
+    // the previous tile's stores have read their stage: refill it
+    if (t >= 1) {
+      tma_wait_read<1>();
+      if (t - 1 + R.stages < ntiles) issue(t - 1 + R.stages);
+    }
+  }
+  tma_wait_all();       // every store performed before the flag is released
+  fence_proxy_async();
+  R.it += ntiles;
+}
+
 // ------------------------------------------------------------------ waits
 struct Ctl {
   uint64_t epoch;
@@ -308,7 +443,10 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
   __shared__ const char* srcs[kMaxRanks + 1];
   __shared__ char* dsts[kMaxRanks + 1];
   __shared__ int s_nsrc, s_ndst, s_ok;
+  __shared__ __align__(8) uint64_t s_full[kMaxStages];
+  extern __shared__ __align__(128) char s_ring[];
   const DevTask t = a.tasks[blockIdx.x];
+  Ring ring{s_ring, s_full, 1, 16, 0};
   const int v = t.rank;
   const Ctl ctl{a.epoch, a.timeout_ns, a.err};
   uint64_t* myflags = a.flags[v];
@@ -353,8 +491,19 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
       s_nsrc = ns;
       s_ndst = nd;
       s_ok = ok;
+      if (VEC)
+        for (int k = 0; k < kMaxStages; ++k) mbar_init(&s_full[k], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (VEC) {
+      // ring geometry: tile bytes per source, stages that fit kSmemBytes
+      const int ns = t.role == kRoleReduce ? s_nsrc : 1;
+      int tile = ns == 1 ? 16384 : (ns <= 4 ? 8192 : (ns <= 8 ? 4096 : 2048));
+      int stages = kSmemBytes / (tile * ns);
+      ring.tile = tile;
+      ring.stages = stages < 1 ? 1 : (stages > kMaxStages ? kMaxStages : stages);
+    }
     bool alive = s_ok;
     __syncthreads();  // everyone read s_ok before thread 0 may overwrite it
     const bool need_bflag = (t.role == kRoleBcast) && !((a.coll == kBroadcast) && is_root);
@@ -375,10 +524,20 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
       if (!alive) break;
       const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
       const int64_t b1 = min(tr.hi, b0 + tr.chunk);
-      if (t.role == kRoleReduce)
+      if (VEC && a.use_tma) {
+        const int64_t body = ((b1 - b0) >> 4) << 4;
+        if (t.role == kRoleReduce) {
+          reduce_body_tma<DT, OP>(srcs, s_nsrc, dsts, s_ndst, b0, body, ring);
+          reduce_range<DT, OP, false>(srcs, s_nsrc, dsts, s_ndst, b0 + body, b1);
+        } else {
+          copy_body_tma(srcs[0], dsts, s_ndst, b0, body, ring);
+          copy_range<false>(srcs[0], dsts, s_ndst, b0 + body, b1);
+        }
+      } else if (t.role == kRoleReduce) {
         reduce_range<DT, OP, VEC>(srcs, s_nsrc, dsts, s_ndst, b0, b1);
-      else
+      } else {
         copy_range<VEC>(srcs[0], dsts, s_ndst, b0, b1);
+      }
       __syncthreads();  // every thread's stores of chunk c are issued
       if (threadIdx.x == 0) {
         fence_sys();
@@ -457,7 +616,15 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = vec ? kSmemBytes : 0;
+  static bool attr_set[2][3][4][2] = {};
+  bool& done = attr_set[a.coll][a.dtype][a.op][vec];
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         vec ? kSmemBytes : 0);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -470,7 +637,10 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
 int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll) {
   ExecFn fn = pick(coll, dtype, op, vec);
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, 0) != cudaSuccess) return 0;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, vec ? kSmemBytes : 0);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, vec ? kSmemBytes : 0) !=
+      cudaSuccess)
+    return 0;
   return n;
 }
 

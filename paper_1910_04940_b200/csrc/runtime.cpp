@@ -361,6 +361,15 @@ int co_resident_budget(blink_comm_t comm, int device, int dtype, int op, int col
   return cap;
 }
 
+// BLINK_TMA=0 selects the register (LSU) data path instead of TMA staging.
+int use_tma() {
+  static int v = [] {
+    const char* e = getenv("BLINK_TMA");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtype, int op,
@@ -436,6 +445,7 @@ blink_result_t clique_launch(Clique* q) {
     a.op = q->op;
     a.exit_wait = all_one_launch ? 0 : 1;
     a.bcast_root = q->coll == kBroadcast ? q->root : -1;
+    a.use_tma = use_tma();
     a.epoch = q->epoch;
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
     a.err = q->err_dev[dev];
@@ -608,6 +618,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.op = op;
   a.exit_wait = 1;
   a.bcast_root = coll == kBroadcast ? root : -1;
+  a.use_tma = use_tma();
   a.epoch = comm->epoch;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
   a.err = comm->err_dev;
