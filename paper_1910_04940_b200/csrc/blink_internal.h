@@ -108,6 +108,8 @@ struct LaunchArgs {
   int exit_wait;             // 1 when ranks live in different launches
   int bcast_root;            // Broadcast root rank
   int use_tma;               // stage aligned bodies through TMA bulk copies
+  int smem_bytes;            // dynamic shared memory of the TMA ring
+  int tile_bytes;            // 0 = default tile per source
   uint64_t epoch;
   uint64_t timeout_ns;
   int* err;                  // host-mapped error word (0 = ok)
@@ -119,8 +121,9 @@ struct LaunchArgs {
 // exec.cu
 cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,
                         bool cooperative);
+constexpr int kMaxSmemBytes = 224 * 1024;  // + static smem <= 227 KB opt-in
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream);
-int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll);
+int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll, int smem_bytes);
 
 // plan.cpp -------------------------------------------------------------
 struct Graph {

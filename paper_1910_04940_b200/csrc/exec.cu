@@ -281,7 +281,7 @@ __device__ __forceinline__ void copy_range(const char* src, char* const* dsts, i
 // Bulk asynchronous copies (cp.async.bulk, the 1-D TMA path) move tiles of
 // every source into a shared-memory ring; an mbarrier per stage counts the
 // arriving bytes.  Bytes in flight are set by the ring size, not by registers.
-constexpr int kSmemBytes = 96 * 1024;  // dynamic smem per CTA (2 CTAs / SM)
+constexpr int kOutBufs = 3;            // output tiles for TMA bulk stores
 constexpr int kMaxStages = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -327,91 +327,6 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
 
-struct Ring {
-  char* buf;        // kSmemBytes
-  uint64_t* full;   // kMaxStages mbarriers
-  int stages;       // stages in use
-  int tile;         // bytes per source per stage
-  uint32_t it;      // tiles consumed so far (phase tracking)
-};
-
-// Reduce the 16-byte-aligned body [b0, b0 + body) with TMA-staged sources and
-// 128-bit LSU stores to every destination.
-template <int DT, int OP>
-__device__ __forceinline__ void reduce_body_tma(const char* const* srcs, int nsrc, char* const* dsts,
-                                                int ndst, int64_t b0, int64_t body, Ring& R) {
-  const int T = blockDim.x;
-  const int ntiles = int((body + R.tile - 1) / R.tile);
-  auto issue = [&](int t) {
-    const uint32_t g = R.it + t;
-    const int s = int(g % uint32_t(R.stages));
-    const int64_t off = int64_t(t) * R.tile;
-    const uint32_t tb = uint32_t(min(int64_t(R.tile), body - off));
-    mbar_expect_tx(&R.full[s], tb * uint32_t(nsrc));
-    char* st = R.buf + size_t(s) * R.tile * nsrc;
-    for (int k = 0; k < nsrc; ++k) tma_load(st + size_t(k) * R.tile, srcs[k] + b0 + off, tb, &R.full[s]);
-  };
-  if (threadIdx.x == 0) {
-    fence_proxy_async();
-    for (int t = 0; t < min(R.stages, ntiles); ++t) issue(t);
-  }
-  for (int t = 0; t < ntiles; ++t) {
-    const uint32_t g = R.it + t;
-    const int s = int(g % uint32_t(R.stages));
-    mbar_wait(&R.full[s], (g / uint32_t(R.stages)) & 1u);
-    const int64_t off = int64_t(t) * R.tile;
-    const int vecs = int(min(int64_t(R.tile), body - off) >> 4);
-    const uint4* st = reinterpret_cast<const uint4*>(R.buf + size_t(s) * R.tile * nsrc);
-    const int vstride = R.tile >> 4;
-    for (int v = threadIdx.x; v < vecs; v += T) {
-      Acc<DT> acc;
-      widen<DT>(acc, st[v]);
-      for (int k = 1; k < nsrc; ++k) combine<DT, OP>(acc, st[k * vstride + v]);
-      const uint4 o = narrow<DT>(acc);
-      const int64_t gb = b0 + off + int64_t(v) * 16;
-      for (int d = 0; d < ndst; ++d) __stcg(reinterpret_cast<uint4*>(dsts[d] + gb), o);
-    }
-    __syncthreads();  // stage s fully read
-    if (threadIdx.x == 0 && t + R.stages < ntiles) issue(t + R.stages);
-  }
-  R.it += ntiles;
-}
-
-// Copy the 16-byte-aligned body [b0, b0 + body) from src to every dst with TMA
-// loads into the ring and TMA bulk stores out of it (one thread drives it).
-__device__ __forceinline__ void copy_body_tma(const char* src, char* const* dsts, int ndst, int64_t b0,
-                                              int64_t body, Ring& R) {
-  if (threadIdx.x != 0) return;
-  const int ntiles = int((body + R.tile - 1) / R.tile);
-  auto issue = [&](int t) {
-    const uint32_t g = R.it + t;
-    const int s = int(g % uint32_t(R.stages));
-    const int64_t off = int64_t(t) * R.tile;
-    const uint32_t tb = uint32_t(min(int64_t(R.tile), body - off));
-    mbar_expect_tx(&R.full[s], tb);
-    tma_load(R.buf + size_t(s) * R.tile, src + b0 + off, tb, &R.full[s]);
-  };
-  fence_proxy_async();
-  for (int t = 0; t < min(R.stages, ntiles); ++t) issue(t);
-  for (int t = 0; t < ntiles; ++t) {
-    const uint32_t g = R.it + t;
-    const int s = int(g % uint32_t(R.stages));
-    mbar_wait(&R.full[s], (g / uint32_t(R.stages)) & 1u);
-    const int64_t off = int64_t(t) * R.tile;
-    const uint32_t tb = uint32_t(min(int64_t(R.tile), body - off));
-    for (int d = 0; d < ndst; ++d) tma_store(dsts[d] + b0 + off, R.buf + size_t(s) * R.tile, tb);
-    tma_commit();
-    // the previous tile's stores have read their stage: refill it
-    if (t >= 1) {
-      tma_wait_read<1>();
-      if (t - 1 + R.stages < ntiles) issue(t - 1 + R.stages);
-    }
-  }
-  tma_wait_all();       // every store performed before the flag is released
-  fence_proxy_async();
-  R.it += ntiles;
-}
-
 // ------------------------------------------------------------------ waits
 struct Ctl {
   uint64_t epoch;
@@ -438,18 +353,213 @@ __device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
 __device__ __forceinline__ void signal(uint64_t* p, uint64_t epoch) { st_release_sys(p, epoch); }
 
 // ------------------------------------------------------------------ the kernel
+struct Shared {
+  const char* srcs[kMaxRanks + 1];
+  char* dsts[kMaxRanks + 1];
+  int nsrc, ndst, ok;
+  volatile int abort;
+  uint64_t full[kMaxStages], empty[kMaxStages], ofull[kOutBufs], oempty[kOutBufs];
+};
+
+// mbarrier wait that gives up when the CTA aborted (flag timeout elsewhere).
+__device__ __forceinline__ bool mbar_wait_or_abort(uint64_t* bar, uint32_t phase, Shared& sh) {
+  for (int spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) return true;
+    if ((spin & 63) == 63 && sh.abort) return false;
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Per-chunk readiness (a5): the producer acquires the chunk's inputs.
+__device__ __forceinline__ bool wait_chunk_inputs(const LaunchArgs& a, const DevTask& t, int c,
+                                                  bool need_bflag, const Ctl& ctl) {
+  uint64_t* myflags = a.flags[t.rank];
+  bool ok = true;
+  if (t.role == kRoleReduce) {
+    const uint32_t internal = t.children & ~t.leafmask;
+    for (int u = 0; u < a.nranks && ok; ++u)
+      if ((internal >> u) & 1u) ok = wait_ge(myflags + pflag_idx(t.tree, u, c), ctl);
+  } else if (need_bflag) {
+    ok = wait_ge(myflags + bflag_idx(t.tree, c), ctl);
+  }
+  return ok;
+}
+
+// Publish chunk c (all its stores are complete and fenced by the caller).
+__device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask& t, int c, bool is_root) {
+  fence_sys();
+  if (t.role == kRoleReduce && !is_root) {
+    signal(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), a.epoch);
+  } else {
+    for (int u = 0; u < a.nranks; ++u)
+      if ((t.children >> u) & 1u) signal(a.flags[u] + bflag_idx(t.tree, c), a.epoch);
+  }
+}
+
+// Warp-specialised TMA pipeline over this CTA's chunks (aligned buffers):
+//   warp 0 lane 0  producer: acquires the chunk flags, issues cp.async.bulk
+//                  loads of every source tile into the stage ring (full[s]);
+//   warps 2..      consumers (REDUCE only): combine the stage's source tiles
+//                  in ascending-rank order into an output tile (ofull[o]);
+//   warp 1 lane 0  store: cp.async.bulk stores of the output tile (or, for a
+//                  copy, of the stage itself) to every destination, then at
+//                  chunk end waits for completion and releases the flags.
+// A chunk with a sub-16-byte tail (only the last chunk of the last tree) runs
+// on all threads with 128-bit LSU accesses instead.
+template <int DT, int OP>
+__device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
+                       bool need_bflag, Shared& sh, char* ring) {
+  const Ctl ctl{a.epoch, a.timeout_ns, a.err};
+  const bool reduce = t.role == kRoleReduce;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncons = reduce ? (blockDim.x >> 5) - 2 : 0;
+  const int nsrc = sh.nsrc, ndst = sh.ndst;
+  const int ns = reduce ? nsrc : 1;
+  int tile = ns == 1 ? 32768 : (ns <= 8 ? 8192 : 4096);
+  if (a.tile_bytes > 0) tile = ns == 1 ? 4 * a.tile_bytes : a.tile_bytes;
+  const int avail = a.smem_bytes - (reduce ? kOutBufs * tile : 0);
+  const int stages = max(1, min(kMaxStages, avail / (tile * ns)));
+  char* out = ring + avail;
+  const uint32_t NS = uint32_t(stages), K = uint32_t(kOutBufs);
+  uint32_t g = 0;  // tile sequence number (identical in every role)
+  for (int c = t.cta_idx; c < tr.nchunks; c += t.cta_cnt) {
+    const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
+    const int64_t b1 = min(tr.hi, b0 + tr.chunk);
+    const int64_t body = ((b1 - b0) >> 4) << 4;
+    if (body != b1 - b0) {
+      // ---- tail chunk: every thread, LSU path
+      if (threadIdx.x == 0) sh.ok = !sh.abort && wait_chunk_inputs(a, t, c, need_bflag, ctl);
+      __syncthreads();
+      const bool ok = sh.ok;
+      if (ok) {
+        if (reduce)
+          reduce_range<DT, OP, true>(sh.srcs, nsrc, sh.dsts, ndst, b0, b1);
+        else
+          copy_range<true>(sh.srcs[0], sh.dsts, ndst, b0, b1);
+      }
+      __syncthreads();
+      if (!ok) {
+        if (threadIdx.x == 0) sh.abort = 1;
+        break;
+      }
+      if (threadIdx.x == 0) signal_chunk(a, t, c, is_root);
+      continue;
+    }
+    const int ntiles = int((body + tile - 1) / tile);
+    if (warp == 0 && lane == 0) {
+      // ---------------- producer
+      if (sh.abort || !wait_chunk_inputs(a, t, c, need_bflag, ctl)) {
+        sh.abort = 1;
+      } else {
+        fence_proxy_async();
+        for (int k = 0; k < ntiles; ++k) {
+          const uint32_t gg = g + k, s = gg % NS;
+          if (!mbar_wait_or_abort(&sh.empty[s], ((gg / NS) & 1u) ^ 1u, sh)) break;
+          const int64_t off = int64_t(k) * tile;
+          const uint32_t tb = uint32_t(min(int64_t(tile), body - off));
+          mbar_expect_tx(&sh.full[s], tb * uint32_t(ns));
+          char* st = ring + size_t(s) * tile * ns;
+          for (int j = 0; j < ns; ++j) tma_load(st + size_t(j) * tile, sh.srcs[j] + b0 + off, tb, &sh.full[s]);
+        }
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------- store
+      bool ok = true;
+      for (int k = 0; k < ntiles && ok; ++k) {
+        const uint32_t gg = g + k;
+        const int64_t off = int64_t(k) * tile;
+        const uint32_t tb = uint32_t(min(int64_t(tile), body - off));
+        if (reduce) {
+          const uint32_t o = gg % K;
+          if (!(ok = mbar_wait_or_abort(&sh.ofull[o], (gg / K) & 1u, sh))) break;
+          for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, out + size_t(o) * tile, tb);
+          tma_commit();
+          tma_wait_read<0>();
+          mbar_arrive(&sh.oempty[o]);
+        } else {
+          const uint32_t s = gg % NS;
+          if (!(ok = mbar_wait_or_abort(&sh.full[s], (gg / NS) & 1u, sh))) break;
+          for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, ring + size_t(s) * tile, tb);
+          tma_commit();
+          tma_wait_read<0>();
+          mbar_arrive(&sh.empty[s]);
+        }
+      }
+      tma_wait_all();
+      fence_proxy_async();
+      if (ok) signal_chunk(a, t, c, is_root);
+    } else if (reduce && warp >= 2) {
+      // ---------------- consumers
+      const int ct = threadIdx.x - 64, CT = ncons * 32;
+      for (int k = 0; k < ntiles; ++k) {
+        const uint32_t gg = g + k, s = gg % NS, o = gg % K;
+        if (!mbar_wait_or_abort(&sh.full[s], (gg / NS) & 1u, sh)) break;
+        if (!mbar_wait_or_abort(&sh.oempty[o], ((gg / K) & 1u) ^ 1u, sh)) break;
+        const int64_t off = int64_t(k) * tile;
+        const int vecs = int(min(int64_t(tile), body - off) >> 4);
+        const uint4* st = reinterpret_cast<const uint4*>(ring + size_t(s) * tile * ns);
+        uint4* ob = reinterpret_cast<uint4*>(out + size_t(o) * tile);
+        const int vstride = tile >> 4;
+        for (int vv = ct; vv < vecs; vv += CT) {
+          Acc<DT> acc;
+          widen<DT>(acc, st[vv]);
+          for (int j = 1; j < nsrc; ++j) combine<DT, OP>(acc, st[j * vstride + vv]);
+          ob[vv] = narrow<DT>(acc);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sh.empty[s]);
+          mbar_arrive(&sh.ofull[o]);
+        }
+      }
+    }
+    g += uint32_t(ntiles);
+    if (sh.abort) break;
+  }
+  __syncthreads();
+}
+
+// Register/LSU path (misaligned buffers, BLINK_TMA=0): all threads per chunk.
+template <int DT, int OP, bool VEC>
+__device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
+                        bool need_bflag, Shared& sh) {
+  const Ctl ctl{a.epoch, a.timeout_ns, a.err};
+  for (int c = t.cta_idx; c < tr.nchunks; c += t.cta_cnt) {
+    if (threadIdx.x == 0) sh.ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
+    __syncthreads();
+    const bool ok = sh.ok;
+    if (ok) {
+      const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
+      const int64_t b1 = min(tr.hi, b0 + tr.chunk);
+      if (t.role == kRoleReduce)
+        reduce_range<DT, OP, VEC>(sh.srcs, sh.nsrc, sh.dsts, sh.ndst, b0, b1);
+      else
+        copy_range<VEC>(sh.srcs[0], sh.dsts, sh.ndst, b0, b1);
+    }
+    __syncthreads();  // every thread's stores of chunk c are issued (and sh.ok read)
+    if (!ok) break;
+    if (threadIdx.x == 0) signal_chunk(a, t, c, is_root);
+  }
+}
+
 template <int DT, int OP, bool VEC>
 __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
-  __shared__ const char* srcs[kMaxRanks + 1];
-  __shared__ char* dsts[kMaxRanks + 1];
-  __shared__ int s_nsrc, s_ndst, s_ok;
-  __shared__ __align__(8) uint64_t s_full[kMaxStages];
+  __shared__ Shared sh;
   extern __shared__ __align__(128) char s_ring[];
   const DevTask t = a.tasks[blockIdx.x];
-  Ring ring{s_ring, s_full, 1, 16, 0};
   const int v = t.rank;
   const Ctl ctl{a.epoch, a.timeout_ns, a.err};
   uint64_t* myflags = a.flags[v];
+  const bool ws = VEC && a.use_tma && blockDim.x >= 128;
 
   // entry: my send is ready and my recv may be overwritten (epoch e)
   if (t.do_entry && threadIdx.x == 0) {
@@ -468,86 +578,49 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
         const uint32_t ops = t.children | (1u << v);
         for (int u = 0; u < a.nranks; ++u) {
           if (!((ops >> u) & 1u)) continue;
-          srcs[ns++] = (u == v || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
+          sh.srcs[ns++] = (u == v || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
         }
-        dsts[nd++] = a.recv[v];
+        sh.dsts[nd++] = a.recv[v];
         if (is_root)
           for (int u = 0; u < a.nranks; ++u)
-            if ((t.children >> u) & 1u) dsts[nd++] = a.recv[u];
+            if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
         // leaf children: their send is ready once they entered
         for (int u = 0; u < a.nranks && ok; ++u)
           if ((t.leafmask >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       } else {
         const bool src_root = (a.coll == kBroadcast) && is_root;
-        srcs[ns++] = src_root ? a.send[v] : a.recv[v];
-        if (src_root && a.send[v] != a.recv[v]) dsts[nd++] = a.recv[v];
+        sh.srcs[ns++] = src_root ? a.send[v] : a.recv[v];
+        if (src_root && a.send[v] != a.recv[v]) sh.dsts[nd++] = a.recv[v];
         for (int u = 0; u < a.nranks; ++u)
-          if ((t.children >> u) & 1u) dsts[nd++] = a.recv[u];
+          if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
         // Broadcast pushes into children's recv: they must have entered
         if (a.coll == kBroadcast)
           for (int u = 0; u < a.nranks && ok; ++u)
             if ((t.children >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       }
-      s_nsrc = ns;
-      s_ndst = nd;
-      s_ok = ok;
-      if (VEC)
-        for (int k = 0; k < kMaxStages; ++k) mbar_init(&s_full[k], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      sh.nsrc = ns;
+      sh.ndst = nd;
+      sh.abort = ok ? 0 : 1;
+      if (ws) {
+        const uint32_t ncw = t.role == kRoleReduce ? (blockDim.x >> 5) - 2 : 1;
+        for (int k = 0; k < kMaxStages; ++k) {
+          mbar_init(&sh.full[k], 1);
+          mbar_init(&sh.empty[k], ncw);
+        }
+        for (int k = 0; k < kOutBufs; ++k) {
+          mbar_init(&sh.ofull[k], ncw);
+          mbar_init(&sh.oempty[k], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
     }
     __syncthreads();
-    if (VEC) {
-      // ring geometry: tile bytes per source, stages that fit kSmemBytes
-      const int ns = t.role == kRoleReduce ? s_nsrc : 1;
-      int tile = ns == 1 ? 16384 : (ns <= 4 ? 8192 : (ns <= 8 ? 4096 : 2048));
-      int stages = kSmemBytes / (tile * ns);
-      ring.tile = tile;
-      ring.stages = stages < 1 ? 1 : (stages > kMaxStages ? kMaxStages : stages);
-    }
-    bool alive = s_ok;
-    __syncthreads();  // everyone read s_ok before thread 0 may overwrite it
     const bool need_bflag = (t.role == kRoleBcast) && !((a.coll == kBroadcast) && is_root);
-    for (int c = t.cta_idx; alive && c < tr.nchunks; c += t.cta_cnt) {
-      if (threadIdx.x == 0) {
-        bool ok = true;
-        if (t.role == kRoleReduce) {
-          const uint32_t internal = t.children & ~t.leafmask;
-          for (int u = 0; u < a.nranks && ok; ++u)
-            if ((internal >> u) & 1u) ok = wait_ge(myflags + pflag_idx(t.tree, u, c), ctl);
-        } else if (need_bflag) {
-          ok = wait_ge(myflags + bflag_idx(t.tree, c), ctl);
-        }
-        s_ok = ok;
-      }
-      __syncthreads();
-      alive = s_ok;
-      if (!alive) break;
-      const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
-      const int64_t b1 = min(tr.hi, b0 + tr.chunk);
-      if (VEC && a.use_tma) {
-        const int64_t body = ((b1 - b0) >> 4) << 4;
-        if (t.role == kRoleReduce) {
-          reduce_body_tma<DT, OP>(srcs, s_nsrc, dsts, s_ndst, b0, body, ring);
-          reduce_range<DT, OP, false>(srcs, s_nsrc, dsts, s_ndst, b0 + body, b1);
-        } else {
-          copy_body_tma(srcs[0], dsts, s_ndst, b0, body, ring);
-          copy_range<false>(srcs[0], dsts, s_ndst, b0 + body, b1);
-        }
-      } else if (t.role == kRoleReduce) {
-        reduce_range<DT, OP, VEC>(srcs, s_nsrc, dsts, s_ndst, b0, b1);
-      } else {
-        copy_range<VEC>(srcs[0], dsts, s_ndst, b0, b1);
-      }
-      __syncthreads();  // every thread's stores of chunk c are issued
-      if (threadIdx.x == 0) {
-        fence_sys();
-        if (t.role == kRoleReduce && !is_root) {
-          signal(a.flags[t.parent] + pflag_idx(t.tree, v, c), a.epoch);
-        } else {
-          for (int u = 0; u < a.nranks; ++u)
-            if ((t.children >> u) & 1u) signal(a.flags[u] + bflag_idx(t.tree, c), a.epoch);
-        }
-      }
+    if (!sh.abort) {
+      if (ws)
+        run_ws<DT, OP>(a, t, tr, is_root, need_bflag, sh, s_ring);
+      else
+        run_lsu<DT, OP, VEC>(a, t, tr, is_root, need_bflag, sh);
     }
   }
 
@@ -616,12 +689,12 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = vec ? kSmemBytes : 0;
+  cfg.dynamicSmemBytes = vec ? a.smem_bytes : 0;
   static bool attr_set[2][3][4][2] = {};
   bool& done = attr_set[a.coll][a.dtype][a.op][vec];
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         vec ? kSmemBytes : 0);
+                                         vec ? kMaxSmemBytes : 0);
     if (e != cudaSuccess) return e;
     done = true;
   }
@@ -634,11 +707,11 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   return cudaLaunchKernelEx(&cfg, fn, a);
 }
 
-int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll) {
+int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll, int smem_bytes) {
   ExecFn fn = pick(coll, dtype, op, vec);
   int n = 0;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, vec ? kSmemBytes : 0);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, vec ? kSmemBytes : 0) !=
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, vec ? kMaxSmemBytes : 0);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, vec ? smem_bytes : 0) !=
       cudaSuccess)
     return 0;
   return n;

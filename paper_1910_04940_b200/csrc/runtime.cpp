@@ -155,8 +155,16 @@ blink_result_t fail(blink_comm_t comm, blink_result_t r, const std::string& msg)
 blink_config_t resolve_cfg(const blink_config_t* c) {
   blink_config_t d;
   blink_config_default(&d);
-  if (!c) return d;
+  blink_config_t tmp;
+  if (!c) {
+    tmp = d;
+    c = &tmp;
+  }
   blink_config_t r = *c;
+  // environment overrides (tuning): BLINK_THREADS, BLINK_CTAS, BLINK_CHUNK_BYTES
+  if (const char* e = getenv("BLINK_THREADS")) r.threads = atoi(e);
+  if (const char* e = getenv("BLINK_CTAS")) r.ctas = atoi(e);
+  if (const char* e = getenv("BLINK_CHUNK_BYTES")) r.chunk_bytes = size_t(atoll(e));
   if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
   if (!(r.ilp_gap > 0 && r.ilp_gap < 1)) r.ilp_gap = d.ilp_gap;
   if (r.threads <= 0) r.threads = d.threads;
@@ -350,24 +358,46 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
   return BLINK_SUCCESS;
 }
 
+// Data path: BLINK_TMA=0 register/LSU loads and stores, 1 TMA loads + LSU
+// stores, 2 TMA loads + TMA bulk stores (default).
+int use_tma() {
+  static int v = [] {
+    const char* e = getenv("BLINK_TMA");
+    if (!e || !e[0]) return 2;
+    return e[0] == '0' ? 0 : (e[0] == '1' ? 1 : 2);
+  }();
+  return v;
+}
+
+// Shared-memory ring size and tile (tuning knobs; defaults from bench sweeps).
+int smem_bytes() {
+  static int v = [] {
+    const char* e = getenv("BLINK_SMEM_KB");
+    int kb = e ? atoi(e) : 200;
+    if (kb < 16) kb = 16;
+    if (kb > 224) kb = 224;
+    return kb * 1024;
+  }();
+  return v;
+}
+int tile_bytes() {
+  static int v = [] {
+    const char* e = getenv("BLINK_TILE");
+    int t = e ? atoi(e) : 0;
+    return t > 0 ? (t + 15) / 16 * 16 : 0;
+  }();
+  return v;
+}
+
 int co_resident_budget(blink_comm_t comm, int device, int dtype, int op, int coll) {
   DeviceGuard g(device);
-  int per_sm = exec_max_ctas_per_sm(comm->cfg.threads, true, dtype, op, coll);
-  int per_sm2 = exec_max_ctas_per_sm(comm->cfg.threads, false, dtype, op, coll);
+  int per_sm = exec_max_ctas_per_sm(comm->cfg.threads, true, dtype, op, coll, smem_bytes());
+  int per_sm2 = exec_max_ctas_per_sm(comm->cfg.threads, false, dtype, op, coll, 0);
   per_sm = std::min(per_sm, per_sm2);
   if (per_sm <= 0) per_sm = 1;
   int cap = per_sm * comm->sms;
   if (comm->cfg.ctas > 0) cap = std::min(cap, comm->cfg.ctas);
   return cap;
-}
-
-// BLINK_TMA=0 selects the register (LSU) data path instead of TMA staging.
-int use_tma() {
-  static int v = [] {
-    const char* e = getenv("BLINK_TMA");
-    return (e && e[0] == '0') ? 0 : 1;
-  }();
-  return v;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -446,6 +476,8 @@ blink_result_t clique_launch(Clique* q) {
     a.exit_wait = all_one_launch ? 0 : 1;
     a.bcast_root = q->coll == kBroadcast ? q->root : -1;
     a.use_tma = use_tma();
+    a.smem_bytes = smem_bytes();
+    a.tile_bytes = tile_bytes();
     a.epoch = q->epoch;
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
     a.err = q->err_dev[dev];
@@ -533,6 +565,7 @@ blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* 
   if (++q->nposted < q->nranks) return BLINK_SUCCESS;
   blink_result_t r = BLINK_SUCCESS;
   if (count > 0) r = clique_launch(q);
+  if (r != BLINK_SUCCESS) comm->last_error = g_last_error;
   for (auto& pp : q->pending) pp = Pending();
   q->nposted = 0;
   return r;
@@ -619,6 +652,8 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.exit_wait = 1;
   a.bcast_root = coll == kBroadcast ? root : -1;
   a.use_tma = use_tma();
+  a.smem_bytes = smem_bytes();
+  a.tile_bytes = tile_bytes();
   a.epoch = comm->epoch;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
   a.err = comm->err_dev;
