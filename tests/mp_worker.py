@@ -1,0 +1,126 @@
+"""Worker for the multi-process tests (launched by torch.distributed.run).
+
+MODE=cpu : host logic only (gloo): blob exchange, plan agreement, max-over-ranks.
+MODE=gpu : the real multi-process path on GPU(s): CUDA-IPC flag/staging
+           mappings, symmetric registration, entry handshake and exit waits.
+           With BLINK_SAME_GPU=1 every rank uses cuda:0 (two processes
+           time-share one B200; IPC maps the peer's allocations).
+Exits non-zero on any mismatch against the oracle.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from oracle import collectives as OC  # noqa: E402
+from oracle import graphs as OG  # noqa: E402
+
+
+def cpu_mode(rank, world):
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    ex = BD.exchange()
+    blobs = ex(bytes([rank]) * 7)
+    assert blobs == [bytes([r]) * 7 for r in range(world)], blobs
+    d = BD.check_same_plan(world, True, 0, 12345, "bf16")
+    tri, _ = OG.induced(OG.dgx1p(), [0, 1, 3])
+    if world == 3:
+        BD.check_same_plan(3, False, 0, 262144, graph=B.Graph.from_pairs(3, tri[1]))
+    # a rank that would plan a different split must be detected on every rank
+    try:
+        BD.check_same_plan(world, True, 0, 1000 + 16 * rank)
+        mismatch = False
+    except B.BlinkError:
+        mismatch = True
+    assert mismatch
+    assert BD.max_over_ranks(float(rank)) == world - 1
+    print(f"rank {rank}: cpu ok {d[:12]}")
+
+
+def gpu_mode(rank, world):
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    dev = 0 if os.environ.get("BLINK_SAME_GPU") == "1" else rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    comm = BD.init(cfg=B.config(timeout_s=60.0, staging_bytes=1 << 20), device=dev)
+    ex = BD.exchange()
+
+    def check(got, want, what):
+        g = got.view(torch.int16).cpu().numpy().view(np.uint16) if got.dtype == torch.bfloat16 \
+            else got.cpu().numpy()
+        gb = g.view(np.uint16 if g.dtype.itemsize == 2 else np.uint32)
+        wb = np.asarray(want).view(gb.dtype)
+        bad = np.nonzero(gb != wb)[0]
+        if bad.size:
+            raise SystemExit(f"rank {rank}: {what}: {bad.size} mismatches, first {bad[:4]}")
+
+    # 1) unregistered buffers -> staging path, several pieces (count > staging)
+    count = 300001
+    sends = synth.inputs(40, world, count, "f32")
+    x = torch.from_numpy(sends[rank]).cuda()
+    y = torch.full_like(x, float("nan"))
+    comm.allreduce(x, y, op="sum")
+    torch.cuda.synchronize()
+    check(y, OC.naive_reduce(sends, "f32", "sum"), "staging allreduce f32")
+
+    # 2) registered symmetric buffers (zero-copy), bf16, in place and out of place
+    count = 1 << 20
+    bs = synth.inputs(41, world, count, "bf16")
+    xb = torch.from_numpy(bs[rank].view(np.int16).copy()).cuda().view(torch.bfloat16)
+    yb = torch.empty_like(xb)
+    comm.register(xb, xb.numel() * 2, ex)
+    comm.register(yb, yb.numel() * 2, ex)
+    comm.allreduce(xb, yb, op="sum")
+    torch.cuda.synchronize()
+    check(yb, OC.naive_reduce(bs, "bf16", "sum"), "registered allreduce bf16")
+    comm.allreduce(xb, xb, op="max")
+    torch.cuda.synchronize()
+    check(xb, OC.naive_reduce(bs, "bf16", "max"), "registered in-place max bf16")
+
+    # 3) broadcast from the last rank: registered recv, then staging
+    root = world - 1
+    src = synth.rank_input(42, root, count, "i32")
+    xs = torch.from_numpy(src).cuda() if rank == root else None
+    yr = torch.zeros(count, dtype=torch.int32, device="cuda")
+    comm.register(yr, count * 4, ex)
+    comm.broadcast(xs, yr, root=root, count=count, dtype="i32")
+    torch.cuda.synchronize()
+    check(yr, src, "registered broadcast")
+    yu = torch.zeros(count + 5, dtype=torch.int32, device="cuda")
+    comm.broadcast(xs, yu[:count], root=root, count=count, dtype="i32")
+    torch.cuda.synchronize()
+    check(yu[:count], src, "staging broadcast")
+
+    # 4) many back-to-back calls (epochs) on registered buffers
+    for _ in range(5):
+        comm.allreduce(xb, yb, op="sum")
+    torch.cuda.synchronize()
+    check(yb, OC.naive_reduce([OC.naive_reduce(bs, "bf16", "max")] * world, "bf16", "sum"),
+          "back-to-back")
+    st = comm.stats()
+    comm.destroy()
+    print(f"rank {rank}: gpu ok launches={st['launches']} ctas={st['last_ctas']}")
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    dist.init_process_group("gloo")
+    try:
+        if os.environ.get("MODE", "cpu") == "cpu":
+            cpu_mode(rank, world)
+        else:
+            gpu_mode(rank, world)
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

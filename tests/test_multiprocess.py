@@ -1,0 +1,48 @@
+"""Multi-process (one rank per process) path.
+
+* CPU (gloo, world_size 2 and 3): the host logic of the N > 1 path --
+  handle-blob exchange, plan agreement across ranks (and detection of a rank
+  planning different trees), max-over-ranks timing reduction.
+* GPU: two processes time-sharing cuda:0 run the real multi-process data path
+  (CUDA-IPC peer mappings of flags/staging/registered buffers, entry handshake,
+  exit waits) against the oracle.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "mp_worker.py")
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch(n, mode, extra_env=None, timeout=600):
+    env = dict(os.environ, MODE=mode, PYTHONPATH=ROOT)
+    env.update(extra_env or {})
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), WORKER]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return r.stdout
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_gloo_host_logic(n):
+    out = launch(n, "cpu", timeout=300)
+    assert out.count("cpu ok") == n
+
+
+@pytest.mark.gpu
+def test_two_processes_share_one_gpu():
+    out = launch(2, "gpu", {"BLINK_SAME_GPU": "1"}, timeout=900)
+    assert out.count("gpu ok") == 2
