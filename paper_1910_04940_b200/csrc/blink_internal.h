@@ -110,6 +110,8 @@ struct LaunchArgs {
   int use_tma;               // stage aligned bodies through TMA bulk copies
   int smem_bytes;            // dynamic shared memory of the TMA ring
   int tile_bytes;            // 0 = default tile per source
+  int scope_sys;             // 1: flags cross devices/processes (.sys), 0: one device (.gpu)
+  int pad2;
   uint64_t epoch;
   uint64_t timeout_ns;
   int* err;                  // host-mapped error word (0 = ok)

@@ -35,15 +35,29 @@ namespace blink {
 namespace {
 
 // ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+// Flag accesses are relaxed; ordering comes from one fence per group of
+// waits (acquire pattern) or per group of signals (release pattern).  Scope is
+// .gpu when every rank lives on this device (virtual ranks), else .sys.
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p, bool sys) {
   uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (sys)
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool sys) {
+  if (sys)
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acqrel(bool sys) {
+  if (sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -332,14 +346,16 @@ struct Ctl {
   uint64_t epoch;
   uint64_t timeout_ns;
   int* err;
+  bool sys;
 };
 
-// Spin (one thread) until *p >= epoch.  Returns false on timeout / abort.
+// Spin (one thread) until *p >= epoch with relaxed loads.  The caller issues
+// fence_acqrel() after its group of waits.  Returns false on timeout / abort.
 __device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
-  if (ld_acquire_sys(p) >= c.epoch) return true;
+  if (ld_relaxed(p, c.sys) >= c.epoch) return true;
   uint64_t t0 = globaltimer();
   for (int spin = 0;; ++spin) {
-    if (ld_acquire_sys(p) >= c.epoch) return true;
+    if (ld_relaxed(p, c.sys) >= c.epoch) return true;
     if ((spin & 255) == 255) {
       if (ld_volatile_int(c.err) != 0) return false;
       if (globaltimer() - t0 > c.timeout_ns) {
@@ -349,8 +365,6 @@ __device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
     }
   }
 }
-
-__device__ __forceinline__ void signal(uint64_t* p, uint64_t epoch) { st_release_sys(p, epoch); }
 
 // ------------------------------------------------------------------ the kernel
 struct Shared {
@@ -390,17 +404,19 @@ __device__ __forceinline__ bool wait_chunk_inputs(const LaunchArgs& a, const Dev
   } else if (need_bflag) {
     ok = wait_ge(myflags + bflag_idx(t.tree, c), ctl);
   }
+  fence_acqrel(ctl.sys);
   return ok;
 }
 
 // Publish chunk c (all its stores are complete and fenced by the caller).
 __device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask& t, int c, bool is_root) {
-  fence_sys();
+  const bool sys = a.scope_sys;
+  fence_acqrel(sys);
   if (t.role == kRoleReduce && !is_root) {
-    signal(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), a.epoch);
+    st_relaxed(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), a.epoch, sys);
   } else {
     for (int u = 0; u < a.nranks; ++u)
-      if ((t.children >> u) & 1u) signal(a.flags[u] + bflag_idx(t.tree, c), a.epoch);
+      if ((t.children >> u) & 1u) st_relaxed(a.flags[u] + bflag_idx(t.tree, c), a.epoch, sys);
   }
 }
 
@@ -417,7 +433,7 @@ __device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask&
 template <int DT, int OP>
 __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
                        bool need_bflag, Shared& sh, char* ring) {
-  const Ctl ctl{a.epoch, a.timeout_ns, a.err};
+  const Ctl ctl{a.epoch, a.timeout_ns, a.err, a.scope_sys != 0};
   const bool reduce = t.role == kRoleReduce;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncons = reduce ? (blockDim.x >> 5) - 2 : 0;
@@ -532,7 +548,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
 template <int DT, int OP, bool VEC>
 __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
                         bool need_bflag, Shared& sh) {
-  const Ctl ctl{a.epoch, a.timeout_ns, a.err};
+  const Ctl ctl{a.epoch, a.timeout_ns, a.err, a.scope_sys != 0};
   for (int c = t.cta_idx; c < tr.nchunks; c += t.cta_cnt) {
     if (threadIdx.x == 0) sh.ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
     __syncthreads();
@@ -557,15 +573,15 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
   extern __shared__ __align__(128) char s_ring[];
   const DevTask t = a.tasks[blockIdx.x];
   const int v = t.rank;
-  const Ctl ctl{a.epoch, a.timeout_ns, a.err};
+  const Ctl ctl{a.epoch, a.timeout_ns, a.err, a.scope_sys != 0};
   uint64_t* myflags = a.flags[v];
   const bool ws = VEC && a.use_tma && blockDim.x >= 128;
 
   // entry: my send is ready and my recv may be overwritten (epoch e)
   if (t.do_entry && threadIdx.x == 0) {
-    fence_sys();
+    fence_acqrel(ctl.sys);
     for (int u = 0; u < a.nranks; ++u)
-      if (u != v) signal(a.flags[u] + entry_idx(v), a.epoch);
+      if (u != v) st_relaxed(a.flags[u] + entry_idx(v), a.epoch, ctl.sys);
   }
 
   if (t.role == kRoleReduce || t.role == kRoleBcast) {
@@ -598,6 +614,7 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
           for (int u = 0; u < a.nranks && ok; ++u)
             if ((t.children >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       }
+      fence_acqrel(ctl.sys);
       sh.nsrc = ns;
       sh.ndst = nd;
       sh.abort = ok ? 0 : 1;
@@ -638,6 +655,7 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
         wait_ge(myflags + bflag_idx(i, c), ctl);
       }
     }
+    fence_acqrel(ctl.sys);
     __syncthreads();
   }
 }

@@ -474,6 +474,7 @@ blink_result_t clique_launch(Clique* q) {
     a.dtype = q->dtype;
     a.op = q->op;
     a.exit_wait = all_one_launch ? 0 : 1;
+    a.scope_sys = all_one_launch ? 0 : 1;
     a.bcast_root = q->coll == kBroadcast ? q->root : -1;
     a.use_tma = use_tma();
     a.smem_bytes = smem_bytes();
@@ -650,6 +651,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.dtype = dtype;
   a.op = op;
   a.exit_wait = 1;
+  a.scope_sys = 1;
   a.bcast_root = coll == kBroadcast ? root : -1;
   a.use_tma = use_tma();
   a.smem_bytes = smem_bytes();

@@ -1,0 +1,164 @@
+#!/usr/bin/env python
+"""Size sweeps for every BASELINE.json config on one B200 (virtual ranks).
+
+    python scripts/sweep.py [--out profiles/sweep_rNN.json] [--quick]
+
+Rows: config, collective, plan, m, dtype, bytes per rank S, ms per call (CUDA
+events, mean of `reps` back-to-back calls after warm-up), algBW = S/t,
+busBW = algBW * f (f = 2(m-1)/m AllReduce, 1 Broadcast), and, because virtual
+ranks share one HBM, the algorithmic HBM bytes per call and their fraction of
+MEASURED_PEAKS.json hbm_gbs:
+  AllReduce : 2 m S   (every send read once, every recv written once)
+  Broadcast : (m+1) S (root send read once, every recv written once)
+Config 5 replays the App. C DDP bucket sequences back to back on one stream.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1910_04940_b200 as B  # noqa: E402
+import synth  # noqa: E402
+from oracle import graphs as OG  # noqa: E402  (topology presets only: the emulated link graphs)
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+TD = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}
+ES = {"f32": 4, "bf16": 2, "i32": 4}
+
+
+def time_calls(fn, nbytes):
+    reps = 50 if nbytes <= (1 << 20) else (20 if nbytes <= (64 << 20) else 5)
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def run_coll(comms, coll, S, dtype, root=0, tag=""):
+    m = len(comms)
+    cnt = max(1, S // ES[dtype])
+    sends = [torch.randn(cnt, device="cuda").to(TD[dtype]) if dtype != "i32" else
+             torch.randint(-1000, 1000, (cnt,), device="cuda", dtype=torch.int32) for _ in range(m)]
+    recvs = [torch.empty_like(s) for s in sends]
+    if coll == "allreduce":
+        def fn():
+            for r, c in enumerate(comms):
+                c.allreduce(sends[r], recvs[r])
+        hbm = 2 * m * cnt * ES[dtype]
+        f = 2 * (m - 1) / m
+    else:
+        def fn():
+            for r, c in enumerate(comms):
+                c.broadcast(sends[root] if r == root else None, recvs[r], root=root)
+        hbm = (m + 1) * cnt * ES[dtype]
+        f = 1.0
+    ms = time_calls(fn, cnt * ES[dtype])
+    Sb = cnt * ES[dtype]
+    alg = Sb / (ms * 1e-3) / 1e9
+    plan = comms[0].plan(coll == "allreduce", root, cnt, dtype)
+    return {"config": tag, "coll": coll, "m": m, "dtype": dtype, "bytes": Sb, "ms": round(ms, 5),
+            "algbw": round(alg, 2), "busbw": round(alg * f, 2),
+            "hbm_gbs": round(hbm / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(hbm / (ms * 1e-3) / 1e9 / PEAK, 4),
+            "trees": len(plan["trees"]), "ctas": plan["ctas"],
+            "max_depth": max(t["depth"] for t in plan["trees"])}
+
+
+def sizes(lo, hi, step):
+    s = lo
+    while s <= hi:
+        yield s
+        s *= step
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep.json"))
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    step = 16 if args.quick else 4
+    rows = []
+
+    def log(r):
+        rows.append(r)
+        print(json.dumps(r), flush=True)
+
+    t0 = time.time()
+    # config 1: the paper's 3-GPU fully connected example (DGX-1P {0,1,3})
+    tri, _ = OG.induced(OG.dgx1p(), [0, 1, 3])
+    comms = B.init_all([0] * 3, graph=B.Graph.from_pairs(3, tri[1]))
+    for S in sizes(1 << 10, 1 << 30, step):
+        log(run_coll(comms, "broadcast", S, "f32", 0, "c1-3gpu-triangle"))
+        log(run_coll(comms, "allreduce", S, "f32", 0, "c1-3gpu-triangle"))
+    for c in comms:
+        c.destroy()
+    # config 2: emulated DGX-1V, Broadcast from root 0 (6 ILP trees)
+    g = OG.dgx1v()
+    comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]))
+    for S in sizes(1 << 10, 1 << 30, step):
+        log(run_coll(comms, "broadcast", S, "f32", 0, "c2-dgx1v-emulated"))
+    for S in sizes(1 << 20, 1 << 28, 16):
+        log(run_coll(comms, "allreduce", S, "f32", 0, "c2-dgx1v-emulated"))
+    for c in comms:
+        c.destroy()
+    # config 3: 8-rank switch, one-hop AllReduce fp32 / bf16 (+ switch Broadcast)
+    comms = B.init_all([0] * 8)
+    for dt in ("f32", "bf16"):
+        for S in sizes(1 << 10, 1 << 30, step):
+            log(run_coll(comms, "allreduce", S, dt, 0, "c3-switch-onehop"))
+    for S in sizes(1 << 10, 1 << 30, step):
+        log(run_coll(comms, "broadcast", S, "f32", 0, "c3-switch"))
+    for c in comms:
+        c.destroy()
+    # config 4: fragmented allocations, re-packed
+    for m in (3, 5, 6, 7):
+        comms = B.init_all([0] * m)
+        for S in sizes(1 << 10, 1 << 30, step * 4):
+            log(run_coll(comms, "allreduce", S, "f32", 0, f"c4-switch-m{m}"))
+        for c in comms:
+            c.destroy()
+    for nodes in ([0, 1, 4], [0, 1, 3, 4, 5, 7], [1, 4, 5, 6]):
+        sub, _ = OG.induced(g, nodes)
+        comms = B.init_all([0] * len(nodes), graph=B.Graph.from_pairs(len(nodes), sub[1]))
+        log(run_coll(comms, "allreduce", 64 << 20, "f32", 0, f"c4-dgx1v-{''.join(map(str, nodes))}"))
+        for c in comms:
+            c.destroy()
+    # config 5: DDP bucket sequences (App. C) at m = 2, 4, 8
+    for m in (2, 4, 8):
+        comms = B.init_all([0] * m)
+        for (model, dt), buckets in synth.BUCKETS.items():
+            bufs = [[torch.randn(n, device="cuda").to(TD[dt]) for _ in range(m)] for n in buckets]
+
+            def seq():
+                for bb in bufs:
+                    for r, c in enumerate(comms):
+                        c.allreduce(bb[r], bb[r])
+            tot = sum(buckets) * ES[dt]
+            ms = time_calls(seq, tot)
+            alg = tot / (ms * 1e-3) / 1e9
+            log({"config": f"c5-{model}-buckets", "coll": "allreduce", "m": m, "dtype": dt,
+                 "bytes": tot, "buckets": len(buckets), "ms": round(ms, 4), "algbw": round(alg, 2),
+                 "busbw": round(alg * 2 * (m - 1) / m, 2),
+                 "hbm_gbs": round(2 * m * tot / (ms * 1e-3) / 1e9, 1),
+                 "hbm_frac": round(2 * m * tot / (ms * 1e-3) / 1e9 / PEAK, 4)})
+            del bufs
+        for c in comms:
+            c.destroy()
+    json.dump({"peak_hbm_gbs": PEAK, "device": torch.cuda.get_device_name(0), "rows": rows,
+               "seconds": round(time.time() - t0, 1)}, open(args.out, "w"), indent=1)
+    print("wrote", args.out)
+
+
+if __name__ == "__main__":
+    main()
