@@ -112,7 +112,9 @@ struct LaunchArgs {
   int tile_bytes;            // 0 = default tile per source
   int scope_sys;             // 1: flags cross devices/processes (.sys), 0: one device (.gpu)
   int pad2;
-  uint64_t epoch;
+  uint64_t epoch;            // set by the kernel from ctrl[0] + 1
+  uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
+                             // [1] CTAs finished in the current launch (graph-safe epochs)
   uint64_t timeout_ns;
   int* err;                  // host-mapped error word (0 = ok)
   char* send[kMaxArgRanks];

@@ -409,14 +409,15 @@ __device__ __forceinline__ bool wait_chunk_inputs(const LaunchArgs& a, const Dev
 }
 
 // Publish chunk c (all its stores are complete and fenced by the caller).
-__device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask& t, int c, bool is_root) {
-  const bool sys = a.scope_sys;
+__device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask& t, int c, bool is_root,
+                                             const Ctl& ctl) {
+  const bool sys = ctl.sys;
   fence_acqrel(sys);
   if (t.role == kRoleReduce && !is_root) {
-    st_relaxed(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), a.epoch, sys);
+    st_relaxed(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), ctl.epoch, sys);
   } else {
     for (int u = 0; u < a.nranks; ++u)
-      if ((t.children >> u) & 1u) st_relaxed(a.flags[u] + bflag_idx(t.tree, c), a.epoch, sys);
+      if ((t.children >> u) & 1u) st_relaxed(a.flags[u] + bflag_idx(t.tree, c), ctl.epoch, sys);
   }
 }
 
@@ -432,8 +433,7 @@ __device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask&
 // on all threads with 128-bit LSU accesses instead.
 template <int DT, int OP>
 __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
-                       bool need_bflag, Shared& sh, char* ring) {
-  const Ctl ctl{a.epoch, a.timeout_ns, a.err, a.scope_sys != 0};
+                       bool need_bflag, Shared& sh, char* ring, const Ctl& ctl) {
   const bool reduce = t.role == kRoleReduce;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncons = reduce ? (blockDim.x >> 5) - 2 : 0;
@@ -466,7 +466,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         if (threadIdx.x == 0) sh.abort = 1;
         break;
       }
-      if (threadIdx.x == 0) signal_chunk(a, t, c, is_root);
+      if (threadIdx.x == 0) signal_chunk(a, t, c, is_root, ctl);
       continue;
     }
     const int ntiles = int((body + tile - 1) / tile);
@@ -511,7 +511,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
       tma_wait_all();
       fence_proxy_async();
-      if (ok) signal_chunk(a, t, c, is_root);
+      if (ok) signal_chunk(a, t, c, is_root, ctl);
     } else if (reduce && warp >= 2) {
       // ---------------- consumers
       const int ct = threadIdx.x - 64, CT = ncons * 32;
@@ -547,8 +547,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
 // Register/LSU path (misaligned buffers, BLINK_TMA=0): all threads per chunk.
 template <int DT, int OP, bool VEC>
 __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
-                        bool need_bflag, Shared& sh) {
-  const Ctl ctl{a.epoch, a.timeout_ns, a.err, a.scope_sys != 0};
+                        bool need_bflag, Shared& sh, const Ctl& ctl) {
   for (int c = t.cta_idx; c < tr.nchunks; c += t.cta_cnt) {
     if (threadIdx.x == 0) sh.ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
     __syncthreads();
@@ -563,17 +562,23 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
     }
     __syncthreads();  // every thread's stores of chunk c are issued (and sh.ok read)
     if (!ok) break;
-    if (threadIdx.x == 0) signal_chunk(a, t, c, is_root);
+    if (threadIdx.x == 0) signal_chunk(a, t, c, is_root, ctl);
   }
 }
 
 template <int DT, int OP, bool VEC>
-__global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
+__global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a_in) {
   __shared__ Shared sh;
+  __shared__ uint64_t s_epoch;
   extern __shared__ __align__(128) char s_ring[];
+  // Epoch = launches completed on this device group + 1, read from device
+  // memory so that CUDA-graph replays get fresh epochs.
+  const LaunchArgs& a = a_in;
   const DevTask t = a.tasks[blockIdx.x];
+  if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
+  __syncthreads();
   const int v = t.rank;
-  const Ctl ctl{a.epoch, a.timeout_ns, a.err, a.scope_sys != 0};
+  const Ctl ctl{s_epoch, a.timeout_ns, a.err, a.scope_sys != 0};
   uint64_t* myflags = a.flags[v];
   const bool ws = VEC && a.use_tma && blockDim.x >= 128;
 
@@ -581,7 +586,7 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
   if (t.do_entry && threadIdx.x == 0) {
     fence_acqrel(ctl.sys);
     for (int u = 0; u < a.nranks; ++u)
-      if (u != v) st_relaxed(a.flags[u] + entry_idx(v), a.epoch, ctl.sys);
+      if (u != v) st_relaxed(a.flags[u] + entry_idx(v), ctl.epoch, ctl.sys);
   }
 
   if (t.role == kRoleReduce || t.role == kRoleBcast) {
@@ -635,9 +640,9 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
     const bool need_bflag = (t.role == kRoleBcast) && !((a.coll == kBroadcast) && is_root);
     if (!sh.abort) {
       if (ws)
-        run_ws<DT, OP>(a, t, tr, is_root, need_bflag, sh, s_ring);
+        run_ws<DT, OP>(a, t, tr, is_root, need_bflag, sh, s_ring, ctl);
       else
-        run_lsu<DT, OP, VEC>(a, t, tr, is_root, need_bflag, sh);
+        run_lsu<DT, OP, VEC>(a, t, tr, is_root, need_bflag, sh, ctl);
     }
   }
 
@@ -656,7 +661,17 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a) {
       }
     }
     fence_acqrel(ctl.sys);
-    __syncthreads();
+  }
+  // the last CTA to finish advances the device epoch for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long prev = atomicAdd(reinterpret_cast<unsigned long long*>(a.ctrl + 1), 1ull);
+    if (prev + 1 == gridDim.x) {
+      a.ctrl[1] = 0;
+      __threadfence();
+      atomicExch(reinterpret_cast<unsigned long long*>(a.ctrl), (unsigned long long)ctl.epoch);
+    }
   }
 }
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -929,7 +930,8 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
     int64_t bytes = hi - lo;
     // a8: static chunk table.  Aim for >= `per_cta` chunks per CTA of the
     // channel (deeper trees pipeline better with more chunks: (c+h-1)/c,
-    // P:511-513), chunks >= 64 KiB unless the range is smaller, <= 4 MiB.
+    // P:511-513), chunks >= 4 KiB (BLINK_MIN_CHUNK) unless the range is
+    // smaller, <= 4 MiB.
     int64_t cb;
     if (cfg.chunk_bytes > 0) {
       cb = int64_t(cfg.chunk_bytes);
@@ -937,7 +939,11 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
       int per_cta = p.trees[i].depth >= 2 ? 4 : 1;
       int64_t want = int64_t(std::max(1, ctas_hint)) * per_cta;
       cb = (bytes + want - 1) / want;
-      cb = std::max<int64_t>(cb, 64 << 10);
+      static const int64_t min_chunk = [] {
+        const char* e = getenv("BLINK_MIN_CHUNK");
+        return e ? std::max<int64_t>(16, atoll(e)) : int64_t(4 << 10);
+      }();
+      cb = std::max<int64_t>(cb, min_chunk);
       cb = std::min<int64_t>(cb, 4 << 20);
     }
     cb = (cb + kGrain - 1) / kGrain * kGrain;

@@ -99,6 +99,7 @@ struct blink_comm {
   uint64_t* peer_flags[kMaxRanks] = {};
   int* err_host = nullptr;  // multi-process error word
   int* err_dev = nullptr;
+  uint64_t* ctrl = nullptr;  // multi-process: device launch epoch + done counter
   int sms = 148;
   std::map<std::pair<int, int>, std::unique_ptr<Plan>> plans;  // (coll, root|variant)
   std::map<SizedKey, Sized> sized;                             // multi-process launches
@@ -133,6 +134,7 @@ struct Clique {
   std::vector<Pending> pending;
   // per device state
   std::map<int, int*> err_host, err_dev;
+  std::map<int, uint64_t*> ctrl;  // per device: launch epoch + done counter
   std::map<SizedKey, Sized> sized;
   int64_t launches = 0;
   bool sticky_error = false;
@@ -360,6 +362,16 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
 
 // Data path: BLINK_TMA=0 register/LSU loads and stores, 1 TMA loads + LSU
 // stores, 2 TMA loads + TMA bulk stores (default).
+// BLINK_COOP=0 launches without the cooperative attribute (co-residency then
+// relies on grid <= occupancy x SMs and an otherwise idle device).
+bool use_coop() {
+  static bool v = [] {
+    const char* e = getenv("BLINK_COOP");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 int use_tma() {
   static int v = [] {
     const char* e = getenv("BLINK_TMA");
@@ -479,7 +491,7 @@ blink_result_t clique_launch(Clique* q) {
     a.use_tma = use_tma();
     a.smem_bytes = smem_bytes();
     a.tile_bytes = tile_bytes();
-    a.epoch = q->epoch;
+    a.ctrl = q->ctrl[dev];
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
     a.err = q->err_dev[dev];
     for (int v = 0; v < n; ++v) {
@@ -505,7 +517,7 @@ blink_result_t clique_launch(Clique* q) {
       CUDA_TRY(cd, cudaStreamWaitEvent(ls, e, 0));
       evs.push_back(e);
     }
-    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, true);
+    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, use_coop());
     if (le != cudaSuccess)
       return fail(cd, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
     q->launches++;
@@ -656,7 +668,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.use_tma = use_tma();
   a.smem_bytes = smem_bytes();
   a.tile_bytes = tile_bytes();
-  a.epoch = comm->epoch;
+  a.ctrl = comm->ctrl;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
   a.err = comm->err_dev;
   for (int u = 0; u < n; ++u) {
@@ -664,7 +676,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     a.recv[u] = recv[u];
     a.flags[u] = comm->peer_flags[u];
   }
-  cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, true);
+  cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, use_coop());
   if (le != cudaSuccess)
     return fail(comm, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
   comm->stats.launches++;
@@ -859,6 +871,11 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
     *h = 0;
     q->err_host[d] = h;
     q->err_dev[d] = dp;
+    uint64_t* ctrl = nullptr;
+    if (cudaMalloc(&ctrl, 2 * sizeof(uint64_t)) != cudaSuccess ||
+        cudaMemset(ctrl, 0, 2 * sizeof(uint64_t)) != cudaSuccess)
+      return fail(nullptr, BLINK_ERR_CUDA, "control word allocation failed");
+    q->ctrl[d] = ctrl;
   }
   q->alive = ndev;
   return BLINK_SUCCESS;
@@ -894,6 +911,9 @@ blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_dev
   CUDA_TRY(c, cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped));
   CUDA_TRY(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   *c->err_host = 0;
+  CUDA_TRY(c, cudaMalloc(&c->ctrl, 2 * sizeof(uint64_t)));
+  CUDA_TRY(c, cudaMemset(c->ctrl, 0, 2 * sizeof(uint64_t)));
+  CUDA_TRY(c, cudaDeviceSynchronize());
   *comm = c;
   return BLINK_SUCCESS;
 }
@@ -1113,6 +1133,7 @@ blink_result_t blink_destroy(blink_comm_t comm) {
       for (auto& kv : comm->opened) cudaIpcCloseMemHandle(kv.second);
       if (comm->staging) cudaFree(comm->staging);
       if (comm->err_host) cudaFreeHost(comm->err_host);
+      if (comm->ctrl) cudaFree(comm->ctrl);
     }
     if (comm->flags) cudaFree(comm->flags);
   }
@@ -1129,6 +1150,7 @@ blink_result_t blink_destroy(blink_comm_t comm) {
         cudaFree(kv.second.d_trees);
       }
       for (auto& kv : q->err_host) cudaFreeHost(kv.second);
+      for (auto& kv : q->ctrl) cudaFree(kv.second);
       delete q;
     }
   }

@@ -336,3 +336,35 @@ def test_fullsize_config3_sampled(B):
     # the last element and a tail window
     tail = [s[-37:].cpu().numpy() for s in sends]
     assert_bitwise(recvs[0][-37:].cpu().numpy(), OC.naive_reduce(tail, "f32", "sum"))
+
+
+def test_cuda_graph_capture_and_replay(B):
+    """Epochs live in device memory, so a captured call replays correctly
+    (warm-up call first: the first call of a size uploads its tables)."""
+    m, count = 8, 100003
+    comms = make_comms(B, m)
+    dsend = [torch.empty(count, device="cuda") for _ in range(m)]
+    drecv = [torch.empty(count, device="cuda") for _ in range(m)]
+    for r, c in enumerate(comms):          # warm-up (eager)
+        c.allreduce(dsend[r], drecv[r])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for r, c in enumerate(comms):
+            c.allreduce(dsend[r], drecv[r])
+    for it in range(4):
+        sends = synth.inputs(90 + it, m, count, "f32")
+        for d, s in zip(dsend, sends):
+            d.copy_(torch.from_numpy(s))
+        g.replay()
+        torch.cuda.synchronize()
+        want = OC.naive_reduce(sends, "f32", "sum")
+        for x in drecv:
+            assert_bitwise(x.cpu().numpy(), want)
+    # eager calls after replays still agree on epochs
+    for r, c in enumerate(comms):
+        c.allreduce(dsend[r], drecv[r], op="max")
+    torch.cuda.synchronize()
+    want = OC.naive_reduce(sends, "f32", "max")
+    for x in drecv:
+        assert_bitwise(x.cpu().numpy(), want)
