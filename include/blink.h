@@ -89,8 +89,9 @@ typedef struct {
  *   mwu_eps        MWU approximation parameter, default 0.1
  *   ilp_gap        ILP relaxation threshold "(e.g., 5%)", default 0.05
  *   chunk_bytes    0 = size-dependent static table (a8), else fixed chunk size
- *   ctas           CTA budget per device launch; 0 = 2 x SM count
- *   threads        threads per CTA (multiple of 32, <= 1024); 0 = 512
+ *   ctas           CTA budget per device launch; 0 = all co-resident CTAs
+ *                  (occupancy x SM count)
+ *   threads        threads per CTA (multiple of 32, <= 512); default 256
  *   timeout_s      flag-wait bound; expiry aborts the launch and the next call
  *                  returns BLINK_ERR_TIMEOUT; default 30
  *   onehop_bcast_max_bytes  switch graphs: Broadcast below this size uses the
@@ -167,6 +168,21 @@ blink_result_t blink_broadcast(blink_comm_t comm, const void* sendbuf, void* rec
  * per-node operand order (ascending rank, R#12). */
 blink_result_t blink_allreduce(blink_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
                                blink_dtype_t dtype, blink_redop_t op, void* stream);
+
+/* ReduceScatter (NEXT-3: the reduce half of the one-hop AllReduce).
+ * sendbuf holds nranks blocks of recvcount elements; rank j's recvbuf
+ * (recvcount elements) receives block j reduced over all ranks in ascending
+ * rank order.  Switch (one-hop) topologies only; BLINK_ERR_UNSUPPORTED on
+ * explicit link graphs. */
+blink_result_t blink_reduce_scatter(blink_comm_t comm, const void* sendbuf, void* recvbuf,
+                                    size_t recvcount, blink_dtype_t dtype, blink_redop_t op,
+                                    void* stream);
+/* AllGather (NEXT-3: "AllReduce without using a reduction function").
+ * Every rank's sendcount elements land at block `rank` of every recvbuf
+ * (nranks*sendcount elements).  In place iff sendbuf == recvbuf + rank*sendcount.
+ * Switch (one-hop) topologies only. */
+blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
+                               size_t sendcount, blink_dtype_t dtype, void* stream);
 
 /* ---------------------------------------------------------------- introspection
  * Same JSON as blink_plan_json, for the plan this comm would run, plus "ctas"

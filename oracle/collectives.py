@@ -169,3 +169,23 @@ def broadcast(plan, sends, root, dtype):
                     nxt.append(c)
             frontier = nxt
     return recvs
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3 duals on one-hop trees ("Gather is the inverse of Broadcast,
+# and AllGather is AllReduce without using a reduction function")
+# ---------------------------------------------------------------------------
+def reduce_scatter(sends, dtype, op):
+    """The reduce half of the one-hop AllReduce: every rank's send
+    holds m blocks of B elements; block j is reduced at its tree root j over
+    the ranks in ascending order (R#12, one rounding).  Returns the m results
+    (rank j receives block j)."""
+    m = len(sends)
+    B = len(sends[0]) // m
+    return [reduce_operands([s[j * B:(j + 1) * B] for s in sends], dtype, op) for j in range(m)]
+
+
+def allgather(sends):
+    """AllReduce without a reduction: root j's block is broadcast to everyone,
+    so every rank receives the blocks in rank order."""
+    return np.concatenate([np.asarray(s) for s in sends])

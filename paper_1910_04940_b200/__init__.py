@@ -66,6 +66,8 @@ _SIGS = {
     "blink_register_connect": (_i, [_vp, _vp, _vp, _sz]),
     "blink_broadcast": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
     "blink_allreduce": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
+    "blink_reduce_scatter": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
+    "blink_allgather": (_i, [_vp, _vp, _vp, _sz, _i, _vp]),
     "blink_get_plan": (_i, [_vp, _i, _i, _sz, _i, _cp, ctypes.POINTER(_sz)]),
     "blink_get_stats": (_i, [_vp, ctypes.POINTER(_Stats)]),
     "blink_comm_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
@@ -201,6 +203,23 @@ class Comm:
         dt = _dtype_of(ref, dtype)
         cnt = ref.numel() if count is None else count
         _check(_lib.blink_broadcast(self._h, _ptr(send), _ptr(recv), cnt, DTYPES[dt], int(root),
+                                    _stream(stream)), self._h)
+        return recv
+
+    def reduce_scatter(self, send, recv, op="sum", recvcount=None, dtype=None, stream=None):
+        """ReduceScatter (NEXT-3): send holds nranks blocks of recvcount; rank j
+        receives block j reduced over all ranks."""
+        dt = _dtype_of(recv, dtype)
+        cnt = recv.numel() if recvcount is None else recvcount
+        _check(_lib.blink_reduce_scatter(self._h, _ptr(send), _ptr(recv), cnt, DTYPES[dt], OPS[op],
+                                         _stream(stream)), self._h)
+        return recv
+
+    def allgather(self, send, recv, sendcount=None, dtype=None, stream=None):
+        """AllGather (NEXT-3): block `rank` of every recv gets this send."""
+        dt = _dtype_of(send, dtype)
+        cnt = send.numel() if sendcount is None else sendcount
+        _check(_lib.blink_allgather(self._h, _ptr(send), _ptr(recv), cnt, DTYPES[dt],
                                     _stream(stream)), self._h)
         return recv
 

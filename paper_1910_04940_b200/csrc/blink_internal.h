@@ -39,7 +39,9 @@ __host__ __device__ inline size_t bflag_idx(int tree, int chunk) {
   return kEntryWords + kPflagWords + size_t(tree) * kMaxChunks + chunk;
 }
 
-enum Coll : int { kBroadcast = 0, kAllReduce = 1 };
+enum Coll : int { kBroadcast = 0, kAllReduce = 1, kReduceScatter = 2, kAllGather = 3 };
+// ReduceScatter / AllGather: tree j is the one-hop star rooted at j and owns block j.
+inline bool is_block_coll(int c) { return c == kReduceScatter || c == kAllGather; }
 
 // ---------------------------------------------------------------- plans
 struct Tree {
@@ -59,6 +61,7 @@ struct Plan {                // size-independent (TreeGen output)
   double c_star = 0.0;       // MWU rate (0 for closed forms)
   int grid = 1;              // accepted relaxation level g
   bool switch_model = false;
+  bool blocks = false;       // tree i covers block i = [i*count, (i+1)*count) (RS / AG)
 };
 
 struct TreeRange {           // per call size

@@ -602,20 +602,20 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a_in) {
           sh.srcs[ns++] = (u == v || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
         }
         sh.dsts[nd++] = a.recv[v];
-        if (is_root)
+        if (is_root && a.coll == kAllReduce)  // ReduceScatter keeps the result at the root
           for (int u = 0; u < a.nranks; ++u)
             if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
         // leaf children: their send is ready once they entered
         for (int u = 0; u < a.nranks && ok; ++u)
           if ((t.leafmask >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       } else {
-        const bool src_root = (a.coll == kBroadcast) && is_root;
+        const bool src_root = (a.coll == kBroadcast || a.coll == kAllGather) && is_root;
         sh.srcs[ns++] = src_root ? a.send[v] : a.recv[v];
         if (src_root && a.send[v] != a.recv[v]) sh.dsts[nd++] = a.recv[v];
         for (int u = 0; u < a.nranks; ++u)
           if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
-        // Broadcast pushes into children's recv: they must have entered
-        if (a.coll == kBroadcast)
+        // Broadcast / AllGather push into children's recv: they must have entered
+        if (a.coll == kBroadcast || a.coll == kAllGather)
           for (int u = 0; u < a.nranks && ok; ++u)
             if ((t.children >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       }
@@ -637,7 +637,8 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a_in) {
       }
     }
     __syncthreads();
-    const bool need_bflag = (t.role == kRoleBcast) && !((a.coll == kBroadcast) && is_root);
+    const bool need_bflag =
+        (t.role == kRoleBcast) && !((a.coll == kBroadcast || a.coll == kAllGather) && is_root);
     if (!sh.abort) {
       if (ws)
         run_ws<DT, OP>(a, t, tr, is_root, need_bflag, sh, s_ring, ctl);
@@ -703,7 +704,7 @@ ExecFn pick_op(int op) {
 }
 
 ExecFn pick(int coll, int dtype, int op, bool vec) {
-  if (coll == kBroadcast) return vec ? exec_kernel<BLINK_FLOAT32, BLINK_SUM, true>
+  if (coll == kBroadcast || coll == kAllGather) return vec ? exec_kernel<BLINK_FLOAT32, BLINK_SUM, true>
                                      : exec_kernel<BLINK_FLOAT32, BLINK_SUM, false>;
   switch (dtype) {
     case BLINK_FLOAT32: return vec ? pick_op<BLINK_FLOAT32, true>(op) : pick_op<BLINK_FLOAT32, false>(op);
@@ -723,7 +724,7 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = vec ? a.smem_bytes : 0;
-  static bool attr_set[2][3][4][2] = {};
+  static bool attr_set[4][3][4][2] = {};
   bool& done = attr_set[a.coll][a.dtype][a.op][vec];
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -903,8 +903,8 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
 blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
                          int ctas_hint, std::vector<TreeRange>* out, std::string* err) {
   out->clear();
-  const size_t S = count * size_t(esize);
   const int k = int(p.trees.size());
+  const size_t S = count * size_t(esize) * (p.blocks ? size_t(k) : 1);
   // R#11: b_i = floor(G * sum_{j<i} w_j / W) with exact rationals
   int64_t L = 1;
   for (const Tree& t : p.trees) L = L / gcd64(L, t.wden) * t.wden;
@@ -925,6 +925,10 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
   for (int i = 0; i < k; ++i) {
     TreeRange r;
     int64_t lo = b[i] * kGrain, hi = (i == k - 1) ? int64_t(S) : b[i + 1] * kGrain;
+    if (p.blocks) {  // RS / AG: block i = [i*count, (i+1)*count) elements
+      lo = int64_t(i) * int64_t(count) * esize;
+      hi = lo + int64_t(count) * esize;
+    }
     r.lo = lo / esize;
     r.hi = hi / esize;
     int64_t bytes = hi - lo;
@@ -967,7 +971,8 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
 std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vector<TreeRange>& r,
                          int ctas) {
   std::ostringstream o;
-  o << "{\"coll\":\"" << (p.coll == kAllReduce ? "allreduce" : "broadcast") << "\",\"root\":"
+  static const char* names[] = {"broadcast", "allreduce", "reduce_scatter", "allgather"};
+  o << "{\"coll\":\"" << names[p.coll] << "\",\"root\":"
     << p.root << ",\"nranks\":" << p.nranks << ",\"count\":" << count << ",\"esize\":" << esize
     << ",\"switch\":" << (p.switch_model ? "true" : "false") << ",\"rate\":[" << p.rate_num << ","
     << p.rate_den << "],\"c_star\":" << p.c_star << ",\"grid\":" << p.grid << ",\"ctas\":" << ctas

@@ -181,7 +181,10 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
 // Plan cache: key (coll, root) with root = -1 for AllReduce, and root + 1000
 // for the one-hop Broadcast star variant on switches.
 blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, const Plan** out) {
-  int key_root = coll == kAllReduce ? -1 : root;
+  int key_root = coll == kBroadcast ? root : -1;
+  if (is_block_coll(coll) && !comm->graph.switch_model)
+    return fail(comm, BLINK_ERR_UNSUPPORTED,
+                "ReduceScatter/AllGather run on one-hop trees: switch topologies only");
   bool star = coll == kBroadcast && comm->graph.switch_model && comm->nranks > 2 &&
               bytes <= comm->cfg.onehop_bcast_max_bytes;
   if (star) key_root += 1000;
@@ -208,7 +211,12 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
     p->rate_num = 1;
     r = BLINK_SUCCESS;
   } else {
-    r = make_plan(comm->graph, coll, root, comm->cfg, p.get(), &err);
+    r = make_plan(comm->graph, is_block_coll(coll) ? kAllReduce : coll, root, comm->cfg, p.get(),
+                  &err);
+    if (is_block_coll(coll)) {  // one-hop stars; tree j owns block j
+      p->coll = coll;
+      p->blocks = true;
+    }
   }
   if (r != BLINK_SUCCESS) return fail(comm, r, err);
   if (getenv("BLINK_DEBUG")) {
@@ -259,6 +267,8 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
         double wr = bytes * ((nc + 1) + (par < 0 ? nc + 1 : 1));
         chans.push_back({v, i, kRoleReduce, par, c, leaf, wr});
         if (par >= 0) chans.push_back({v, i, kRoleBcast, par, c, leaf, bytes * (1 + nc)});
+      } else if (plan.coll == kReduceScatter) {
+        chans.push_back({v, i, kRoleReduce, par, c, leaf, bytes * (nc + 2)});
       } else {
         chans.push_back({v, i, kRoleBcast, par, c, leaf, bytes * (1 + nc + (par < 0 ? 1 : 0))});
       }
@@ -419,7 +429,7 @@ blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtyp
   if (!comm) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "comm is NULL");
   if (esize_of(dtype) == 0)
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported dtype " + std::to_string(dtype));
-  if (coll == kAllReduce && (op < BLINK_SUM || op > BLINK_MAX))
+  if ((coll == kAllReduce || coll == kReduceScatter) && (op < BLINK_SUM || op > BLINK_MAX))
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported op " + std::to_string(op));
   if (coll == kBroadcast && (root < 0 || root >= comm->nranks))
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT,
@@ -452,9 +462,11 @@ blink_result_t clique_launch(Clique* q) {
   bool vec = true;
   for (int v = 0; v < n; ++v) {
     const Pending& p = q->pending[v];
-    if ((q->coll == kAllReduce || v == q->root) && !aligned16(p.send)) vec = false;
+    const bool reads_send = q->coll != kBroadcast || v == q->root;
+    if (reads_send && !aligned16(p.send)) vec = false;
     if (!aligned16(p.recv)) vec = false;
   }
+  if (is_block_coll(q->coll) && (bytes % kGrain) != 0) vec = false;  // block starts unaligned
   const bool all_one_launch = q->devices.size() == 1;
   for (int dev : q->devices) {
     uint64_t mask = 0;
@@ -498,6 +510,9 @@ blink_result_t clique_launch(Clique* q) {
       a.send[v] = const_cast<char*>(static_cast<const char*>(q->pending[v].send));
       a.recv[v] = static_cast<char*>(q->pending[v].recv);
       a.flags[v] = q->comms[v]->flags;
+      // block collectives address rank v's short buffer through tree v's range
+      if (q->coll == kReduceScatter) a.recv[v] -= size_t(v) * bytes;
+      if (q->coll == kAllGather && a.send[v]) a.send[v] -= size_t(v) * bytes;
     }
     DeviceGuard g(dev);
     // launch on the first rank's stream of this device after the others' streams
@@ -561,7 +576,8 @@ blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* 
     q->op = op;
     q->count = count;
   } else if (q->coll != coll || q->count != count || q->dtype != int(dtype) ||
-             (coll == kAllReduce && q->op != op) || (coll == kBroadcast && q->root != root)) {
+             (coll != kBroadcast && coll != kAllGather && q->op != op) ||
+             (coll == kBroadcast && q->root != root)) {
     return fail(comm, BLINK_ERR_INVALID_USAGE,
                 "rank " + std::to_string(comm->rank) +
                     " called a different collective/count/dtype/op/root than the ranks already "
@@ -651,9 +667,9 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   Sized& s = it->second;
   bool vec = true;
   for (int u = 0; u < n; ++u) {
-    if ((coll == kAllReduce || u == root) && !aligned16(send[u])) vec = false;
-    if (!aligned16(recv[u])) vec = false;
+    if (!aligned16(send[u]) || !aligned16(recv[u])) vec = false;  // (NULLs are aligned)
   }
+  if (is_block_coll(coll) && (bytes % kGrain) != 0) vec = false;
   LaunchArgs a{};
   a.tasks = s.d_tasks;
   a.trees = s.d_trees;
@@ -675,6 +691,8 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     a.send[u] = send[u];
     a.recv[u] = recv[u];
     a.flags[u] = comm->peer_flags[u];
+    if (coll == kReduceScatter && a.recv[u]) a.recv[u] -= size_t(u) * bytes;
+    if (coll == kAllGather && a.send[u]) a.send[u] -= size_t(u) * bytes;
   }
   cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, use_coop());
   if (le != cudaSuccess)
@@ -683,6 +701,55 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   comm->stats.last_ctas = s.ctas;
   comm->stats.last_chunks = s.chunks;
   comm->stats.last_trees = int(plan->trees.size());
+  return BLINK_SUCCESS;
+}
+
+// ReduceScatter / AllGather across processes.  RS: peers read this rank's
+// send (register it or it is staged), only the own recv is written.  AG: peers
+// write this rank's recv (register it or it is staged), only the own send is
+// read.  Staged calls run in pieces of P elements per block.
+blink_result_t mp_block_collective(blink_comm_t comm, int coll, const void* sendbuf, void* recvbuf,
+                                   size_t count, blink_dtype_t dtype, int op, cudaStream_t stream) {
+  const int m = comm->nranks, me = comm->rank;
+  const int es = esize_of(dtype);
+  const char* sb = static_cast<const char*>(sendbuf);
+  char* rb = static_cast<char*>(recvbuf);
+  char* sp[kMaxRanks] = {};
+  char* rp[kMaxRanks] = {};
+  if (coll == kReduceScatter) {
+    rp[me] = rb;
+    if (resolve(comm, sendbuf, size_t(m) * count * es, sp))
+      return mp_run(comm, coll, sp, rp, count, dtype, op, -1, stream);
+  } else {
+    sp[me] = const_cast<char*>(sb);
+    if (resolve(comm, recvbuf, size_t(m) * count * es, rp))
+      return mp_run(comm, coll, sp, rp, count, dtype, op, -1, stream);
+  }
+  const size_t P = std::max<size_t>(1, comm->staging_bytes / (size_t(m) * es));
+  char* st[kMaxRanks];
+  for (int u = 0; u < m; ++u) st[u] = comm->peer_staging[u];
+  for (size_t k0 = 0; k0 < count; k0 += P) {
+    const size_t cnt = std::min(P, count - k0);
+    char* s2[kMaxRanks] = {};
+    char* r2[kMaxRanks] = {};
+    blink_result_t r;
+    if (coll == kReduceScatter) {
+      for (int j = 0; j < m; ++j)
+        CUDA_TRY(comm, launch_copy(comm->staging + size_t(j) * cnt * es,
+                                   sb + (size_t(j) * count + k0) * es, cnt * es, stream));
+      r2[me] = rb + k0 * es;
+      r = mp_run(comm, coll, st, r2, cnt, dtype, op, -1, stream);
+      if (r != BLINK_SUCCESS) return r;
+    } else {
+      CUDA_TRY(comm, launch_copy(comm->staging + size_t(me) * cnt * es, sb + k0 * es, cnt * es, stream));
+      s2[me] = comm->staging + size_t(me) * cnt * es;
+      r = mp_run(comm, coll, s2, st, cnt, dtype, op, -1, stream);
+      if (r != BLINK_SUCCESS) return r;
+      for (int j = 0; j < m; ++j)
+        CUDA_TRY(comm, launch_copy(rb + (size_t(j) * count + k0) * es,
+                                   comm->staging + size_t(j) * cnt * es, cnt * es, stream));
+    }
+  }
   return BLINK_SUCCESS;
 }
 
@@ -700,6 +767,7 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
     comm->stats.launches++;
     return BLINK_SUCCESS;
   }
+  if (is_block_coll(coll)) return mp_block_collective(comm, coll, sendbuf, recvbuf, count, dtype, op, stream);
   char* sp[kMaxRanks] = {};
   char* rp[kMaxRanks] = {};
   const bool recv_ok = resolve(comm, recvbuf, bytes, rp);
@@ -1074,6 +1142,33 @@ blink_result_t blink_allreduce(blink_comm_t comm, const void* sendbuf, void* rec
     return mp_collective(comm, kAllReduce, sendbuf, recvbuf, count, dtype, op, -1, stream);
   }
   return clique_post(comm, kAllReduce, sendbuf, recvbuf, count, dtype, op, -1, stream);
+}
+
+blink_result_t blink_reduce_scatter(blink_comm_t comm, const void* sendbuf, void* recvbuf,
+                                    size_t recvcount, blink_dtype_t dtype, blink_redop_t op,
+                                    void* stream) {
+  blink_result_t r = validate_call(comm, recvcount, dtype, op, 0, kReduceScatter);
+  if (r != BLINK_SUCCESS) return r;
+  if (recvcount > 0 && (!recvbuf || !sendbuf))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (comm->multiprocess) {
+    if (recvcount == 0) return BLINK_SUCCESS;
+    return mp_collective(comm, kReduceScatter, sendbuf, recvbuf, recvcount, dtype, op, -1, stream);
+  }
+  return clique_post(comm, kReduceScatter, sendbuf, recvbuf, recvcount, dtype, op, -1, stream);
+}
+
+blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
+                               size_t sendcount, blink_dtype_t dtype, void* stream) {
+  blink_result_t r = validate_call(comm, sendcount, dtype, BLINK_SUM, 0, kAllGather);
+  if (r != BLINK_SUCCESS) return r;
+  if (sendcount > 0 && (!recvbuf || !sendbuf))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (comm->multiprocess) {
+    if (sendcount == 0) return BLINK_SUCCESS;
+    return mp_collective(comm, kAllGather, sendbuf, recvbuf, sendcount, dtype, BLINK_SUM, -1, stream);
+  }
+  return clique_post(comm, kAllGather, sendbuf, recvbuf, sendcount, dtype, BLINK_SUM, -1, stream);
 }
 
 blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, size_t count,

@@ -75,6 +75,31 @@ def run_coll(comms, coll, S, dtype, root=0, tag=""):
             "max_depth": max(t["depth"] for t in plan["trees"])}
 
 
+def run_block(comms, coll, S, dtype, tag):
+    """ReduceScatter / AllGather; S = full (m-block) buffer bytes per rank.
+    Algorithmic HBM bytes: RS reads m*S, writes S; AG reads S, writes m*S."""
+    m = len(comms)
+    B = max(1, S // ES[dtype] // m)
+    full = [torch.randn(m * B, device="cuda").to(TD[dtype]) for _ in range(m)]
+    part = [torch.randn(B, device="cuda").to(TD[dtype]) for _ in range(m)]
+    if coll == "reduce_scatter":
+        def fn():
+            for r, c in enumerate(comms):
+                c.reduce_scatter(full[r], part[r])
+    else:
+        def fn():
+            for r, c in enumerate(comms):
+                c.allgather(part[r], full[r])
+    Sb = m * B * ES[dtype]
+    ms = time_calls(fn, Sb)
+    hbm = (m + 1) * Sb
+    alg = Sb / (ms * 1e-3) / 1e9
+    return {"config": tag, "coll": coll, "m": m, "dtype": dtype, "bytes": Sb, "ms": round(ms, 5),
+            "algbw": round(alg, 2), "busbw": round(alg * (m - 1) / m, 2),
+            "hbm_gbs": round(hbm / (ms * 1e-3) / 1e9, 1),
+            "hbm_frac": round(hbm / (ms * 1e-3) / 1e9 / PEAK, 4)}
+
+
 def sizes(lo, hi, step):
     s = lo
     while s <= hi:
@@ -119,6 +144,10 @@ def main():
             log(run_coll(comms, "allreduce", S, dt, 0, "c3-switch-onehop"))
     for S in sizes(1 << 10, 1 << 30, step):
         log(run_coll(comms, "broadcast", S, "f32", 0, "c3-switch"))
+    # NEXT-3 duals on the same one-hop trees (S = bytes per rank of the full buffer)
+    for S in sizes(1 << 16, 1 << 30, step * 4):
+        for coll in ("reduce_scatter", "allgather"):
+            log(run_block(comms, coll, S, "f32", "c3-switch-next3"))
     for c in comms:
         c.destroy()
     # config 4: fragmented allocations, re-packed

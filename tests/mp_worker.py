@@ -103,6 +103,26 @@ def gpu_mode(rank, world):
     torch.cuda.synchronize()
     check(yb, OC.naive_reduce([OC.naive_reduce(bs, "bf16", "max")] * world, "bf16", "sum"),
           "back-to-back")
+    # 5) ReduceScatter / AllGather: staged (unregistered) then registered
+    B_ = 70001
+    rsends = synth.inputs(43, world, world * B_, "f32")
+    xs_ = torch.from_numpy(rsends[rank]).cuda()
+    out = torch.full((B_,), float("nan"), device="cuda")
+    comm.reduce_scatter(xs_, out, op="sum")
+    torch.cuda.synchronize()
+    blocks = OC.reduce_scatter(rsends, "f32", "sum")
+    check(out, blocks[rank], "staged reduce_scatter")
+    ag = torch.full((world * B_,), float("nan"), device="cuda")
+    comm.allgather(out, ag)
+    torch.cuda.synchronize()
+    check(ag, OC.allgather(blocks), "staged allgather")
+    comm.register(xs_, xs_.numel() * 4, ex)
+    comm.register(ag, ag.numel() * 4, ex)
+    out2 = torch.full((B_,), float("nan"), device="cuda")
+    comm.reduce_scatter(xs_, out2, op="max")
+    comm.allgather(out2, ag)
+    torch.cuda.synchronize()
+    check(ag, OC.allgather(OC.reduce_scatter(rsends, "f32", "max")), "registered rs+ag")
     st = comm.stats()
     comm.destroy()
     print(f"rank {rank}: gpu ok launches={st['launches']} ctas={st['last_ctas']}")

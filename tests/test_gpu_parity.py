@@ -368,3 +368,66 @@ def test_cuda_graph_capture_and_replay(B):
     want = OC.naive_reduce(sends, "f32", "max")
     for x in drecv:
         assert_bitwise(x.cpu().numpy(), want)
+
+
+# ----------------------------------------------------------------- NEXT-3: ReduceScatter / AllGather
+@pytest.mark.parametrize("m", [2, 3, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+@pytest.mark.parametrize("B_", [1, 5, 4096, 33333])      # 16-byte aligned blocks and ragged ones
+def test_reduce_scatter_and_allgather(B, m, dtype, B_):
+    comms = make_comms(B, m, chunk_bytes=8192)
+    sends = synth.inputs(100 + m, m, m * B_, dtype)
+    ds = [to_dev(s, dtype) for s in sends]
+    rs = [sentinel(B_, dtype) for _ in range(m)]
+    for r, c in enumerate(comms):
+        c.reduce_scatter(ds[r], rs[r], op="sum", recvcount=B_, dtype=dtype)
+    torch.cuda.synchronize()
+    want = OC.reduce_scatter(sends, dtype, "sum")
+    for r in range(m):
+        assert_bitwise(to_host(rs[r], dtype), want[r])
+    # AllGather of the reduced blocks reproduces the one-hop AllReduce
+    ag = [sentinel(m * B_, dtype) for _ in range(m)]
+    for r, c in enumerate(comms):
+        c.allgather(rs[r], ag[r], sendcount=B_, dtype=dtype)
+    torch.cuda.synchronize()
+    full = OC.allgather(want)
+    assert_bitwise(full, OC.naive_reduce(sends, dtype, "sum"))
+    for r in range(m):
+        assert_bitwise(to_host(ag[r], dtype), full)
+
+
+def test_allgather_inplace_and_rs_max(B):
+    m, B_ = 5, 12345
+    comms = make_comms(B, m)
+    sends = synth.inputs(110, m, B_, "f32")
+    bufs = [sentinel(m * B_, "f32") for _ in range(m)]
+    for r in range(m):
+        bufs[r][r * B_:(r + 1) * B_] = torch.from_numpy(sends[r]).cuda()
+    for r, c in enumerate(comms):
+        c.allgather(bufs[r][r * B_:(r + 1) * B_], bufs[r], sendcount=B_)
+    torch.cuda.synchronize()
+    for x in bufs:
+        assert_bitwise(x.cpu().numpy(), OC.allgather(sends))
+    big = synth.inputs(111, m, m * B_, "f32")
+    ds = [to_dev(s, "f32") for s in big]
+    out = [sentinel(B_, "f32") for _ in range(m)]
+    for r, c in enumerate(comms):
+        c.reduce_scatter(ds[r], out[r], op="max")
+    torch.cuda.synchronize()
+    want = OC.reduce_scatter(big, "f32", "max")
+    for r in range(m):
+        assert_bitwise(out[r].cpu().numpy(), want[r])
+
+
+def test_block_collectives_need_a_switch(B):
+    tri = triangle()
+    comms = make_comms(B, 3, graph=B.Graph.from_pairs(3, tri[1]))
+    x = torch.zeros(48, device="cuda")
+    y = torch.zeros(16, device="cuda")
+    for r, c in enumerate(comms):
+        if r < 2:
+            c.reduce_scatter(x, y)
+        else:
+            with pytest.raises(B.BlinkError) as e:
+                c.reduce_scatter(x, y)
+            assert e.value.code == 9

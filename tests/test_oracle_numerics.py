@@ -169,3 +169,37 @@ def test_c1_allreduce_split_matches_survey():
     plan = packing.plan_switch_allreduce(3)
     rngs = C.tree_element_ranges(plan, 262144, "f32")
     assert [hi - lo for lo, hi in rngs] == [87380, 87380, 87384]
+
+
+# ------------------------------------------------------------------ NEXT-3 duals
+@pytest.mark.parametrize("m", [1, 2, 3, 8])
+def test_reduce_scatter_then_allgather_is_onehop_allreduce(m):
+    # structural identity: RS followed by AG reproduces the one-hop AllReduce
+    # bit for bit (same trees, same operand order)
+    B = 1031
+    for dtype in ("f32", "bf16", "i32"):
+        sends = synth.inputs(12, m, m * B, dtype)
+        rs = C.reduce_scatter(sends, dtype, "sum")
+        ag = C.allgather(rs)
+        ar = C.allreduce(packing.plan_switch_allreduce(m), sends, dtype, "sum")
+        # the AllReduce splits by 16-byte grains, RS by blocks; compare element-wise
+        # on the union: both are the per-element ascending-rank reduction
+        assert np.array_equal(bits_of(ag), bits_of(C.naive_reduce(sends, dtype, "sum")))
+        assert np.array_equal(bits_of(ar), bits_of(ag))
+
+
+def bits_of(a):
+    a = np.asarray(a)
+    return a.view(np.uint16) if a.dtype.itemsize == 2 else a.view(np.uint32)
+
+
+def test_reduce_scatter_int_exact_and_allgather_blocks():
+    m, B = 5, 77
+    sends = synth.inputs(13, m, m * B, "i32")
+    rs = C.reduce_scatter(sends, "i32", "max")
+    for j in range(m):
+        for e in range(B):
+            assert int(rs[j][e]) == max(int(s[j * B + e]) for s in sends)
+    ag = C.allgather([s[:B] for s in sends])
+    for j in range(m):
+        assert ag[j * B:(j + 1) * B].tobytes() == sends[j][:B].tobytes()
