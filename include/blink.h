@@ -97,7 +97,10 @@ typedef struct {
  *   onehop_bcast_max_bytes  switch graphs: Broadcast below this size uses the
  *                  single one-hop star, above it the m-1 two-level trees
  *   staging_bytes  multi-process: size of the library-owned symmetric staging
- *                  buffer used for unregistered user buffers; default 64 MiB */
+ *                  buffer used for unregistered user buffers; default 64 MiB
+ *   autotune       1 = MIAD chunk-size selection across calls (P:526-535,
+ *                  single-process comms; chunking never changes results);
+ *                  0 = the static table (default) */
 typedef struct {
   double mwu_eps;
   double ilp_gap;
@@ -107,7 +110,25 @@ typedef struct {
   double timeout_s;
   size_t onehop_bcast_max_bytes;
   size_t staging_bytes;
+  int autotune;
 } blink_config_t;
+
+/* MIAD controller: "initialize the chunk size with a small value
+ * and increase the chunk size by a multiplicative factor as long as the
+ * measured throughput is increasing.  If the throughput decreases we additively
+ * decrease the chunk size until we reach a steady state."  init = 1 MiB,
+ * factor 2, additive step = init, "increasing" = more than 1% better.
+ * blink_miad_init sets the state; each blink_miad_step feeds the throughput
+ * measured with state->chunk and returns the chunk size to use next.  Pure host
+ * function (the runtime drives it from CUDA-event timings when cfg.autotune). */
+typedef struct {
+  size_t chunk, best, init, step, min_chunk, max_chunk;
+  double last_thr, best_thr, tol;
+  int phase; /* 0 multiplicative increase, 1 additive decrease, 2 steady */
+  int iters;
+} blink_miad_t;
+void blink_miad_init(blink_miad_t* st, size_t init, size_t min_chunk, size_t max_chunk);
+size_t blink_miad_step(blink_miad_t* st, double throughput);
 
 void blink_config_default(blink_config_t* cfg);
 
@@ -196,6 +217,7 @@ typedef struct {
   int last_ctas;
   int last_chunks;
   int last_trees;
+  int64_t last_chunk_bytes;  /* chunk size of tree 0 in the last launch (MIAD trace) */
 } blink_stats_t;
 blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* stats);
 blink_result_t blink_comm_info(blink_comm_t comm, int* nranks, int* rank, int* device);

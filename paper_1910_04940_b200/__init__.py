@@ -19,6 +19,9 @@ __all__ = ["BlinkError", "Comm", "Graph", "config", "plan_json", "init_all", "in
            "DTYPES", "OPS", "LIB_PATH"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libblink.so")
+from . import build as _build  # noqa: E402  (no package imports inside)
+if _build._stale() and os.path.exists(_build.NVCC):
+    _build.build()             # sources changed since the last build (dev checkout)
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1910_04940_b200.build` "
                       "(there is no fallback implementation)")
@@ -44,12 +47,22 @@ class _Config(ctypes.Structure):
     _fields_ = [("mwu_eps", ctypes.c_double), ("ilp_gap", ctypes.c_double),
                 ("chunk_bytes", ctypes.c_size_t), ("ctas", ctypes.c_int), ("threads", ctypes.c_int),
                 ("timeout_s", ctypes.c_double), ("onehop_bcast_max_bytes", ctypes.c_size_t),
-                ("staging_bytes", ctypes.c_size_t)]
+                ("staging_bytes", ctypes.c_size_t), ("autotune", ctypes.c_int)]
+
+
+class Miad(ctypes.Structure):
+    """blink_miad_t: the MIAD chunk-size controller state."""
+    _fields_ = [("chunk", ctypes.c_size_t), ("best", ctypes.c_size_t), ("init", ctypes.c_size_t),
+                ("step", ctypes.c_size_t), ("min_chunk", ctypes.c_size_t),
+                ("max_chunk", ctypes.c_size_t), ("last_thr", ctypes.c_double),
+                ("best_thr", ctypes.c_double), ("tol", ctypes.c_double), ("phase", ctypes.c_int),
+                ("iters", ctypes.c_int)]
 
 
 class _Stats(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("last_ctas", ctypes.c_int),
-                ("last_chunks", ctypes.c_int), ("last_trees", ctypes.c_int)]
+                ("last_chunks", ctypes.c_int), ("last_trees", ctypes.c_int),
+                ("last_chunk_bytes", ctypes.c_int64)]
 
 
 _vp, _sz, _i, _cp = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_char_p
@@ -72,6 +85,8 @@ _SIGS = {
     "blink_get_stats": (_i, [_vp, ctypes.POINTER(_Stats)]),
     "blink_comm_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "blink_destroy": (_i, [_vp]),
+    "blink_miad_init": (None, [ctypes.POINTER(Miad), _sz, _sz, _sz]),
+    "blink_miad_step": (_sz, [ctypes.POINTER(Miad), ctypes.c_double]),
     "blink_result_string": (_cp, [_i]),
     "blink_last_error": (_cp, [_vp]),
 }
@@ -121,6 +136,13 @@ class Graph:
 
     def ptr(self):
         return ctypes.byref(self._g)
+
+
+def miad(init=1 << 20, min_chunk=16 << 10, max_chunk=64 << 20):
+    """A MIAD controller: returns (state, step) where step(throughput) -> next chunk."""
+    st = Miad()
+    _lib.blink_miad_init(ctypes.byref(st), init, min_chunk, max_chunk)
+    return st, (lambda thr: _lib.blink_miad_step(ctypes.byref(st), float(thr)))
 
 
 def _gptr(graph):
@@ -231,7 +253,7 @@ class Comm:
         s = _Stats()
         _check(_lib.blink_get_stats(self._h, ctypes.byref(s)), self._h)
         return dict(launches=s.launches, last_ctas=s.last_ctas, last_chunks=s.last_chunks,
-                    last_trees=s.last_trees)
+                    last_trees=s.last_trees, last_chunk_bytes=s.last_chunk_bytes)
 
     def register(self, buf, nbytes, exchange):
         """Symmetric registration (multi-process).  `exchange(bytes) -> list[bytes]`

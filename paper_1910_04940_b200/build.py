@@ -6,6 +6,8 @@ The library statically links the CUDA runtime and never links libcuda (driver
 symbols are fetched through cudaGetDriverEntryPoint), so it loads on a
 GPU-less box for the symbol-export tests.
 """
+import fcntl
+import hashlib
 import os
 import subprocess
 import sys
@@ -20,17 +22,35 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-O3,-Wall", "-Xptxas", "-v", "-cudart", "static"]
 
 
+def _src_hash():
+    h = hashlib.sha256()
+    for d in [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [__file__]:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def _stale():
-    if not os.path.exists(LIB):
+    """The library is stale when the hash of its sources changed (content, not
+    mtimes: snapshots copied to the GPU box keep a fresh build fresh)."""
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".srchash"):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [__file__]
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(LIB + ".srchash") as f:
+        return f.read().strip() != _src_hash()
 
 
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
+    os.makedirs(os.path.join(CSRC, "build"), exist_ok=True)
+    with open(os.path.join(CSRC, "build", ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)     # concurrent importers build once
+        if not force and not _stale():
+            return LIB
+        return _build(verbose)
+
+
+def _build(verbose):
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, "build", src + ".o")
@@ -53,6 +73,8 @@ def build(force=False, verbose=False):
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
     os.replace(tmp, LIB)
+    with open(LIB + ".srchash", "w") as f:
+        f.write(_src_hash())
     return LIB
 
 

@@ -22,6 +22,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <unistd.h>
 #include <vector>
@@ -51,7 +52,9 @@ struct SizedKey {
   int coll, root, dtype;
   size_t count;
   uint64_t launch_mask;
+  size_t chunk = 0;  // MIAD override (0 = static table)
   bool operator<(const SizedKey& o) const {
+    if (chunk != o.chunk) return chunk < o.chunk;
     if (coll != o.coll) return coll < o.coll;
     if (root != o.root) return root < o.root;
     if (dtype != o.dtype) return dtype < o.dtype;
@@ -135,6 +138,12 @@ struct Clique {
   // per device state
   std::map<int, int*> err_host, err_dev;
   std::map<int, uint64_t*> ctrl;  // per device: launch epoch + done counter
+  struct MiadRun {
+    blink_miad_t st;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool pending = false;
+  };
+  std::map<std::tuple<int, int, int, size_t>, MiadRun> miad;  // (coll, root, dtype, count)
   std::map<SizedKey, Sized> sized;
   int64_t launches = 0;
   bool sticky_error = false;
@@ -167,6 +176,7 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
   if (const char* e = getenv("BLINK_THREADS")) r.threads = atoi(e);
   if (const char* e = getenv("BLINK_CTAS")) r.ctas = atoi(e);
   if (const char* e = getenv("BLINK_CHUNK_BYTES")) r.chunk_bytes = size_t(atoll(e));
+  if (const char* e = getenv("BLINK_MIAD")) r.autotune = atoi(e);
   if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
   if (!(r.ilp_gap > 0 && r.ilp_gap < 1)) r.ilp_gap = d.ilp_gap;
   if (r.threads <= 0) r.threads = d.threads;
@@ -238,7 +248,9 @@ struct Channel {
 // CTA / channel assignment for the ranks in `launch_mask` (a6) and the device
 // tables of one launch.
 blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, int esize,
-                           uint64_t launch_mask, int budget, Sized* s) {
+                           uint64_t launch_mask, int budget, Sized* s, size_t chunk_override = 0) {
+  blink_config_t cfg = comm->cfg;
+  if (chunk_override) cfg.chunk_bytes = chunk_override;
   const int n = plan.nranks;
   const int k = int(plan.trees.size());
   std::vector<std::vector<uint32_t>> ch(k, std::vector<uint32_t>(n, 0));
@@ -248,7 +260,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   // provisional byte shares (equal CTAs hint) to weigh channels
   std::vector<TreeRange> r0;
   std::string err;
-  blink_result_t rr = size_plan(plan, count, esize, comm->cfg, 1, &r0, &err);
+  blink_result_t rr = size_plan(plan, count, esize, cfg, 1, &r0, &err);
   if (rr != BLINK_SUCCESS) return fail(comm, rr, err);
   std::vector<Channel> chans;
   std::vector<int> rank_has(n, 0);
@@ -302,7 +314,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   s->ranges.clear();
   for (int i = 0; i < k; ++i) {
     std::vector<TreeRange> ri;
-    rr = size_plan(plan, count, esize, comm->cfg, hint[i], &ri, &err);
+    rr = size_plan(plan, count, esize, cfg, hint[i], &ri, &err);
     if (rr != BLINK_SUCCESS) return fail(comm, rr, err);
     s->ranges.push_back(ri[i]);
   }
@@ -468,6 +480,27 @@ blink_result_t clique_launch(Clique* q) {
   }
   if (is_block_coll(q->coll) && (bytes % kGrain) != 0) vec = false;  // block starts unaligned
   const bool all_one_launch = q->devices.size() == 1;
+  // MIAD: the chunk size for this call from the previous calls'
+  // measured throughput (single host thread decides for every rank)
+  Clique::MiadRun* mr = nullptr;
+  size_t chunk_override = 0;
+  if (c0->cfg.autotune) {
+    auto mk = std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count);
+    auto mit = q->miad.find(mk);
+    if (mit == q->miad.end()) {
+      mit = q->miad.emplace(mk, Clique::MiadRun()).first;
+      blink_miad_init(&mit->second.st, size_t(1) << 20, 16 << 10, size_t(64) << 20);
+    }
+    mr = &mit->second;
+    if (mr->pending && cudaEventQuery(mr->ev1) == cudaSuccess) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, mr->ev0, mr->ev1);
+      if (ms > 0.f) blink_miad_step(&mr->st, double(bytes) / (double(ms) * 1e-3));
+      mr->pending = false;
+    }
+    chunk_override = mr->st.phase == 2 ? mr->st.best : mr->st.chunk;
+  }
+  bool timed = false;
   for (int dev : q->devices) {
     uint64_t mask = 0;
     for (int v = 0; v < n; ++v)
@@ -477,12 +510,13 @@ blink_result_t clique_launch(Clique* q) {
       if ((mask >> v) & 1) cd = q->comms[v];
     SizedKey key{q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count,
                  mask | (uint64_t(plan->trees.size()) << 32) |
-                     (uint64_t(q->coll == kBroadcast && plan->trees.size() == 1) << 48)};
+                     (uint64_t(q->coll == kBroadcast && plan->trees.size() == 1) << 48),
+                 chunk_override};
     auto it = q->sized.find(key);
     if (it == q->sized.end()) {
       Sized s;
       int budget = co_resident_budget(cd, dev, q->dtype, q->op, q->coll);
-      r = build_sized(cd, *plan, q->count, es, mask, budget, &s);
+      r = build_sized(cd, *plan, q->count, es, mask, budget, &s, chunk_override);
       if (r != BLINK_SUCCESS) return r;
       r = finalize_tables(cd, dev, es, &s);
       if (r != BLINK_SUCCESS) return r;
@@ -532,9 +566,22 @@ blink_result_t clique_launch(Clique* q) {
       CUDA_TRY(cd, cudaStreamWaitEvent(ls, e, 0));
       evs.push_back(e);
     }
+    const bool time_it = mr && !timed && !mr->pending && mr->st.phase != 2;
+    if (time_it) {
+      if (!mr->ev0) {
+        CUDA_TRY(cd, cudaEventCreate(&mr->ev0));
+        CUDA_TRY(cd, cudaEventCreate(&mr->ev1));
+      }
+      CUDA_TRY(cd, cudaEventRecord(mr->ev0, ls));
+    }
     cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, use_coop());
     if (le != cudaSuccess)
       return fail(cd, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
+    if (time_it) {
+      CUDA_TRY(cd, cudaEventRecord(mr->ev1, ls));
+      mr->pending = true;
+      timed = true;
+    }
     q->launches++;
     for (int v = 0; v < n; ++v) {
       if (!((mask >> v) & 1)) continue;
@@ -542,6 +589,7 @@ blink_result_t clique_launch(Clique* q) {
       q->comms[v]->stats.last_ctas = s.ctas;
       q->comms[v]->stats.last_chunks = s.chunks;
       q->comms[v]->stats.last_trees = int(plan->trees.size());
+      q->comms[v]->stats.last_chunk_bytes = s.ranges.empty() ? 0 : s.ranges[0].chunk * es;
     }
     if (!evs.empty()) {
       cudaEvent_t done;
@@ -701,6 +749,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   comm->stats.last_ctas = s.ctas;
   comm->stats.last_chunks = s.chunks;
   comm->stats.last_trees = int(plan->trees.size());
+  comm->stats.last_chunk_bytes = s.ranges.empty() ? 0 : s.ranges[0].chunk * es;
   return BLINK_SUCCESS;
 }
 
@@ -811,6 +860,54 @@ void blink_config_default(blink_config_t* c) {
   c->timeout_s = 30.0;
   c->onehop_bcast_max_bytes = 256 << 10;
   c->staging_bytes = 64 << 20;
+  c->autotune = 0;
+}
+
+void blink_miad_init(blink_miad_t* st, size_t init, size_t min_chunk, size_t max_chunk) {
+  if (!st) return;
+  memset(st, 0, sizeof *st);
+  st->min_chunk = std::max<size_t>(kGrain, min_chunk);
+  st->max_chunk = std::max(st->min_chunk, max_chunk);
+  st->init = std::min(std::max(init, st->min_chunk), st->max_chunk);
+  st->step = st->init;
+  st->chunk = st->init;
+  st->best = st->init;
+  st->tol = 0.01;
+}
+
+size_t blink_miad_step(blink_miad_t* st, double thr) {
+  if (!st) return 0;
+  st->iters++;
+  const bool first = st->iters == 1;
+  if (first || thr > st->best_thr) {
+    st->best_thr = thr;
+    st->best = st->chunk;
+  }
+  const bool increasing = first || thr > st->last_thr * (1.0 + st->tol);
+  st->last_thr = thr;
+  if (st->phase == 0) {                  // multiplicative increase
+    if (increasing && st->chunk * 2 <= st->max_chunk) {
+      st->chunk *= 2;
+    } else if (increasing) {             // hit the ceiling while still improving
+      st->phase = 2;
+      st->chunk = st->best;
+    } else {                             // throughput dropped: additive decrease
+      st->phase = 1;
+      st->chunk = st->chunk > st->step + st->min_chunk ? st->chunk - st->step : st->best;
+      if (st->chunk == st->best) st->phase = 2;
+    }
+  } else if (st->phase == 1) {           // additive decrease while it helps
+    if (increasing && st->chunk > st->step + st->min_chunk) {
+      st->chunk -= st->step;
+    } else {
+      st->phase = 2;
+      st->chunk = st->best;
+    }
+  } else {
+    st->chunk = st->best;
+  }
+  st->chunk = (st->chunk + kGrain - 1) / kGrain * kGrain;
+  return st->chunk;
 }
 
 const char* blink_result_string(blink_result_t r) {
@@ -1246,6 +1343,10 @@ blink_result_t blink_destroy(blink_comm_t comm) {
       }
       for (auto& kv : q->err_host) cudaFreeHost(kv.second);
       for (auto& kv : q->ctrl) cudaFree(kv.second);
+      for (auto& kv : q->miad) {
+        if (kv.second.ev0) cudaEventDestroy(kv.second.ev0);
+        if (kv.second.ev1) cudaEventDestroy(kv.second.ev1);
+      }
       delete q;
     }
   }

@@ -431,3 +431,25 @@ def test_block_collectives_need_a_switch(B):
             with pytest.raises(B.BlinkError) as e:
                 c.reduce_scatter(x, y)
             assert e.value.code == 9
+
+
+def test_miad_autotune_changes_chunking_not_results(B):
+    """NEXT-2: with cfg.autotune the chunk size moves across calls (MIAD,
+    P:526-535) while every call stays bit-exact (chunking never changes the
+    per-element operations)."""
+    m, count = 8, (2 << 20) + 7
+    comms = make_comms(B, m, autotune=1)
+    sends = synth.inputs(120, m, count, "f32")
+    want = OC.naive_reduce(sends, "f32", "sum")
+    ds = [to_dev(s, "f32") for s in sends]
+    out = [torch.empty_like(d) for d in ds]
+    chunks = set()
+    for it in range(14):
+        for r, c in enumerate(comms):
+            c.allreduce(ds[r], out[r])
+        torch.cuda.synchronize()
+        chunks.add(comms[0].stats()["last_chunks"])
+        if it % 4 == 0 or it == 13:
+            for x in out:
+                assert_bitwise(x.cpu().numpy(), want)
+    assert len(chunks) >= 2          # the tuner explored several chunk sizes
