@@ -142,6 +142,7 @@ struct Clique {
     blink_miad_t st;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool pending = false;
+    int calls = 0;  // the first call (plan + table build) is not timed
   };
   std::map<std::tuple<int, int, int, size_t>, MiadRun> miad;  // (coll, root, dtype, count)
   std::map<SizedKey, Sized> sized;
@@ -488,8 +489,17 @@ blink_result_t clique_launch(Clique* q) {
     auto mk = std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count);
     auto mit = q->miad.find(mk);
     if (mit == q->miad.end()) {
+      // start from the static table's chunk ("a small value"; the
+      // paper's 1 MB was for its hardware, R#15)
+      std::vector<TreeRange> rr;
+      std::string err;
+      const int hint = std::max(1, co_resident_budget(c0, c0->device, q->dtype, q->op, q->coll) /
+                                       std::max<int>(1, int(plan->trees.size())));
+      size_t init = size_t(1) << 20;
+      if (size_plan(*plan, q->count, es, c0->cfg, hint, &rr, &err) == BLINK_SUCCESS && !rr.empty())
+        init = size_t(rr[0].chunk) * es;
       mit = q->miad.emplace(mk, Clique::MiadRun()).first;
-      blink_miad_init(&mit->second.st, size_t(1) << 20, 16 << 10, size_t(64) << 20);
+      blink_miad_init(&mit->second.st, init, 16 << 10, size_t(64) << 20);
     }
     mr = &mit->second;
     if (mr->pending && cudaEventQuery(mr->ev1) == cudaSuccess) {
@@ -499,6 +509,7 @@ blink_result_t clique_launch(Clique* q) {
       mr->pending = false;
     }
     chunk_override = mr->st.phase == 2 ? mr->st.best : mr->st.chunk;
+    mr->calls++;
   }
   bool timed = false;
   for (int dev : q->devices) {
@@ -566,7 +577,7 @@ blink_result_t clique_launch(Clique* q) {
       CUDA_TRY(cd, cudaStreamWaitEvent(ls, e, 0));
       evs.push_back(e);
     }
-    const bool time_it = mr && !timed && !mr->pending && mr->st.phase != 2;
+    const bool time_it = mr && !timed && !mr->pending && mr->st.phase != 2 && mr->calls > 1;
     if (time_it) {
       if (!mr->ev0) {
         CUDA_TRY(cd, cudaEventCreate(&mr->ev0));

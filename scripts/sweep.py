@@ -11,6 +11,7 @@ MEASURED_PEAKS.json hbm_gbs:
   AllReduce : 2 m S   (every send read once, every recv written once)
   Broadcast : (m+1) S (root send read once, every recv written once)
 Config 5 replays the App. C DDP bucket sequences back to back on one stream.
+Times are device times of CUDA-graph replays (no host enqueue cost).
 """
 import argparse
 import json
@@ -33,14 +34,22 @@ ES = {"f32": 4, "bf16": 2, "i32": 4}
 
 
 def time_calls(fn, nbytes):
+    """Device time per call: one call is captured into a CUDA graph (epochs are
+    device-resident, so replays are valid) and replayed `reps` times; the
+    host-side cost of m binding calls per collective is not in the number."""
     reps = 50 if nbytes <= (1 << 20) else (20 if nbytes <= (64 << 20) else 5)
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        fn()
+        g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
