@@ -91,7 +91,7 @@ typedef struct {
  *   chunk_bytes    0 = size-dependent static table (a8), else fixed chunk size
  *   ctas           CTA budget per device launch; 0 = all co-resident CTAs
  *                  (occupancy x SM count)
- *   threads        threads per CTA (multiple of 32, <= 512); default 256
+ *   threads        threads per CTA (multiple of 32, 128..256); default 256
  *   timeout_s      flag-wait bound; expiry aborts the launch and the next call
  *                  returns BLINK_ERR_TIMEOUT; default 30
  *   onehop_bcast_max_bytes  switch graphs: Broadcast below this size uses the

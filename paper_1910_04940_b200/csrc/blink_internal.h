@@ -87,9 +87,11 @@ struct DevTask {             // one per CTA; 64 bytes
   uint32_t leafmask;         // children that are leaves (their send is read directly)
   int32_t cta_idx, cta_cnt;  // position among the CTAs of this (rank, tree, role)
   int32_t exit_idx, exit_cnt;// position among the CTAs of rank v (exit wait split)
-  int32_t do_entry;          // this CTA publishes rank v's entry flag
+  int32_t do_entry;          // this task publishes rank v's entry flag
+  int32_t next;              // next task (segment) of the same CTA, -1 = none
+  int32_t c0, c1, cstride;   // chunks c = c0, c0+cstride, ... < c1 of tree `tree`
   int32_t pad0;
-  int64_t pad1[3];
+  int64_t pad1;
 };
 static_assert(sizeof(DevTask) == 64, "DevTask layout");
 

@@ -392,20 +392,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Per-chunk readiness (a5): the producer acquires the chunk's inputs.
+// Warp-cooperative wait: lane u polls flag ptr_of(u) for every bit u of
+// `mask`, so the round trips overlap; each polling lane fences (acquire
+// pattern) and the warp agrees with __all_sync.  Call with the full warp.
+template <class F>
+__device__ __forceinline__ bool warp_wait(uint32_t mask, F ptr_of, const Ctl& ctl) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  if ((mask >> lane) & 1u) {
+    ok = wait_ge(ptr_of(lane), ctl);
+    fence_acqrel(ctl.sys);
+  }
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Per-chunk readiness (a5): the producer warp acquires the chunk's inputs
+// (internal children's partials, or the parent's final value).
 __device__ __forceinline__ bool wait_chunk_inputs(const LaunchArgs& a, const DevTask& t, int c,
                                                   bool need_bflag, const Ctl& ctl) {
   uint64_t* myflags = a.flags[t.rank];
-  bool ok = true;
-  if (t.role == kRoleReduce) {
-    const uint32_t internal = t.children & ~t.leafmask;
-    for (int u = 0; u < a.nranks && ok; ++u)
-      if ((internal >> u) & 1u) ok = wait_ge(myflags + pflag_idx(t.tree, u, c), ctl);
-  } else if (need_bflag) {
-    ok = wait_ge(myflags + bflag_idx(t.tree, c), ctl);
-  }
-  fence_acqrel(ctl.sys);
-  return ok;
+  if (t.role == kRoleReduce)
+    return warp_wait(t.children & ~t.leafmask,
+                     [&](int u) { return myflags + pflag_idx(t.tree, u, c); }, ctl);
+  return warp_wait(need_bflag ? 1u : 0u, [&](int) { return myflags + bflag_idx(t.tree, c); }, ctl);
 }
 
 // Publish chunk c (all its stores are complete and fenced by the caller).
@@ -446,13 +455,16 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
   char* out = ring + avail;
   const uint32_t NS = uint32_t(stages), K = uint32_t(kOutBufs);
   uint32_t g = 0;  // tile sequence number (identical in every role)
-  for (int c = t.cta_idx; c < tr.nchunks; c += t.cta_cnt) {
+  for (int c = t.c0; c < t.c1; c += t.cstride) {
     const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
     const int64_t b1 = min(tr.hi, b0 + tr.chunk);
     const int64_t body = ((b1 - b0) >> 4) << 4;
     if (body != b1 - b0) {
       // ---- tail chunk: every thread, LSU path
-      if (threadIdx.x == 0) sh.ok = !sh.abort && wait_chunk_inputs(a, t, c, need_bflag, ctl);
+      if (warp == 0) {
+        const bool ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
+        if (lane == 0) sh.ok = ok && !sh.abort;
+      }
       __syncthreads();
       const bool ok = sh.ok;
       if (ok) {
@@ -470,9 +482,11 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       continue;
     }
     const int ntiles = int((body + tile - 1) / tile);
-    if (warp == 0 && lane == 0) {
-      // ---------------- producer
-      if (sh.abort || !wait_chunk_inputs(a, t, c, need_bflag, ctl)) {
+    if (warp == 0) {
+      // ---------------- producer (the warp acquires, lane 0 issues)
+      const bool ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
+      if (lane != 0) {
+      } else if (!ok || sh.abort) {
         sh.abort = 1;
       } else {
         fence_proxy_async();
@@ -548,8 +562,11 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
 template <int DT, int OP, bool VEC>
 __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
                         bool need_bflag, Shared& sh, const Ctl& ctl) {
-  for (int c = t.cta_idx; c < tr.nchunks; c += t.cta_cnt) {
-    if (threadIdx.x == 0) sh.ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
+  for (int c = t.c0; c < t.c1; c += t.cstride) {
+    if (threadIdx.x < 32) {
+      const bool ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
+      if (threadIdx.x == 0) sh.ok = ok;
+    }
     __syncthreads();
     const bool ok = sh.ok;
     if (ok) {
@@ -567,63 +584,78 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
 }
 
 template <int DT, int OP, bool VEC>
-__global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a_in) {
+__global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   __shared__ Shared sh;
   __shared__ uint64_t s_epoch;
   extern __shared__ __align__(128) char s_ring[];
   // Epoch = launches completed on this device group + 1, read from device
   // memory so that CUDA-graph replays get fresh epochs.
   const LaunchArgs& a = a_in;
-  const DevTask t = a.tasks[blockIdx.x];
+  const DevTask t0 = a.tasks[blockIdx.x];
   if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
   __syncthreads();
-  const int v = t.rank;
+  const int v = t0.rank;
   const Ctl ctl{s_epoch, a.timeout_ns, a.err, a.scope_sys != 0};
   uint64_t* myflags = a.flags[v];
   const bool ws = VEC && a.use_tma && blockDim.x >= 128;
 
-  // entry: my send is ready and my recv may be overwritten (epoch e)
-  if (t.do_entry && threadIdx.x == 0) {
-    fence_acqrel(ctl.sys);
-    for (int u = 0; u < a.nranks; ++u)
-      if (u != v) st_relaxed(a.flags[u] + entry_idx(v), ctl.epoch, ctl.sys);
+  // entry: my send is ready and my recv may be overwritten (epoch e).  Every
+  // segment of this CTA publishes its entry before any segment waits.
+  if (threadIdx.x == 0) {
+    bool fenced = false;
+    for (int ti = blockIdx.x; ti >= 0; ti = a.tasks[ti].next) {
+      const DevTask& tt = a.tasks[ti];
+      if (!tt.do_entry) continue;
+      if (!fenced) fence_acqrel(ctl.sys);
+      fenced = true;
+      for (int u = 0; u < a.nranks; ++u)
+        if (u != tt.rank) st_relaxed(a.flags[u] + entry_idx(tt.rank), ctl.epoch, ctl.sys);
+    }
   }
 
-  if (t.role == kRoleReduce || t.role == kRoleBcast) {
+  // segments: usually one; packed launches chain contiguous chunk ranges of
+  // independent channels so that every SM carries the same number of bytes
+  for (int ti = blockIdx.x; ti >= 0;) {
+    const DevTask t = a.tasks[ti];
+    ti = t.next;
+    if (t.role != kRoleReduce && t.role != kRoleBcast) continue;
+    const int w = t.rank;
+    uint64_t* wflags = a.flags[w];
     const DevTree tr = a.trees[t.tree];
     const bool is_root = t.parent < 0;
+    // entry handshake (warp 0): leaf children's send is ready once they
+    // entered; Broadcast / AllGather push into children's recv only after they
+    // entered
+    bool entry_ok = true;
+    if (threadIdx.x < 32) {
+      const bool pushes = a.coll == kBroadcast || a.coll == kAllGather;
+      const uint32_t emask = t.role == kRoleReduce ? t.leafmask : (pushes ? t.children : 0u);
+      entry_ok = warp_wait(emask, [&](int u) { return wflags + entry_idx(u); }, ctl);
+    }
     if (threadIdx.x == 0) {
       int ns = 0, nd = 0;
-      bool ok = true;
+      const bool ok = entry_ok;
       if (t.role == kRoleReduce) {
-        const uint32_t ops = t.children | (1u << v);
+        const uint32_t ops = t.children | (1u << w);
         for (int u = 0; u < a.nranks; ++u) {
           if (!((ops >> u) & 1u)) continue;
-          sh.srcs[ns++] = (u == v || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
+          sh.srcs[ns++] = (u == w || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
         }
-        sh.dsts[nd++] = a.recv[v];
+        sh.dsts[nd++] = a.recv[w];
         if (is_root && a.coll == kAllReduce)  // ReduceScatter keeps the result at the root
           for (int u = 0; u < a.nranks; ++u)
             if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
-        // leaf children: their send is ready once they entered
-        for (int u = 0; u < a.nranks && ok; ++u)
-          if ((t.leafmask >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       } else {
         const bool src_root = (a.coll == kBroadcast || a.coll == kAllGather) && is_root;
-        sh.srcs[ns++] = src_root ? a.send[v] : a.recv[v];
-        if (src_root && a.send[v] != a.recv[v]) sh.dsts[nd++] = a.recv[v];
+        sh.srcs[ns++] = src_root ? a.send[w] : a.recv[w];
+        if (src_root && a.send[w] != a.recv[w]) sh.dsts[nd++] = a.recv[w];
         for (int u = 0; u < a.nranks; ++u)
           if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
-        // Broadcast / AllGather push into children's recv: they must have entered
-        if (a.coll == kBroadcast || a.coll == kAllGather)
-          for (int u = 0; u < a.nranks && ok; ++u)
-            if ((t.children >> u) & 1u) ok = wait_ge(myflags + entry_idx(u), ctl);
       }
-      fence_acqrel(ctl.sys);
       sh.nsrc = ns;
       sh.ndst = nd;
       sh.abort = ok ? 0 : 1;
-      if (ws) {
+      if (ws) {  // (re)initialise the ring's barriers: every segment starts drained
         const uint32_t ncw = t.role == kRoleReduce ? (blockDim.x >> 5) - 2 : 1;
         for (int k = 0; k < kMaxStages; ++k) {
           mbar_init(&sh.full[k], 1);
@@ -639,13 +671,17 @@ __global__ void __launch_bounds__(512, 1) exec_kernel(const LaunchArgs a_in) {
     __syncthreads();
     const bool need_bflag =
         (t.role == kRoleBcast) && !((a.coll == kBroadcast || a.coll == kAllGather) && is_root);
-    if (!sh.abort) {
+    const bool aborted = sh.abort;
+    if (!aborted) {
       if (ws)
         run_ws<DT, OP>(a, t, tr, is_root, need_bflag, sh, s_ring, ctl);
       else
         run_lsu<DT, OP, VEC>(a, t, tr, is_root, need_bflag, sh, ctl);
     }
+    __syncthreads();  // segment drained; smem (lists, barriers) may be reused
+    if (aborted) break;
   }
+  const DevTask& t = t0;
 
   // exit: every final chunk of every tree not rooted here has arrived, which
   // also means every peer finished reading this rank's buffers (causality).

@@ -22,6 +22,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <numeric>
 #include <tuple>
 #include <string>
 #include <unistd.h>
@@ -181,7 +182,8 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
   if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
   if (!(r.ilp_gap > 0 && r.ilp_gap < 1)) r.ilp_gap = d.ilp_gap;
   if (r.threads <= 0) r.threads = d.threads;
-  if (r.threads > 512) r.threads = 512;
+  if (r.threads > 256) r.threads = 256;  // __launch_bounds__(256, 1)
+  if (r.threads < 128) r.threads = 128;  // producer + store + >= 2 consumer warps
   r.threads = (r.threads + 31) / 32 * 32;
   if (!(r.timeout_s > 0)) r.timeout_s = d.timeout_s;
   if (r.staging_bytes == 0) r.staging_bytes = d.staging_bytes;
@@ -309,6 +311,113 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
     --it->ctas;
     --used;
   }
+  // ---- packed assignment (opt-in, BLINK_PACK=1; measured no faster than the
+  // per-channel split on the 1-GPU bench): one launch holding every rank whose channels are
+  // independent (no chunk-level waits: one-hop roots) and equally loaded.
+  // Every CTA gets the same number of chunks as a contiguous range of the
+  // global chunk list, possibly spanning two trees (chained segments).
+  {
+    bool packable = launch_mask == ((n >= 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1)) &&
+                    !chans.empty() && cfg.chunk_bytes == 0 && getenv("BLINK_PACK") != nullptr;
+    for (auto& c : chans) {
+      const bool indep =
+          c.parent < 0 && ((c.role == kRoleReduce && c.leafmask == c.children) ||
+                           (c.role == kRoleBcast && (plan.coll == kBroadcast || plan.coll == kAllGather)));
+      packable = packable && indep && std::fabs(c.work - chans[0].work) <= 1e-3 * chans[0].work + 64;
+    }
+    const int B = budget;
+    const int nch = int(chans.size());
+    if (packable) {
+      const int g = std::gcd(nch, B);
+      const int per = B * (nch / g) / nch;  // chunks per channel; total = B * (nch / g)
+      const int64_t tbytes = (r0[chans[0].tree].hi - r0[chans[0].tree].lo) * esize;
+      int64_t chunk = ((tbytes + per - 1) / per + kGrain - 1) / kGrain * kGrain;
+      if (per <= kMaxChunks && chunk >= (4 << 10)) {
+        blink_config_t c2 = cfg;
+        c2.chunk_bytes = size_t(chunk);
+        std::vector<TreeRange> ri;
+        if (size_plan(plan, count, esize, c2, 1, &ri, &err) != BLINK_SUCCESS)
+          return fail(comm, BLINK_ERR_INTERNAL, err);
+        s->ranges = ri;
+        // global chunk list: channel-major
+        std::vector<std::pair<int, int>> items;  // (channel, chunk)
+        for (int ci = 0; ci < nch; ++ci)
+          for (int c = 0; c < s->ranges[chans[ci].tree].nchunks; ++c) items.push_back({ci, c});
+        const int64_t T = int64_t(items.size());
+        s->tasks.assign(B, DevTask{});
+        std::vector<DevTask> extra;
+        std::vector<int> entry_done(n, 0);
+        auto mk = [&](int ci, int c0, int c1) {
+          const Channel& ch = chans[ci];
+          DevTask t{};
+          t.rank = int16_t(ch.rank);
+          t.tree = int16_t(ch.tree);
+          t.role = int16_t(ch.role);
+          t.parent = int16_t(ch.parent);
+          t.children = ch.children;
+          t.leafmask = ch.leafmask;
+          t.c0 = c0;
+          t.c1 = c1;
+          t.cstride = 1;
+          t.cta_cnt = 1;
+          t.exit_cnt = 1;
+          t.next = -1;
+          if (!entry_done[ch.rank]) {
+            t.do_entry = 1;
+            entry_done[ch.rank] = 1;
+          }
+          return t;
+        };
+        for (int k = 0; k < B; ++k) {
+          const int64_t a0 = k * T / B, a1 = (k + 1) * T / B;
+          std::vector<DevTask> segs;
+          int64_t i = a0;
+          while (i < a1) {
+            const int ci = items[i].first;
+            int64_t j = i;
+            while (j < a1 && items[j].first == ci) ++j;
+            segs.push_back(mk(ci, items[i].second, items[j - 1].second + 1));
+            i = j;
+          }
+          if (segs.empty()) {  // more CTAs than chunks: an idle CTA
+            DevTask t{};
+            t.role = kRoleExit;
+            t.parent = -1;
+            t.cta_cnt = 1;
+            t.exit_cnt = 1;
+            t.next = -1;
+            segs.push_back(t);
+          }
+          s->tasks[k] = segs[0];
+          int* link = &s->tasks[k].next;
+          for (size_t q = 1; q < segs.size(); ++q) {
+            *link = B + int(extra.size());
+            extra.push_back(segs[q]);
+            link = &extra.back().next;
+          }
+        }
+        // ranks without a channel still publish their entry (chained on CTA 0)
+        for (int v = 0; v < n; ++v) {
+          if (entry_done[v]) continue;
+          DevTask t{};
+          t.rank = int16_t(v);
+          t.role = kRoleExit;
+          t.parent = -1;
+          t.cta_cnt = 1;
+          t.exit_cnt = 1;
+          t.do_entry = 1;
+          t.next = s->tasks[0].next;
+          s->tasks[0].next = B + int(extra.size());
+          extra.push_back(t);
+        }
+        s->tasks.insert(s->tasks.end(), extra.begin(), extra.end());
+        s->ctas = B;
+        s->chunks = int(T);
+        s->plan = &plan;
+        return BLINK_SUCCESS;
+      }
+    }
+  }
   // chunking with the CTA count of the busiest channel of each tree
   std::vector<int> hint(k, 1);
   for (auto& c : chans) hint[c.tree] = std::max(hint[c.tree], c.ctas);
@@ -339,6 +448,10 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
         t.leafmask = c.leafmask;
         t.cta_idx = j;
         t.cta_cnt = c.ctas;
+        t.next = -1;
+        t.c0 = j;
+        t.c1 = s->ranges[c.tree].nchunks;
+        t.cstride = c.ctas;
         s->tasks.push_back(t);
       }
     }
@@ -348,6 +461,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
       t.role = kRoleExit;
       t.parent = -1;
       t.cta_cnt = 1;
+      t.next = -1;
       s->tasks.push_back(t);
     }
     int cnt = int(s->tasks.size() - first);
