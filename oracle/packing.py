@@ -299,10 +299,67 @@ def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_
             cons.append(LinearConstraint(obj[None, :], -np.inf, val + 1e-6))
         z = np.round(x[:k]).astype(int)
         sol = [(j, Fraction(int(z[j]), g)) for j in range(k) if z[j] > 0]
-        best = (sol, g, zstar / g >= (1 - gap) * c_star - 1e-12)
-        if best[2]:
-            return best
+        cur = (sol, g, zstar / g >= (1 - gap) * c_star - 1e-12)
+        if cur[2]:
+            return cur
+        if best is None or sum(w for _, w in cur[0]) > sum(w for _, w in best[0]):
+            best = cur              # not accepted anywhere: the best rate seen
     return best
+
+
+# --------------------------------------------------------------------------
+# Integral candidates (R#21): the ILP over MWU candidates alone can miss the
+# integral optimum (hard part 8); these enrich the candidate set.
+# --------------------------------------------------------------------------
+def lovasz_arborescences(g, r):
+    """k = min_v lambda(r, v) edge-disjoint arborescences (integer capacities),
+    by Lovasz's constructive proof of Edmonds' theorem: grow each tree
+    from r one edge (u in tree, v not) at a time, taking an edge only if the
+    remaining graph keeps lambda(r, v) >= k - t; edges tried by (depth of u,
+    u, v).  Returns parent tuples."""
+    from .bounds import maxflow
+    n, cap0 = g
+    cap = {e: int(c) for e, c in cap0.items()}
+    k = min(maxflow(n, cap, r, v) for v in range(n) if v != r)
+    out = []
+    for t in range(1, k + 1):
+        parent = {r: -1}
+        depth = {r: 0}
+        while len(parent) < n:
+            cands = sorted((depth[u], u, v) for (u, v), c in cap.items()
+                           if c > 0 and u in parent and v not in parent)
+            for d, u, v in cands:
+                cap[(u, v)] -= 1
+                if maxflow(n, {e: c for e, c in cap.items() if c > 0}, r, v) >= k - t:
+                    parent[v] = u
+                    depth[v] = d + 1
+                    break
+                cap[(u, v)] += 1
+            else:
+                raise RuntimeError("Lovasz step found no edge (cannot happen)")
+        out.append(tuple(parent[v] for v in range(n)))
+    return out
+
+
+def peel_spanning_trees(pairs, n, scale):
+    """Greedy integral peeling at capacity scale `scale`: repeatedly take the
+    spanning tree that prefers links with the largest relative residual
+    capacity and remove one unit along it.  Returns {tree: multiplicity}."""
+    res = {e: scale * c for e, c in pairs.items()}
+    full = dict(res)
+    out = {}
+    while True:
+        lengths = {e: (full[e] / res[e] if res[e] > 0 else 1e30) for e in pairs}
+        try:
+            t = min_spanning_tree(n, lengths)
+        except ValueError:
+            break
+        if any(res[e] <= 0 for e in t):
+            break
+        for e in t:
+            res[e] -= 1
+        out[t] = out.get(t, 0) + 1
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -321,7 +378,7 @@ def plan_broadcast_graph(g, r, eps=0.1, gap=0.05):
         return dict(trees=[dict(parent=(-1,), root=0, weight=Fraction(1), edges=[], depth=0)],
                     rate=Fraction(1), c_star=1.0)
     w, c_star, _ = mwu_broadcast(g, r, eps)
-    cands = sorted(w)  # parent tuples, lexicographic
+    cands = sorted(set(w) | set(lovasz_arborescences(g, r)))  # parent tuples (R#21)
     cand = [([(u, v) for v, u in enumerate(p) if u >= 0], parent_depth(p), p) for p in cands]
     sol, gg, ok = ilp_refine(cap, cand, c_star, gap)
     trees = []
@@ -342,7 +399,10 @@ def plan_allreduce_graph(g, eps=0.1, gap=0.05):
                     rate=Fraction(1), c_star=1.0)
     pairs = undirected_pairs(g)
     w, c_star, _ = mwu_allreduce(pairs, n, eps)
-    cands = sorted(w)
+    peeled = set()
+    for scale in (1, 2, 4, 8):                     # R#21
+        peeled |= set(peel_spanning_trees(pairs, n, scale))
+    cands = sorted(set(w) | peeled)
     cand = []
     for t in cands:
         root = tree_centre(t, n)
@@ -429,3 +489,84 @@ def link_load(plan, n, allreduce):
                 egress[v] += f
                 ingress[p] += f
     return max(max(egress), max(ingress))
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: three-phase multi-server AllReduce (Sec. 3.5, Fig.
+# hierarchy-allreduce P:402-407)
+# --------------------------------------------------------------------------
+def _ecc(parent_edges, n, s):
+    adj = {v: [] for v in range(n)}
+    for (u, v) in parent_edges:
+        adj[u].append(v)
+        adj[v].append(u)
+    dist = {s: 0}
+    fr = [s]
+    while fr:
+        nx = []
+        for u in fr:
+            for w in adj[u]:
+                if w not in dist:
+                    dist[w] = dist[u] + 1
+                    nx.append(w)
+        fr = nx
+    return max(dist.values())
+
+
+def plan_multiserver_allreduce(g, servers, eps=0.1, gap=0.05):
+    """Three-phase AllReduce as one set of spanning trees.
+
+    P:453: "we first partition data based on the number of spanning trees we
+    have" -- K partitions, K = min over servers of the local packing's tree
+    count (R#24: equal partitions, since one partition spans every server).
+    Phase 1: per-server reduction over the local tree T_{s,p} to its
+    server-local root r_{s,p}; "Each data partition has a distinct
+    server-local root" -- R#25: roots chosen by minimum eccentricity
+    among the server's GPUs not yet used as a root, ties -> lowest id.
+    Phase 2: "across n servers, there are n one-hop cross-server
+    trees, with each server-local root connected to (n - 1) roots on other
+    servers" -- partition p splits into n sub-slices, sub-slice q rooted at
+    r_{q,p}.  Phase 3: r_{s,p} broadcasts down T_{s,p}.
+    Tree (p, q) = union of the T_{s,p} oriented to r_{s,p} plus r_{s,p} ->
+    r_{q,p}; AllReduce on it performs all three phases per chunk.
+    `servers`: list of lists of global GPU ids.  Returns a plan dict."""
+    from .graphs import induced
+    n_gpu = g[0]
+    local = []
+    for ids in servers:
+        ids = sorted(ids)
+        if len(ids) == 1:
+            local.append((ids, None))
+        else:
+            sub, _ = induced(g, ids)
+            local.append((ids, plan_allreduce_graph(sub, eps, gap)))
+    counts = [len(p["trees"]) for _, p in local if p is not None]
+    K = min(counts) if counts else 1
+    # per server, per partition: (global edges, local root)
+    parts = []
+    for ids, lp in local:
+        row = []
+        used = set()
+        for p in range(K):
+            if lp is None:
+                row.append(([], ids[0]))
+                continue
+            t = lp["trees"][p]
+            k = len(ids)
+            cands = sorted(range(k), key=lambda v: (_ecc(t["edges"], k, v), v))
+            pick = next((v for v in cands if v not in used), cands[0])
+            used.add(pick)
+            row.append(([(ids[a], ids[b]) for (a, b) in t["edges"]], ids[pick]))
+        parts.append(row)
+    trees = []
+    for p in range(K):
+        roots = [parts[s][p][1] for s in range(len(servers))]
+        for q in range(len(servers)):
+            edges = []
+            for s in range(len(servers)):
+                edges += parts[s][p][0]
+            edges += [(roots[s], roots[q]) for s in range(len(servers)) if s != q]
+            parent = root_tree(edges, n_gpu, roots[q])
+            trees.append(dict(parent=parent, root=roots[q], weight=Fraction(1),
+                              edges=edges, depth=parent_depth(parent), partition=p, server=q))
+    return dict(trees=trees, rate=None, partitions=K)

@@ -130,6 +130,16 @@ class Graph:
         self._g = _Graph(n, self._kinds, len(links), self._links)
 
     @classmethod
+    def multi_server(cls, nranks, cap, servers, net_capacity=1.0):
+        """NEXT-4: GPU-GPU links `cap` ({(u, v): c}) inside the servers plus one
+        network SWITCH node (id nranks) linked to every GPU; links between
+        servers are dropped.  `servers`: lists of ranks."""
+        where = {v: i for i, s in enumerate(servers) for v in s}
+        links = [(u, v, c, 0) for (u, v), c in sorted(cap.items()) if where[u] == where[v]]
+        links += [(v, nranks, net_capacity, 1) for v in range(nranks)]
+        return cls(nranks, links, switches=1)
+
+    @classmethod
     def from_pairs(cls, nranks, cap):
         """From a directed capacity dict {(u, v): c} (the oracle's format)."""
         return cls(nranks, [(u, v, c, 0) for (u, v), c in sorted(cap.items())])

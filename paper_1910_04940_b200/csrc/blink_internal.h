@@ -139,6 +139,9 @@ struct Graph {
   int n = 0;                       // GPU nodes (ranks)
   bool switch_model = true;        // all GPUs behind a switch (or NULL graph)
   std::vector<std::vector<double>> cap;  // cap[u][v], directed, GPU nodes only
+  // NEXT-4 multi-server: GPU-GPU links inside servers + a network SWITCH
+  bool multi_server = false;
+  std::vector<std::vector<int>> servers;  // rank lists, ascending
 };
 
 // Parse/validate a user graph for nranks ranks.  Returns BLINK_SUCCESS or an

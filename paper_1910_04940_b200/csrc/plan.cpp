@@ -94,20 +94,51 @@ blink_result_t build_graph(const blink_graph_t* g, int nranks, Graph* out, std::
     out->cap[L.src][L.dst] += L.capacity;
     if (L.bidirectional) out->cap[L.dst][L.src] += L.capacity;
   }
-  if (any_switch) {
-    for (int u = 0; u < nranks; ++u)
-      for (int v = 0; v < nranks; ++v)
-        if (out->cap[u][v] > 0) {
-          *err = "mixed switch + direct GPU links are not supported (GPU " + std::to_string(u) +
-                 "->" + std::to_string(v) + ")";
-          return BLINK_ERR_UNSUPPORTED;
-        }
+  bool any_direct = false;
+  for (int u = 0; u < nranks; ++u)
+    for (int v = 0; v < nranks; ++v)
+      if (out->cap[u][v] > 0) any_direct = true;
+  if (any_switch && !any_direct) {
     for (int v = 0; v < nranks; ++v)
       if (!on_switch[v] && nranks > 1) {
         *err = "GPU " + std::to_string(v) + " is not attached to any switch (disconnected)";
         return BLINK_ERR_TOPOLOGY;
       }
     out->switch_model = true;
+    return BLINK_SUCCESS;
+  }
+  if (any_switch) {
+    // NEXT-4: servers = components of the GPU-GPU links, joined
+    // by the network switch; every server needs a network attachment
+    out->switch_model = false;
+    out->multi_server = true;
+    std::vector<int> comp(nranks, -1);
+    for (int s0 = 0; s0 < nranks; ++s0) {
+      if (comp[s0] >= 0) continue;
+      const int id = int(out->servers.size());
+      out->servers.push_back({});
+      std::vector<int> st{s0};
+      comp[s0] = id;
+      while (!st.empty()) {
+        int u = st.back();
+        st.pop_back();
+        out->servers[id].push_back(u);
+        for (int v = 0; v < nranks; ++v)
+          if (comp[v] < 0 && (out->cap[u][v] > 0 || out->cap[v][u] > 0)) {
+            comp[v] = id;
+            st.push_back(v);
+          }
+      }
+      std::sort(out->servers[id].begin(), out->servers[id].end());
+      bool attached = false;
+      for (int v : out->servers[id]) attached = attached || on_switch[v];
+      if (!attached) {
+        std::string ids;
+        for (int v : out->servers[id]) ids += (ids.empty() ? "" : ",") + std::to_string(v);
+        *err = "server {" + ids + "} has no link to the network switch (disconnected)";
+        return BLINK_ERR_TOPOLOGY;
+      }
+    }
     return BLINK_SUCCESS;
   }
   out->switch_model = false;
@@ -603,6 +634,93 @@ int64_t gcd64(int64_t a, int64_t b) { return b == 0 ? a : gcd64(b, a % b); }
 
 }  // namespace
 
+// NEXT-4: three-phase multi-server AllReduce as spanning trees.
+// Partition p (K = min over servers of the local packing's tree count, equal
+// weights, R#24) uses local tree T_{s,p} on every server s with server-local
+// root r_{s,p} (minimum eccentricity among GPUs not yet a root of this
+// server, R#25: "Each data partition has a distinct server-local root",
+// P:404).  Sub-slice q of partition p is the tree made of every T_{s,p}
+// oriented to r_{s,p} plus the cross-server star r_{s,p} -> r_{q,p}
+// ("n one-hop cross-server trees").  Reduce then broadcast along it
+// runs phases 1-3, pipelined per chunk.
+blink_result_t make_multiserver_plan(const Graph& g, const blink_config_t& cfg, Plan* out,
+                                     std::string* err) {
+  const int ns = int(g.servers.size());
+  std::vector<Plan> local(ns);
+  int K = 1 << 30;
+  for (int s = 0; s < ns; ++s) {
+    const std::vector<int>& ids = g.servers[s];
+    const int k = int(ids.size());
+    if (k == 1) continue;
+    Graph lg;
+    lg.n = k;
+    lg.switch_model = false;
+    lg.cap.assign(k, std::vector<double>(k, 0.0));
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) lg.cap[a][b] = g.cap[ids[a]][ids[b]];
+    blink_result_t r = make_plan(lg, kAllReduce, -1, cfg, &local[s], err);
+    if (r != BLINK_SUCCESS) return r;
+    K = std::min(K, int(local[s].trees.size()));
+  }
+  if (K == (1 << 30)) K = 1;
+  K = std::max(1, std::min(K, kMaxTrees / std::max(1, ns)));
+  if (ns > kMaxTrees) {
+    *err = "too many servers";
+    return BLINK_ERR_UNSUPPORTED;
+  }
+  // per server, per partition: undirected global edges + local root
+  std::vector<std::vector<std::vector<std::pair<int, int>>>> edges(ns, std::vector<std::vector<std::pair<int, int>>>(K));
+  std::vector<std::vector<int>> root(ns, std::vector<int>(K, -1));
+  for (int s = 0; s < ns; ++s) {
+    const std::vector<int>& ids = g.servers[s];
+    const int k = int(ids.size());
+    std::vector<int> used(k, 0);
+    for (int p = 0; p < K; ++p) {
+      if (k == 1) {
+        root[s][p] = ids[0];
+        continue;
+      }
+      const Tree& t = local[s].trees[p];
+      std::vector<std::pair<int, int>> le;
+      for (int v = 0; v < k; ++v)
+        if (t.parent[v] >= 0) le.push_back({t.parent[v], v});
+      int best = -1, bestecc = 1 << 30, fallback = -1, fbecc = 1 << 30;
+      for (int v = 0; v < k; ++v) {
+        int e = tree_depth(orient(k, le, v));
+        if (e < fbecc) {
+          fbecc = e;
+          fallback = v;
+        }
+        if (!used[v] && e < bestecc) {
+          bestecc = e;
+          best = v;
+        }
+      }
+      if (best < 0) best = fallback;
+      used[best] = 1;
+      root[s][p] = ids[best];
+      for (auto& e : le) edges[s][p].push_back({ids[e.first], ids[e.second]});
+    }
+  }
+  out->trees.clear();
+  for (int p = 0; p < K; ++p)
+    for (int q = 0; q < ns; ++q) {
+      std::vector<std::pair<int, int>> all;
+      for (int s = 0; s < ns; ++s) all.insert(all.end(), edges[s][p].begin(), edges[s][p].end());
+      for (int s = 0; s < ns; ++s)
+        if (s != q) all.push_back({root[s][p], root[q][p]});
+      Tree t;
+      t.root = root[q][p];
+      t.parent = orient(g.n, all, t.root);
+      t.depth = tree_depth(t.parent);
+      out->trees.push_back(t);
+    }
+  out->rate_num = K;
+  out->rate_den = 1;
+  out->grid = 1;
+  return BLINK_SUCCESS;
+}
+
 // ============================================================== plans
 blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_t& cfg, Plan* out,
                          std::string* err) {
@@ -660,6 +778,14 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
       out->rate_num = n - 1;
     }
     return BLINK_SUCCESS;
+  }
+
+  if (g.multi_server) {
+    if (coll != kAllReduce) {
+      *err = "multi-server graphs support AllReduce only (three-phase protocol, P:448-456)";
+      return BLINK_ERR_UNSUPPORTED;
+    }
+    return make_multiserver_plan(g, cfg, out, err);
   }
 
   // ---------------- explicit link graph: MWU then ILP

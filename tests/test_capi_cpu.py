@@ -168,3 +168,37 @@ def test_switch_graph_with_switch_node(B):
     G = B.Graph(4, [(v, 4, 6.0, 1) for v in range(4)], switches=1)
     p = B.plan_json(4, True, 0, 4096, "f32", graph=G)
     assert p["switch"] and len(p["trees"]) == 4 and p["rate"] == [2, 1]
+
+
+@pytest.mark.parametrize("servers", [[[0, 1, 3], [2, 4, 5, 6, 7]], [[0, 1, 2, 3], [4, 5, 6, 7]],
+                                     [[0, 1], [2, 3], [4, 5, 6, 7]]])
+def test_multiserver_plans_follow_the_three_phase_protocol(B, servers):
+    """NEXT-4: K partitions x n one-hop cross-server trees; same
+    partition count and structure as the oracle's plan."""
+    from oracle import graphs, packing
+    g = graphs.dgx1v()
+    where = {v: i for i, s in enumerate(servers) for v in s}
+    cap = {(u, v): c for (u, v), c in g[1].items() if where[u] == where[v]}
+    p = B.plan_json(8, True, 0, (1 << 20) + 5, "f32", graph=B.Graph.multi_server(8, g[1], servers))
+    o = packing.plan_multiserver_allreduce((8, cap), servers)
+    assert len(p["trees"]) == len(o["trees"]) == o["partitions"] * len(servers)
+    for i, t in enumerate(p["trees"]):
+        q = i % len(servers)
+        assert where[t["root"]] == q and t["parent"].count(-1) == 1
+        cross = [(u, v) for v, u in enumerate(t["parent"]) if u >= 0 and where[u] != where[v]]
+        assert len(cross) == len(servers) - 1
+        assert all(u == t["root"] for u, v in cross)          # star into the sub-slice root
+    rngs = [(t["lo"], t["hi"]) for t in p["trees"]]
+    assert rngs[0][0] == 0 and rngs[-1][1] == (1 << 20) + 5
+
+
+def test_multiserver_errors(B):
+    # a server with no network attachment is disconnected; Broadcast unsupported
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(4, True, 0, 64, graph=B.Graph(4, [(0, 1, 1, 1), (2, 3, 1, 1), (0, 4, 1, 1)], switches=1))
+    assert e.value.code == 8 and "{2,3}" in str(e.value)
+    G = B.Graph(4, [(0, 1, 1, 1), (2, 3, 1, 1), (0, 4, 1, 1), (2, 4, 1, 1)], switches=1)
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(4, False, 0, 64, graph=G)
+    assert e.value.code == 9
+    assert len(B.plan_json(4, True, 0, 64, graph=G)["trees"]) == 2

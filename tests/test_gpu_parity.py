@@ -453,3 +453,25 @@ def test_miad_autotune_changes_chunking_not_results(B):
             for x in out:
                 assert_bitwise(x.cpu().numpy(), want)
     assert len(chunks) >= 2          # the tuner explored several chunk sizes
+
+
+# ----------------------------------------------------------------- NEXT-4: three-phase multi-server
+@pytest.mark.parametrize("servers", [[[0, 1, 3], [2, 4, 5, 6, 7]], [[0, 1, 2, 3], [4, 5, 6, 7]]])
+def test_multiserver_three_phase_allreduce(B, servers):
+    """2 emulated servers (the paper's 3+5 split, P:715-721, and 4+4) on one
+    GPU: exact int32, and fp32 bit-exact vs the oracle's tree-order evaluation
+    of the library's plan plus the naive-sum tolerance."""
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.multi_server(8, g[1], servers), chunk_bytes=16384)
+    count = 300007
+    isends = synth.inputs(130, 8, count, "i32")
+    for x in run_allreduce(B, comms, isends, "i32", "sum"):
+        assert_bitwise(x, OC.naive_reduce(isends, "i32", "sum"))
+    sends = synth.inputs(131, 8, count, "f32")
+    got = run_allreduce(B, comms, sends, "f32", "sum")
+    plan = oracle_plan_from_json(comms[0].plan(True, 0, count, "f32"))
+    want = OC.allreduce(plan, sends, "f32", "sum")
+    for x in got:
+        assert_bitwise(x, want)
+    absum = sum(np.abs(s).astype(np.float64) for s in sends)
+    assert np.all(np.abs(want.astype(np.float64) - OC.naive_reduce(sends, "f32", "sum")) <= 1e-5 * absum + 1e-30)

@@ -10,7 +10,10 @@ import random
 from fractions import Fraction
 from itertools import product
 
+import numpy as np
 import pytest
+
+import synth
 
 from oracle import bounds, graphs, packing
 
@@ -264,3 +267,43 @@ def test_split_properties(S):
         W = sum(Fraction(w) for w in ws)
         for (lo, hi), w in zip(rngs[:-1], ws[:-1]):
             assert abs(Fraction(hi - lo) - Fraction(S) * Fraction(w) / W) < 32
+
+
+# ------------------------------------------------------------------ NEXT-4
+def test_multiserver_plan_structure_3_plus_5():
+    # the paper's 2 x DGX-1V experiment allocates 3 + 5 GPUs;
+    # here: DGX-1V GPUs {0,1,3} on server 0 and {2,4,5,6,7} on server 1
+    from oracle import collectives as C
+    g = graphs.dgx1v()
+    servers = [[0, 1, 3], [2, 4, 5, 6, 7]]
+    # cross-server links are not NVLink: drop GPU-GPU links between servers
+    cap = {(u, v): c for (u, v), c in g[1].items()
+           if any(u in s and v in s for s in servers)}
+    gg = (8, cap)
+    plan = packing.plan_multiserver_allreduce(gg, servers)
+    K = plan["partitions"]
+    assert len(plan["trees"]) == K * len(servers)           # n one-hop cross trees per partition
+    for t in plan["trees"]:
+        assert t["parent"].count(-1) == 1 and t["root"] in servers[t["server"]]
+        cross = [(u, v) for (u, v) in t["edges"] if not any(u in s and v in s for s in servers)]
+        assert len(cross) == len(servers) - 1                # one hop between local roots
+        assert len(t["edges"]) == 7                          # spanning tree of 8 GPUs
+    for p in range(K):
+        roots = {t["root"] for t in plan["trees"] if t["partition"] == p}
+        assert len(roots) == len(servers)                    # one root per server per partition
+    # distinct server-local roots across partitions where the server has room
+    for s, ids in enumerate(servers):
+        rs = [t["root"] for t in plan["trees"] if t["server"] == s]
+        assert len(set(rs)) == min(K, len(ids))
+    # integer AllReduce along it is exact (any tree order)
+    sends = synth.inputs(7, 8, 999, "i32")
+    assert np.array_equal(C.allreduce(plan, sends, "i32", "sum"), C.naive_reduce(sends, "i32", "sum"))
+
+
+def test_multiserver_single_gpu_servers_is_the_dgx2_onehop_plan():
+    # n servers of one GPU each: phase 1 and 3 vanish and phase 2 is exactly
+    # the m one-hop trees of P:440-442
+    m = 5
+    plan = packing.plan_multiserver_allreduce((m, {}), [[v] for v in range(m)])
+    ref = packing.plan_switch_allreduce(m)
+    assert [t["parent"] for t in plan["trees"]] == [t["parent"] for t in ref["trees"]]
