@@ -172,6 +172,14 @@ def main():
         log(run_coll(comms, "allreduce", 64 << 20, "f32", 0, f"c4-dgx1v-{''.join(map(str, nodes))}"))
         for c in comms:
             c.destroy()
+    # NEXT-4: three-phase multi-server AllReduce, 3+5 and 4+4 emulated servers
+    for servers in ([[0, 1, 3], [2, 4, 5, 6, 7]], [[0, 1, 2, 3], [4, 5, 6, 7]]):
+        comms = B.init_all([0] * 8, graph=B.Graph.multi_server(8, g[1], servers))
+        tag = "next4-" + "+".join(str(len(s)) for s in servers)
+        for S in sizes(1 << 20, 1 << 28, 16):
+            log(run_coll(comms, "allreduce", S, "f32", 0, tag))
+        for c in comms:
+            c.destroy()
     # config 5: DDP bucket sequences (App. C) at m = 2, 4, 8
     for m in (2, 4, 8):
         comms = B.init_all([0] * m)
