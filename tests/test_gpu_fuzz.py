@@ -1,0 +1,166 @@
+"""Seeded randomized parity (GPU): many small configurations drawn from one
+seed, each compared against the oracle.  Graphs: NVSwitch model, DGX-1P/V
+sub-allocations, random connected link graphs, emulated multi-server.
+Values: int32 and MIN/MAX must be exact under any plan; fp32/bf16 SUM must be
+bit-exact against the oracle's tree-order evaluation of the library's plan and
+within R#20's tolerance of the naive sum; Broadcast / AllGather are bitwise
+copies."""
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import collectives as OC
+from oracle import graphs as OG
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TD = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    import paper_1910_04940_b200 as B
+    return B
+
+
+def to_dev(a, dtype):
+    a = np.ascontiguousarray(a)
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def to_host(t, dtype):
+    if dtype == "bf16":
+        return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.contiguous().cpu().numpy()
+
+
+def bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint16) if a.dtype.itemsize == 2 else a.view(np.uint32)
+
+
+def random_graph(B, rng):
+    kind = rng.choice(["switch", "dgx1", "random", "multiserver"])
+    if kind == "switch":
+        m = rng.randint(2, 8)
+        return m, None, kind
+    if kind == "dgx1":
+        base = rng.choice([OG.dgx1p(), OG.dgx1v()])
+        while True:
+            nodes = sorted(rng.sample(range(8), rng.randint(2, 8)))
+            sub, _ = OG.induced(base, nodes)
+            if OG.is_connected(sub):
+                return len(nodes), B.Graph.from_pairs(len(nodes), sub[1]), kind
+    if kind == "random":
+        m = rng.randint(2, 6)
+        while True:
+            cap = {}
+            for u in range(m):
+                for v in range(u + 1, m):
+                    if rng.random() < 0.6:
+                        c = rng.randint(1, 2)
+                        cap[(u, v)] = cap[(v, u)] = c
+            if OG.is_connected((m, cap)):
+                return m, B.Graph.from_pairs(m, cap), kind
+    m = 8
+    cut = rng.randint(2, 6)
+    servers = [list(range(cut)), list(range(cut, 8))]
+    return m, B.Graph.multi_server(m, OG.dgx1v()[1], servers), kind
+
+
+def oracle_plan(p):
+    return dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"],
+                            weight=Fraction(*t["weight"])) for t in p["trees"]])
+
+
+@pytest.mark.parametrize("seed", range(128))
+def test_random_configuration(B, seed):
+    rng = random.Random(7000 + seed)
+    m, graph, kind = random_graph(B, rng)
+    coll = "allreduce" if kind == "multiserver" else rng.choice(["allreduce", "allreduce", "broadcast"] +
+                      (["reduce_scatter", "allgather"] if kind == "switch" else []))
+    dtype = rng.choice(["f32", "bf16", "i32"])
+    op = rng.choice(["sum", "min", "max"] + (["prod"] if dtype == "i32" else []))
+    count = rng.choice([1, 7, 255, 4096, 65537, 300001, rng.randint(1, 200000)])
+    inplace = rng.random() < 0.25 and coll in ("allreduce", "broadcast")
+    misalign = rng.random() < 0.15 and not inplace
+    chunk = rng.choice([0, 4096, 65536])
+    comms = B.init_all([0] * m, graph=graph, cfg=B.config(timeout_s=30.0, chunk_bytes=chunk))
+    es = OC.ESIZE[dtype]
+    if coll == "reduce_scatter":
+        sends = synth.inputs(seed, m, m * count, dtype)
+    else:
+        sends = synth.inputs(seed, m, count, dtype)
+    if op == "prod":
+        sends = [(s % 3 - 1).astype(np.int32) for s in sends]
+
+    def dev(a, extra=0):
+        if not misalign:
+            return to_dev(a, dtype)
+        raw = torch.empty(len(a) + 1, dtype=TD[dtype], device="cuda")
+        raw[1:] = to_dev(a, dtype)
+        return raw[1:]
+
+    def out(n):
+        raw = torch.full((n * es + 16,), 0xFF, dtype=torch.uint8, device="cuda")
+        off = es if misalign else 0
+        return raw[off:off + n * es].view(TD[dtype])
+
+    root = rng.randrange(m)
+    ds = [dev(s) for s in sends]
+    if coll == "allreduce":
+        rs = ds if inplace else [out(count) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.allreduce(ds[r], rs[r], op=op, count=count, dtype=dtype)
+    elif coll == "broadcast":
+        rs = ds if inplace else [out(count) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.broadcast(ds[r] if r == root or inplace else None, rs[r], root=root, count=count, dtype=dtype)
+    elif coll == "reduce_scatter":
+        rs = [out(count) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.reduce_scatter(ds[r], rs[r], op=op, recvcount=count, dtype=dtype)
+    else:
+        rs = [out(m * count) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.allgather(ds[r], rs[r], sendcount=count, dtype=dtype)
+    torch.cuda.synchronize()
+    got = [to_host(x, dtype) for x in rs]
+    what = f"{kind} m={m} {coll} {dtype} {op} n={count} inplace={inplace} misalign={misalign} chunk={chunk}"
+    if coll == "broadcast":
+        for g in got:
+            assert np.array_equal(bits(g), bits(sends[root])), what
+        return
+    if coll == "allgather":
+        for g in got:
+            assert np.array_equal(bits(g), bits(OC.allgather(sends))), what
+        return
+    if coll == "reduce_scatter":
+        want = OC.reduce_scatter(sends, dtype, op)
+        for r in range(m):
+            assert np.array_equal(bits(got[r]), bits(want[r])), what
+        return
+    exact_any_order = dtype == "i32" or op in ("min", "max")
+    if exact_any_order:
+        want = OC.naive_reduce(sends, dtype, op)
+    else:
+        want = OC.allreduce(oracle_plan(comms[0].plan(True, 0, count, dtype)), sends, dtype, op)
+        w = OC.bf16_to_f32(want) if dtype == "bf16" else want
+        nv = OC.naive_reduce(sends, dtype, op)
+        nv = OC.bf16_to_f32(nv) if dtype == "bf16" else nv
+        xs = [OC.bf16_to_f32(s) if dtype == "bf16" else s for s in sends]
+        absum = sum(np.abs(x).astype(np.float64) for x in xs)
+        rtol = 1e-5 if dtype == "f32" else 1e-2
+        assert np.all(np.abs(w.astype(np.float64) - nv) <= rtol * absum + 1e-30), what
+    for g in got:
+        assert np.array_equal(bits(g), bits(want)), what
+    for c in comms:
+        c.destroy()
