@@ -128,13 +128,39 @@ def gpu_mode(rank, world):
     print(f"rank {rank}: gpu ok launches={st['launches']} ctas={st['last_ctas']}")
 
 
+def timeout_mode(rank, world):
+    """Failure detection: rank 1 never joins the collective; rank 0's flag
+    waits time out (cfg.timeout_s), the launch aborts instead of hanging, and
+    the next call on rank 0 reports BLINK_ERR_TIMEOUT."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    torch.cuda.set_device(0)
+    comm = BD.init(cfg=B.config(timeout_s=1.0), device=0)
+    x = torch.ones(4096, device="cuda")
+    if rank == 0:
+        comm.allreduce(x)                  # enqueued; the kernel waits for rank 1's entry
+        torch.cuda.synchronize()           # returns once the wait timed out
+        try:
+            comm.allreduce(x)
+            raise SystemExit("rank 0: expected BLINK_ERR_TIMEOUT")
+        except B.BlinkError as e:
+            assert e.code == 10, e
+        print("rank 0: timeout ok")
+    else:
+        print("rank 1: skipped the collective")
+    dist.barrier()
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo")
     try:
-        if os.environ.get("MODE", "cpu") == "cpu":
+        mode = os.environ.get("MODE", "cpu")
+        if mode == "cpu":
             cpu_mode(rank, world)
+        elif mode == "timeout":
+            timeout_mode(rank, world)
         else:
             gpu_mode(rank, world)
     finally:

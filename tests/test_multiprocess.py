@@ -46,3 +46,9 @@ def test_gloo_host_logic(n):
 def test_two_processes_share_one_gpu():
     out = launch(2, "gpu", {"BLINK_SAME_GPU": "1"}, timeout=900)
     assert out.count("gpu ok") == 2
+
+
+@pytest.mark.gpu
+def test_missing_rank_times_out_instead_of_hanging():
+    out = launch(2, "timeout", {"BLINK_SAME_GPU": "1"}, timeout=300)
+    assert "rank 0: timeout ok" in out
