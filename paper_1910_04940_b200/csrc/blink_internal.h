@@ -116,7 +116,7 @@ struct LaunchArgs {
   int smem_bytes;            // dynamic shared memory of the TMA ring
   int tile_bytes;            // 0 = default tile per source
   int scope_sys;             // 1: flags cross devices/processes (.sys), 0: one device (.gpu)
-  int pad2;
+  int store_depth;           // bulk-store groups kept in flight (-1 = default)
   uint64_t epoch;            // set by the kernel from ctrl[0] + 1
   uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
                              // [1] CTAs finished in the current launch (graph-safe epochs)

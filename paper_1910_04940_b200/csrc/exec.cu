@@ -502,29 +502,47 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
     } else if (warp == 1 && lane == 0) {
       // ---------------- store
+      // keep up to D bulk-store groups reading smem before releasing a buffer
+      const int Dwant = a.store_depth >= 0 ? a.store_depth : 2;
+      const int D = min(Dwant, (reduce ? int(K) : int(NS)) - 1);
+      auto release = [&](uint32_t gt) {
+        if (reduce)
+          mbar_arrive(&sh.oempty[gt % K]);
+        else
+          mbar_arrive(&sh.empty[gt % NS]);
+      };
       bool ok = true;
+      int kept = 0;
       for (int k = 0; k < ntiles && ok; ++k) {
         const uint32_t gg = g + k;
         const int64_t off = int64_t(k) * tile;
         const uint32_t tb = uint32_t(min(int64_t(tile), body - off));
+        const char* src;
         if (reduce) {
           const uint32_t o = gg % K;
           if (!(ok = mbar_wait_or_abort(&sh.ofull[o], (gg / K) & 1u, sh))) break;
-          for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, out + size_t(o) * tile, tb);
-          tma_commit();
-          tma_wait_read<0>();
-          mbar_arrive(&sh.oempty[o]);
+          src = out + size_t(o) * tile;
         } else {
           const uint32_t s = gg % NS;
           if (!(ok = mbar_wait_or_abort(&sh.full[s], (gg / NS) & 1u, sh))) break;
-          for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, ring + size_t(s) * tile, tb);
-          tma_commit();
-          tma_wait_read<0>();
-          mbar_arrive(&sh.empty[s]);
+          src = ring + size_t(s) * tile;
+        }
+        for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, src, tb);
+        tma_commit();
+        if (++kept > D) {
+          if (D >= 2)
+            tma_wait_read<2>();
+          else if (D == 1)
+            tma_wait_read<1>();
+          else
+            tma_wait_read<0>();
+          release(gg - uint32_t(D));
+          --kept;
         }
       }
       tma_wait_all();
       fence_proxy_async();
+      for (int j = ntiles - kept; j < ntiles; ++j) release(g + uint32_t(j));
       if (ok) signal_chunk(a, t, c, is_root, ctl);
     } else if (reduce && warp >= 2) {
       // ---------------- consumers

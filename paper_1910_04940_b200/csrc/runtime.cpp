@@ -529,6 +529,13 @@ int smem_bytes() {
   }();
   return v;
 }
+int store_depth() {
+  static int v = [] {
+    const char* e = getenv("BLINK_STORE_DEPTH");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
 int tile_bytes() {
   static int v = [] {
     const char* e = getenv("BLINK_TILE");
@@ -662,6 +669,7 @@ blink_result_t clique_launch(Clique* q) {
     a.use_tma = use_tma();
     a.smem_bytes = smem_bytes();
     a.tile_bytes = tile_bytes();
+    a.store_depth = store_depth();
     a.ctrl = q->ctrl[dev];
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
     a.err = q->err_dev[dev];
@@ -857,6 +865,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.use_tma = use_tma();
   a.smem_bytes = smem_bytes();
   a.tile_bytes = tile_bytes();
+  a.store_depth = store_depth();
   a.ctrl = comm->ctrl;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
   a.err = comm->err_dev;
