@@ -117,6 +117,8 @@ struct LaunchArgs {
   int tile_bytes;            // 0 = default tile per source
   int scope_sys;             // 1: flags cross devices/processes (.sys), 0: one device (.gpu)
   int store_depth;           // bulk-store groups kept in flight (-1 = default)
+  int l2_hint;               // 1: TMA loads/stores carry an L2 evict-first policy
+  int pad3;
   uint64_t epoch;            // set by the kernel from ctrl[0] + 1
   uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
                              // [1] CTAs finished in the current launch (graph-safe epochs)

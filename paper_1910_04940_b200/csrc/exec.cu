@@ -331,6 +331,26 @@ __device__ __forceinline__ void tma_store(void* dst, const void* src_smem, uint3
                "r"(smem_u32(src_smem)), "r"(bytes)
                : "memory");
 }
+// Streaming variants with an L2 evict-first policy (every byte is touched once).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_hint(void* dst_smem, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_hint(void* dst, const void* src_smem, uint32_t bytes,
+                                               uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void tma_wait_read() {
@@ -497,7 +517,13 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
           const uint32_t tb = uint32_t(min(int64_t(tile), body - off));
           mbar_expect_tx(&sh.full[s], tb * uint32_t(ns));
           char* st = ring + size_t(s) * tile * ns;
-          for (int j = 0; j < ns; ++j) tma_load(st + size_t(j) * tile, sh.srcs[j] + b0 + off, tb, &sh.full[s]);
+          if (a.l2_hint) {
+            const uint64_t pol = l2_evict_first_policy();
+            for (int j = 0; j < ns; ++j)
+              tma_load_hint(st + size_t(j) * tile, sh.srcs[j] + b0 + off, tb, &sh.full[s], pol);
+          } else {
+            for (int j = 0; j < ns; ++j) tma_load(st + size_t(j) * tile, sh.srcs[j] + b0 + off, tb, &sh.full[s]);
+          }
         }
       }
     } else if (warp == 1 && lane == 0) {
@@ -527,7 +553,12 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
           if (!(ok = mbar_wait_or_abort(&sh.full[s], (gg / NS) & 1u, sh))) break;
           src = ring + size_t(s) * tile;
         }
-        for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, src, tb);
+        if (a.l2_hint) {
+          const uint64_t pol = l2_evict_first_policy();
+          for (int d = 0; d < ndst; ++d) tma_store_hint(sh.dsts[d] + b0 + off, src, tb, pol);
+        } else {
+          for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, src, tb);
+        }
         tma_commit();
         if (++kept > D) {
           if (D >= 2)

@@ -536,6 +536,13 @@ int store_depth() {
   }();
   return v;
 }
+int l2_hint() {
+  static int v = [] {
+    const char* e = getenv("BLINK_L2HINT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 int tile_bytes() {
   static int v = [] {
     const char* e = getenv("BLINK_TILE");
@@ -670,6 +677,7 @@ blink_result_t clique_launch(Clique* q) {
     a.smem_bytes = smem_bytes();
     a.tile_bytes = tile_bytes();
     a.store_depth = store_depth();
+    a.l2_hint = l2_hint();
     a.ctrl = q->ctrl[dev];
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
     a.err = q->err_dev[dev];
@@ -866,6 +874,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.smem_bytes = smem_bytes();
   a.tile_bytes = tile_bytes();
   a.store_depth = store_depth();
+  a.l2_hint = l2_hint();
   a.ctrl = comm->ctrl;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
   a.err = comm->err_dev;
