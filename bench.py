@@ -49,7 +49,8 @@ class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+         "utilization.gpu")
 
     def __init__(self, index=0):
         self.index = index
@@ -62,7 +63,7 @@ class Clocks:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         except Exception:
@@ -86,12 +87,15 @@ class Clocks:
             if len(parts) < 9:
                 continue
             try:
+                util = float(parts[9]) if len(parts) > 9 else 100.0
                 rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), hw=parts[5], hwt=parts[6],
-                                 swt=parts[7], pcap=parts[8]))
+                                 swt=parts[7], pcap=parts[8], util=util))
             except ValueError:
                 continue
         if not rows:
             return None
+        busy = [r for r in rows if r["util"] >= 50]
+        rows = busy or rows        # samples under load (the timed region)
         reasons = set()
         for r in rows:
             for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
@@ -100,7 +104,7 @@ class Clocks:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(r["sm"] for r in rows),
                 "sm_max_mhz": max(r["smax"] for r in rows), "reasons": sorted(reasons),
-                "samples": len(rows)}
+                "samples_under_load": len(busy), "samples": len(rows)}
 
 
 def cpu_oracle_baseline(m, count, budget_s=10.0, max_s=30.0):
@@ -372,8 +376,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="blink", choices=["blink", "reference"])
     ap.add_argument("--ranks", type=int, default=DEFAULT_M, help="virtual ranks at N=1")
     ap.add_argument("--count", type=int, default=DEFAULT_COUNT, help="fp32 elements per rank")
