@@ -475,3 +475,64 @@ def test_multiserver_three_phase_allreduce(B, servers):
         assert_bitwise(x, want)
     absum = sum(np.abs(s).astype(np.float64) for s in sends)
     assert np.all(np.abs(want.astype(np.float64) - OC.naive_reduce(sends, "f32", "sum")) <= 1e-5 * absum + 1e-30)
+
+
+# ----------------------------------------------------------------- full sizes of the other configs
+def _sample_check(sends, recvs, op, dtype, nsamp=32768, seed=0):
+    count = sends[0].numel()
+    idx = torch.from_numpy(np.random.default_rng(seed).integers(0, count, nsamp)).cuda()
+    idx = torch.cat([idx, torch.arange(max(0, count - 19), count, device="cuda")])
+    cols = [to_host(s[idx], dtype) for s in sends]
+    want = OC.naive_reduce(cols, dtype, op)
+    for r in recvs:
+        assert_bitwise(to_host(r[idx], dtype), want)
+
+
+def test_fullsize_config2_dgx1v_broadcast_1gib(B):
+    """Config 2 at its top size: 1 GiB Broadcast over the 6 emulated DGX-1V
+    trees; every byte compared (device-side equality with the root's input)."""
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), timeout_s=60.0)
+    count = (1 << 30) // 4 + 3
+    send = synth.device_input(2, 0, count, "f32")
+    recvs = [torch.full_like(send, float("nan")) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.broadcast(send if r == 0 else None, recvs[r], root=0)
+    torch.cuda.synchronize()
+    for x in recvs:
+        assert torch.equal(x.view(torch.int32), send.view(torch.int32))
+
+
+def test_fullsize_config3_bf16_1gib_and_config4_m7(B):
+    for m, dtype, nbytes in ((8, "bf16", 1 << 30), (7, "f32", 1 << 30)):
+        comms = make_comms(B, m, timeout_s=60.0)
+        count = nbytes // OC.ESIZE[dtype]
+        sends = [synth.device_input(3, r, count, dtype) for r in range(m)]
+        recvs = [torch.empty_like(s) for s in sends]
+        for r, c in enumerate(comms):
+            c.allreduce(sends[r], recvs[r])
+        torch.cuda.synchronize()
+        _sample_check(sends, recvs, "sum", dtype)
+        del sends, recvs
+        for c in comms:
+            c.destroy()
+        torch.cuda.empty_cache()
+
+
+def test_fullsize_config5_vgg16_bucket_sequence(B):
+    """Config 5: the VGG-16 DDP bucket sequence (App. C) back to back, in place,
+    at m = 8; every bucket sampled against the oracle."""
+    m = 8
+    comms = make_comms(B, m, timeout_s=60.0)
+    for dtype in ("f32", "bf16"):
+        buckets = synth.BUCKETS[("vgg16", dtype)]
+        ins = [[synth.device_input(50 + i, r, n, dtype) for r in range(m)] for i, n in enumerate(buckets)]
+        outs = [[x.clone() for x in b] for b in ins]
+        for b in outs:
+            for r, c in enumerate(comms):
+                c.allreduce(b[r])                 # in place, back to back
+        torch.cuda.synchronize()
+        for b_in, b_out in zip(ins, outs):
+            _sample_check(b_in, b_out, "sum", dtype, nsamp=8192)
+        del ins, outs
+        torch.cuda.empty_cache()
