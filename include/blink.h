@@ -220,6 +220,13 @@ typedef struct {
   int64_t last_chunk_bytes;  /* chunk size of tree 0 in the last launch (MIAD trace) */
 } blink_stats_t;
 blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* stats);
+/* Device-side trace of the last launch on this comm's device when the
+ * environment variable BLINK_TRACE is set (single-process comms): 8 %globaltimer
+ * stamps (ns) per CTA -- start, epoch read, entry handshake done, first TMA
+ * load, first bulk store, last stores complete, end of work, after the epoch
+ * update (0 where a CTA has no such event).  *n_words in/out like
+ * blink_plan_json; synchronous copy.  *n_words = 0 when tracing is off. */
+blink_result_t blink_get_trace(blink_comm_t comm, uint64_t* out, size_t* n_words);
 blink_result_t blink_comm_info(blink_comm_t comm, int* nranks, int* rank, int* device);
 
 blink_result_t blink_destroy(blink_comm_t comm);

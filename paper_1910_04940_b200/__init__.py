@@ -83,6 +83,7 @@ _SIGS = {
     "blink_allgather": (_i, [_vp, _vp, _vp, _sz, _i, _vp]),
     "blink_get_plan": (_i, [_vp, _i, _i, _sz, _i, _cp, ctypes.POINTER(_sz)]),
     "blink_get_stats": (_i, [_vp, ctypes.POINTER(_Stats)]),
+    "blink_get_trace": (_i, [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(_sz)]),
     "blink_comm_info": (_i, [_vp, ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "blink_destroy": (_i, [_vp]),
     "blink_miad_init": (None, [ctypes.POINTER(Miad), _sz, _sz, _sz]),
@@ -264,6 +265,17 @@ class Comm:
         _check(_lib.blink_get_stats(self._h, ctypes.byref(s)), self._h)
         return dict(launches=s.launches, last_ctas=s.last_ctas, last_chunks=s.last_chunks,
                     last_trees=s.last_trees, last_chunk_bytes=s.last_chunk_bytes)
+
+    def trace(self):
+        """Per-CTA %globaltimer stamps of the last launch (BLINK_TRACE=1), as a
+        list of 8-tuples (ns); empty when tracing is off."""
+        n = _sz(0)
+        _check(_lib.blink_get_trace(self._h, None, ctypes.byref(n)), self._h)
+        if n.value == 0:
+            return []
+        buf = (ctypes.c_uint64 * n.value)()
+        _check(_lib.blink_get_trace(self._h, buf, ctypes.byref(n)), self._h)
+        return [tuple(buf[i:i + 8]) for i in range(0, n.value, 8)]
 
     def register(self, buf, nbytes, exchange):
         """Symmetric registration (multi-process).  `exchange(bytes) -> list[bytes]`

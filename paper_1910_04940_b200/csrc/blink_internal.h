@@ -16,7 +16,9 @@ namespace blink {
 constexpr int kMaxRanks = 16;       // ranks per comm (one NVSwitch node; DGX-2 = 16)
 constexpr int kMaxTrees = 32;       // trees per plan
 constexpr int kMaxChunks = 512;     // chunks per tree per call
-constexpr int kGrain = 16;          // split grain in bytes (R#11) == one 128-bit vector
+constexpr int kGrain = 16;
+constexpr int kTraceSlots = 8;      // per-CTA trace stamps (BLINK_TRACE)
+constexpr int kMaxCounters = 4096;  // dynamic chunk counters per launch (ctrl[2..])          // split grain in bytes (R#11) == one 128-bit vector
 
 // Flag region of one rank (uint64 words, monotonically increasing epochs,
 // never reset).  Producers write into the CONSUMER's region:
@@ -90,8 +92,9 @@ struct DevTask {             // one per CTA; 64 bytes
   int32_t do_entry;          // this task publishes rank v's entry flag
   int32_t next;              // next task (segment) of the same CTA, -1 = none
   int32_t c0, c1, cstride;   // chunks c = c0, c0+cstride, ... < c1 of tree `tree`
-  int32_t pad0;
-  int64_t pad1;
+  int32_t ctr;               // >= 0: chunks are taken from counter ctrl[2 + ctr] (dynamic)
+  int32_t merged;            // chunk ids span every tree (one-hop AllReduce, single launch)
+  int32_t pad1;
 };
 static_assert(sizeof(DevTask) == 64, "DevTask layout");
 
@@ -119,6 +122,9 @@ struct LaunchArgs {
   int store_depth;           // bulk-store groups kept in flight (-1 = default)
   int l2_hint;               // 1: TMA loads/stores carry an L2 evict-first policy
   int pad3;
+  uint64_t* trace;           // BLINK_TRACE: kTraceSlots globaltimer stamps per CTA, else NULL
+  int nctr;                  // chunk counters ctrl[2 .. 2 + nctr) zeroed by the last CTA
+  int pad4;
   uint64_t epoch;            // set by the kernel from ctrl[0] + 1
   uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
                              // [1] CTAs finished in the current launch (graph-safe epochs)

@@ -387,7 +387,24 @@ __device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// Trace points (BLINK_TRACE): 0 start, 1 epoch read, 2 setup done (entry
+// handshake), 3 first TMA load issued, 4 first bulk store issued, 5 last
+// chunk's stores complete, 6 end of work, 7 after the epoch update.
+__device__ __forceinline__ void trace(const LaunchArgs& a, int slot) {
+  if (a.trace) a.trace[size_t(blockIdx.x) * kTraceSlots + slot] = globaltimer();
+}
+
+struct TileMeta {
+  int64_t off;  // byte offset of the tile in every buffer
+  int c;        // chunk (-1: end of stream)
+  int tb;       // tile bytes (0: tail-only chunk)
+  int last;     // last tile of chunk c
+  int pad;
+};
+
 struct Shared {
+  TileMeta smeta[kMaxStages];
+  TileMeta ometa[kOutBufs];
   const char* srcs[kMaxRanks + 1];
   char* dsts[kMaxRanks + 1];
   int nsrc, ndst, ok;
@@ -451,15 +468,22 @@ __device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask&
 }
 
 // Warp-specialised TMA pipeline over this CTA's chunks (aligned buffers):
-//   warp 0 lane 0  producer: acquires the chunk flags, issues cp.async.bulk
-//                  loads of every source tile into the stage ring (full[s]);
-//   warps 2..      consumers (REDUCE only): combine the stage's source tiles
-//                  in ascending-rank order into an output tile (ofull[o]);
-//   warp 1 lane 0  store: cp.async.bulk stores of the output tile (or, for a
-//                  copy, of the stage itself) to every destination, then at
-//                  chunk end waits for completion and releases the flags.
-// A chunk with a sub-16-byte tail (only the last chunk of the last tree) runs
-// on all threads with 128-bit LSU accesses instead.
+//   warp 0   producer: takes the next chunk (an atomic per-channel counter
+//            when the task is dynamic, else the static stride), acquires its
+//            flags (warp-cooperative), then lane 0 issues cp.async.bulk loads
+//            of every source tile into the stage ring; each stage carries a
+//            TileMeta (chunk, offset, bytes, last-of-chunk);
+//   warps 2..  consumers (REDUCE only): combine the stage's source tiles in
+//            ascending-rank order into an output tile + its meta;
+//   warp 1   store: cp.async.bulk stores of the output tile (or, for a copy,
+//            of the stage) to every destination; at the last tile of a chunk
+//            whose completion somebody waits for, it drains the stores and
+//            releases the chunk's flags.
+// A sub-16-byte chunk tail (only the last chunk of the last tree) is
+// combined by the producer warp with scalar accesses before the chunk's tiles
+// are issued (ordered before the chunk's signal through the mbarrier chain).
+// Dynamic chunk grabbing balances CTAs that drain at different speeds; every
+// CTA still takes chunks in increasing order (deadlock freedom, DESIGN 2b).
 template <int DT, int OP>
 __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr, bool is_root,
                        bool need_bflag, Shared& sh, char* ring, const Ctl& ctl) {
@@ -474,47 +498,76 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
   const int stages = max(1, min(kMaxStages, avail / (tile * ns)));
   char* out = ring + avail;
   const uint32_t NS = uint32_t(stages), K = uint32_t(kOutBufs);
-  uint32_t g = 0;  // tile sequence number (identical in every role)
-  for (int c = t.c0; c < t.c1; c += t.cstride) {
-    const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
-    const int64_t b1 = min(tr.hi, b0 + tr.chunk);
-    const int64_t body = ((b1 - b0) >> 4) << 4;
-    if (body != b1 - b0) {
-      // ---- tail chunk: every thread, LSU path
-      if (warp == 0) {
-        const bool ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
-        if (lane == 0) sh.ok = ok && !sh.abort;
+  // does anybody wait for this channel's per-chunk signals?
+  const bool need_signal = (reduce && !is_root) || a.exit_wait || ((t.children & ~t.leafmask) != 0u);
+  unsigned int* ctr = t.ctr >= 0 ? reinterpret_cast<unsigned int*>(a.ctrl + 2) + t.ctr : nullptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer
+    uint32_t g = 0;
+    int cs = t.c0;  // static sequence
+    for (;;) {
+      int c;
+      if (ctr) {
+        unsigned int got = 0;
+        if (lane == 0) got = atomicAdd(ctr, 1u);
+        c = int(__shfl_sync(0xffffffffu, got, 0));
+        if (c >= (t.merged ? t.c1 : tr.nchunks)) break;
+      } else {
+        c = cs;
+        cs += t.cstride;
+        if (c >= t.c1) break;
       }
-      __syncthreads();
-      const bool ok = sh.ok;
-      if (ok) {
-        if (reduce)
-          reduce_range<DT, OP, true>(sh.srcs, nsrc, sh.dsts, ndst, b0, b1);
-        else
-          copy_range<true>(sh.srcs[0], sh.dsts, ndst, b0, b1);
-      }
-      __syncthreads();
+      if (sh.abort) break;
+      const uint32_t wmask = reduce ? (t.children & ~t.leafmask) : (need_bflag ? 1u : 0u);
+      const bool ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
       if (!ok) {
-        if (threadIdx.x == 0) sh.abort = 1;
+        if (lane == 0) sh.abort = 1;
         break;
       }
-      if (threadIdx.x == 0) signal_chunk(a, t, c, is_root, ctl);
-      continue;
-    }
-    const int ntiles = int((body + tile - 1) / tile);
-    if (warp == 0) {
-      // ---------------- producer (the warp acquires, lane 0 issues)
-      const bool ok = wait_chunk_inputs(a, t, c, need_bflag, ctl);
-      if (lane != 0) {
-      } else if (!ok || sh.abort) {
-        sh.abort = 1;
+      int64_t b0, b1;
+      if (t.merged) {  // chunk c of the concatenation of every tree's chunks
+        int cc = c, i = 0;
+        while (i + 1 < a.ntrees && cc >= a.trees[i].nchunks) cc -= a.trees[i++].nchunks;
+        const DevTree ti = a.trees[i];
+        b0 = ti.lo + int64_t(cc) * ti.chunk;
+        b1 = min(ti.hi, b0 + ti.chunk);
       } else {
-        fence_proxy_async();
-        for (int k = 0; k < ntiles; ++k) {
-          const uint32_t gg = g + k, s = gg % NS;
-          if (!mbar_wait_or_abort(&sh.empty[s], ((gg / NS) & 1u) ^ 1u, sh)) break;
+        b0 = tr.lo + int64_t(c) * tr.chunk;
+        b1 = min(tr.hi, b0 + tr.chunk);
+      }
+      const int64_t body = ((b1 - b0) >> 4) << 4;
+      if (body != b1 - b0) {  // sub-16-byte tail: scalar, by the producer warp
+        if (reduce) {
+          const int es = DT == BLINK_BFLOAT16 ? 2 : 4;
+          for (int64_t off = b0 + body + int64_t(lane) * es; off < b1; off += 32 * es)
+            Scalar<DT, OP>::reduce(sh.srcs, nsrc, sh.dsts, ndst, off);
+        } else {
+          for (int64_t off = b0 + body + lane; off < b1; off += 32) {
+            const char ch = __ldcg(sh.srcs[0] + off);
+            for (int d = 0; d < ndst; ++d) sh.dsts[d][off] = ch;
+          }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (wmask) fence_proxy_async();  // acquired flags order the TMA reads below
+        if (c == t.c0 || (ctr && g == 0)) trace(a, 3);
+        const int ntiles = body > 0 ? int((body + tile - 1) / tile) : 1;
+        for (int k = 0; k < ntiles; ++k, ++g) {
+          const uint32_t s = g % NS;
+          if (!mbar_wait_or_abort(&sh.empty[s], ((g / NS) & 1u) ^ 1u, sh)) break;
           const int64_t off = int64_t(k) * tile;
-          const uint32_t tb = uint32_t(min(int64_t(tile), body - off));
+          const uint32_t tb = uint32_t(max(int64_t(0), min(int64_t(tile), body - off)));
+          TileMeta& mt = sh.smeta[s];
+          mt.off = b0 + off;
+          mt.c = c;
+          mt.tb = int(tb);
+          mt.last = k == ntiles - 1;
+          if (tb == 0) {
+            mbar_arrive(&sh.full[s]);  // empty tile (tail-only chunk): meta only
+            continue;
+          }
           mbar_expect_tx(&sh.full[s], tb * uint32_t(ns));
           char* st = ring + size_t(s) * tile * ns;
           if (a.l2_hint) {
@@ -526,67 +579,87 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
           }
         }
       }
-    } else if (warp == 1 && lane == 0) {
-      // ---------------- store
-      // keep up to D bulk-store groups reading smem before releasing a buffer
-      const int Dwant = a.store_depth >= 0 ? a.store_depth : 2;
-      const int D = min(Dwant, (reduce ? int(K) : int(NS)) - 1);
-      auto release = [&](uint32_t gt) {
-        if (reduce)
-          mbar_arrive(&sh.oempty[gt % K]);
-        else
-          mbar_arrive(&sh.empty[gt % NS]);
-      };
-      bool ok = true;
-      int kept = 0;
-      for (int k = 0; k < ntiles && ok; ++k) {
-        const uint32_t gg = g + k;
-        const int64_t off = int64_t(k) * tile;
-        const uint32_t tb = uint32_t(min(int64_t(tile), body - off));
-        const char* src;
-        if (reduce) {
-          const uint32_t o = gg % K;
-          if (!(ok = mbar_wait_or_abort(&sh.ofull[o], (gg / K) & 1u, sh))) break;
-          src = out + size_t(o) * tile;
-        } else {
-          const uint32_t s = gg % NS;
-          if (!(ok = mbar_wait_or_abort(&sh.full[s], (gg / NS) & 1u, sh))) break;
-          src = ring + size_t(s) * tile;
-        }
-        if (a.l2_hint) {
-          const uint64_t pol = l2_evict_first_policy();
-          for (int d = 0; d < ndst; ++d) tma_store_hint(sh.dsts[d] + b0 + off, src, tb, pol);
-        } else {
-          for (int d = 0; d < ndst; ++d) tma_store(sh.dsts[d] + b0 + off, src, tb);
-        }
-        tma_commit();
-        if (++kept > D) {
-          if (D >= 2)
-            tma_wait_read<2>();
-          else if (D == 1)
-            tma_wait_read<1>();
-          else
-            tma_wait_read<0>();
-          release(gg - uint32_t(D));
-          --kept;
-        }
+      __syncwarp();
+    }
+    if (lane == 0) {  // end of stream
+      const uint32_t s = g % NS;
+      if (mbar_wait_or_abort(&sh.empty[s], ((g / NS) & 1u) ^ 1u, sh)) {
+        sh.smeta[s].c = -1;
+        mbar_arrive(&sh.full[s]);
       }
-      tma_wait_all();
-      fence_proxy_async();
-      for (int j = ntiles - kept; j < ntiles; ++j) release(g + uint32_t(j));
-      if (ok) signal_chunk(a, t, c, is_root, ctl);
-    } else if (reduce && warp >= 2) {
-      // ---------------- consumers
-      const int ct = threadIdx.x - 64, CT = ncons * 32;
-      for (int k = 0; k < ntiles; ++k) {
-        const uint32_t gg = g + k, s = gg % NS, o = gg % K;
-        if (!mbar_wait_or_abort(&sh.full[s], (gg / NS) & 1u, sh)) break;
-        if (!mbar_wait_or_abort(&sh.oempty[o], ((gg / K) & 1u) ^ 1u, sh)) break;
-        const int64_t off = int64_t(k) * tile;
-        const int vecs = int(min(int64_t(tile), body - off) >> 4);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------ store
+    const int Dwant = a.store_depth >= 0 ? a.store_depth : 2;
+    const int D = min(Dwant, (reduce ? int(K) : int(NS)) - 1);
+    auto release = [&](uint32_t gt) {
+      if (reduce)
+        mbar_arrive(&sh.oempty[gt % K]);
+      else
+        mbar_arrive(&sh.empty[gt % NS]);
+    };
+    int kept = 0;
+    bool first = true;
+    for (uint32_t g = 0;; ++g) {
+      TileMeta mt;
+      const char* src;
+      if (reduce) {
+        const uint32_t o = g % K;
+        if (!mbar_wait_or_abort(&sh.ofull[o], (g / K) & 1u, sh)) break;
+        mt = sh.ometa[o];
+        src = out + size_t(o) * tile;
+      } else {
+        const uint32_t s = g % NS;
+        if (!mbar_wait_or_abort(&sh.full[s], (g / NS) & 1u, sh)) break;
+        mt = sh.smeta[s];
+        src = ring + size_t(s) * tile;
+      }
+      if (mt.c < 0) break;
+      if (a.l2_hint) {
+        const uint64_t pol = l2_evict_first_policy();
+        for (int d = 0; d < ndst && mt.tb > 0; ++d) tma_store_hint(sh.dsts[d] + mt.off, src, uint32_t(mt.tb), pol);
+      } else {
+        for (int d = 0; d < ndst && mt.tb > 0; ++d) tma_store(sh.dsts[d] + mt.off, src, uint32_t(mt.tb));
+      }
+      tma_commit();
+      if (first) {
+        trace(a, 4);
+        first = false;
+      }
+      if (++kept > D) {
+        if (D >= 2)
+          tma_wait_read<2>();
+        else if (D == 1)
+          tma_wait_read<1>();
+        else
+          tma_wait_read<0>();
+        release(g - uint32_t(D));
+        --kept;
+      }
+      if (mt.last && need_signal) {  // chunk complete: drain, publish
+        tma_wait_all();
+        fence_proxy_async();
+        for (int j = kept - 1; j >= 0; --j) release(g - uint32_t(j));
+        kept = 0;
+        signal_chunk(a, t, mt.c, is_root, ctl);
+      }
+    }
+    tma_wait_all();
+    fence_proxy_async();
+    trace(a, 5);
+  } else if (reduce && warp >= 2) {
+    // ------------------------------------------------ consumers
+    const int ct = threadIdx.x - 64, CT = ncons * 32;
+    const int vstride = tile >> 4;
+    for (uint32_t g = 0;; ++g) {
+      const uint32_t s = g % NS, o = g % K;
+      if (!mbar_wait_or_abort(&sh.full[s], (g / NS) & 1u, sh)) break;
+      const TileMeta mt = sh.smeta[s];
+      if (!mbar_wait_or_abort(&sh.oempty[o], ((g / K) & 1u) ^ 1u, sh)) break;
+      if (mt.c >= 0) {
+        const int vecs = mt.tb >> 4;
         const uint4* st = reinterpret_cast<const uint4*>(ring + size_t(s) * tile * ns);
         uint4* ob = reinterpret_cast<uint4*>(out + size_t(o) * tile);
-        const int vstride = tile >> 4;
         for (int vv = ct; vv < vecs; vv += CT) {
           Acc<DT> acc;
           widen<DT>(acc, st[vv]);
@@ -594,15 +667,15 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
           ob[vv] = narrow<DT>(acc);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&sh.empty[s]);
-          mbar_arrive(&sh.ofull[o]);
-        }
       }
+      if (ct == 0) sh.ometa[o] = mt;
+      __syncwarp();
+      if (lane == 0) {
+        if (mt.c >= 0) mbar_arrive(&sh.empty[s]);
+        mbar_arrive(&sh.ofull[o]);
+      }
+      if (mt.c < 0) break;
     }
-    g += uint32_t(ntiles);
-    if (sh.abort) break;
   }
   __syncthreads();
 }
@@ -619,8 +692,15 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
     __syncthreads();
     const bool ok = sh.ok;
     if (ok) {
-      const int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
-      const int64_t b1 = min(tr.hi, b0 + tr.chunk);
+      DevTree ti = tr;
+      int cc = c;
+      if (t.merged) {  // chunk c of the concatenation of every tree's chunks
+        int i = 0;
+        while (i + 1 < a.ntrees && cc >= a.trees[i].nchunks) cc -= a.trees[i++].nchunks;
+        ti = a.trees[i];
+      }
+      const int64_t b0 = ti.lo + int64_t(cc) * ti.chunk;
+      const int64_t b1 = min(ti.hi, b0 + ti.chunk);
       if (t.role == kRoleReduce)
         reduce_range<DT, OP, VEC>(sh.srcs, sh.nsrc, sh.dsts, sh.ndst, b0, b1);
       else
@@ -628,7 +708,9 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
     }
     __syncthreads();  // every thread's stores of chunk c are issued (and sh.ok read)
     if (!ok) break;
-    if (threadIdx.x == 0) signal_chunk(a, t, c, is_root, ctl);
+    // merged channels exist only in single launches of independent roots:
+    // nobody waits for their per-chunk signals
+    if (threadIdx.x == 0 && !t.merged) signal_chunk(a, t, c, is_root, ctl);
   }
 }
 
@@ -641,7 +723,13 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   // memory so that CUDA-graph replays get fresh epochs.
   const LaunchArgs& a = a_in;
   const DevTask t0 = a.tasks[blockIdx.x];
-  if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
+  if (threadIdx.x == 0) {
+    if (a.trace)
+      for (int k = 1; k < kTraceSlots; ++k) a.trace[size_t(blockIdx.x) * kTraceSlots + k] = 0;
+    trace(a, 0);
+    s_epoch = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
+    trace(a, 1);
+  }
   __syncthreads();
   const int v = t0.rank;
   const Ctl ctl{s_epoch, a.timeout_ns, a.err, a.scope_sys != 0};
@@ -650,12 +738,14 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
 
   // entry: my send is ready and my recv may be overwritten (epoch e).  Every
   // segment of this CTA publishes its entry before any segment waits.
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && a.exit_wait) {
     bool fenced = false;
     for (int ti = blockIdx.x; ti >= 0; ti = a.tasks[ti].next) {
       const DevTask& tt = a.tasks[ti];
       if (!tt.do_entry) continue;
-      if (!fenced) fence_acqrel(ctl.sys);
+      // earlier kernels' writes to send are ordered by the launch boundary;
+      // across devices / processes publish with a release fence anyway
+      if (!fenced && ctl.sys) fence_acqrel(true);
       fenced = true;
       for (int u = 0; u < a.nranks; ++u)
         if (u != tt.rank) st_relaxed(a.flags[u] + entry_idx(tt.rank), ctl.epoch, ctl.sys);
@@ -678,7 +768,10 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
     bool entry_ok = true;
     if (threadIdx.x < 32) {
       const bool pushes = a.coll == kBroadcast || a.coll == kAllGather;
-      const uint32_t emask = t.role == kRoleReduce ? t.leafmask : (pushes ? t.children : 0u);
+      // one launch holding every rank: all inputs are final at launch and all
+      // outputs free, so there is nothing to hand shake
+      const uint32_t emask = !a.exit_wait ? 0u
+                             : (t.role == kRoleReduce ? t.leafmask : (pushes ? t.children : 0u));
       entry_ok = warp_wait(emask, [&](int u) { return wflags + entry_idx(u); }, ctl);
     }
     if (threadIdx.x == 0) {
@@ -718,6 +811,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) trace(a, 2);
     const bool need_bflag =
         (t.role == kRoleBcast) && !((a.coll == kBroadcast || a.coll == kAllGather) && is_root);
     const bool aborted = sh.abort;
@@ -751,13 +845,15 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   // the last CTA to finish advances the device epoch for the next launch
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    trace(a, 6);
+    // the next launch is stream-ordered after this one: no fences needed here
     const unsigned long long prev = atomicAdd(reinterpret_cast<unsigned long long*>(a.ctrl + 1), 1ull);
     if (prev + 1 == gridDim.x) {
       a.ctrl[1] = 0;
-      __threadfence();
+      for (int k = 0; k < a.nctr; ++k) reinterpret_cast<unsigned int*>(a.ctrl + 2)[k] = 0u;
       atomicExch(reinterpret_cast<unsigned long long*>(a.ctrl), (unsigned long long)ctl.epoch);
     }
+    trace(a, 7);
   }
 }
 

@@ -1060,20 +1060,33 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
     int64_t bytes = hi - lo;
     // a8: static chunk table.  Aim for >= `per_cta` chunks per CTA of the
     // channel (deeper trees pipeline better with more chunks: (c+h-1)/c,
-    // P:511-513), chunks >= 4 KiB (BLINK_MIN_CHUNK) unless the range is
+    // P:511-513), chunks >= 16 KiB (BLINK_MIN_CHUNK) unless the range is
     // smaller, <= 4 MiB.
     int64_t cb;
     if (cfg.chunk_bytes > 0) {
       cb = int64_t(cfg.chunk_bytes);
     } else {
-      int per_cta = p.trees[i].depth >= 2 ? 4 : 1;
+      // ~32 chunks per CTA (>= 16 KiB each): deeper trees pipeline
+      // and dynamic chunk grabbing balances CTAs to the last
+      // chunk (A/B in profiles/README.md; BLINK_CHUNKS_PER_CTA overrides)
+      static const int per_cta_env = [] {
+        const char* e = getenv("BLINK_CHUNKS_PER_CTA");
+        return e ? std::max(1, atoi(e)) : 0;
+      }();
+      int per_cta = per_cta_env ? per_cta_env : 32;
       int64_t want = int64_t(std::max(1, ctas_hint)) * per_cta;
       cb = (bytes + want - 1) / want;
       static const int64_t min_chunk = [] {
         const char* e = getenv("BLINK_MIN_CHUNK");
-        return e ? std::max<int64_t>(16, atoll(e)) : int64_t(4 << 10);
+        return e ? std::max<int64_t>(16, atoll(e)) : int64_t(16 << 10);
       }();
-      cb = std::max<int64_t>(cb, min_chunk);
+      // multi-hop trees signal every chunk (flags + a store drain): keep
+      // their chunks larger (BLINK_MIN_CHUNK_DEEP)
+      static const int64_t min_chunk_deep = [] {
+        const char* e = getenv("BLINK_MIN_CHUNK_DEEP");
+        return e ? std::max<int64_t>(16, atoll(e)) : int64_t(64 << 10);
+      }();
+      cb = std::max<int64_t>(cb, p.trees[i].depth >= 2 ? std::max(min_chunk, min_chunk_deep) : min_chunk);
       cb = std::min<int64_t>(cb, 4 << 20);
     }
     cb = (cb + kGrain - 1) / kGrain * kGrain;

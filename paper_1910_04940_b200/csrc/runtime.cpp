@@ -72,6 +72,7 @@ struct Sized {
   DevTree* d_trees = nullptr;
   int ctas = 0;
   int chunks = 0;
+  int nctr = 0;  // dynamic chunk counters used by the launch
 };
 
 struct Reg {
@@ -139,6 +140,8 @@ struct Clique {
   // per device state
   std::map<int, int*> err_host, err_dev;
   std::map<int, uint64_t*> ctrl;  // per device: launch epoch + done counter
+  std::map<int, uint64_t*> trace; // per device: BLINK_TRACE stamps of the last launch
+  std::map<int, int> trace_ctas;
   struct MiadRun {
     blink_miad_t st;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -311,6 +314,53 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
     --it->ctas;
     --used;
   }
+  // ---- merged one-hop AllReduce (single launch): every tree's root channel
+  // reads every rank's send and writes every rank's recv, so one channel over
+  // the concatenated chunks of all trees, fed by one dynamic counter, uses
+  // every co-resident CTA and balances them to the last chunk.
+  {
+    const uint64_t all = (n >= 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
+    const uint32_t allm = uint32_t(all);
+    bool mergeable = launch_mask == all && plan.coll == kAllReduce && !chans.empty() &&
+                     !(getenv("BLINK_MERGE") && getenv("BLINK_MERGE")[0] == '0');
+    for (auto& c : chans)
+      mergeable = mergeable && c.role == kRoleReduce && c.parent < 0 && c.leafmask == c.children &&
+                  (c.children | (1u << c.rank)) == allm;
+    if (mergeable && int(chans.size()) == k) {
+      const int B = budget;
+      std::vector<TreeRange> ri;
+      if (size_plan(plan, count, esize, cfg, std::max(1, B / k), &ri, &err) != BLINK_SUCCESS)
+        return fail(comm, BLINK_ERR_INTERNAL, err);
+      s->ranges = ri;
+      int total = 0;
+      for (auto& r : ri) total += r.nchunks;
+      const int ctas = std::max(1, std::min(B, total));
+      s->tasks.assign(ctas, DevTask{});
+      for (int j = 0; j < ctas; ++j) {
+        DevTask& t = s->tasks[j];
+        t.rank = 0;
+        t.tree = 0;
+        t.role = kRoleReduce;
+        t.parent = -1;
+        t.children = allm & ~1u;
+        t.leafmask = allm & ~1u;
+        t.cta_idx = j;
+        t.cta_cnt = ctas;
+        t.exit_cnt = 1;
+        t.next = -1;
+        t.c0 = j;
+        t.c1 = total;
+        t.cstride = ctas;
+        t.ctr = 0;
+        t.merged = 1;
+      }
+      s->nctr = 1;
+      s->ctas = ctas;
+      s->chunks = total;
+      s->plan = &plan;
+      return BLINK_SUCCESS;
+    }
+  }
   // ---- packed assignment (opt-in, BLINK_PACK=1; measured no faster than the
   // per-channel split on the 1-GPU bench): one launch holding every rank whose channels are
   // independent (no chunk-level waits: one-hop roots) and equally loaded.
@@ -359,6 +409,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
           t.c0 = c0;
           t.c1 = c1;
           t.cstride = 1;
+          t.ctr = -1;
           t.cta_cnt = 1;
           t.exit_cnt = 1;
           t.next = -1;
@@ -386,6 +437,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
             t.cta_cnt = 1;
             t.exit_cnt = 1;
             t.next = -1;
+            t.ctr = -1;
             segs.push_back(t);
           }
           s->tasks[k] = segs[0];
@@ -406,6 +458,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
           t.cta_cnt = 1;
           t.exit_cnt = 1;
           t.do_entry = 1;
+          t.ctr = -1;
           t.next = s->tasks[0].next;
           s->tasks[0].next = B + int(extra.size());
           extra.push_back(t);
@@ -433,10 +486,14 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   s->tasks.clear();
   s->chunks = 0;
   for (auto& r : s->ranges) s->chunks += r.nchunks;
+  const bool dynamic = !(getenv("BLINK_DYNAMIC") && getenv("BLINK_DYNAMIC")[0] == '0') &&
+                       int(chans.size()) <= kMaxCounters;
+  s->nctr = dynamic ? int(chans.size()) : 0;
   for (int v = 0; v < n; ++v) {
     if (!((launch_mask >> v) & 1)) continue;
     size_t first = s->tasks.size();
-    for (auto& c : chans) {
+    for (size_t ci = 0; ci < chans.size(); ++ci) {
+      const Channel& c = chans[ci];
       if (c.rank != v) continue;
       for (int j = 0; j < c.ctas; ++j) {
         DevTask t{};
@@ -452,6 +509,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
         t.c0 = j;
         t.c1 = s->ranges[c.tree].nchunks;
         t.cstride = c.ctas;
+        t.ctr = dynamic ? int(ci) : -1;
         s->tasks.push_back(t);
       }
     }
@@ -462,6 +520,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
       t.parent = -1;
       t.cta_cnt = 1;
       t.next = -1;
+      t.ctr = -1;
       s->tasks.push_back(t);
     }
     int cnt = int(s->tasks.size() - first);
@@ -678,7 +737,14 @@ blink_result_t clique_launch(Clique* q) {
     a.tile_bytes = tile_bytes();
     a.store_depth = store_depth();
     a.l2_hint = l2_hint();
+    a.nctr = s.nctr;
     a.ctrl = q->ctrl[dev];
+    if (getenv("BLINK_TRACE")) {
+      uint64_t*& tb = q->trace[dev];
+      if (!tb) CUDA_TRY(cd, cudaMalloc(&tb, sizeof(uint64_t) * kTraceSlots * 4096));
+      a.trace = tb;
+      q->trace_ctas[dev] = s.ctas;
+    }
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
     a.err = q->err_dev[dev];
     for (int v = 0; v < n; ++v) {
@@ -875,6 +941,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.tile_bytes = tile_bytes();
   a.store_depth = store_depth();
   a.l2_hint = l2_hint();
+  a.nctr = s.nctr;
   a.ctrl = comm->ctrl;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
   a.err = comm->err_dev;
@@ -1180,8 +1247,8 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
     q->err_host[d] = h;
     q->err_dev[d] = dp;
     uint64_t* ctrl = nullptr;
-    if (cudaMalloc(&ctrl, 2 * sizeof(uint64_t)) != cudaSuccess ||
-        cudaMemset(ctrl, 0, 2 * sizeof(uint64_t)) != cudaSuccess)
+    const size_t cb = 2 * sizeof(uint64_t) + kMaxCounters * sizeof(unsigned int);
+    if (cudaMalloc(&ctrl, cb) != cudaSuccess || cudaMemset(ctrl, 0, cb) != cudaSuccess)
       return fail(nullptr, BLINK_ERR_CUDA, "control word allocation failed");
     q->ctrl[d] = ctrl;
   }
@@ -1219,8 +1286,9 @@ blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_dev
   CUDA_TRY(c, cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped));
   CUDA_TRY(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   *c->err_host = 0;
-  CUDA_TRY(c, cudaMalloc(&c->ctrl, 2 * sizeof(uint64_t)));
-  CUDA_TRY(c, cudaMemset(c->ctrl, 0, 2 * sizeof(uint64_t)));
+  const size_t cb = 2 * sizeof(uint64_t) + kMaxCounters * sizeof(unsigned int);
+  CUDA_TRY(c, cudaMalloc(&c->ctrl, cb));
+  CUDA_TRY(c, cudaMemset(c->ctrl, 0, cb));
   CUDA_TRY(c, cudaDeviceSynchronize());
   *comm = c;
   return BLINK_SUCCESS;
@@ -1441,6 +1509,22 @@ blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, siz
   return BLINK_SUCCESS;
 }
 
+blink_result_t blink_get_trace(blink_comm_t comm, uint64_t* out, size_t* n_words) {
+  if (!comm || !n_words) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (comm->multiprocess || !comm->clique->trace.count(comm->device)) {
+    *n_words = 0;
+    return BLINK_SUCCESS;
+  }
+  const size_t need = size_t(comm->clique->trace_ctas[comm->device]) * kTraceSlots;
+  const size_t cap = *n_words;
+  *n_words = need;
+  if (!out || cap < need) return BLINK_SUCCESS;
+  DeviceGuard g(comm->device);
+  CUDA_TRY(comm, cudaMemcpy(out, comm->clique->trace[comm->device], need * sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost));
+  return BLINK_SUCCESS;
+}
+
 blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* st) {
   if (!comm || !st) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
   *st = comm->stats;
@@ -1486,6 +1570,7 @@ blink_result_t blink_destroy(blink_comm_t comm) {
       }
       for (auto& kv : q->err_host) cudaFreeHost(kv.second);
       for (auto& kv : q->ctrl) cudaFree(kv.second);
+      for (auto& kv : q->trace) cudaFree(kv.second);
       for (auto& kv : q->miad) {
         if (kv.second.ev0) cudaEventDestroy(kv.second.ev0);
         if (kv.second.ev1) cudaEventDestroy(kv.second.ev1);
