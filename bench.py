@@ -262,6 +262,8 @@ def run_multiprocess(args):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if os.environ.get("BENCH_SAME_GPU") == "1":   # test harness: all ranks share cuda:0
+        local = 0
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     ex = B.torch_exchange()
@@ -312,7 +314,7 @@ def run_multiprocess(args):
     et = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64)
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
     m = world
-    peak_nvl = 900.0
+    peak_nvl = 770.0   # B200_PROFILING.md: measured peer copy per direction (900 nominal)
     out = None
     if rank == 0:
         workload = f"c3-onehop-allreduce-m{m}-nvswitch-f32-{S >> 20}MiB"
@@ -324,11 +326,13 @@ def run_multiprocess(args):
             "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
                        "ranks_kind": "one process per GPU", "bytes_per_rank": S,
                        "bus_bw_gbs": round(algbw * 2 * (m - 1) / m, 3),
-                       "l2": "256 MiB/rank send+recv > L2"},
+                       "l2": f"{2 * S >> 20} MiB send+recv per rank per step"
+                             + (" > 126 MB L2" if 2 * S > (126 << 20) else " (fits L2)")},
             "roofline": {"bound": "nvlink", "achieved": round(algbw * 2 * (m - 1) / m, 2),
                          "peak": peak_nvl, "unit": "GB/s",
                          "frac": round(algbw * 2 * (m - 1) / m / peak_nvl, 4),
-                         "traffic": None, "peak_source": "nominal NVLink-5 per direction"},
+                         "traffic": None,
+                         "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"},
             "e2e": {"value": round(S / (float(et.item()) * 1e-3) / 1e9, 3), "unit": UNIT,
                     "h2d_bytes_per_step": S, "d2h_bytes_per_step": S},
             "gpu_launches": launches, "clocks": clk.summary(),
