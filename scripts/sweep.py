@@ -10,6 +10,9 @@ ranks share one HBM, the algorithmic HBM bytes per call and their fraction of
 MEASURED_PEAKS.json hbm_gbs:
   AllReduce : 2 m S   (every send read once, every recv written once)
   Broadcast : (m+1) S (root send read once, every recv written once)
+plus `plan_hbm_frac`: the HBM bytes the chosen plan must move (multi-hop
+trees re-read partials / forwarded chunks) over the same time -- the
+executor's efficiency on its plan.
 Config 5 replays the App. C DDP bucket sequences back to back on one stream.
 Times are device times of CUDA-graph replays (no host enqueue cost).
 """
@@ -55,6 +58,32 @@ def time_calls(fn, nbytes):
     return e0.elapsed_time(e1) / reps
 
 
+def plan_traffic(plan, coll, esize):
+    """HBM bytes the executor must move for this plan when every rank shares
+    one HBM (virtual ranks): per tree of range S_i --
+      AllReduce: REDUCE at v with k children reads (1+k) S_i and writes S_i
+      (partial) or, at the root, (1+k) S_i (own + children's recv); an inner
+      node's BCAST reads S_i and writes k S_i.
+      Broadcast: the root reads S_i and writes (k+1) S_i (own recv + k
+      children); an inner node reads S_i and writes k S_i."""
+    tot = 0
+    for t in plan["trees"]:
+        Si = (t["hi"] - t["lo"]) * esize
+        par = t["parent"]
+        kids = {v: sum(1 for u in par if u == v) for v in range(len(par))}
+        for v, k in kids.items():
+            if k == 0:
+                continue
+            is_root = par[v] < 0
+            if coll == "allreduce":
+                tot += (1 + k) * Si + ((1 + k) * Si if is_root else Si)
+                if not is_root:
+                    tot += Si + k * Si
+            else:
+                tot += Si + (k + (1 if is_root else 0)) * Si
+    return tot
+
+
 def run_coll(comms, coll, S, dtype, root=0, tag=""):
     m = len(comms)
     cnt = max(1, S // ES[dtype])
@@ -77,9 +106,11 @@ def run_coll(comms, coll, S, dtype, root=0, tag=""):
     Sb = cnt * ES[dtype]
     alg = Sb / (ms * 1e-3) / 1e9
     plan = comms[0].plan(coll == "allreduce", root, cnt, dtype)
+    pt = plan_traffic(plan, coll, ES[dtype])
     return {"config": tag, "coll": coll, "m": m, "dtype": dtype, "bytes": Sb, "ms": round(ms, 5),
             "algbw": round(alg, 2), "busbw": round(alg * f, 2),
             "hbm_gbs": round(hbm / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(hbm / (ms * 1e-3) / 1e9 / PEAK, 4),
+            "plan_hbm_bytes": pt, "plan_hbm_frac": round(pt / (ms * 1e-3) / 1e9 / PEAK, 4),
             "trees": len(plan["trees"]), "ctas": plan["ctas"],
             "max_depth": max(t["depth"] for t in plan["trees"])}
 
