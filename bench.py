@@ -63,7 +63,7 @@ class Clocks:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         except Exception:
@@ -89,13 +89,16 @@ class Clocks:
             try:
                 util = float(parts[9]) if len(parts) > 9 else 100.0
                 rows.append(dict(sm=float(parts[1]), smax=float(parts[2]), hw=parts[5], hwt=parts[6],
-                                 swt=parts[7], pcap=parts[8], util=util))
+                                 swt=parts[7], pcap=parts[8], util=util, pw=float(parts[3])))
             except ValueError:
                 continue
         if not rows:
             return None
-        busy = [r for r in rows if r["util"] >= 50]
-        rows = busy or rows        # samples under load (the timed region)
+        # under load = drawing well above the idle floor (utilization.gpu is a
+        # coarse running average and lags a short timed region)
+        floor = min(r["pw"] for r in rows)
+        busy = [r for r in rows if r["pw"] >= floor * 1.5 or r["util"] >= 50]
+        rows = busy or rows
         reasons = set()
         for r in rows:
             for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
