@@ -94,11 +94,10 @@ class Clocks:
                 continue
         if not rows:
             return None
-        # under load = drawing well above the idle floor (utilization.gpu is a
-        # coarse running average and lags a short timed region)
-        floor = min(r["pw"] for r in rows)
-        busy = [r for r in rows if r["pw"] >= floor * 1.5 or r["util"] >= 50]
-        rows = busy or rows
+        # every sample falls inside the timed region (the sampler starts 0.3 s
+        # before it); nvidia-smi's utilization / power are slow running
+        # averages, so they are reported but not used to select samples
+        busy = rows
         reasons = set()
         for r in rows:
             for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
@@ -107,7 +106,8 @@ class Clocks:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(r["sm"] for r in rows),
                 "sm_max_mhz": max(r["smax"] for r in rows), "reasons": sorted(reasons),
-                "samples_under_load": len(busy), "samples": len(rows)}
+                "samples": len(rows), "max_power_w": max(r["pw"] for r in rows),
+                "note": "10 ms nvidia-smi samples spanning the timed region"}
 
 
 def cpu_oracle_baseline(m, count, budget_s=10.0, max_s=30.0):
