@@ -250,7 +250,8 @@ def root_tree(edges, n, root):
 # --------------------------------------------------------------------------
 # ILP refinement (Sec. 3.2.1)
 # --------------------------------------------------------------------------
-def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_limit=500):
+def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_limit=500,
+               multiplicity=False):
     """Eqs. 4-7 with the relaxation grid (R#5).
 
     `caps`: {edge: c_e}; `candidates`: list of (edge_list, depth, key) in a
@@ -273,12 +274,16 @@ def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_
     depth = np.array([d for (_, d, _) in candidates], dtype=float)
     best = None
     for g in grids:
-        # variables: z (k, integer 0..g), y (k, binary) ; z_T <= g y_T
+        # variables: z (k, integer 0..g*u_T), y (k, binary); z_T <= g u_T y_T with
+        # u_T = 1 (the paper's w_i <= 1) or, in the multiplicity fallback
+        # (R#26), the tree's bottleneck link count floor(min_{e in T} c_e)
+        ub = np.array([g * (int(min(caps[e] for e in te)) if multiplicity else 1)
+                       for (te, _, _) in candidates], dtype=float)
         Z = np.hstack([A, np.zeros_like(A)])
-        link = np.hstack([np.eye(k), -g * np.eye(k)])
+        link = np.hstack([np.eye(k), -np.diag(ub)])
         cons = [LinearConstraint(Z, -np.inf, g * cvec), LinearConstraint(link, -np.inf, 0.0)]
         integ = np.ones(2 * k)
-        bnds = Bounds(np.zeros(2 * k), np.concatenate([np.full(k, g), np.ones(k)]))
+        bnds = Bounds(np.zeros(2 * k), np.concatenate([ub, np.ones(k)]))
         ones_z = np.concatenate([np.ones(k), np.zeros(k)])
         ones_y = np.concatenate([np.zeros(k), np.ones(k)])
         dep_y = np.concatenate([np.zeros(k), depth])
@@ -381,6 +386,10 @@ def plan_broadcast_graph(g, r, eps=0.1, gap=0.05):
     cands = sorted(set(w) | set(lovasz_arborescences(g, r)))  # parent tuples (R#21)
     cand = [([(u, v) for v, u in enumerate(p) if u >= 0], parent_depth(p), p) for p in cands]
     sol, gg, ok = ilp_refine(cap, cand, c_star, gap)
+    if not ok:  # R#26: let a tree carry up to its bottleneck link count
+        sol2, gg2, ok2 = ilp_refine(cap, cand, c_star, gap, multiplicity=True)
+        if sum(w for _, w in sol2) > sum(w for _, w in sol):
+            sol, gg, ok = sol2, gg2, ok2
     trees = []
     for j, wt in sol:
         p = cands[j]
@@ -408,6 +417,10 @@ def plan_allreduce_graph(g, eps=0.1, gap=0.05):
         root = tree_centre(t, n)
         cand.append((list(t), parent_depth(root_tree(t, n, root)), t))
     sol, gg, ok = ilp_refine(pairs, cand, c_star, gap)
+    if not ok:  # R#26
+        sol2, gg2, ok2 = ilp_refine(pairs, cand, c_star, gap, multiplicity=True)
+        if sum(w for _, w in sol2) > sum(w for _, w in sol):
+            sol, gg, ok = sol2, gg2, ok2
     trees = []
     for j, wt in sol:
         t = cands[j]

@@ -368,10 +368,23 @@ struct IlpSol {
 class Ilp {
  public:
   Ilp(const std::vector<IlpCand>& cand, const std::vector<double>& c, int g,
-      const std::function<int64_t(const std::vector<int64_t>&)>& cut_bound, int64_t node_limit)
+      const std::function<int64_t(const std::vector<int64_t>&)>& cut_bound, int64_t node_limit,
+      bool multiplicity = false)
       : cand_(cand), g_(g), cut_bound_(cut_bound), node_limit_(node_limit) {
     res_.resize(c.size());
     for (size_t e = 0; e < c.size(); ++e) res_[e] = int64_t(std::floor(g * c[e] + 1e-9));
+    // z_T <= g u_T: u_T = 1 (the paper's w_i <= 1) or, in the multiplicity
+    // fallback (R#26), the tree's bottleneck link count
+    ub_.resize(cand.size());
+    for (size_t j = 0; j < cand.size(); ++j) {
+      int64_t u = 1;
+      if (multiplicity) {
+        double b = 1e30;
+        for (int e : cand[j].res) b = std::min(b, c[e]);
+        u = std::max<int64_t>(1, int64_t(std::floor(b + 1e-9)));
+      }
+      ub_[j] = g * u;
+    }
     order_.resize(cand.size());
     std::iota(order_.begin(), order_.end(), 0);
     std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) {
@@ -393,8 +406,8 @@ class Ilp {
     std::vector<int> z(cand_.size(), 0);
     for (int pass = 0; pass < 2; ++pass)
       for (int j : order_) {
-        int64_t want = pass == 0 ? int64_t(std::floor(g_ * cand_[j].x + 1e-9)) : g_;
-        int64_t m = std::min<int64_t>(want, g_) - z[j];
+        int64_t want = pass == 0 ? int64_t(std::floor(g_ * cand_[j].x + 1e-9)) : ub_[j];
+        int64_t m = std::min<int64_t>(want, ub_[j]) - z[j];
         for (int e : cand_[j].res) m = std::min(m, res[e]);
         if (m <= 0) continue;
         z[j] += int(m);
@@ -419,7 +432,7 @@ class Ilp {
     }
   }
   int64_t cap_of(int j) const {
-    int64_t m = g_;
+    int64_t m = ub_[j];
     for (int e : cand_[j].res) m = std::min(m, res_[e]);
     return std::max<int64_t>(m, 0);
   }
@@ -472,6 +485,7 @@ class Ilp {
   int64_t node_limit_;
   int64_t nodes_ = 0;
   std::vector<int64_t> res_;
+  std::vector<int64_t> ub_;
   std::vector<int> order_;
   std::vector<int> z_;
   IlpSol best_;
@@ -961,26 +975,30 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
   // ILP with the relaxation grid g = 1, 2, 4, 8, 16 (R#5)
   IlpSol best;
   int bestg = 1;
-  for (int gi = 0; gi < 5; ++gi) {
-    const int gg = 1 << gi;
-    // integral candidates first: the exact packing (Broadcast) or the peeling
-    // at this grid scale, seeded with their multiplicity
-    std::vector<IlpCand> cg = cands;
-    for (auto& c : cg) {
-      c.prio = (c.lovasz || c.mult[gi] > 0) ? 1 : 0;
-      if (c.lovasz) c.x = 1.0;
-      if (c.mult[gi] > 0) c.x = double(c.mult[gi]) / gg;
-    }
-    Ilp ilp(cg, caps, gg, cut, 200000);
-    IlpSol s = ilp.solve();
-    if (best.sumz < 0 || double(s.sumz) / gg > double(best.sumz) / bestg + 1e-12) {
-      best = s;
-      bestg = gg;
-    }
-    if (double(s.sumz) / gg >= (1.0 - gap) * c_star - 1e-12) {
-      best = s;
-      bestg = gg;
-      break;
+  bool accepted = false;
+  for (int pass = 0; pass < 2 && !accepted; ++pass) {  // pass 1: multiplicity fallback (R#26)
+    for (int gi = 0; gi < 5; ++gi) {
+      const int gg = 1 << gi;
+      // integral candidates first: the exact packing (Broadcast) or the peeling
+      // at this grid scale, seeded with their multiplicity
+      std::vector<IlpCand> cg = cands;
+      for (auto& c : cg) {
+        c.prio = (c.lovasz || c.mult[gi] > 0) ? 1 : 0;
+        if (c.lovasz) c.x = 1.0;
+        if (c.mult[gi] > 0) c.x = double(c.mult[gi]) / gg;
+      }
+      Ilp ilp(cg, caps, gg, cut, 200000, pass == 1);
+      IlpSol s = ilp.solve();
+      if (best.sumz < 0 || double(s.sumz) / gg > double(best.sumz) / bestg + 1e-12) {
+        best = s;
+        bestg = gg;
+      }
+      if (double(s.sumz) / gg >= (1.0 - gap) * c_star - 1e-12) {
+        best = s;
+        bestg = gg;
+        accepted = true;
+        break;
+      }
     }
   }
   std::vector<std::vector<std::pair<int, int>>> keys;

@@ -55,17 +55,21 @@ def _oracle_plan(p):
 
 
 def _check_plan(p, g, allreduce):
+    """Plan weights are in units of the graph's smallest link capacity (R#23):
+    scale by it before comparing with the raw-capacity optimum."""
     from oracle import bounds, graphs
     n, cap = g
+    unit = min(cap.values())
     W = sum(Fraction(*t["weight"]) for t in p["trees"])
     assert Fraction(*p["rate"]) == W
+    W = W * unit
     if allreduce:
         pairs = graphs.undirected_pairs(g)
         load = {e: Fraction(0) for e in pairs}
         for t in p["trees"]:
             for v, u in enumerate(t["parent"]):
                 if u >= 0:
-                    load[(min(u, v), max(u, v))] += Fraction(*t["weight"])
+                    load[(min(u, v), max(u, v))] += Fraction(*t["weight"]) * unit
         assert all(load[e] <= pairs[e] for e in pairs)
         opt = bounds.nash_williams_rate(pairs, n)
     else:
@@ -74,7 +78,7 @@ def _check_plan(p, g, allreduce):
             assert t["parent"][p["root"]] == -1
             for v, u in enumerate(t["parent"]):
                 if u >= 0:
-                    load[(u, v)] += Fraction(*t["weight"])
+                    load[(u, v)] += Fraction(*t["weight"]) * unit
         assert all(load[e] <= cap[e] for e in cap)
         opt = bounds.edmonds_rate(g, p["root"])
     # rate within the ILP gap of the true optimum (MWU is (1-eps)-optimal)
@@ -202,3 +206,42 @@ def test_multiserver_errors(B):
         B.plan_json(4, False, 0, 64, graph=G)
     assert e.value.code == 9
     assert len(B.plan_json(4, True, 0, 64, graph=G)["trees"]) == 2
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_graph_plans_satisfy_the_oracle_invariants(B, seed):
+    """C++ control plane on random connected link graphs (2-7 GPUs, capacities
+    1-3): Broadcast plans are arborescences from the root, AllReduce plans are
+    spanning trees; both are feasible (Eqs. 2, 5) and reach >= 95% of the
+    (1 - eps)-optimal MWU rate, and never exceed the Edmonds / Nash-Williams
+    optimum."""
+    import random
+    from oracle import bounds, graphs
+    rng = random.Random(4000 + seed)
+    n = rng.randint(2, 7)
+    while True:
+        cap = {}
+        for u in range(n):
+            for v in range(u + 1, n):
+                if rng.random() < 0.55:
+                    c = rng.randint(1, 3)
+                    cap[(u, v)] = cap[(v, u)] = c
+        if graphs.is_connected((n, cap)):
+            break
+    G = B.Graph.from_pairs(n, cap)
+    root = rng.randrange(n)
+    pb = B.plan_json(n, False, root, 123457, "f32", graph=G)
+    _check_plan(pb, (n, cap), False)
+    for t in pb["trees"]:
+        par = t["parent"]
+        assert par[root] == -1 and all((par[v], v) in cap for v in range(n) if v != root)
+    unit = min(cap.values())
+    assert Fraction(*pb["rate"]) * unit <= bounds.edmonds_rate((n, cap), root) + Fraction(1, 10**9)
+    pa = B.plan_json(n, True, 0, 123457, "bf16", graph=G)
+    _check_plan(pa, (n, cap), True)
+    pairs = graphs.undirected_pairs((n, cap))
+    assert float(Fraction(*pa["rate"]) * unit) <= bounds.nash_williams_rate(pairs, n) + 1e-9
+    for t in pa["trees"]:
+        par = t["parent"]
+        assert par.count(-1) == 1
+        assert all((min(par[v], v), max(par[v], v)) in pairs for v in range(n) if par[v] >= 0)
