@@ -506,13 +506,26 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
     // ------------------------------------------------ producer
     uint32_t g = 0;
     int cs = t.c0;  // static sequence
+    // dynamic tasks: the first chunk is the CTA's own index (no atomic round
+    // trip on the critical path); later chunks come from the counter, offset
+    // by the number of CTAs.  When every CTA owns at most one chunk the
+    // counter is never touched.
+    const int nch = t.merged ? t.c1 : tr.nchunks;
+    bool first_chunk = true;
     for (;;) {
       int c;
       if (ctr) {
-        unsigned int got = 0;
-        if (lane == 0) got = atomicAdd(ctr, 1u);
-        c = int(__shfl_sync(0xffffffffu, got, 0));
-        if (c >= (t.merged ? t.c1 : tr.nchunks)) break;
+        if (first_chunk) {
+          c = t.cta_idx;
+          first_chunk = false;
+        } else if (nch <= t.cta_cnt) {
+          break;
+        } else {
+          unsigned int got = 0;
+          if (lane == 0) got = atomicAdd(ctr, 1u);
+          c = int(__shfl_sync(0xffffffffu, got, 0)) + t.cta_cnt;
+        }
+        if (c >= nch) break;
       } else {
         c = cs;
         cs += t.cstride;

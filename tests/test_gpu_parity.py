@@ -536,3 +536,23 @@ def test_fullsize_config5_vgg16_bucket_sequence(B):
             _sample_check(b_in, b_out, "sum", dtype, nsamp=8192)
         del ins, outs
         torch.cuda.empty_cache()
+
+
+def test_device_trace_api(B):
+    """BLINK_TRACE: per-CTA %globaltimer stamps of the last launch, ordered."""
+    import os
+    os.environ["BLINK_TRACE"] = "1"
+    try:
+        m, count = 8, 1 << 20
+        comms = make_comms(B, m)
+        xs = [torch.randn(count, device="cuda") for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.allreduce(xs[r])
+        torch.cuda.synchronize()
+        tr = comms[0].trace()
+        assert len(tr) == comms[0].stats()["last_ctas"] > 0
+        for t in tr:
+            stamps = [x for x in (t[0], t[1], t[2], t[6], t[7]) if x]
+            assert stamps == sorted(stamps) and t[0] > 0
+    finally:
+        del os.environ["BLINK_TRACE"]
