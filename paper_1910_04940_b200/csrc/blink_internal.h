@@ -80,7 +80,13 @@ enum Role : int {
   kRoleExit = 2,    // only entry/exit bookkeeping for this rank
 };
 
-struct DevTask {             // one per CTA; 64 bytes
+struct DevTree {             // 32 bytes; byte offsets into every rank's buffers
+  int64_t lo, hi, chunk;
+  int32_t nchunks;
+  int32_t root;
+};
+
+struct DevTask {             // one per CTA segment; 96 bytes
   int16_t rank;              // acting rank v
   int16_t tree;              // tree index i
   int16_t role;
@@ -95,14 +101,11 @@ struct DevTask {             // one per CTA; 64 bytes
   int32_t ctr;               // >= 0: chunks are taken from counter ctrl[2 + ctr] (dynamic)
   int32_t merged;            // chunk ids span every tree (one-hop AllReduce, single launch)
   int32_t pad1;
+  DevTree tr;                // copy of trees[tree] (saves a dependent load at launch)
 };
-static_assert(sizeof(DevTask) == 64, "DevTask layout");
+static_assert(sizeof(DevTask) == 96, "DevTask layout");
 
-struct DevTree {             // 32 bytes; byte offsets into every rank's buffers
-  int64_t lo, hi, chunk;
-  int32_t nchunks;
-  int32_t root;
-};
+
 
 constexpr int kMaxArgRanks = kMaxRanks;
 struct LaunchArgs {

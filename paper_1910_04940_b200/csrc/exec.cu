@@ -403,6 +403,7 @@ struct TileMeta {
 };
 
 struct Shared {
+  int tree_end[kMaxTrees];  // merged tasks: prefix sums of the trees' chunk counts
   TileMeta smeta[kMaxStages];
   TileMeta ometa[kOutBufs];
   const char* srcs[kMaxRanks + 1];
@@ -540,8 +541,9 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
       int64_t b0, b1;
       if (t.merged) {  // chunk c of the concatenation of every tree's chunks
-        int cc = c, i = 0;
-        while (i + 1 < a.ntrees && cc >= a.trees[i].nchunks) cc -= a.trees[i++].nchunks;
+        int i = 0;
+        while (i + 1 < a.ntrees && c >= sh.tree_end[i]) ++i;
+        const int cc = c - (i ? sh.tree_end[i - 1] : 0);
         const DevTree ti = a.trees[i];
         b0 = ti.lo + int64_t(cc) * ti.chunk;
         b1 = min(ti.hi, b0 + ti.chunk);
@@ -768,12 +770,12 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   // segments: usually one; packed launches chain contiguous chunk ranges of
   // independent channels so that every SM carries the same number of bytes
   for (int ti = blockIdx.x; ti >= 0;) {
-    const DevTask t = a.tasks[ti];
+    const DevTask t = ti == int(blockIdx.x) ? t0 : a.tasks[ti];
     ti = t.next;
     if (t.role != kRoleReduce && t.role != kRoleBcast) continue;
     const int w = t.rank;
     uint64_t* wflags = a.flags[w];
-    const DevTree tr = a.trees[t.tree];
+    const DevTree tr = t.tr;
     const bool is_root = t.parent < 0;
     // entry handshake (warp 0): leaf children's send is ready once they
     // entered; Broadcast / AllGather push into children's recv only after they
@@ -786,6 +788,15 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
       const uint32_t emask = !a.exit_wait ? 0u
                              : (t.role == kRoleReduce ? t.leafmask : (pushes ? t.children : 0u));
       entry_ok = warp_wait(emask, [&](int u) { return wflags + entry_idx(u); }, ctl);
+      if (t.merged) {  // prefix sums of the trees' chunk counts (one parallel load)
+        const int lane = threadIdx.x;
+        int v = lane < a.ntrees ? a.trees[lane].nchunks : 0;
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, v, d);
+          if (lane >= d) v += y;
+        }
+        if (lane < a.ntrees) sh.tree_end[lane] = v;
+      }
     }
     if (threadIdx.x == 0) {
       int ns = 0, nd = 0;

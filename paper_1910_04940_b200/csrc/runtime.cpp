@@ -545,7 +545,8 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
     trees[i].nchunks = s->ranges[i].nchunks;
     trees[i].root = s->plan->trees[i].root;
   }
-  // the last tree's hi may not be a multiple of esize*... it is count*esize
+  for (auto& t : s->tasks)
+    if (t.tree >= 0 && size_t(t.tree) < trees.size()) t.tr = trees[t.tree];
   CUDA_TRY(comm, cudaMalloc(&s->d_tasks, sizeof(DevTask) * s->tasks.size()));
   CUDA_TRY(comm, cudaMalloc(&s->d_trees, sizeof(DevTree) * std::max<size_t>(1, trees.size())));
   CUDA_TRY(comm, cudaMemcpy(s->d_tasks, s->tasks.data(), sizeof(DevTask) * s->tasks.size(),
