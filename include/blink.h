@@ -205,6 +205,14 @@ blink_result_t blink_reduce_scatter(blink_comm_t comm, const void* sendbuf, void
 blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
                                size_t sendcount, blink_dtype_t dtype, void* stream);
 
+/* Gather (NEXT-3: "Gather is the inverse of Broadcast").  Every rank's
+ * sendcount elements land at block `rank` of the root's recvbuf
+ * (nranks*sendcount elements); recvbuf is unused (may be NULL) on other
+ * ranks.  One-hop trees: rank j's block travels the single edge j -> root.
+ * Switch (one-hop) topologies only. */
+blink_result_t blink_gather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
+                            size_t sendcount, blink_dtype_t dtype, int root, void* stream);
+
 /* ---------------------------------------------------------------- introspection
  * Same JSON as blink_plan_json, for the plan this comm would run, plus "ctas"
  * (CTAs of this rank's launch). */

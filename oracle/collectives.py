@@ -189,3 +189,10 @@ def allgather(sends):
     """AllReduce without a reduction: root j's block is broadcast to everyone,
     so every rank receives the blocks in rank order."""
     return np.concatenate([np.asarray(s) for s in sends])
+
+
+def gather(sends, root):
+    """Gather ("the inverse of Broadcast"): the root receives every
+    rank's block in rank order; the other ranks receive nothing (None)."""
+    return [np.concatenate([np.asarray(s) for s in sends]) if r == root else None
+            for r in range(len(sends))]

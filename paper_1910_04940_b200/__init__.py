@@ -81,6 +81,7 @@ _SIGS = {
     "blink_allreduce": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
     "blink_reduce_scatter": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
     "blink_allgather": (_i, [_vp, _vp, _vp, _sz, _i, _vp]),
+    "blink_gather": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
     "blink_get_plan": (_i, [_vp, _i, _i, _sz, _i, _cp, ctypes.POINTER(_sz)]),
     "blink_get_stats": (_i, [_vp, ctypes.POINTER(_Stats)]),
     "blink_get_trace": (_i, [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(_sz)]),
@@ -254,6 +255,15 @@ class Comm:
         cnt = send.numel() if sendcount is None else sendcount
         _check(_lib.blink_allgather(self._h, _ptr(send), _ptr(recv), cnt, DTYPES[dt],
                                     _stream(stream)), self._h)
+        return recv
+
+    def gather(self, send, recv=None, root=0, sendcount=None, dtype=None, stream=None):
+        """Gather (NEXT-3): block `rank` of the root's recv gets this
+        send; recv is ignored (may be None) on the other ranks."""
+        dt = _dtype_of(send, dtype)
+        cnt = send.numel() if sendcount is None else sendcount
+        _check(_lib.blink_gather(self._h, _ptr(send), _ptr(recv), cnt, DTYPES[dt], int(root),
+                                 _stream(stream)), self._h)
         return recv
 
     def plan(self, is_allreduce=True, root=0, count=0, dtype="f32"):

@@ -41,14 +41,17 @@ __host__ __device__ inline size_t bflag_idx(int tree, int chunk) {
   return kEntryWords + kPflagWords + size_t(tree) * kMaxChunks + chunk;
 }
 
-enum Coll : int { kBroadcast = 0, kAllReduce = 1, kReduceScatter = 2, kAllGather = 3 };
-// ReduceScatter / AllGather: tree j is the one-hop star rooted at j and owns block j.
-inline bool is_block_coll(int c) { return c == kReduceScatter || c == kAllGather; }
+enum Coll : int { kBroadcast = 0, kAllReduce = 1, kReduceScatter = 2, kAllGather = 3, kGather = 4 };
+// ReduceScatter / AllGather / Gather: tree j is the one-hop star rooted at j and owns block j
+// (Gather: the star has the single leaf `root`; other ranks are not members, parent -2).
+inline bool is_block_coll(int c) { return c == kReduceScatter || c == kAllGather || c == kGather; }
+// collectives whose tree roots push their own send down the tree
+inline __host__ __device__ bool is_push_coll(int c) { return c == kBroadcast || c == kAllGather || c == kGather; }
 
 // ---------------------------------------------------------------- plans
 struct Tree {
   int root = 0;
-  std::vector<int> parent;   // parent[root] = -1
+  std::vector<int> parent;   // parent[root] = -1; -2 = not in this tree (Gather)
   int64_t wnum = 1;          // weight = wnum / wden (exact rational, P:390 grid)
   int64_t wden = 1;
   int depth = 0;
@@ -80,13 +83,15 @@ enum Role : int {
   kRoleExit = 2,    // only entry/exit bookkeeping for this rank
 };
 
-struct DevTree {             // 32 bytes; byte offsets into every rank's buffers
+struct DevTree {             // 40 bytes; byte offsets into every rank's buffers
   int64_t lo, hi, chunk;
   int32_t nchunks;
   int32_t root;
+  uint32_t members;          // ranks in the tree (Gather trees span root + one leaf)
+  int32_t pad;
 };
 
-struct DevTask {             // one per CTA segment; 96 bytes
+struct DevTask {             // one per CTA segment; 104 bytes
   int16_t rank;              // acting rank v
   int16_t tree;              // tree index i
   int16_t role;
@@ -103,7 +108,7 @@ struct DevTask {             // one per CTA segment; 96 bytes
   int32_t pad1;
   DevTree tr;                // copy of trees[tree] (saves a dependent load at launch)
 };
-static_assert(sizeof(DevTask) == 96, "DevTask layout");
+static_assert(sizeof(DevTask) == 104, "DevTask layout");
 
 
 

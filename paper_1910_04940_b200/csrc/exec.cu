@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
     // entered
     bool entry_ok = true;
     if (threadIdx.x < 32) {
-      const bool pushes = a.coll == kBroadcast || a.coll == kAllGather;
+      const bool pushes = is_push_coll(a.coll);
       // one launch holding every rank: all inputs are final at launch and all
       // outputs free, so there is nothing to hand shake
       const uint32_t emask = !a.exit_wait ? 0u
@@ -812,9 +812,11 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
           for (int u = 0; u < a.nranks; ++u)
             if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
       } else {
-        const bool src_root = (a.coll == kBroadcast || a.coll == kAllGather) && is_root;
+        const bool src_root = is_push_coll(a.coll) && is_root;
         sh.srcs[ns++] = src_root ? a.send[w] : a.recv[w];
-        if (src_root && a.send[w] != a.recv[w]) sh.dsts[nd++] = a.recv[w];
+        // the root's own copy (Gather: only the gather root holds a recv)
+        if (src_root && a.send[w] != a.recv[w] && (a.coll != kGather || w == a.bcast_root))
+          sh.dsts[nd++] = a.recv[w];
         for (int u = 0; u < a.nranks; ++u)
           if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
       }
@@ -836,8 +838,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
     }
     __syncthreads();
     if (threadIdx.x == 0) trace(a, 2);
-    const bool need_bflag =
-        (t.role == kRoleBcast) && !((a.coll == kBroadcast || a.coll == kAllGather) && is_root);
+    const bool need_bflag = (t.role == kRoleBcast) && !(is_push_coll(a.coll) && is_root);
     const bool aborted = sh.abort;
     if (!aborted) {
       if (ws)
@@ -857,7 +858,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
     int k = 0;
     for (int i = 0; i < a.ntrees; ++i) {
       const DevTree tr = a.trees[i];
-      if (tr.root == v) continue;
+      if (tr.root == v || !((tr.members >> v) & 1u)) continue;
       for (int c = 0; c < tr.nchunks; ++c, ++k) {
         if (k % t.exit_cnt != t.exit_idx) continue;
         if (((k / t.exit_cnt) % blockDim.x) != threadIdx.x) continue;
@@ -909,7 +910,7 @@ ExecFn pick_op(int op) {
 }
 
 ExecFn pick(int coll, int dtype, int op, bool vec) {
-  if (coll == kBroadcast || coll == kAllGather) return vec ? exec_kernel<BLINK_FLOAT32, BLINK_SUM, true>
+  if (is_push_coll(coll)) return vec ? exec_kernel<BLINK_FLOAT32, BLINK_SUM, true>
                                      : exec_kernel<BLINK_FLOAT32, BLINK_SUM, false>;
   switch (dtype) {
     case BLINK_FLOAT32: return vec ? pick_op<BLINK_FLOAT32, true>(op) : pick_op<BLINK_FLOAT32, false>(op);
@@ -929,7 +930,7 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = vec ? a.smem_bytes : 0;
-  static bool attr_set[4][3][4][2] = {};
+  static bool attr_set[5][3][4][2] = {};
   bool& done = attr_set[a.coll][a.dtype][a.op][vec];
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

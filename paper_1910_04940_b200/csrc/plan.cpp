@@ -1128,7 +1128,7 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
 std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vector<TreeRange>& r,
                          int ctas) {
   std::ostringstream o;
-  static const char* names[] = {"broadcast", "allreduce", "reduce_scatter", "allgather"};
+  static const char* names[] = {"broadcast", "allreduce", "reduce_scatter", "allgather", "gather"};
   o << "{\"coll\":\"" << names[p.coll] << "\",\"root\":"
     << p.root << ",\"nranks\":" << p.nranks << ",\"count\":" << count << ",\"esize\":" << esize
     << ",\"switch\":" << (p.switch_model ? "true" : "false") << ",\"rate\":[" << p.rate_num << ","

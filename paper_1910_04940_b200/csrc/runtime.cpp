@@ -197,7 +197,7 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
 // Plan cache: key (coll, root) with root = -1 for AllReduce, and root + 1000
 // for the one-hop Broadcast star variant on switches.
 blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, const Plan** out) {
-  int key_root = coll == kBroadcast ? root : -1;
+  int key_root = (coll == kBroadcast || coll == kGather) ? root : -1;
   if (is_block_coll(coll) && !comm->graph.switch_model)
     return fail(comm, BLINK_ERR_UNSUPPORTED,
                 "ReduceScatter/AllGather run on one-hop trees: switch topologies only");
@@ -232,6 +232,10 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
     if (is_block_coll(coll)) {  // one-hop stars; tree j owns block j
       p->coll = coll;
       p->blocks = true;
+      if (coll == kGather)  // star j keeps the single leaf `root`
+        for (Tree& t : p->trees)
+          for (int v = 0; v < int(t.parent.size()); ++v)
+            if (t.parent[v] >= 0 && v != root) t.parent[v] = -2;
     }
   }
   if (r != BLINK_SUCCESS) return fail(comm, r, err);
@@ -274,7 +278,8 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
     if (!((launch_mask >> v) & 1)) continue;
     for (int i = 0; i < k; ++i) {
       uint32_t c = ch[i][v];
-      if (!c) continue;
+      const bool own_block = plan.blocks && is_push_coll(plan.coll) && plan.trees[i].root == v;
+      if (!c && !own_block) continue;
       int nc = __builtin_popcount(c);
       uint32_t leaf = 0;
       for (int u = 0; u < n; ++u)
@@ -544,6 +549,10 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
     trees[i].chunk = s->ranges[i].chunk * esize;
     trees[i].nchunks = s->ranges[i].nchunks;
     trees[i].root = s->plan->trees[i].root;
+    uint32_t mem = 0;
+    for (size_t v = 0; v < s->plan->trees[i].parent.size(); ++v)
+      if (s->plan->trees[i].parent[v] != -2) mem |= 1u << v;
+    trees[i].members = mem;
   }
   for (auto& t : s->tasks)
     if (t.tree >= 0 && size_t(t.tree) < trees.size()) t.tr = trees[t.tree];
@@ -632,7 +641,7 @@ blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtyp
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported dtype " + std::to_string(dtype));
   if ((coll == kAllReduce || coll == kReduceScatter) && (op < BLINK_SUM || op > BLINK_MAX))
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported op " + std::to_string(op));
-  if (coll == kBroadcast && (root < 0 || root >= comm->nranks))
+  if ((coll == kBroadcast || coll == kGather) && (root < 0 || root >= comm->nranks))
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT,
                 "root " + std::to_string(root) + " out of range [0," + std::to_string(comm->nranks) + ")");
   if (count > (size_t(1) << 40))
@@ -707,7 +716,7 @@ blink_result_t clique_launch(Clique* q) {
     blink_comm_t cd = nullptr;
     for (int v = 0; v < n && !cd; ++v)
       if ((mask >> v) & 1) cd = q->comms[v];
-    SizedKey key{q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count,
+    SizedKey key{q->coll, (q->coll == kBroadcast || q->coll == kGather) ? q->root : -1, q->dtype, q->count,
                  mask | (uint64_t(plan->trees.size()) << 32) |
                      (uint64_t(q->coll == kBroadcast && plan->trees.size() == 1) << 48),
                  chunk_override};
@@ -732,7 +741,7 @@ blink_result_t clique_launch(Clique* q) {
     a.op = q->op;
     a.exit_wait = all_one_launch ? 0 : 1;
     a.scope_sys = all_one_launch ? 0 : 1;
-    a.bcast_root = q->coll == kBroadcast ? q->root : -1;
+    a.bcast_root = (q->coll == kBroadcast || q->coll == kGather) ? q->root : -1;
     a.use_tma = use_tma();
     a.smem_bytes = smem_bytes();
     a.tile_bytes = tile_bytes();
@@ -754,7 +763,7 @@ blink_result_t clique_launch(Clique* q) {
       a.flags[v] = q->comms[v]->flags;
       // block collectives address rank v's short buffer through tree v's range
       if (q->coll == kReduceScatter) a.recv[v] -= size_t(v) * bytes;
-      if (q->coll == kAllGather && a.send[v]) a.send[v] -= size_t(v) * bytes;
+      if ((q->coll == kAllGather || q->coll == kGather) && a.send[v]) a.send[v] -= size_t(v) * bytes;
     }
     DeviceGuard g(dev);
     // launch on the first rank's stream of this device after the others' streams
@@ -832,8 +841,8 @@ blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* 
     q->op = op;
     q->count = count;
   } else if (q->coll != coll || q->count != count || q->dtype != int(dtype) ||
-             (coll != kBroadcast && coll != kAllGather && q->op != op) ||
-             (coll == kBroadcast && q->root != root)) {
+             (!is_push_coll(coll) && q->op != op) ||
+             ((coll == kBroadcast || coll == kGather) && q->root != root)) {
     return fail(comm, BLINK_ERR_INVALID_USAGE,
                 "rank " + std::to_string(comm->rank) +
                     " called a different collective/count/dtype/op/root than the ranks already "
@@ -908,7 +917,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   blink_result_t r = get_plan(comm, coll, root, bytes, &plan);
   if (r != BLINK_SUCCESS) return r;
   uint64_t mask = uint64_t(1) << comm->rank;
-  SizedKey key{coll, coll == kBroadcast ? root : -1, int(dtype), count,
+  SizedKey key{coll, (coll == kBroadcast || coll == kGather) ? root : -1, int(dtype), count,
                mask | (uint64_t(plan->trees.size()) << 32)};
   auto it = comm->sized.find(key);
   if (it == comm->sized.end()) {
@@ -936,7 +945,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.op = op;
   a.exit_wait = 1;
   a.scope_sys = 1;
-  a.bcast_root = coll == kBroadcast ? root : -1;
+  a.bcast_root = (coll == kBroadcast || coll == kGather) ? root : -1;
   a.use_tma = use_tma();
   a.smem_bytes = smem_bytes();
   a.tile_bytes = tile_bytes();
@@ -951,7 +960,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     a.recv[u] = recv[u];
     a.flags[u] = comm->peer_flags[u];
     if (coll == kReduceScatter && a.recv[u]) a.recv[u] -= size_t(u) * bytes;
-    if (coll == kAllGather && a.send[u]) a.send[u] -= size_t(u) * bytes;
+    if ((coll == kAllGather || coll == kGather) && a.send[u]) a.send[u] -= size_t(u) * bytes;
   }
   cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, use_coop());
   if (le != cudaSuccess)
@@ -969,7 +978,8 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
 // write this rank's recv (register it or it is staged), only the own send is
 // read.  Staged calls run in pieces of P elements per block.
 blink_result_t mp_block_collective(blink_comm_t comm, int coll, const void* sendbuf, void* recvbuf,
-                                   size_t count, blink_dtype_t dtype, int op, cudaStream_t stream) {
+                                   size_t count, blink_dtype_t dtype, int op, int root,
+                                   cudaStream_t stream) {
   const int m = comm->nranks, me = comm->rank;
   const int es = esize_of(dtype);
   const char* sb = static_cast<const char*>(sendbuf);
@@ -982,8 +992,8 @@ blink_result_t mp_block_collective(blink_comm_t comm, int coll, const void* send
       return mp_run(comm, coll, sp, rp, count, dtype, op, -1, stream);
   } else {
     sp[me] = const_cast<char*>(sb);
-    if (resolve(comm, recvbuf, size_t(m) * count * es, rp))
-      return mp_run(comm, coll, sp, rp, count, dtype, op, -1, stream);
+    if (recvbuf && resolve(comm, recvbuf, size_t(m) * count * es, rp))
+      return mp_run(comm, coll, sp, rp, count, dtype, op, root, stream);
   }
   const size_t P = std::max<size_t>(1, comm->staging_bytes / (size_t(m) * es));
   char* st[kMaxRanks];
@@ -1003,11 +1013,12 @@ blink_result_t mp_block_collective(blink_comm_t comm, int coll, const void* send
     } else {
       CUDA_TRY(comm, launch_copy(comm->staging + size_t(me) * cnt * es, sb + k0 * es, cnt * es, stream));
       s2[me] = comm->staging + size_t(me) * cnt * es;
-      r = mp_run(comm, coll, s2, st, cnt, dtype, op, -1, stream);
+      r = mp_run(comm, coll, s2, st, cnt, dtype, op, root, stream);
       if (r != BLINK_SUCCESS) return r;
-      for (int j = 0; j < m; ++j)
-        CUDA_TRY(comm, launch_copy(rb + (size_t(j) * count + k0) * es,
-                                   comm->staging + size_t(j) * cnt * es, cnt * es, stream));
+      if (coll == kAllGather || me == root)
+        for (int j = 0; j < m; ++j)
+          CUDA_TRY(comm, launch_copy(rb + (size_t(j) * count + k0) * es,
+                                     comm->staging + size_t(j) * cnt * es, cnt * es, stream));
     }
   }
   return BLINK_SUCCESS;
@@ -1027,7 +1038,8 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
     comm->stats.launches++;
     return BLINK_SUCCESS;
   }
-  if (is_block_coll(coll)) return mp_block_collective(comm, coll, sendbuf, recvbuf, count, dtype, op, stream);
+  if (is_block_coll(coll))
+    return mp_block_collective(comm, coll, sendbuf, recvbuf, count, dtype, op, root, stream);
   char* sp[kMaxRanks] = {};
   char* rp[kMaxRanks] = {};
   const bool recv_ok = resolve(comm, recvbuf, bytes, rp);
@@ -1478,6 +1490,19 @@ blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* rec
     return mp_collective(comm, kAllGather, sendbuf, recvbuf, sendcount, dtype, BLINK_SUM, -1, stream);
   }
   return clique_post(comm, kAllGather, sendbuf, recvbuf, sendcount, dtype, BLINK_SUM, -1, stream);
+}
+
+blink_result_t blink_gather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
+                            size_t sendcount, blink_dtype_t dtype, int root, void* stream) {
+  blink_result_t r = validate_call(comm, sendcount, dtype, BLINK_SUM, root, kGather);
+  if (r != BLINK_SUCCESS) return r;
+  if (sendcount > 0 && (!sendbuf || (comm->rank == root && !recvbuf)))
+    return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL buffer");
+  if (comm->multiprocess) {
+    if (sendcount == 0) return BLINK_SUCCESS;
+    return mp_collective(comm, kGather, sendbuf, recvbuf, sendcount, dtype, BLINK_SUM, root, stream);
+  }
+  return clique_post(comm, kGather, sendbuf, recvbuf, sendcount, dtype, BLINK_SUM, root, stream);
 }
 
 blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, size_t count,

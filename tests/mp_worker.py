@@ -123,6 +123,15 @@ def gpu_mode(rank, world):
     comm.allgather(out2, ag)
     torch.cuda.synchronize()
     check(ag, OC.allgather(OC.reduce_scatter(rsends, "f32", "max")), "registered rs+ag")
+    # 6) Gather to the last rank (staged: only the root holds a recv)
+    gsends = synth.inputs(44, world, 9001, "f32")
+    gx = torch.from_numpy(gsends[rank]).cuda()
+    groot = world - 1
+    gout = torch.full((world * 9001,), float("nan"), device="cuda") if rank == groot else None
+    comm.gather(gx, gout, root=groot)
+    torch.cuda.synchronize()
+    if rank == groot:
+        check(gout, OC.gather(gsends, groot)[groot], "staged gather")
     st = comm.stats()
     comm.destroy()
     print(f"rank {rank}: gpu ok launches={st['launches']} ctas={st['last_ctas']}")

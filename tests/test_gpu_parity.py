@@ -556,3 +556,17 @@ def test_device_trace_api(B):
             assert stamps == sorted(stamps) and t[0] > 0
     finally:
         del os.environ["BLINK_TRACE"]
+
+
+@pytest.mark.parametrize("m", [2, 3, 8])
+@pytest.mark.parametrize("B_", [1, 6, 4096, 25001])
+def test_gather(B, m, B_):
+    comms = make_comms(B, m, chunk_bytes=16384)
+    for root in sorted({0, m - 1, m // 2}):
+        sends = synth.inputs(140 + root, m, B_, "f32")
+        ds = [to_dev(s, "f32") for s in sends]
+        out = sentinel(m * B_, "f32")
+        for r, c in enumerate(comms):
+            c.gather(ds[r], out if r == root else None, root=root, sendcount=B_, dtype="f32")
+        torch.cuda.synchronize()
+        assert_bitwise(out.cpu().numpy(), OC.gather(sends, root)[root])

@@ -203,3 +203,14 @@ def test_reduce_scatter_int_exact_and_allgather_blocks():
     ag = C.allgather([s[:B] for s in sends])
     for j in range(m):
         assert ag[j * B:(j + 1) * B].tobytes() == sends[j][:B].tobytes()
+
+
+def test_gather_is_allgather_at_the_root_only():
+    m, B = 4, 33
+    sends = synth.inputs(14, m, B, "bf16")
+    g = C.gather(sends, 2)
+    assert g[0] is None and g[1] is None and g[3] is None
+    assert g[2].tobytes() == C.allgather(sends).tobytes()
+    # inverse of Broadcast: block j of the root's result is exactly rank j's send
+    for j in range(m):
+        assert g[2][j * B:(j + 1) * B].tobytes() == sends[j].tobytes()
