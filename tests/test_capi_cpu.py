@@ -245,3 +245,11 @@ def test_random_graph_plans_satisfy_the_oracle_invariants(B, seed):
         par = t["parent"]
         assert par.count(-1) == 1
         assert all((min(par[v], v), max(par[v], v)) in pairs for v in range(n) if par[v] >= 0)
+
+
+def test_init_all_rejects_too_many_ranks_before_touching_cuda(B):
+    import ctypes
+    hs = (ctypes.c_void_p * 17)()
+    devs = (ctypes.c_int * 17)(*([0] * 17))
+    assert B._lib.blink_init_all(hs, 17, devs, None, None) == 9       # BLINK_ERR_UNSUPPORTED
+    assert b"16" in B._lib.blink_last_error(None)

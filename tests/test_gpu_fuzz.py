@@ -86,7 +86,7 @@ def test_random_configuration(B, seed):
     rng = random.Random(7000 + seed)
     m, graph, kind = random_graph(B, rng)
     coll = "allreduce" if kind == "multiserver" else rng.choice(["allreduce", "allreduce", "broadcast"] +
-                      (["reduce_scatter", "allgather"] if kind == "switch" else []))
+                      (["reduce_scatter", "allgather", "gather"] if kind == "switch" else []))
     dtype = rng.choice(["f32", "bf16", "i32"])
     op = rng.choice(["sum", "min", "max"] + (["prod"] if dtype == "i32" else []))
     count = rng.choice([1, 7, 255, 4096, 65537, 300001, rng.randint(1, 200000)])
@@ -128,16 +128,23 @@ def test_random_configuration(B, seed):
         rs = [out(count) for _ in range(m)]
         for r, c in enumerate(comms):
             c.reduce_scatter(ds[r], rs[r], op=op, recvcount=count, dtype=dtype)
+    elif coll == "gather":
+        rs = [out(m * count) if r == root else None for r in range(m)]
+        for r, c in enumerate(comms):
+            c.gather(ds[r], rs[r], root=root, sendcount=count, dtype=dtype)
     else:
         rs = [out(m * count) for _ in range(m)]
         for r, c in enumerate(comms):
             c.allgather(ds[r], rs[r], sendcount=count, dtype=dtype)
     torch.cuda.synchronize()
-    got = [to_host(x, dtype) for x in rs]
+    got = [to_host(x, dtype) if x is not None else None for x in rs]
     what = f"{kind} m={m} {coll} {dtype} {op} n={count} inplace={inplace} misalign={misalign} chunk={chunk}"
     if coll == "broadcast":
         for g in got:
             assert np.array_equal(bits(g), bits(sends[root])), what
+        return
+    if coll == "gather":
+        assert np.array_equal(bits(got[root]), bits(OC.allgather(sends))), what
         return
     if coll == "allgather":
         for g in got:

@@ -570,3 +570,16 @@ def test_gather(B, m, B_):
             c.gather(ds[r], out if r == root else None, root=root, sendcount=B_, dtype="f32")
         torch.cuda.synchronize()
         assert_bitwise(out.cpu().numpy(), OC.gather(sends, root)[root])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_sixteen_ranks_max(B, dtype):
+    """kMaxRanks = 16 (a DGX-2-sized switch): one-hop AllReduce with
+    16 sources per root (2-stage ring of 4 KiB tiles)."""
+    m, count = 16, 16 * 3000 + 5
+    comms = make_comms(B, m)
+    sends = synth.inputs(150, m, count, dtype)
+    got = run_allreduce(B, comms, sends, dtype, "sum")
+    want = OC.allreduce(OP.plan_switch_allreduce(m), sends, dtype, "sum")
+    for g in got:
+        assert_bitwise(g, want)
