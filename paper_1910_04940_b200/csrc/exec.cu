@@ -1,13 +1,20 @@
-// Device executor for tree-packed Broadcast / AllReduce on sm_100a.
+// Device executor for tree-packed collectives on sm_100a (Broadcast,
+// AllReduce; ReduceScatter / AllGather / Gather on one-hop trees).
 //
 // One persistent, cooperative launch per device per collective.  Every CTA
-// owns one slice of a "channel" = (rank v, tree i, role) and walks that
-// tree's chunks c = cta_idx, cta_idx + cta_cnt, ... in increasing order, so
-// chunks of all trees and all hops are in flight at once (pipelining,
-// P:510-517; concurrency across trees with fair interleaving).
+// runs one slice of a "channel" = (rank v, tree i, role).  A channel's CTAs
+// take its chunks in increasing order -- from a per-channel atomic counter
+// (dynamic balancing) or a static stride -- so chunks of all trees and all
+// hops are in flight at once (pipelining; concurrency across
+// trees).  A single launch of one-hop AllReduce roots is one
+// merged channel over every tree's chunks.
 //
-// Data movement is SM load/store over NVLink/NVSwitch peer mappings (or plain
-// HBM for virtual ranks sharing one GPU):
+// Data movement (TMA path, aligned buffers): a warp-specialised pipeline --
+// producer warp (cp.async.bulk loads of every source tile into a shared-
+// memory stage ring, mbarrier full/empty), consumer warps (fp32 combine in
+// ascending-rank order into an output tile), store warp (cp.async.bulk
+// stores to every destination) -- over NVLink/NVSwitch peer mappings, or HBM
+// for virtual ranks sharing one GPU:
 //   REDUCE (a3)  pull the children's chunk (leaf child: its send buffer;
 //                internal child: the partial it left in its own recv
 //                buffer), combine with the own send chunk in ascending-rank
@@ -19,12 +26,12 @@
 //   BCAST  (a2/a4) wait bflag[i][c] (non-root), read the chunk from the own
 //                recv (root: send), push it into the children's recv,
 //                release their bflag[i][c].
-// Readiness (a5): 64-bit epoch flags in the consumer's memory, written with
-// st.release.sys after a CTA barrier + fence, polled with ld.acquire.sys by
-// one thread; data is read with ld.global.cg (L2, never a stale L1 line).
-// 128-bit vectors on the aligned body, scalar elements on tails / misaligned
-// buffers.  Timeouts (globaltimer) abort the launch and set a host-mapped
-// error word instead of hanging.
+// Readiness (a5): 64-bit epoch flags in the consumer's memory: one
+// fence.acq_rel then relaxed stores to signal, relaxed polls by the lanes of
+// one warp then a fence to wait; .gpu scope inside one device, .sys across.
+// Epochs live in device memory (CUDA-graph safe).  Misaligned buffers run a
+// 128-bit / scalar LSU path with ld.global.cg.  Timeouts (globaltimer) abort
+// the launch through a host-mapped error word instead of hanging.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -308,16 +315,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
 }
 __device__ __forceinline__ void tma_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

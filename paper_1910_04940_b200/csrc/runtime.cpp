@@ -99,7 +99,7 @@ struct blink_comm {
   bool multiprocess = false;
   bool connected = false;
   Clique* clique = nullptr;
-  uint64_t epoch = 0;  // multi-process
+  uint64_t calls = 0;  // multi-process: collectives launched (epochs live on the device)
   uint64_t* flags = nullptr;
   uint64_t* peer_flags[kMaxRanks] = {};
   int* err_host = nullptr;  // multi-process error word
@@ -110,12 +110,6 @@ struct blink_comm {
   std::map<SizedKey, Sized> sized;                             // multi-process launches
   std::vector<Reg> regs;
   std::map<std::string, char*> opened;  // peer IPC handle bytes -> mapped base
-  struct PendingReg {
-    void* buf;
-    size_t bytes;
-    size_t offset;
-  };
-  std::vector<PendingReg> pending_regs;
   char* staging = nullptr;
   size_t staging_bytes = 0;
   char* peer_staging[kMaxRanks] = {};
@@ -131,7 +125,7 @@ struct Clique {
   std::vector<blink_comm*> comms;
   std::vector<int> devices;  // distinct devices
   int alive = 0;
-  uint64_t epoch = 0;
+  uint64_t calls = 0;  // batches launched (epochs live on the device)
   // the batch being assembled
   int nposted = 0;
   int coll = -1, root = -1, dtype = -1, op = -1;
@@ -151,7 +145,6 @@ struct Clique {
   std::map<std::tuple<int, int, int, size_t>, MiadRun> miad;  // (coll, root, dtype, count)
   std::map<SizedKey, Sized> sized;
   int64_t launches = 0;
-  bool sticky_error = false;
 };
 
 blink_result_t fail(blink_comm_t comm, blink_result_t r, const std::string& msg) {
@@ -656,7 +649,7 @@ blink_result_t clique_launch(Clique* q) {
   const int n = q->nranks;
   const int es = esize_of(blink_dtype_t(q->dtype));
   const size_t bytes = q->count * es;
-  q->epoch++;
+  q->calls++;
   blink_comm_t c0 = q->comms[0];
   if (n == 1) {
     DeviceGuard g(c0->device);
@@ -829,7 +822,6 @@ blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* 
   std::lock_guard<std::mutex> lk(q->mu);
   for (auto& kv : q->err_host)
     if (*kv.second != 0) {
-      q->sticky_error = true;
       return fail(comm, blink_result_t(*kv.second),
                   "a previous launch aborted (flag wait timed out on device " +
                       std::to_string(kv.first) + ")");
@@ -912,7 +904,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   const int n = comm->nranks;
   const int es = esize_of(dtype);
   const size_t bytes = count * es;
-  comm->epoch++;
+  comm->calls++;
   const Plan* plan = nullptr;
   blink_result_t r = get_plan(comm, coll, root, bytes, &plan);
   if (r != BLINK_SUCCESS) return r;
