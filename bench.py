@@ -316,6 +316,8 @@ def run_multiprocess(args):
     torch.cuda.synchronize()
     et = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64)
     dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    nccl = nccl_same_buffers(args, send, recv, stream) if os.environ.get("BENCH_SAME_GPU") != "1" else \
+        {"unavailable": "all ranks share one GPU (NCCL needs one GPU per rank)"}
     m = world
     peak_nvl = 770.0   # B200_PROFILING.md: measured peer copy per direction (900 nominal)
     out = None
@@ -339,11 +341,44 @@ def run_multiprocess(args):
             "e2e": {"value": round(S / (float(et.item()) * 1e-3) / 1e9, 3), "unit": UNIT,
                     "h2d_bytes_per_step": S, "d2h_bytes_per_step": S},
             "gpu_launches": launches, "clocks": clk.summary(),
+            "nccl": nccl,
         }
     comm.destroy()
     dist.barrier()
     dist.destroy_process_group()
     return out
+
+
+def nccl_same_buffers(args, send, recv, stream):
+    """NCCL AllReduce (torch.distributed nccl group) on the same buffers,
+    stream and step count: the comparison the metric names.  Max over ranks."""
+    import torch
+    import torch.distributed as dist
+    try:
+        g = dist.new_group(backend="nccl")
+        S = send.numel() * send.element_size()
+        recv.copy_(send)
+        for _ in range(args.warmup):
+            dist.all_reduce(recv, group=g)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            dist.all_reduce(recv, group=g)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        world = dist.get_world_size()
+        alg = S / (ms * 1e-3) / 1e9
+        return {"value": round(alg, 3), "unit": UNIT, "ms_per_step": round(ms, 4),
+                "bus_bw_gbs": round(alg * 2 * (world - 1) / world, 3),
+                "impl": f"NCCL {'.'.join(map(str, torch.cuda.nccl.version()))} via torch.distributed, in place"}
+    except Exception as e:  # pragma: no cover - depends on the box
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
 
 # --------------------------------------------------------------------------- reference arm

@@ -100,7 +100,25 @@ typedef struct {
  *                  buffer used for unregistered user buffers; default 64 MiB
  *   autotune       1 = MIAD chunk-size selection across calls (P:526-535,
  *                  single-process comms; chunking never changes results);
- *                  0 = the static table (default) */
+ *                  0 = the static table (default)
+ *   launch_per_rank  single-process comms only: 1 = every rank runs in its own
+ *                  launch on a library-owned stream (forked from and joined
+ *                  back into the rank's stream), with the cross-launch
+ *                  protocol of the multi-process path (entry handshake,
+ *                  per-chunk flags, exit waits) even when ranks share a
+ *                  device.  Each launch gets 1/m of the device's co-resident
+ *                  CTAs.  This runs the one-process-per-GPU data path
+ *                  concurrently on one GPU (separate processes time-slice).
+ *                  0 = ranks sharing a device are batched into one launch
+ *                  (default)
+ *   ll_max_bytes   switch plans: AllReduce (m one-hop trees) and the one-hop
+ *                  Broadcast star up to this many bytes per rank run the
+ *                  low-latency protocol (readiness flags inside the data
+ *                  lines, no handshake; NEXT-2); 0 = off.
+ *                  Default 256 KiB (64 KiB when one launch holds every rank,
+ *                  which has no handshake to save).
+ *                  Costs 64 * m * (ll_max_bytes / (8 m) + 8) bytes of device
+ *                  memory per rank.  Must agree across ranks */
 typedef struct {
   double mwu_eps;
   double ilp_gap;
@@ -111,6 +129,8 @@ typedef struct {
   size_t onehop_bcast_max_bytes;
   size_t staging_bytes;
   int autotune;
+  int launch_per_rank;
+  size_t ll_max_bytes;
 } blink_config_t;
 
 /* MIAD controller: "initialize the chunk size with a small value

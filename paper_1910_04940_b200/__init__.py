@@ -47,7 +47,8 @@ class _Config(ctypes.Structure):
     _fields_ = [("mwu_eps", ctypes.c_double), ("ilp_gap", ctypes.c_double),
                 ("chunk_bytes", ctypes.c_size_t), ("ctas", ctypes.c_int), ("threads", ctypes.c_int),
                 ("timeout_s", ctypes.c_double), ("onehop_bcast_max_bytes", ctypes.c_size_t),
-                ("staging_bytes", ctypes.c_size_t), ("autotune", ctypes.c_int)]
+                ("staging_bytes", ctypes.c_size_t), ("autotune", ctypes.c_int),
+                ("launch_per_rank", ctypes.c_int), ("ll_max_bytes", ctypes.c_size_t)]
 
 
 class Miad(ctypes.Structure):

@@ -143,7 +143,48 @@ struct LaunchArgs {
   uint64_t* flags[kMaxArgRanks];
 };
 
+// Low-latency (LL) protocol for small calls on switch plans (NEXT-2's
+// small-message protocol).  The same one-hop trees, but
+// readiness travels inside the data: every 16-byte line is {d0, flag, d1,
+// flag} written with one 128-bit store (each {data, flag} 8-byte half is
+// single-copy atomic), the flag being the call's epoch.  A leaf pushes its
+// slice j into root j's LL area, root j polls its own memory, reduces in
+// ascending-rank order and pushes the result lines into every leaf's LL area;
+// a leaf polls and copies out.  No rank touches a peer's user buffers, so
+// there is no entry handshake and no exit wait; areas alternate by epoch
+// parity (a rank cannot reach call e+2 before every peer finished reading call
+// e).  Per rank, after the flag words:
+//   IN [p][src][cap]   lines from leaf src for this rank's slice (parity p)
+//   OUT[p][j][cap]     result lines of root j's slice (Broadcast: one
+//                      contiguous run of the whole buffer from OUT[p][0])
+constexpr int kLLThreads = 256;
+inline size_t ll_cap_lines(size_t ll_max_bytes, int m) {
+  return ll_max_bytes / (8 * size_t(m)) + 8;
+}
+inline size_t ll_area_bytes(size_t ll_max_bytes, int m) {
+  return ll_max_bytes ? 4 * size_t(m) * ll_cap_lines(ll_max_bytes, m) * 16 : 0;
+}
+struct LLArgs {
+  int nranks, coll, dtype, op;
+  int root;                    // Broadcast root
+  int nlocal;                  // ranks run by this launch: ranks[0 .. nlocal)
+  int ctas_per_rank;
+  int pad;
+  int8_t ranks[kMaxRanks];
+  int64_t bytes;               // S per rank
+  int64_t cap;                 // lines per slice area (ll_cap_lines)
+  int64_t lo[kMaxRanks + 1];   // AllReduce: slice j = bytes [lo[j], lo[j+1]) (tree rooted at j)
+  uint64_t* ctrl;              // launch epoch words (shared with the tree executor)
+  int* err;
+  uint64_t timeout_ns;
+  uint64_t* trace;
+  const char* send[kMaxRanks];
+  char* recv[kMaxRanks];
+  uint4* ll[kMaxRanks];        // rank u's LL area (peer-mapped)
+};
+
 // exec.cu
+cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative);
 cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,
                         bool cooperative);
 constexpr int kMaxSmemBytes = 224 * 1024;  // + static smem <= 227 KB opt-in

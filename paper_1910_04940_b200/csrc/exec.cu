@@ -893,6 +893,282 @@ __global__ void copy_kernel(char* dst, const char* src, int64_t bytes) {
   for (int64_t j = vb + tid; j < bytes; j += T) dst[j] = src[j];
 }
 
+// ------------------------------------------------------------------ LL protocol
+// Small calls on switch plans (blink_internal.h "LL protocol").  Lines are
+// two u64 words {data32 | flag << 32}: each word is single-copy atomic, so a
+// word whose flag equals the call's epoch carries that call's data.
+__device__ __forceinline__ void ll_store(uint4* p, uint2 d, uint32_t f) {
+  const uint64_t w0 = uint64_t(d.x) | (uint64_t(f) << 32), w1 = uint64_t(d.y) | (uint64_t(f) << 32);
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+// 8 payload bytes of a user buffer; `valid` (a multiple of the element size)
+// bytes are read, the rest is zero.  Buffers are element-aligned.
+__device__ __forceinline__ uint2 ld8(const char* p, int valid) {
+  if (valid == 8 && (reinterpret_cast<uintptr_t>(p) & 7) == 0) return __ldcg(reinterpret_cast<const uint2*>(p));
+  uint2 r = make_uint2(0u, 0u);
+  unsigned short* h = reinterpret_cast<unsigned short*>(&r);
+  for (int b = 0; b < valid; b += 2) h[b >> 1] = __ldcg(reinterpret_cast<const unsigned short*>(p + b));
+  return r;
+}
+__device__ __forceinline__ void st8(char* p, uint2 v, int valid) {
+  if (valid == 8 && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+    *reinterpret_cast<uint2*>(p) = v;
+    return;
+  }
+  const unsigned short* h = reinterpret_cast<const unsigned short*>(&v);
+  for (int b = 0; b < valid; b += 2) *reinterpret_cast<unsigned short*>(p + b) = h[b >> 1];
+}
+// Combine of 8-byte payloads with the executor's arithmetic (R#12, R#13):
+// fp32 accumulation, RNE, no FMA; bf16 widened exactly and rounded once.
+template <int DT, int OP>
+struct Acc8 {
+  static constexpr int N = DT == BLINK_BFLOAT16 ? 4 : 2;
+  float f[N];
+  int i[N];
+  __device__ __forceinline__ void unpack(uint2 x, float* g, int* j) const {
+    if constexpr (DT == BLINK_BFLOAT16) {
+      g[0] = bf_lo(x.x); g[1] = bf_hi(x.x); g[2] = bf_lo(x.y); g[3] = bf_hi(x.y);
+    } else if constexpr (DT == BLINK_FLOAT32) {
+      g[0] = __uint_as_float(x.x); g[1] = __uint_as_float(x.y);
+    } else {
+      j[0] = int(x.x); j[1] = int(x.y);
+    }
+  }
+  __device__ __forceinline__ void init(uint2 x) { unpack(x, f, i); }
+  __device__ __forceinline__ void add(uint2 x) {
+    float g[N];
+    int j[N];
+    unpack(x, g, j);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if constexpr (DT == BLINK_INT32)
+        i[k] = iop<OP>(i[k], j[k]);
+      else
+        f[k] = fop<OP>(f[k], g[k]);
+    }
+  }
+  __device__ __forceinline__ uint2 out() const {
+    if constexpr (DT == BLINK_BFLOAT16)
+      return make_uint2(f2bf(f[0]) | (f2bf(f[1]) << 16), f2bf(f[2]) | (f2bf(f[3]) << 16));
+    else if constexpr (DT == BLINK_FLOAT32)
+      return make_uint2(__float_as_uint(f[0]), __float_as_uint(f[1]));
+    else
+      return make_uint2(unsigned(i[0]), unsigned(i[1]));
+  }
+};
+
+__device__ __forceinline__ void ll_trace(const LLArgs& a, int slot) {
+  if (a.trace) a.trace[size_t(blockIdx.x) * kTraceSlots + slot] = globaltimer();
+}
+
+// Batched poll: the lines ptr(u) of every u < U with bit u of `act` set are
+// loaded back to back, then only the ones whose flags are not yet `f` are
+// reloaded, so a thread's round trips overlap.  d[u] gets line u's payload.
+// (Unrolled with compile-time indices: no local-memory arrays.)  False on
+// timeout / abort.
+template <int U, class P>
+__device__ __forceinline__ bool ll_poll_n(P ptr, uint32_t act, uint32_t f, uint2* d, const LLArgs& a) {
+  uint64_t w0[U], w1[U];
+  bool done[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    done[u] = !((act >> u) & 1u);
+    if (!done[u])
+      asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0[u]), "=l"(w1[u]) : "l"(ptr(u)) : "memory");
+  }
+  uint64_t t0 = 0;
+  for (int spin = 0;; ++spin) {
+    bool all = true;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (done[u]) continue;
+      if (uint32_t(w0[u] >> 32) == f && uint32_t(w1[u] >> 32) == f) {
+        d[u] = make_uint2(uint32_t(w0[u]), uint32_t(w1[u]));
+        done[u] = true;
+      } else {
+        all = false;
+      }
+    }
+    if (all) return true;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (!done[u])
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0[u]), "=l"(w1[u]) : "l"(ptr(u)) : "memory");
+    if ((spin & 255) == 255) {
+      if (ld_volatile_int(a.err) != 0) return false;
+      const uint64_t now = globaltimer();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > a.timeout_ns) {
+        *reinterpret_cast<volatile int*>(a.err) = int(BLINK_ERR_TIMEOUT);
+        return false;
+      }
+    }
+  }
+}
+
+// One launch runs ranks a.ranks[0 .. nlocal), a.ctas_per_rank CTAs each.
+// AllReduce on m one-hop trees (tree j rooted at j owns slice j):
+//   P1 (leaf)  push my send slice j into root j's IN[p][me], every j != me;
+//   P2 (root)  for my slice: poll IN[p][u] of every leaf u, combine with my
+//              send in ascending rank order, write my recv and push the
+//              result into OUT[p][me] of every leaf;
+//   P3 (leaf)  poll my OUT[p][j] for every j != me and write my recv.
+// Broadcast (one-hop star): the root pushes its send into every other rank's
+// OUT[p] run; the others poll and copy out.  Every thread runs its P1 share
+// before any wait, so progress needs only that every CTA eventually runs.
+// Work items are (slice, line) pairs spread over all threads of the rank, and
+// each thread issues the loads of up to kLLU items (or, in P2, of all m
+// operands of a line) before waiting on any of them: a phase costs about one
+// round trip, not one per peer.
+constexpr int kLLU = 4;
+template <int DT, int OP>
+__global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
+  const int v = a.ranks[blockIdx.x / a.ctas_per_rank];
+  const int cta = blockIdx.x % a.ctas_per_rank;
+  if (threadIdx.x == 0) ll_trace(a, 0);
+  const int m = a.nranks;
+  const int64_t T = int64_t(a.ctas_per_rank) * blockDim.x;
+  const int64_t t0 = int64_t(cta) * blockDim.x + threadIdx.x;
+  const size_t cap = size_t(a.cap);
+  // every thread reads the epoch (one broadcast load; no block barrier); the
+  // CTA's finish counter is bumped only after __syncthreads below
+  const uint64_t e = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
+  const uint32_t f = uint32_t(e);
+  const size_t p = size_t(e & 1u);
+  uint4* const my = a.ll[v];
+  auto in_area = [&](uint4* base, int src) { return base + (p * m + src) * cap; };
+  auto out_area = [&](uint4* base, int j) { return base + ((2 + p) * m + j) * cap; };
+  bool ok = true;
+  if (a.coll == kAllReduce) {
+    int64_t lmax = 0;
+    for (int j = 0; j < m; ++j) lmax = max(lmax, a.lo[j + 1] - a.lo[j]);
+    const int64_t nlmax = (lmax + 7) >> 3;
+    const int64_t tot = int64_t(m - 1) * nlmax;  // (slice j != v, line k) items
+    auto item = [&](int64_t i, int& j, int64_t& k, int& valid) {
+      const int jj = int(i / nlmax);
+      k = i - int64_t(jj) * nlmax;
+      j = jj + (jj >= v ? 1 : 0);
+      const int64_t len = a.lo[j + 1] - a.lo[j];
+      valid = int(min(int64_t(8), len - 8 * k));
+      return i < tot && 8 * k < len;
+    };
+    // P1
+    for (int64_t i0 = t0; i0 < tot; i0 += kLLU * T) {
+      uint2 x[kLLU];
+      int jv[kLLU];
+      int64_t kv[kLLU];
+      bool act[kLLU];
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u) {
+        int valid;
+        act[u] = item(i0 + u * T, jv[u], kv[u], valid);
+        if (act[u]) x[u] = ld8(a.send[v] + a.lo[jv[u]] + 8 * kv[u], valid);
+      }
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u)
+        if (act[u]) ll_store(in_area(a.ll[jv[u]], v) + kv[u], x[u], f);
+    }
+    if (threadIdx.x == 0) ll_trace(a, 2);
+    {  // P2
+      const int64_t lo = a.lo[v], len = a.lo[v + 1] - lo, nl = (len + 7) >> 3;
+      const uint32_t leaves = ((m >= 32 ? 0u : (1u << m)) - 1u) & ~(1u << v);
+      for (int64_t k = t0; k < nl; k += T) {
+        const int valid = int(min(int64_t(8), len - 8 * k));
+        const uint2 own = ld8(a.send[v] + lo + 8 * k, valid);
+        uint2 d[kMaxRanks];
+        if (!ll_poll_n<kMaxRanks>([&](int u) { return in_area(my, u) + k; }, leaves, f, d, a)) {
+          ok = false;
+          break;
+        }
+        Acc8<DT, OP> acc;
+#pragma unroll
+        for (int u = 0; u < kMaxRanks; ++u) {
+          if (u >= m) break;
+          const uint2 x = u == v ? own : d[u];
+          if (u == 0)
+            acc.init(x);
+          else
+            acc.add(x);
+        }
+        const uint2 r = acc.out();
+        st8(a.recv[v] + lo + 8 * k, r, valid);
+        for (int u = 0; u < m; ++u)
+          if (u != v) ll_store(out_area(a.ll[u], v) + k, r, f);
+      }
+    }
+    if (threadIdx.x == 0) ll_trace(a, 3);
+    // P3
+    for (int64_t i0 = t0; i0 < tot && ok; i0 += kLLU * T) {
+      const uint4* ps[kLLU];
+      char* dst[kLLU];
+      int val[kLLU];
+      uint2 d[kLLU];
+      uint32_t act = 0;
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u) {
+        int j, valid;
+        int64_t k;
+        ps[u] = nullptr;
+        dst[u] = nullptr;
+        val[u] = 0;
+        if (item(i0 + u * T, j, k, valid)) {
+          ps[u] = out_area(my, j) + k;
+          dst[u] = a.recv[v] + a.lo[j] + 8 * k;
+          val[u] = valid;
+          act |= 1u << u;
+        }
+      }
+      if (!ll_poll_n<kLLU>([&](int u) { return ps[u]; }, act, f, d, a)) {
+        ok = false;
+        break;
+      }
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u)
+        if ((act >> u) & 1u) st8(dst[u], d[u], val[u]);
+    }
+  } else {  // Broadcast, one-hop star
+    const int r = a.root;
+    const int64_t len = a.bytes, nl = (len + 7) >> 3;
+    if (v == r) {
+      for (int64_t k = t0; k < nl; k += T) {
+        const int valid = int(min(int64_t(8), len - 8 * k));
+        const uint2 x = ld8(a.send[r] + 8 * k, valid);
+        if (a.recv[r] != a.send[r]) st8(a.recv[r] + 8 * k, x, valid);
+        for (int u = 0; u < m; ++u)
+          if (u != r) ll_store(out_area(a.ll[u], 0) + k, x, f);
+      }
+    } else {
+      const uint4* src = out_area(my, 0);
+      for (int64_t k0 = t0; k0 < nl; k0 += kLLU * T) {
+        uint2 d[kLLU];
+        uint32_t act = 0;
+#pragma unroll
+        for (int u = 0; u < kLLU; ++u)
+          if (k0 + u * T < nl) act |= 1u << u;
+        if (!ll_poll_n<kLLU>([&](int u) { return src + k0 + u * T; }, act, f, d, a)) break;
+#pragma unroll
+        for (int u = 0; u < kLLU; ++u)
+          if ((act >> u) & 1u) {
+            const int64_t k = k0 + u * T;
+            st8(a.recv[v] + 8 * k, d[u], int(min(int64_t(8), len - 8 * k)));
+          }
+      }
+    }
+  }
+  // the last CTA to finish advances the device epoch for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ll_trace(a, 6);
+    const unsigned long long prev = atomicAdd(reinterpret_cast<unsigned long long*>(a.ctrl + 1), 1ull);
+    if (prev + 1 == gridDim.x) {
+      a.ctrl[1] = 0;
+      atomicExch(reinterpret_cast<unsigned long long*>(a.ctrl), (unsigned long long)e);
+    }
+    ll_trace(a, 7);
+  }
+}
+
 typedef void (*ExecFn)(const LaunchArgs);
 
 template <int DT, bool VEC>
@@ -935,6 +1211,42 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
     if (e != cudaSuccess) return e;
     done = true;
   }
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = cooperative ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+typedef void (*LLFn)(const LLArgs);
+template <int DT>
+LLFn ll_pick_op(int op) {
+  switch (op) {
+    case BLINK_SUM: return ll_kernel<DT, BLINK_SUM>;
+    case BLINK_PROD: return ll_kernel<DT, BLINK_PROD>;
+    case BLINK_MIN: return ll_kernel<DT, BLINK_MIN>;
+    case BLINK_MAX: return ll_kernel<DT, BLINK_MAX>;
+  }
+  return nullptr;
+}
+
+cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative) {
+  LLFn fn = nullptr;
+  if (a.coll == kBroadcast) {
+    fn = ll_kernel<BLINK_FLOAT32, BLINK_SUM>;  // a byte copy
+  } else {
+    switch (a.dtype) {
+      case BLINK_FLOAT32: fn = ll_pick_op<BLINK_FLOAT32>(a.op); break;
+      case BLINK_BFLOAT16: fn = ll_pick_op<BLINK_BFLOAT16>(a.op); break;
+      case BLINK_INT32: fn = ll_pick_op<BLINK_INT32>(a.op); break;
+    }
+  }
+  if (!fn) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kLLThreads);
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;

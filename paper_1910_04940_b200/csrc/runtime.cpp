@@ -100,8 +100,10 @@ struct blink_comm {
   bool connected = false;
   Clique* clique = nullptr;
   uint64_t calls = 0;  // multi-process: collectives launched (epochs live on the device)
-  uint64_t* flags = nullptr;
+  uint64_t* flags = nullptr;  // kFlagBytes of flag words, then ll_bytes of LL areas
   uint64_t* peer_flags[kMaxRanks] = {};
+  size_t ll_bytes = 0;
+  std::map<std::pair<size_t, int>, std::vector<int64_t>> ll_lo;  // LL slices per (count, esize)
   int* err_host = nullptr;  // multi-process error word
   int* err_dev = nullptr;
   uint64_t* ctrl = nullptr;  // multi-process: device launch epoch + done counter
@@ -124,6 +126,17 @@ struct Clique {
   int nranks = 0;
   std::vector<blink_comm*> comms;
   std::vector<int> devices;  // distinct devices
+  // launch groups: the ranks one launch runs.  One group per device (ranks
+  // sharing a device are batched), or one per rank with cfg.launch_per_rank.
+  // Error words, control words and traces are keyed by the group key.
+  struct Group {
+    int key, device;
+    uint64_t mask;
+  };
+  std::vector<Group> groups;
+  bool per_rank = false;
+  std::vector<cudaStream_t> rstream;  // per_rank: rank v's library-owned launch stream
+  std::vector<cudaEvent_t> rfork, rjoin;
   int alive = 0;
   uint64_t calls = 0;  // batches launched (epochs live on the device)
   // the batch being assembled
@@ -131,10 +144,10 @@ struct Clique {
   int coll = -1, root = -1, dtype = -1, op = -1;
   size_t count = 0;
   std::vector<Pending> pending;
-  // per device state
+  // per launch group state
   std::map<int, int*> err_host, err_dev;
-  std::map<int, uint64_t*> ctrl;  // per device: launch epoch + done counter
-  std::map<int, uint64_t*> trace; // per device: BLINK_TRACE stamps of the last launch
+  std::map<int, uint64_t*> ctrl;  // per group: launch epoch + done counter
+  std::map<int, uint64_t*> trace; // per group: BLINK_TRACE stamps of the last launch
   std::map<int, int> trace_ctas;
   struct MiadRun {
     blink_miad_t st;
@@ -175,6 +188,10 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
   if (const char* e = getenv("BLINK_CTAS")) r.ctas = atoi(e);
   if (const char* e = getenv("BLINK_CHUNK_BYTES")) r.chunk_bytes = size_t(atoll(e));
   if (const char* e = getenv("BLINK_MIAD")) r.autotune = atoi(e);
+  if (const char* e = getenv("BLINK_PER_RANK")) r.launch_per_rank = atoi(e);
+  if (const char* e = getenv("BLINK_LL_MAX")) r.ll_max_bytes = size_t(atoll(e));
+  if (r.ll_max_bytes > (size_t(16) << 20)) r.ll_max_bytes = size_t(16) << 20;
+  r.ll_max_bytes = r.ll_max_bytes / kGrain * kGrain;
   if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
   if (!(r.ilp_gap > 0 && r.ilp_gap < 1)) r.ilp_gap = d.ilp_gap;
   if (r.threads <= 0) r.threads = d.threads;
@@ -644,6 +661,67 @@ blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtyp
   return BLINK_SUCCESS;
 }
 
+// ---------------------------------------------------------------- LL protocol
+constexpr size_t kLLOneLaunchMax = 64 << 10;
+
+// Does this call take the low-latency protocol, and where are the one-hop
+// slices?  The decision depends only on the call and the config, so every rank
+// takes it alike.  AllReduce: the plan's m one-hop trees (tree j rooted at j,
+// slice j = its split range, R#11).  Broadcast: the one-hop star.
+bool ll_slices(blink_comm_t c, const Plan& plan, int coll, size_t count, int es,
+               int64_t lo[kMaxRanks + 1]) {
+  const int m = c->nranks;
+  const size_t bytes = count * size_t(es);
+  if (c->ll_bytes == 0 || m < 2 || bytes == 0 || bytes > c->cfg.ll_max_bytes || !plan.switch_model)
+    return false;
+  if (coll == kBroadcast) {
+    lo[0] = 0;
+    return plan.trees.size() == 1;
+  }
+  if (coll != kAllReduce || int(plan.trees.size()) != m) return false;
+  auto key = std::make_pair(count, es);
+  auto it = c->ll_lo.find(key);
+  if (it == c->ll_lo.end()) {
+    std::vector<TreeRange> rr;
+    std::string err;
+    if (size_plan(plan, count, es, c->cfg, 1, &rr, &err) != BLINK_SUCCESS || int(rr.size()) != m)
+      return false;
+    std::vector<int64_t> b(m + 1);
+    for (int j = 0; j < m; ++j) {
+      if (plan.trees[j].root != j || plan.trees[j].depth != 1) return false;
+      if (j > 0 && rr[j].lo != rr[j - 1].hi) return false;
+      b[j] = rr[j].lo * es;
+    }
+    b[m] = rr[m - 1].hi * es;
+    if (b[0] != 0 || b[m] != int64_t(bytes)) return false;
+    it = c->ll_lo.emplace(key, b).first;
+  }
+  for (int j = 0; j <= m; ++j) lo[j] = it->second[j];
+  return true;
+}
+
+// Everything but the per-rank buffers.  `share` = ranks whose launches share
+// this device (their CTAs split the SMs).
+void fill_ll_args(blink_comm_t c, int coll, int dtype, int op, int root, size_t bytes,
+                  const int64_t lo[kMaxRanks + 1], uint64_t* ctrl, int* err, int share, LLArgs* a) {
+  const int m = c->nranks;
+  a->nranks = m;
+  a->coll = coll;
+  a->dtype = dtype;
+  a->op = op;
+  a->root = root;
+  a->bytes = int64_t(bytes);
+  a->cap = int64_t(ll_cap_lines(c->cfg.ll_max_bytes, m));
+  for (int j = 0; j <= m; ++j) a->lo[j] = lo[j];
+  const int64_t lines = (int64_t(bytes) + 7) / 8;
+  const int want = int((lines + kLLThreads - 1) / kLLThreads);
+  const int cap = std::max(1, c->sms / std::max(1, share));
+  a->ctas_per_rank = std::max(1, std::min(want, cap));
+  a->ctrl = ctrl;
+  a->err = err;
+  a->timeout_ns = uint64_t(c->cfg.timeout_s * 1e9);
+}
+
 // ---------------------------------------------------------------- single-process launch
 blink_result_t clique_launch(Clique* q) {
   const int n = q->nranks;
@@ -670,12 +748,17 @@ blink_result_t clique_launch(Clique* q) {
     if (!aligned16(p.recv)) vec = false;
   }
   if (is_block_coll(q->coll) && (bytes % kGrain) != 0) vec = false;  // block starts unaligned
-  const bool all_one_launch = q->devices.size() == 1;
+  const bool all_one_launch = q->groups.size() == 1;
   // MIAD: the chunk size for this call from the previous calls'
   // measured throughput (single host thread decides for every rank)
   Clique::MiadRun* mr = nullptr;
   size_t chunk_override = 0;
-  if (c0->cfg.autotune) {
+  // one launch holding every rank has no handshake for LL to save; there it
+  // pays only below kLLOneLaunchMax (A/B: scripts/per_rank_trace.py)
+  int64_t ll_lo[kMaxRanks + 1];
+  const bool ll = (q->groups.size() > 1 || bytes <= kLLOneLaunchMax) &&
+                  ll_slices(c0, *plan, q->coll, q->count, es, ll_lo);
+  if (c0->cfg.autotune && !ll) {
     auto mk = std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count);
     auto mit = q->miad.find(mk);
     if (mit == q->miad.end()) {
@@ -702,10 +785,88 @@ blink_result_t clique_launch(Clique* q) {
     mr->calls++;
   }
   bool timed = false;
-  for (int dev : q->devices) {
-    uint64_t mask = 0;
-    for (int v = 0; v < n; ++v)
-      if (q->comms[v]->device == dev) mask |= uint64_t(1) << v;
+  // per-rank launches: fork every rank's launch stream off its stream before
+  // any launch and join after all of them, so that ranks sharing one user
+  // stream still run concurrently
+  if (q->per_rank)
+    for (int v = 0; v < n; ++v) {
+      DeviceGuard g(q->comms[v]->device);
+      CUDA_TRY(c0, cudaEventRecord(q->rfork[v], q->pending[v].stream));
+      CUDA_TRY(c0, cudaStreamWaitEvent(q->rstream[v], q->rfork[v], 0));
+    }
+  if (ll) {  // low-latency protocol: one LL launch per group
+    for (const Clique::Group& grp : q->groups) {
+      LLArgs a{};
+      int lead = -1;
+      for (int v = 0; v < n; ++v)
+        if ((grp.mask >> v) & 1) {
+          if (lead < 0) lead = v;
+          a.ranks[a.nlocal++] = int8_t(v);
+        }
+      blink_comm_t cd = q->comms[lead];
+      DeviceGuard g(grp.device);
+      int share = 0;
+      for (const Clique::Group& g2 : q->groups)
+        if (g2.device == grp.device) share += __builtin_popcountll(g2.mask);
+      fill_ll_args(cd, q->coll, q->dtype, q->op, q->root, bytes, ll_lo, q->ctrl[grp.key],
+                   q->err_dev[grp.key], share, &a);
+      for (int v = 0; v < n; ++v) {
+        a.send[v] = static_cast<const char*>(q->pending[v].send);
+        a.recv[v] = static_cast<char*>(q->pending[v].recv);
+        a.ll[v] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(q->comms[v]->flags) + kFlagBytes);
+      }
+      if (getenv("BLINK_TRACE")) {
+        uint64_t*& tb = q->trace[grp.key];
+        if (!tb) CUDA_TRY(cd, cudaMalloc(&tb, sizeof(uint64_t) * kTraceSlots * 4096));
+        a.trace = tb;
+        q->trace_ctas[grp.key] = a.nlocal * a.ctas_per_rank;
+      }
+      cudaStream_t ls = q->per_rank ? q->rstream[lead] : q->pending[lead].stream;
+      std::vector<cudaEvent_t> evs;
+      for (int v = 0; v < n; ++v) {
+        if (!((grp.mask >> v) & 1) || v == lead || q->pending[v].stream == ls) continue;
+        cudaEvent_t e;
+        CUDA_TRY(cd, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cd, cudaEventRecord(e, q->pending[v].stream));
+        CUDA_TRY(cd, cudaStreamWaitEvent(ls, e, 0));
+        evs.push_back(e);
+      }
+      const int grid = a.nlocal * a.ctas_per_rank;
+      cudaError_t le = launch_ll(a, grid, ls, use_coop() && !q->per_rank);
+      if (le != cudaSuccess)
+        return fail(cd, BLINK_ERR_CUDA, std::string("LL launch: ") + cudaGetErrorString(le));
+      if (q->per_rank) CUDA_TRY(cd, cudaEventRecord(q->rjoin[lead], ls));
+      q->launches++;
+      for (int v = 0; v < n; ++v) {
+        if (!((grp.mask >> v) & 1)) continue;
+        q->comms[v]->stats.launches++;
+        q->comms[v]->stats.last_ctas = grid;
+        q->comms[v]->stats.last_chunks = 0;
+        q->comms[v]->stats.last_trees = int(plan->trees.size());
+        q->comms[v]->stats.last_chunk_bytes = 0;
+      }
+      if (!evs.empty()) {
+        cudaEvent_t done;
+        CUDA_TRY(cd, cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        CUDA_TRY(cd, cudaEventRecord(done, ls));
+        for (int v = 0; v < n; ++v) {
+          if (!((grp.mask >> v) & 1) || v == lead || q->pending[v].stream == ls) continue;
+          CUDA_TRY(cd, cudaStreamWaitEvent(q->pending[v].stream, done, 0));
+        }
+        cudaEventDestroy(done);
+        for (auto e : evs) cudaEventDestroy(e);
+      }
+    }
+    if (q->per_rank)
+      for (int v = 0; v < n; ++v) {
+        DeviceGuard g(q->comms[v]->device);
+        CUDA_TRY(c0, cudaStreamWaitEvent(q->pending[v].stream, q->rjoin[v], 0));
+      }
+    return BLINK_SUCCESS;
+  }
+  for (const Clique::Group& grp : q->groups) {
+    const int dev = grp.device;
+    const uint64_t mask = grp.mask;
     blink_comm_t cd = nullptr;
     for (int v = 0; v < n && !cd; ++v)
       if ((mask >> v) & 1) cd = q->comms[v];
@@ -717,6 +878,10 @@ blink_result_t clique_launch(Clique* q) {
     if (it == q->sized.end()) {
       Sized s;
       int budget = co_resident_budget(cd, dev, q->dtype, q->op, q->coll);
+      // launch groups sharing a device run concurrently: split its CTAs
+      int share = 0;
+      for (const Clique::Group& g2 : q->groups) share += g2.device == dev;
+      budget = std::max(1, budget / std::max(1, share));
       r = build_sized(cd, *plan, q->count, es, mask, budget, &s, chunk_override);
       if (r != BLINK_SUCCESS) return r;
       r = finalize_tables(cd, dev, es, &s);
@@ -733,7 +898,7 @@ blink_result_t clique_launch(Clique* q) {
     a.dtype = q->dtype;
     a.op = q->op;
     a.exit_wait = all_one_launch ? 0 : 1;
-    a.scope_sys = all_one_launch ? 0 : 1;
+    a.scope_sys = q->devices.size() > 1 ? 1 : 0;
     a.bcast_root = (q->coll == kBroadcast || q->coll == kGather) ? q->root : -1;
     a.use_tma = use_tma();
     a.smem_bytes = smem_bytes();
@@ -741,15 +906,15 @@ blink_result_t clique_launch(Clique* q) {
     a.store_depth = store_depth();
     a.l2_hint = l2_hint();
     a.nctr = s.nctr;
-    a.ctrl = q->ctrl[dev];
+    a.ctrl = q->ctrl[grp.key];
     if (getenv("BLINK_TRACE")) {
-      uint64_t*& tb = q->trace[dev];
+      uint64_t*& tb = q->trace[grp.key];
       if (!tb) CUDA_TRY(cd, cudaMalloc(&tb, sizeof(uint64_t) * kTraceSlots * 4096));
       a.trace = tb;
-      q->trace_ctas[dev] = s.ctas;
+      q->trace_ctas[grp.key] = s.ctas;
     }
     a.timeout_ns = uint64_t(cd->cfg.timeout_s * 1e9);
-    a.err = q->err_dev[dev];
+    a.err = q->err_dev[grp.key];
     for (int v = 0; v < n; ++v) {
       a.send[v] = const_cast<char*>(static_cast<const char*>(q->pending[v].send));
       a.recv[v] = static_cast<char*>(q->pending[v].recv);
@@ -767,6 +932,7 @@ blink_result_t clique_launch(Clique* q) {
         break;
       }
     cudaStream_t ls = q->pending[lead].stream;
+    if (q->per_rank) ls = q->rstream[lead];  // forked off the rank's stream above
     std::vector<cudaEvent_t> evs;
     for (int v = 0; v < n; ++v) {
       if (!((mask >> v) & 1) || v == lead || q->pending[v].stream == ls) continue;
@@ -784,9 +950,13 @@ blink_result_t clique_launch(Clique* q) {
       }
       CUDA_TRY(cd, cudaEventRecord(mr->ev0, ls));
     }
-    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, use_coop());
+    // per-rank launches rely on every group's grid fitting the device at once
+    // (each takes 1/m of the co-resident CTAs); the cooperative attribute
+    // cannot promise co-residency across launches
+    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, use_coop() && !q->per_rank);
     if (le != cudaSuccess)
       return fail(cd, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
+    if (q->per_rank) CUDA_TRY(cd, cudaEventRecord(q->rjoin[lead], ls));
     if (time_it) {
       CUDA_TRY(cd, cudaEventRecord(mr->ev1, ls));
       mr->pending = true;
@@ -813,6 +983,11 @@ blink_result_t clique_launch(Clique* q) {
       for (auto e : evs) cudaEventDestroy(e);
     }
   }
+  if (q->per_rank)
+    for (int v = 0; v < n; ++v) {
+      DeviceGuard g(q->comms[v]->device);
+      CUDA_TRY(c0, cudaStreamWaitEvent(q->pending[v].stream, q->rjoin[v], 0));
+    }
   return BLINK_SUCCESS;
 }
 
@@ -823,7 +998,7 @@ blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* 
   for (auto& kv : q->err_host)
     if (*kv.second != 0) {
       return fail(comm, blink_result_t(*kv.second),
-                  "a previous launch aborted (flag wait timed out on device " +
+                  "a previous launch aborted (flag wait timed out in launch group " +
                       std::to_string(kv.first) + ")");
     }
   if (q->nposted == 0) {
@@ -865,6 +1040,7 @@ struct Blob {
   cudaIpcMemHandle_t flags_h;
   cudaIpcMemHandle_t staging_h;
   uint64_t staging_bytes;
+  uint64_t ll_bytes;
 };
 struct RegBlob {
   char magic[8];
@@ -1032,6 +1208,31 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
   }
   if (is_block_coll(coll))
     return mp_block_collective(comm, coll, sendbuf, recvbuf, count, dtype, op, root, stream);
+  {  // low-latency protocol: user buffers are only touched by their own rank
+    const Plan* plan = nullptr;
+    blink_result_t r = get_plan(comm, coll, root, bytes, &plan);
+    if (r != BLINK_SUCCESS) return r;
+    int64_t lo[kMaxRanks + 1];
+    if (ll_slices(comm, *plan, coll, count, es, lo)) {
+      comm->calls++;
+      LLArgs a{};
+      a.ranks[a.nlocal++] = int8_t(comm->rank);
+      fill_ll_args(comm, coll, dtype, op, root, bytes, lo, comm->ctrl, comm->err_dev, 1, &a);
+      a.send[comm->rank] = static_cast<const char*>(sendbuf);
+      a.recv[comm->rank] = static_cast<char*>(recvbuf);
+      for (int u = 0; u < comm->nranks; ++u)
+        a.ll[u] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(comm->peer_flags[u]) + kFlagBytes);
+      cudaError_t le = launch_ll(a, a.ctas_per_rank, stream, false);
+      if (le != cudaSuccess)
+        return fail(comm, BLINK_ERR_CUDA, std::string("LL launch: ") + cudaGetErrorString(le));
+      comm->stats.launches++;
+      comm->stats.last_ctas = a.ctas_per_rank;
+      comm->stats.last_chunks = 0;
+      comm->stats.last_trees = int(plan->trees.size());
+      comm->stats.last_chunk_bytes = 0;
+      return BLINK_SUCCESS;
+    }
+  }
   char* sp[kMaxRanks] = {};
   char* rp[kMaxRanks] = {};
   const bool recv_ok = resolve(comm, recvbuf, bytes, rp);
@@ -1076,6 +1277,8 @@ void blink_config_default(blink_config_t* c) {
   c->onehop_bcast_max_bytes = 256 << 10;
   c->staging_bytes = 64 << 20;
   c->autotune = 0;
+  c->launch_per_rank = 0;
+  c->ll_max_bytes = 256 << 10;
 }
 
 void blink_miad_init(blink_miad_t* st, size_t init, size_t min_chunk, size_t max_chunk) {
@@ -1176,8 +1379,11 @@ blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const bli
 static blink_result_t alloc_comm_common(blink_comm_t c) {
   DeviceGuard g(c->device);
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
-  CUDA_TRY(c, cudaMalloc(&c->flags, kFlagBytes));
-  CUDA_TRY(c, cudaMemset(c->flags, 0, kFlagBytes));
+  // flag words, then the LL protocol's line areas (zero = no flag yet); one
+  // allocation, so the flag mapping also maps the LL area to the peers
+  c->ll_bytes = c->nranks > 1 ? ll_area_bytes(c->cfg.ll_max_bytes, c->nranks) : 0;
+  CUDA_TRY(c, cudaMalloc(&c->flags, kFlagBytes + c->ll_bytes));
+  CUDA_TRY(c, cudaMemset(c->flags, 0, kFlagBytes + c->ll_bytes));
   CUDA_TRY(c, cudaDeviceSynchronize());
   return BLINK_SUCCESS;
 }
@@ -1241,7 +1447,32 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
     q->comms.push_back(c);
     comms[i] = c;
   }
+  q->per_rank = cfg.launch_per_rank != 0 && ndev > 1;
   for (int d : distinct) {
+    uint64_t mask = 0;
+    for (int v = 0; v < ndev; ++v)
+      if (devs[v] == d) mask |= uint64_t(1) << v;
+    if (!q->per_rank) {
+      q->groups.push_back({d, d, mask});
+      continue;
+    }
+    for (int v = 0; v < ndev; ++v)
+      if ((mask >> v) & 1) q->groups.push_back({v, d, uint64_t(1) << v});
+  }
+  if (q->per_rank) {
+    q->rstream.resize(ndev);
+    q->rfork.resize(ndev);
+    q->rjoin.resize(ndev);
+    for (int v = 0; v < ndev; ++v) {
+      DeviceGuard g(devs[v]);
+      if (cudaStreamCreateWithFlags(&q->rstream[v], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&q->rfork[v], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&q->rjoin[v], cudaEventDisableTiming) != cudaSuccess)
+        return fail(nullptr, BLINK_ERR_CUDA, "per-rank stream allocation failed");
+    }
+  }
+  for (const Clique::Group& grp : q->groups) {
+    const int d = grp.device;
     DeviceGuard g(d);
     int* h = nullptr;
     int* dp = nullptr;
@@ -1249,13 +1480,13 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
         cudaHostGetDevicePointer(&dp, h, 0) != cudaSuccess)
       return fail(nullptr, BLINK_ERR_CUDA, "mapped error word allocation failed");
     *h = 0;
-    q->err_host[d] = h;
-    q->err_dev[d] = dp;
+    q->err_host[grp.key] = h;
+    q->err_dev[grp.key] = dp;
     uint64_t* ctrl = nullptr;
     const size_t cb = 2 * sizeof(uint64_t) + kMaxCounters * sizeof(unsigned int);
     if (cudaMalloc(&ctrl, cb) != cudaSuccess || cudaMemset(ctrl, 0, cb) != cudaSuccess)
       return fail(nullptr, BLINK_ERR_CUDA, "control word allocation failed");
-    q->ctrl[d] = ctrl;
+    q->ctrl[grp.key] = ctrl;
   }
   q->alive = ndev;
   return BLINK_SUCCESS;
@@ -1316,6 +1547,7 @@ blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_b
   CUDA_TRY(comm, cudaIpcGetMemHandle(&b.flags_h, comm->flags));
   CUDA_TRY(comm, cudaIpcGetMemHandle(&b.staging_h, comm->staging));
   b.staging_bytes = comm->staging_bytes;
+  b.ll_bytes = comm->ll_bytes;
   memcpy(blob, &b, sizeof b);
   return BLINK_SUCCESS;
 }
@@ -1334,6 +1566,8 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
                   "blob " + std::to_string(u) + " is not rank " + std::to_string(u) + "'s handle");
     if (b.staging_bytes != comm->staging_bytes)
       return fail(comm, BLINK_ERR_INVALID_USAGE, "staging_bytes differs across ranks");
+    if (b.ll_bytes != comm->ll_bytes)
+      return fail(comm, BLINK_ERR_INVALID_USAGE, "ll_max_bytes differs across ranks");
     if (u == comm->rank) {
       comm->peer_flags[u] = comm->flags;
       comm->peer_staging[u] = comm->staging;
@@ -1529,16 +1763,17 @@ blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, siz
 
 blink_result_t blink_get_trace(blink_comm_t comm, uint64_t* out, size_t* n_words) {
   if (!comm || !n_words) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
-  if (comm->multiprocess || !comm->clique->trace.count(comm->device)) {
+  const int key = comm->multiprocess ? -1 : (comm->clique->per_rank ? comm->rank : comm->device);
+  if (comm->multiprocess || !comm->clique->trace.count(key)) {
     *n_words = 0;
     return BLINK_SUCCESS;
   }
-  const size_t need = size_t(comm->clique->trace_ctas[comm->device]) * kTraceSlots;
+  const size_t need = size_t(comm->clique->trace_ctas[key]) * kTraceSlots;
   const size_t cap = *n_words;
   *n_words = need;
   if (!out || cap < need) return BLINK_SUCCESS;
   DeviceGuard g(comm->device);
-  CUDA_TRY(comm, cudaMemcpy(out, comm->clique->trace[comm->device], need * sizeof(uint64_t),
+  CUDA_TRY(comm, cudaMemcpy(out, comm->clique->trace[key], need * sizeof(uint64_t),
                             cudaMemcpyDeviceToHost));
   return BLINK_SUCCESS;
 }
@@ -1589,6 +1824,9 @@ blink_result_t blink_destroy(blink_comm_t comm) {
       for (auto& kv : q->err_host) cudaFreeHost(kv.second);
       for (auto& kv : q->ctrl) cudaFree(kv.second);
       for (auto& kv : q->trace) cudaFree(kv.second);
+      for (auto st : q->rstream) cudaStreamDestroy(st);
+      for (auto ev : q->rfork) cudaEventDestroy(ev);
+      for (auto ev : q->rjoin) cudaEventDestroy(ev);
       for (auto& kv : q->miad) {
         if (kv.second.ev0) cudaEventDestroy(kv.second.ev0);
         if (kv.second.ev1) cudaEventDestroy(kv.second.ev1);

@@ -43,6 +43,13 @@ def cpu_mode(rank, world):
     print(f"rank {rank}: cpu ok {d[:12]}")
 
 
+def to_dev(arr, dtype):
+    a = np.ascontiguousarray(arr)
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
+
+
 def gpu_mode(rank, world):
     import paper_1910_04940_b200 as B
     from paper_1910_04940_b200 import dist as BD
@@ -132,6 +139,34 @@ def gpu_mode(rank, world):
     torch.cuda.synchronize()
     if rank == groot:
         check(gout, OC.gather(gsends, groot)[groot], "staged gather")
+    # 7) low-latency protocol (small calls, unregistered buffers, no handshake):
+    # AllReduce f32/bf16 (ragged), in place, Broadcast; then LL and tree calls
+    # interleaved back to back (the epochs they share stay in step)
+    for cnt, dt in ((1, "f32"), (1001, "f32"), (4099, "bf16")):
+        ls = synth.inputs(45, world, cnt, dt)
+        lx = to_dev(ls[rank], dt)
+        ly = torch.empty_like(lx)
+        comm.allreduce(lx, ly, op="sum")
+        comm.allreduce(lx, lx, op="max")
+        torch.cuda.synchronize()
+        check(ly, OC.naive_reduce(ls, dt, "sum"), f"LL allreduce {dt} {cnt}")
+        check(lx, OC.naive_reduce(ls, dt, "max"), f"LL in-place max {dt} {cnt}")
+    bsrc = synth.rank_input(46, 0, 3333, "f32")
+    bx = torch.from_numpy(bsrc).cuda() if rank == 0 else torch.zeros(3333, device="cuda")
+    comm.broadcast(bx, bx, root=0)
+    torch.cuda.synchronize()
+    check(bx, bsrc, "LL broadcast")
+    small = synth.inputs(47, world, 777, "f32")
+    sx = torch.from_numpy(small[rank]).cuda()
+    outs = []
+    for k in range(6):
+        o = torch.empty_like(sx)
+        comm.allreduce(sx, o, op="sum")
+        outs.append(o)
+        comm.allreduce(xb, yb, op="sum")   # tree path (registered, 2 MiB)
+    torch.cuda.synchronize()
+    for o in outs:
+        check(o, OC.naive_reduce(small, "f32", "sum"), "LL/tree interleaved")
     st = comm.stats()
     comm.destroy()
     print(f"rank {rank}: gpu ok launches={st['launches']} ctas={st['last_ctas']}")
@@ -144,20 +179,24 @@ def timeout_mode(rank, world):
     import paper_1910_04940_b200 as B
     from paper_1910_04940_b200 import dist as BD
     torch.cuda.set_device(0)
-    comm = BD.init(cfg=B.config(timeout_s=1.0), device=0)
-    x = torch.ones(4096, device="cuda")
-    if rank == 0:
-        comm.allreduce(x)                  # enqueued; the kernel waits for rank 1's entry
-        torch.cuda.synchronize()           # returns once the wait timed out
-        try:
-            comm.allreduce(x)
-            raise SystemExit("rank 0: expected BLINK_ERR_TIMEOUT")
-        except B.BlinkError as e:
-            assert e.code == 10, e
-        print("rank 0: timeout ok")
-    else:
-        print("rank 1: skipped the collective")
-    dist.barrier()
+    # the tree executor (entry-flag wait) and the LL protocol (data-line poll)
+    for what, llmax in (("tree", 0), ("LL", 64 << 10)):
+        comm = BD.init(cfg=B.config(timeout_s=1.0, ll_max_bytes=llmax), device=0)
+        x = torch.ones(4096, device="cuda")
+        if rank == 0:
+            comm.allreduce(x)              # enqueued; the kernel waits for rank 1
+            torch.cuda.synchronize()       # returns once the wait timed out
+            try:
+                comm.allreduce(x)
+                raise SystemExit("rank 0: expected BLINK_ERR_TIMEOUT")
+            except B.BlinkError as e:
+                assert e.code == 10, e
+            print(f"rank 0: {what} timeout ok")
+        else:
+            print(f"rank 1: skipped the {what} collective")
+        dist.barrier()
+        comm.destroy()
+        dist.barrier()
 
 
 def main():

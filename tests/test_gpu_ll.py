@@ -1,0 +1,155 @@
+"""GPU parity for the low-latency (LL) protocol (cfg.ll_max_bytes).
+
+Small calls on switch plans run the same one-hop trees with readiness inside
+the data lines (blink_internal.h).  Results must be bit-exact
+against the oracle exactly like the tree executor's: one-hop AllReduce =
+the oracle's own plan = the naive left-to-right order (R#12); Broadcast = the
+root's bytes.  Both launch modes (one batched launch, per-rank launches) and
+the interleaving of LL and tree calls (shared epochs, parity-alternating LL
+areas) are covered.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import collectives as OC
+from oracle import packing as OP
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import B, assert_bitwise, run_allreduce, sentinel, to_dev, to_host  # noqa: E402,F401
+
+LL = 64 << 10
+
+
+def comms_for(B, m, per_rank, ll=LL, **cfg):
+    cfg.setdefault("timeout_s", 20.0)
+    return B.init_all([0] * m, cfg=B.config(launch_per_rank=per_rank, ll_max_bytes=ll, **cfg))
+
+
+@pytest.mark.parametrize("per_rank", [0, 1])
+@pytest.mark.parametrize("m", [2, 3, 5, 8, 16])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_ll_allreduce_bitexact(B, per_rank, m, dtype):
+    comms = comms_for(B, m, per_rank)
+    es = OC.ESIZE[dtype]
+    for count in (1, 3, 7, 1001, LL // es - 1):
+        sends = synth.inputs(200 + m, m, count, dtype)
+        for op in ("sum", "prod", "min", "max"):
+            s = sends
+            if op == "prod" and dtype == "i32":
+                s = [(x % 5 - 2).astype(np.int32) for x in sends]
+            got = run_allreduce(B, comms, s, dtype, op)
+            want = OC.allreduce(OP.plan_switch_allreduce(m), s, dtype, op)
+            for g in got:
+                assert_bitwise(g, want)
+            st = comms[0].stats()
+            assert st["last_chunks"] == 0, "expected the LL protocol"
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("per_rank", [0, 1])
+def test_ll_edge_values_inplace_and_misaligned(B, per_rank):
+    m, count = 6, 4099
+    comms = comms_for(B, m, per_rank)
+    sends = [synth.edge_case_f32(4, r, count) for r in range(m)]
+    for op in ("sum", "min", "max"):
+        got = run_allreduce(B, comms, sends, "f32", op, inplace=(op == "max"))
+        want = OC.allreduce(OP.plan_switch_allreduce(m), sends, "f32", op)
+        for g in got:
+            assert_bitwise(g, want)
+    # element-aligned but not 8-byte aligned views (bf16 at +2 bytes, f32 at +4)
+    for dtype, off in (("bf16", 1), ("f32", 1)):
+        s = synth.inputs(210, m, 999, dtype)
+        raw = [to_dev(np.concatenate([x[:1], x]), dtype) for x in s]
+        xs = [r[off:] for r in raw]
+        ys = [sentinel(1000, dtype)[off:] for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.allreduce(xs[r], ys[r], op="sum")
+        torch.cuda.synchronize()
+        want = OC.naive_reduce(s, dtype, "sum")
+        for y in ys:
+            assert_bitwise(to_host(y, dtype), want)
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("per_rank", [0, 1])
+def test_ll_broadcast(B, per_rank):
+    m = 8
+    comms = comms_for(B, m, per_rank)
+    for count, dtype, root in ((1, "f32", 0), (1001, "bf16", 5), (16383, "i32", 7)):
+        send = synth.rank_input(220, root, count, dtype)
+        dsend = to_dev(send, dtype)
+        recvs = [sentinel(count, dtype) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.broadcast(dsend if r == root else None, recvs[r], root=root, count=count, dtype=dtype)
+        torch.cuda.synchronize()
+        for x in recvs:
+            assert_bitwise(to_host(x, dtype), send)
+        assert comms[0].stats()["last_chunks"] == 0
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("per_rank", [0, 1])
+def test_ll_and_tree_calls_interleaved(B, per_rank):
+    """LL calls (parity-alternating areas) and tree-executor calls share the
+    device epochs: eight mixed calls without a host sync, all exact."""
+    m = 8
+    comms = comms_for(B, m, per_rank)
+    sizes = [100, 300000, 5, 16000, 70000, 1, 2049, 40000]
+    runs = []
+    for k, count in enumerate(sizes):
+        sends = synth.inputs(230 + k, m, count, "f32")
+        ds = [to_dev(s, "f32") for s in sends]
+        dr = [sentinel(count, "f32") for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.allreduce(ds[r], dr[r], op="sum")
+        runs.append((sends, ds, dr))
+    torch.cuda.synchronize()
+    for sends, _, dr in runs:
+        want = OC.naive_reduce(sends, "f32", "sum")
+        for x in dr:
+            assert_bitwise(x.cpu().numpy(), want)
+    for c in comms:
+        c.destroy()
+
+
+def test_ll_cuda_graph_replay(B):
+    m, count = 8, 5000
+    comms = comms_for(B, m, 1)
+    dsend = [torch.empty(count, device="cuda") for _ in range(m)]
+    drecv = [torch.empty(count, device="cuda") for _ in range(m)]
+    for r, c in enumerate(comms):
+        c.allreduce(dsend[r], drecv[r])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for r, c in enumerate(comms):
+            c.allreduce(dsend[r], drecv[r])
+    for it in range(5):   # odd and even epochs: both LL areas
+        sends = synth.inputs(240 + it, m, count, "f32")
+        for d, s in zip(dsend, sends):
+            d.copy_(torch.from_numpy(s))
+        g.replay()
+        torch.cuda.synchronize()
+        want = OC.naive_reduce(sends, "f32", "sum")
+        for x in drecv:
+            assert_bitwise(x.cpu().numpy(), want)
+    for c in comms:
+        c.destroy()
+
+
+def test_ll_off_uses_the_tree_executor(B):
+    m, count = 4, 1000
+    comms = comms_for(B, m, 0, ll=0)
+    sends = synth.inputs(250, m, count, "f32")
+    got = run_allreduce(B, comms, sends, "f32", "sum")
+    for g in got:
+        assert_bitwise(g, OC.naive_reduce(sends, "f32", "sum"))
+    assert comms[0].stats()["last_chunks"] > 0
+    for c in comms:
+        c.destroy()

@@ -51,4 +51,5 @@ def test_two_processes_share_one_gpu():
 @pytest.mark.gpu
 def test_missing_rank_times_out_instead_of_hanging():
     out = launch(2, "timeout", {"BLINK_SAME_GPU": "1"}, timeout=300)
-    assert "rank 0: timeout ok" in out
+    assert "rank 0: tree timeout ok" in out
+    assert "rank 0: LL timeout ok" in out
