@@ -852,15 +852,16 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   // also means every peer finished reading this rank's buffers (causality).
   if (a.exit_wait) {
     __syncthreads();
-    int k = 0;
+    // the (tree, chunk) flags of this rank, flattened; this thread waits for
+    // items g, g + G, ... (walking the trees once, not every item)
+    const int G = t.exit_cnt * int(blockDim.x);
+    int k = t.exit_idx * int(blockDim.x) + int(threadIdx.x);
+    int base = 0;
     for (int i = 0; i < a.ntrees; ++i) {
       const DevTree tr = a.trees[i];
       if (tr.root == v || !((tr.members >> v) & 1u)) continue;
-      for (int c = 0; c < tr.nchunks; ++c, ++k) {
-        if (k % t.exit_cnt != t.exit_idx) continue;
-        if (((k / t.exit_cnt) % blockDim.x) != threadIdx.x) continue;
-        wait_ge(myflags + bflag_idx(i, c), ctl);
-      }
+      for (; k < base + tr.nchunks; k += G) wait_ge(myflags + bflag_idx(i, k - base), ctl);
+      base += tr.nchunks;
     }
     fence_acqrel(ctl.sys);
   }

@@ -265,27 +265,19 @@ struct Channel {
   int ctas = 1;
 };
 
-// CTA / channel assignment for the ranks in `launch_mask` (a6) and the device
-// tables of one launch.
-blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, int esize,
-                           uint64_t launch_mask, int budget, Sized* s, size_t chunk_override = 0) {
-  blink_config_t cfg = comm->cfg;
-  if (chunk_override) cfg.chunk_bytes = chunk_override;
+// Channels of the ranks in `mask` and their CTA shares of `budget` (a6):
+// CTAs in proportion to bytes x operands.  Returns false (with *err) when the
+// channels do not fit the budget.  *nexit = ranks in `mask` without a channel.
+bool alloc_channels(const Plan& plan, const std::vector<std::vector<uint32_t>>& ch,
+                    const std::vector<TreeRange>& r0, int esize, uint64_t mask, int budget,
+                    std::vector<Channel>* out, int* nexit_out, std::string* err) {
   const int n = plan.nranks;
   const int k = int(plan.trees.size());
-  std::vector<std::vector<uint32_t>> ch(k, std::vector<uint32_t>(n, 0));
-  for (int i = 0; i < k; ++i)
-    for (int v = 0; v < n; ++v)
-      if (plan.trees[i].parent[v] >= 0) ch[i][plan.trees[i].parent[v]] |= 1u << v;
-  // provisional byte shares (equal CTAs hint) to weigh channels
-  std::vector<TreeRange> r0;
-  std::string err;
-  blink_result_t rr = size_plan(plan, count, esize, cfg, 1, &r0, &err);
-  if (rr != BLINK_SUCCESS) return fail(comm, rr, err);
-  std::vector<Channel> chans;
+  std::vector<Channel>& chans = *out;
+  chans.clear();
   std::vector<int> rank_has(n, 0);
   for (int v = 0; v < n; ++v) {
-    if (!((launch_mask >> v) & 1)) continue;
+    if (!((mask >> v) & 1)) continue;
     for (int i = 0; i < k; ++i) {
       uint32_t c = ch[i][v];
       const bool own_block = plan.blocks && is_push_coll(plan.coll) && plan.trees[i].root == v;
@@ -310,12 +302,14 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   }
   int nexit = 0;
   for (int v = 0; v < n; ++v)
-    if (((launch_mask >> v) & 1) && !rank_has[v]) ++nexit;
-  int avail = budget - nexit;
-  if (int(chans.size()) > avail)
-    return fail(comm, BLINK_ERR_UNSUPPORTED,
-                "plan needs " + std::to_string(chans.size() + nexit) + " channels but only " +
-                    std::to_string(budget) + " CTAs can be co-resident");
+    if (((mask >> v) & 1) && !rank_has[v]) ++nexit;
+  *nexit_out = nexit;
+  const int avail = budget - nexit;
+  if (int(chans.size()) > avail) {
+    *err = "plan needs " + std::to_string(chans.size() + nexit) + " channels but only " +
+           std::to_string(budget) + " CTAs can be co-resident";
+    return false;
+  }
   double tot = 0;
   for (auto& c : chans) tot += c.work;
   int used = 0;
@@ -328,6 +322,46 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
                                [](const Channel& a, const Channel& b) { return a.ctas < b.ctas; });
     --it->ctas;
     --used;
+  }
+  return true;
+}
+
+// CTA / channel assignment for the ranks in `launch_mask` (a6) and the device
+// tables of one launch.  `group_masks` lists every launch group of the call
+// (one per process, device or rank); the chunking must be the same in all of
+// them, because a chunk's flags name the same bytes on every rank, so the
+// chunk-size hints come from all groups' channel shares, not this group's.
+blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, int esize,
+                           uint64_t launch_mask, const std::vector<uint64_t>& group_masks,
+                           int budget, Sized* s, size_t chunk_override = 0) {
+  blink_config_t cfg = comm->cfg;
+  if (chunk_override) cfg.chunk_bytes = chunk_override;
+  const int n = plan.nranks;
+  const int k = int(plan.trees.size());
+  std::vector<std::vector<uint32_t>> ch(k, std::vector<uint32_t>(n, 0));
+  for (int i = 0; i < k; ++i)
+    for (int v = 0; v < n; ++v)
+      if (plan.trees[i].parent[v] >= 0) ch[i][plan.trees[i].parent[v]] |= 1u << v;
+  // provisional byte shares (equal CTAs hint) to weigh channels
+  std::vector<TreeRange> r0;
+  std::string err;
+  blink_result_t rr = size_plan(plan, count, esize, cfg, 1, &r0, &err);
+  if (rr != BLINK_SUCCESS) return fail(comm, rr, err);
+  std::vector<Channel> chans;
+  int nexit = 0;
+  if (!alloc_channels(plan, ch, r0, esize, launch_mask, budget, &chans, &nexit, &err))
+    return fail(comm, BLINK_ERR_UNSUPPORTED, err);
+  // chunk-size hint per tree: the busiest channel of the tree in any group
+  std::vector<int> hint(k, 1);
+  for (uint64_t gm : group_masks) {
+    std::vector<Channel> gch;
+    int gx = 0;
+    if (gm == launch_mask) {
+      gch = chans;
+    } else if (!alloc_channels(plan, ch, r0, esize, gm, budget, &gch, &gx, &err)) {
+      return fail(comm, BLINK_ERR_UNSUPPORTED, err);
+    }
+    for (auto& c : gch) hint[c.tree] = std::max(hint[c.tree], c.ctas);
   }
   // ---- merged one-hop AllReduce (single launch): every tree's root channel
   // reads every rank's send and writes every rank's recv, so one channel over
@@ -486,9 +520,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
       }
     }
   }
-  // chunking with the CTA count of the busiest channel of each tree
-  std::vector<int> hint(k, 1);
-  for (auto& c : chans) hint[c.tree] = std::max(hint[c.tree], c.ctas);
+  // chunking with the CTA count of the busiest channel of each tree (hint)
   s->ranges.clear();
   for (int i = 0; i < k; ++i) {
     std::vector<TreeRange> ri;
@@ -882,7 +914,9 @@ blink_result_t clique_launch(Clique* q) {
       int share = 0;
       for (const Clique::Group& g2 : q->groups) share += g2.device == dev;
       budget = std::max(1, budget / std::max(1, share));
-      r = build_sized(cd, *plan, q->count, es, mask, budget, &s, chunk_override);
+      std::vector<uint64_t> gm;
+      for (const Clique::Group& g2 : q->groups) gm.push_back(g2.mask);
+      r = build_sized(cd, *plan, q->count, es, mask, gm, budget, &s, chunk_override);
       if (r != BLINK_SUCCESS) return r;
       r = finalize_tables(cd, dev, es, &s);
       if (r != BLINK_SUCCESS) return r;
@@ -1091,7 +1125,9 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   if (it == comm->sized.end()) {
     Sized s;
     int budget = co_resident_budget(comm, comm->device, dtype, op, coll);
-    r = build_sized(comm, *plan, count, es, mask, budget, &s);
+    std::vector<uint64_t> gm;  // one group per process
+    for (int u = 0; u < n; ++u) gm.push_back(uint64_t(1) << u);
+    r = build_sized(comm, *plan, count, es, mask, gm, budget, &s);
     if (r != BLINK_SUCCESS) return r;
     r = finalize_tables(comm, comm->device, es, &s);
     if (r != BLINK_SUCCESS) return r;
@@ -1741,17 +1777,24 @@ blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, siz
   const Plan* plan = nullptr;
   r = get_plan(comm, coll, root, count * es, &plan);
   if (r != BLINK_SUCCESS) return r;
-  // the launch this rank belongs to
+  // the launch this rank belongs to, and every launch group of the call
   uint64_t mask = 0;
+  std::vector<uint64_t> gm;
+  int share = 1;
   if (comm->multiprocess) {
     mask = uint64_t(1) << comm->rank;
+    for (int u = 0; u < comm->nranks; ++u) gm.push_back(uint64_t(1) << u);
   } else {
-    for (int v = 0; v < comm->nranks; ++v)
-      if (comm->clique->comms[v]->device == comm->device) mask |= uint64_t(1) << v;
+    share = 0;
+    for (const Clique::Group& g : comm->clique->groups) {
+      gm.push_back(g.mask);
+      if ((g.mask >> comm->rank) & 1) mask = g.mask;
+      if (g.device == comm->device) ++share;
+    }
   }
   Sized s;
-  int budget = co_resident_budget(comm, comm->device, dtype, BLINK_SUM, coll);
-  r = build_sized(comm, *plan, count, es, mask, budget, &s);
+  int budget = std::max(1, co_resident_budget(comm, comm->device, dtype, BLINK_SUM, coll) / share);
+  r = build_sized(comm, *plan, count, es, mask, gm, budget, &s);
   if (r != BLINK_SUCCESS) return r;
   std::string j = plan_to_json(*plan, count, es, s.ranges, s.ctas);
   size_t need = j.size() + 1, cap = *json_bytes;

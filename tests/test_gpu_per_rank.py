@@ -165,3 +165,53 @@ def test_per_rank_large_sampled(B):
         assert_bitwise(y[ti].cpu().numpy(), want)
     for c in comms:
         c.destroy()
+
+
+@pytest.mark.parametrize("graph_name", ["switch", "dgx1v"])
+def test_per_rank_chunking_agrees_across_ranks(B, graph_name):
+    """A chunk's flags name the same bytes on every rank, so every launch
+    group (rank) must chunk a tree identically, whatever channels it runs
+    (the root of 7 two-level trees vs an inner node with one forward channel)."""
+    graph = None if graph_name == "switch" else B.Graph.from_pairs(8, OG.dgx1v()[1])
+    comms = per_rank_comms(B, 8, graph=graph)
+    for is_ar in (False, True):
+        for count in (1 << 20, (16 << 20) + 3, 64 << 20):
+            views = [c.plan(is_ar, 0, count) for c in comms]
+            key = [[(t["lo"], t["hi"], t["chunk"], t["nchunks"]) for t in p["trees"]] for p in views]
+            assert all(k == key[0] for k in key), (is_ar, count)
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("graph_name", ["switch", "dgx1v"])
+def test_per_rank_large_broadcast_every_byte(B, graph_name):
+    graph = None if graph_name == "switch" else B.Graph.from_pairs(8, OG.dgx1v()[1])
+    comms = per_rank_comms(B, 8, graph=graph)
+    count, root = (16 << 20) + 5, 6
+    x = synth.device_input(2, root, count, "f32")
+    ys = [torch.zeros_like(x) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.broadcast(x if r == root else None, ys[r], root=root)
+    torch.cuda.synchronize()
+    for y in ys:
+        assert torch.equal(y.view(torch.int32), x.view(torch.int32))
+    for c in comms:
+        c.destroy()
+
+
+def test_per_rank_large_multilevel_allreduce_int_exact(B):
+    g = OG.dgx1v()
+    comms = per_rank_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]))
+    count = (8 << 20) + 7
+    xs = [synth.device_input(5, r, count, "i32") for r in range(8)]
+    ys = [torch.empty_like(x) for x in xs]
+    for r, c in enumerate(comms):
+        c.allreduce(xs[r], ys[r])
+    torch.cuda.synchronize()
+    want = xs[0].clone()
+    for x in xs[1:]:
+        want += x   # int32 wraparound sum: exact under any order (definition, SURVEY c-1)
+    for y in ys:
+        assert torch.equal(y, want)
+    for c in comms:
+        c.destroy()
