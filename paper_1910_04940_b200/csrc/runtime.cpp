@@ -1075,6 +1075,7 @@ struct Blob {
   cudaIpcMemHandle_t staging_h;
   uint64_t staging_bytes;
   uint64_t ll_bytes;
+  uint64_t ll_max_bytes;  // the LL-or-tree decision must be the same on every rank
 };
 struct RegBlob {
   char magic[8];
@@ -1584,6 +1585,7 @@ blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_b
   CUDA_TRY(comm, cudaIpcGetMemHandle(&b.staging_h, comm->staging));
   b.staging_bytes = comm->staging_bytes;
   b.ll_bytes = comm->ll_bytes;
+  b.ll_max_bytes = comm->ll_bytes ? comm->cfg.ll_max_bytes : 0;
   memcpy(blob, &b, sizeof b);
   return BLINK_SUCCESS;
 }
@@ -1602,7 +1604,8 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
                   "blob " + std::to_string(u) + " is not rank " + std::to_string(u) + "'s handle");
     if (b.staging_bytes != comm->staging_bytes)
       return fail(comm, BLINK_ERR_INVALID_USAGE, "staging_bytes differs across ranks");
-    if (b.ll_bytes != comm->ll_bytes)
+    if (b.ll_bytes != comm->ll_bytes ||
+        b.ll_max_bytes != (comm->ll_bytes ? comm->cfg.ll_max_bytes : 0))
       return fail(comm, BLINK_ERR_INVALID_USAGE, "ll_max_bytes differs across ranks");
     if (u == comm->rank) {
       comm->peer_flags[u] = comm->flags;

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Small collectives for compute-sanitizer (memcheck / synccheck / racecheck):
 one-hop AllReduce (TMA and LSU paths), emulated DGX-1V Broadcast and
-multi-level AllReduce, ReduceScatter / AllGather, misaligned buffers.
+multi-level AllReduce, ReduceScatter / AllGather, misaligned buffers, the LL
+protocol (batched and per-rank launches) and a per-rank tree AllReduce.
 Every result is checked against the oracle so a clean sanitizer run is also a
 correct run."""
 import os
@@ -82,6 +83,29 @@ def main():
         check(y, OC.naive_reduce(isends, "i32", "sum"), "dgx1v allreduce")
     for c in comms:
         c.destroy()
+    # LL protocol (batched and per-rank launches) and the per-rank tree path
+    for per_rank in (0, 1):
+        comms = B.init_all([0] * 4, cfg=B.config(timeout_s=120.0, launch_per_rank=per_rank))
+        for cnt in (1, 1001):
+            ls = synth.inputs(204, 4, cnt, "f32")
+            lx = [torch.from_numpy(s).cuda() for s in ls]
+            ly = [torch.empty_like(x) for x in lx]
+            for r, c in enumerate(comms):
+                c.allreduce(lx[r], ly[r])
+            for r, c in enumerate(comms):
+                c.broadcast(lx[r] if r == 2 else None, lx[r], root=2)
+            torch.cuda.synchronize()
+            for r in range(4):
+                check(ly[r], OC.naive_reduce(ls, "f32", "sum"), f"LL allreduce pr={per_rank}")
+                check(lx[r], ls[2], f"LL broadcast pr={per_rank}")
+        if per_rank:
+            for r, c in enumerate(comms):
+                c.allreduce(xs[r], ys[r])
+            torch.cuda.synchronize()
+            for y in ys:
+                check(y, want, "per-rank tree allreduce")
+        for c in comms:
+            c.destroy()
     print("sanitize cases ok")
 
 
