@@ -22,6 +22,9 @@ packing      MWU approximate packing (Sec. 3.2), ILP tree-count
              bidirectional AllReduce trees (Sec. 3.3), one-hop trees
              on a switch (Sec. 3.5), weight-proportional split
              (P:477).
+model        chunk-pipelining model (discrete-event simulation vs the
+             (c+h-1)/c closed form) and bytes per directed link of a
+             plan (P:397-400).
 collectives  Broadcast / AllReduce values along packed trees (P:477-487,
              Sec. 4.1): per-tree post-order combine in a fixed operand order,
              fp32 accumulation, one RNE rounding per node (R#12, R#13).

@@ -253,3 +253,29 @@ def test_init_all_rejects_too_many_ranks_before_touching_cuda(B):
     devs = (ctypes.c_int * 17)(*([0] * 17))
     assert B._lib.blink_init_all(hs, 17, devs, None, None) == 9       # BLINK_ERR_UNSUPPORTED
     assert b"16" in B._lib.blink_last_error(None)
+
+
+@pytest.mark.parametrize("name", ["switch8", "dgx1v", "dgx1p", "tri"])
+def test_library_plans_move_the_bytes_of_the_message_bound(B, name):
+    """The library's plans, evaluated with the oracle's byte model
+    (oracle/model.py, pinned in test_oracle_model.py): Broadcast moves
+    (m-1) S and every non-root receives exactly S; AllReduce moves 2 (m-1) S
+    (P:397-400)."""
+    from oracle import graphs, model
+    if name == "switch8":
+        m, G = 8, None
+    elif name == "tri":
+        sub, _ = graphs.induced(graphs.dgx1p(), [0, 1, 3])
+        m, G = 3, B.Graph.from_pairs(3, sub[1])
+    else:
+        g = graphs.dgx1v() if name == "dgx1v" else graphs.dgx1p()
+        m, G = 8, B.Graph.from_pairs(8, g[1])
+    count = 250001
+    S = count * 4
+    pb = _oracle_plan(B.plan_json(m, False, m - 1, count, "f32", graph=G))
+    lb = model.link_bytes(pb, m, S, False)
+    assert sum(lb.values()) == (m - 1) * S
+    for v in range(m):
+        assert sum(b for (_, w), b in lb.items() if w == v) == (0 if v == m - 1 else S)
+    pa = _oracle_plan(B.plan_json(m, True, 0, count, "f32", graph=G))
+    assert sum(model.link_bytes(pa, m, S, True).values()) == 2 * (m - 1) * S
