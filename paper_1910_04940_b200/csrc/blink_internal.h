@@ -141,7 +141,15 @@ struct LaunchArgs {
   char* send[kMaxArgRanks];
   char* recv[kMaxArgRanks];
   uint64_t* flags[kMaxArgRanks];
+  // Per-call tables in the parameter space (constant bank): no dependent
+  // global loads before a CTA's first TMA load.
+  DevTree ptrees[kMaxTrees];     // = trees[0 .. ntrees)
+  int32_t tree_end[kMaxTrees];   // prefix sums of ptrees[i].nchunks (merged tasks)
+  int32_t merged_all;            // every CTA runs mtask (cta_idx = c0 = blockIdx.x): no task load
+  int32_t pad5;
+  DevTask mtask;
 };
+static_assert(sizeof(LaunchArgs) <= 4096, "kernel parameter space");
 
 // Low-latency (LL) protocol for small calls on switch plans (NEXT-2's
 // small-message protocol).  The same one-hop trees, but

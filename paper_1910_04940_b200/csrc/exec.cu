@@ -400,7 +400,6 @@ struct TileMeta {
 };
 
 struct Shared {
-  int tree_end[kMaxTrees];  // merged tasks: prefix sums of the trees' chunk counts
   TileMeta smeta[kMaxStages];
   TileMeta ometa[kOutBufs];
   const char* srcs[kMaxRanks + 1];
@@ -539,9 +538,9 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       int64_t b0, b1;
       if (t.merged) {  // chunk c of the concatenation of every tree's chunks
         int i = 0;
-        while (i + 1 < a.ntrees && c >= sh.tree_end[i]) ++i;
-        const int cc = c - (i ? sh.tree_end[i - 1] : 0);
-        const DevTree ti = a.trees[i];
+        while (i + 1 < a.ntrees && c >= a.tree_end[i]) ++i;
+        const int cc = c - (i ? a.tree_end[i - 1] : 0);
+        const DevTree& ti = a.ptrees[i];
         b0 = ti.lo + int64_t(cc) * ti.chunk;
         b1 = min(ti.hi, b0 + ti.chunk);
       } else {
@@ -708,8 +707,8 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
       int cc = c;
       if (t.merged) {  // chunk c of the concatenation of every tree's chunks
         int i = 0;
-        while (i + 1 < a.ntrees && cc >= a.trees[i].nchunks) cc -= a.trees[i++].nchunks;
-        ti = a.trees[i];
+        while (i + 1 < a.ntrees && cc >= a.ptrees[i].nchunks) cc -= a.ptrees[i++].nchunks;
+        ti = a.ptrees[i];
       }
       const int64_t b0 = ti.lo + int64_t(cc) * ti.chunk;
       const int64_t b1 = min(ti.hi, b0 + ti.chunk);
@@ -734,7 +733,14 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   // Epoch = launches completed on this device group + 1, read from device
   // memory so that CUDA-graph replays get fresh epochs.
   const LaunchArgs& a = a_in;
-  const DevTask t0 = a.tasks[blockIdx.x];
+  DevTask t0;
+  if (a.merged_all) {  // one merged channel: the task differs only by index
+    t0 = a.mtask;
+    t0.cta_idx = blockIdx.x;
+    t0.c0 = blockIdx.x;
+  } else {
+    t0 = a.tasks[blockIdx.x];
+  }
   if (threadIdx.x == 0) {
     if (a.trace)
       for (int k = 1; k < kTraceSlots; ++k) a.trace[size_t(blockIdx.x) * kTraceSlots + k] = 0;
@@ -785,15 +791,6 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
       const uint32_t emask = !a.exit_wait ? 0u
                              : (t.role == kRoleReduce ? t.leafmask : (pushes ? t.children : 0u));
       entry_ok = warp_wait(emask, [&](int u) { return wflags + entry_idx(u); }, ctl);
-      if (t.merged) {  // prefix sums of the trees' chunk counts (one parallel load)
-        const int lane = threadIdx.x;
-        int v = lane < a.ntrees ? a.trees[lane].nchunks : 0;
-        for (int d = 1; d < 32; d <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, v, d);
-          if (lane >= d) v += y;
-        }
-        if (lane < a.ntrees) sh.tree_end[lane] = v;
-      }
     }
     if (threadIdx.x == 0) {
       int ns = 0, nd = 0;
@@ -858,7 +855,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
     int k = t.exit_idx * int(blockDim.x) + int(threadIdx.x);
     int base = 0;
     for (int i = 0; i < a.ntrees; ++i) {
-      const DevTree tr = a.trees[i];
+      const DevTree& tr = a.ptrees[i];
       if (tr.root == v || !((tr.members >> v) & 1u)) continue;
       for (; k < base + tr.nchunks; k += G) wait_ge(myflags + bflag_idx(i, k - base), ctl);
       base += tr.nchunks;

@@ -70,6 +70,8 @@ struct Sized {
   std::vector<DevTask> tasks;
   DevTask* d_tasks = nullptr;
   DevTree* d_trees = nullptr;
+  std::vector<DevTree> htrees;  // host copy (kernel parameters)
+  bool merged_all = false;      // every CTA runs tasks[0] with its own index
   int ctas = 0;
   int chunks = 0;
   int nctr = 0;  // dynamic chunk counters used by the launch
@@ -407,6 +409,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
       s->ctas = ctas;
       s->chunks = total;
       s->plan = &plan;
+      s->merged_all = true;
       return BLINK_SUCCESS;
     }
   }
@@ -598,6 +601,7 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
   }
   for (auto& t : s->tasks)
     if (t.tree >= 0 && size_t(t.tree) < trees.size()) t.tr = trees[t.tree];
+  s->htrees = trees;
   CUDA_TRY(comm, cudaMalloc(&s->d_tasks, sizeof(DevTask) * s->tasks.size()));
   CUDA_TRY(comm, cudaMalloc(&s->d_trees, sizeof(DevTree) * std::max<size_t>(1, trees.size())));
   CUDA_TRY(comm, cudaMemcpy(s->d_tasks, s->tasks.data(), sizeof(DevTask) * s->tasks.size(),
@@ -691,6 +695,18 @@ blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtyp
   if (comm->multiprocess && !comm->connected)
     return fail(comm, BLINK_ERR_INVALID_USAGE, "blink_connect has not been called");
   return BLINK_SUCCESS;
+}
+
+// Per-call tables that travel as kernel parameters (LaunchArgs).
+void fill_param_tables(const Sized& s, LaunchArgs* a) {
+  int acc = 0;
+  for (size_t i = 0; i < s.htrees.size() && i < size_t(kMaxTrees); ++i) {
+    a->ptrees[i] = s.htrees[i];
+    acc += s.htrees[i].nchunks;
+    a->tree_end[i] = acc;
+  }
+  a->merged_all = s.merged_all ? 1 : 0;
+  if (s.merged_all) a->mtask = s.tasks[0];
 }
 
 // ---------------------------------------------------------------- LL protocol
@@ -927,6 +943,7 @@ blink_result_t clique_launch(Clique* q) {
     a.tasks = s.d_tasks;
     a.trees = s.d_trees;
     a.ntrees = int(plan->trees.size());
+    fill_param_tables(s, &a);
     a.nranks = n;
     a.coll = q->coll;
     a.dtype = q->dtype;
@@ -1144,6 +1161,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.tasks = s.d_tasks;
   a.trees = s.d_trees;
   a.ntrees = int(plan->trees.size());
+  fill_param_tables(s, &a);
   a.nranks = n;
   a.coll = coll;
   a.dtype = dtype;
