@@ -138,16 +138,20 @@ struct LaunchArgs {
                              // [1] CTAs finished in the current launch (graph-safe epochs)
   uint64_t timeout_ns;
   int* err;                  // host-mapped error word (0 = ok)
+  // What a CTA reads before its first TMA load sits together here (the
+  // parameter bank's misses serialise, so the fields share few lines).
+  int32_t merged_all;            // every CTA runs mtask (cta_idx = c0 = blockIdx.x): no task load
+  int32_t pad5;
+  int64_t mchunk;                // merged: chunk c = bytes [c*mchunk, min(mbytes, (c+1)*mchunk))
+  int64_t mbytes;                // merged: bytes per rank
+  DevTask mtask;
   char* send[kMaxArgRanks];
   char* recv[kMaxArgRanks];
   uint64_t* flags[kMaxArgRanks];
   // Per-call tables in the parameter space (constant bank): no dependent
   // global loads before a CTA's first TMA load.
   DevTree ptrees[kMaxTrees];     // = trees[0 .. ntrees)
-  int32_t tree_end[kMaxTrees];   // prefix sums of ptrees[i].nchunks (merged tasks)
-  int32_t merged_all;            // every CTA runs mtask (cta_idx = c0 = blockIdx.x): no task load
-  int32_t pad5;
-  DevTask mtask;
+  int32_t tree_end[kMaxTrees];   // prefix sums of ptrees[i].nchunks
 };
 static_assert(sizeof(LaunchArgs) <= 4096, "kernel parameter space");
 

@@ -7,7 +7,9 @@
 // (dynamic balancing) or a static stride -- so chunks of all trees and all
 // hops are in flight at once (pipelining; concurrency across
 // trees).  A single launch of one-hop AllReduce roots is one
-// merged channel over every tree's chunks.
+// merged channel whose chunks are byte ranges of the whole buffer (every tree
+// combines all ranks in the same order, so the tree split does not change a
+// byte's result).
 //
 // Data movement (TMA path, aligned buffers): a warp-specialised pipeline --
 // producer warp (cp.async.bulk loads of every source tile into a shared-
@@ -536,13 +538,9 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         break;
       }
       int64_t b0, b1;
-      if (t.merged) {  // chunk c of the concatenation of every tree's chunks
-        int i = 0;
-        while (i + 1 < a.ntrees && c >= a.tree_end[i]) ++i;
-        const int cc = c - (i ? a.tree_end[i - 1] : 0);
-        const DevTree& ti = a.ptrees[i];
-        b0 = ti.lo + int64_t(cc) * ti.chunk;
-        b1 = min(ti.hi, b0 + ti.chunk);
+      if (t.merged) {  // one-hop roots over every rank: a chunk is a byte range
+        b0 = int64_t(c) * a.mchunk;
+        b1 = min(a.mbytes, b0 + a.mchunk);
       } else {
         b0 = tr.lo + int64_t(c) * tr.chunk;
         b1 = min(tr.hi, b0 + tr.chunk);
@@ -703,15 +701,12 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
     __syncthreads();
     const bool ok = sh.ok;
     if (ok) {
-      DevTree ti = tr;
-      int cc = c;
-      if (t.merged) {  // chunk c of the concatenation of every tree's chunks
-        int i = 0;
-        while (i + 1 < a.ntrees && cc >= a.ptrees[i].nchunks) cc -= a.ptrees[i++].nchunks;
-        ti = a.ptrees[i];
+      int64_t b0 = tr.lo + int64_t(c) * tr.chunk;
+      int64_t b1 = min(tr.hi, b0 + tr.chunk);
+      if (t.merged) {  // one-hop roots over every rank: a chunk is a byte range
+        b0 = int64_t(c) * a.mchunk;
+        b1 = min(a.mbytes, b0 + a.mchunk);
       }
-      const int64_t b0 = ti.lo + int64_t(cc) * ti.chunk;
-      const int64_t b1 = min(ti.hi, b0 + ti.chunk);
       if (t.role == kRoleReduce)
         reduce_range<DT, OP, VEC>(sh.srcs, sh.nsrc, sh.dsts, sh.ndst, b0, b1);
       else
@@ -741,11 +736,15 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   } else {
     t0 = a.tasks[blockIdx.x];
   }
+  // A merged single launch (one-hop AllReduce roots, every rank in this
+  // launch) reads and writes no flag: it needs no epoch, and its last CTA just
+  // advances the counter -- no dependent load before the first TMA load.
+  const bool no_flags = a.merged_all && !a.exit_wait;
   if (threadIdx.x == 0) {
     if (a.trace)
       for (int k = 1; k < kTraceSlots; ++k) a.trace[size_t(blockIdx.x) * kTraceSlots + k] = 0;
     trace(a, 0);
-    s_epoch = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
+    s_epoch = no_flags ? 0 : *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
     trace(a, 1);
   }
   __syncthreads();
@@ -792,42 +791,53 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
                              : (t.role == kRoleReduce ? t.leafmask : (pushes ? t.children : 0u));
       entry_ok = warp_wait(emask, [&](int u) { return wflags + entry_idx(u); }, ctl);
     }
-    if (threadIdx.x == 0) {
-      int ns = 0, nd = 0;
-      const bool ok = entry_ok;
-      if (t.role == kRoleReduce) {
-        const uint32_t ops = t.children | (1u << w);
-        for (int u = 0; u < a.nranks; ++u) {
-          if (!((ops >> u) & 1u)) continue;
-          sh.srcs[ns++] = (u == w || ((t.leafmask >> u) & 1u)) ? a.send[u] : a.recv[u];
+    if (threadIdx.x < 32) {
+      // warp 0 builds the operand / destination lists: lane u looks at rank u
+      // (parallel parameter loads instead of one thread walking the ranks);
+      // sources in ascending rank order (R#12), destinations in rank order
+      const int u = threadIdx.x;
+      const uint32_t me = 1u << w;
+      bool is_src = false, from_send = false, is_dst = false;
+      char* su = nullptr;
+      char* ru = nullptr;
+      if (u < a.nranks) {
+        su = a.send[u];
+        ru = a.recv[u];
+        const uint32_t bit = 1u << u;
+        if (t.role == kRoleReduce) {
+          is_src = ((t.children | me) & bit) != 0u;
+          from_send = ((t.leafmask | me) & bit) != 0u;
+          // ReduceScatter keeps the result at the root
+          is_dst = u == w || (is_root && a.coll == kAllReduce && (t.children & bit));
+        } else {
+          const bool src_root = is_push_coll(a.coll) && is_root;
+          is_src = u == w;
+          from_send = src_root;
+          // the root's own copy (Gather: only the gather root holds a recv)
+          is_dst = (t.children & bit) != 0u ||
+                   (u == w && src_root && su != ru && (a.coll != kGather || w == a.bcast_root));
         }
-        sh.dsts[nd++] = a.recv[w];
-        if (is_root && a.coll == kAllReduce)  // ReduceScatter keeps the result at the root
-          for (int u = 0; u < a.nranks; ++u)
-            if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
-      } else {
-        const bool src_root = is_push_coll(a.coll) && is_root;
-        sh.srcs[ns++] = src_root ? a.send[w] : a.recv[w];
-        // the root's own copy (Gather: only the gather root holds a recv)
-        if (src_root && a.send[w] != a.recv[w] && (a.coll != kGather || w == a.bcast_root))
-          sh.dsts[nd++] = a.recv[w];
-        for (int u = 0; u < a.nranks; ++u)
-          if ((t.children >> u) & 1u) sh.dsts[nd++] = a.recv[u];
       }
-      sh.nsrc = ns;
-      sh.ndst = nd;
-      sh.abort = ok ? 0 : 1;
-      if (ws) {  // (re)initialise the ring's barriers: every segment starts drained
-        const uint32_t ncw = t.role == kRoleReduce ? (blockDim.x >> 5) - 2 : 1;
-        for (int k = 0; k < kMaxStages; ++k) {
-          mbar_init(&sh.full[k], 1);
-          mbar_init(&sh.empty[k], ncw);
+      const uint32_t below = (1u << u) - 1u;
+      const uint32_t sm = __ballot_sync(0xffffffffu, is_src), dm = __ballot_sync(0xffffffffu, is_dst);
+      if (is_src) sh.srcs[__popc(sm & below)] = from_send ? su : ru;
+      if (is_dst) sh.dsts[__popc(dm & below)] = ru;
+      if (u == 0) {
+        sh.nsrc = __popc(sm);
+        sh.ndst = __popc(dm);
+        sh.abort = entry_ok ? 0 : 1;
+        if (ws) {  // (re)initialise the ring's barriers: every segment starts drained
+          const uint32_t ncw = t.role == kRoleReduce ? (blockDim.x >> 5) - 2 : 1;
+          for (int k = 0; k < kMaxStages; ++k) {
+            mbar_init(&sh.full[k], 1);
+            mbar_init(&sh.empty[k], ncw);
+          }
+          for (int k = 0; k < kOutBufs; ++k) {
+            mbar_init(&sh.ofull[k], ncw);
+            mbar_init(&sh.oempty[k], 1);
+          }
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int k = 0; k < kOutBufs; ++k) {
-          mbar_init(&sh.ofull[k], ncw);
-          mbar_init(&sh.oempty[k], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       }
     }
     __syncthreads();
@@ -871,7 +881,10 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
     if (prev + 1 == gridDim.x) {
       a.ctrl[1] = 0;
       for (int k = 0; k < a.nctr; ++k) reinterpret_cast<unsigned int*>(a.ctrl + 2)[k] = 0u;
-      atomicExch(reinterpret_cast<unsigned long long*>(a.ctrl), (unsigned long long)ctl.epoch);
+      if (no_flags)  // = ctrl[0] + 1, the epoch this launch would have read
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.ctrl), 1ull);
+      else
+        atomicExch(reinterpret_cast<unsigned long long*>(a.ctrl), (unsigned long long)ctl.epoch);
     }
     trace(a, 7);
   }

@@ -72,6 +72,7 @@ struct Sized {
   DevTree* d_trees = nullptr;
   std::vector<DevTree> htrees;  // host copy (kernel parameters)
   bool merged_all = false;      // every CTA runs tasks[0] with its own index
+  int64_t mchunk = 0, mbytes = 0;  // merged: byte-range chunks over the whole buffer
   int ctas = 0;
   int chunks = 0;
   int nctr = 0;  // dynamic chunk counters used by the launch
@@ -383,8 +384,17 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
       if (size_plan(plan, count, esize, cfg, std::max(1, B / k), &ri, &err) != BLINK_SUCCESS)
         return fail(comm, BLINK_ERR_INTERNAL, err);
       s->ranges = ri;
-      int total = 0;
-      for (auto& r : ri) total += r.nchunks;
+      // Every tree here is a star over all ranks with the same operand order
+      // (ascending ranks), so a byte's result does not depend on which tree
+      // holds it: the merged channel cuts the whole buffer into chunks of the
+      // trees' (largest) chunk size -- the chunk-to-bytes map is arithmetic.
+      int64_t cb = 0;
+      for (auto& r : ri) cb = std::max<int64_t>(cb, r.chunk * int64_t(esize));
+      cb = std::max<int64_t>(cb, kGrain);
+      const int64_t S = int64_t(count) * esize;
+      const int total = int((S + cb - 1) / cb);
+      s->mchunk = cb;
+      s->mbytes = S;
       const int ctas = std::max(1, std::min(B, total));
       s->tasks.assign(ctas, DevTask{});
       for (int j = 0; j < ctas; ++j) {
@@ -706,6 +716,8 @@ void fill_param_tables(const Sized& s, LaunchArgs* a) {
     a->tree_end[i] = acc;
   }
   a->merged_all = s.merged_all ? 1 : 0;
+  a->mchunk = s.mchunk;
+  a->mbytes = s.mbytes;
   if (s.merged_all) a->mtask = s.tasks[0];
 }
 
