@@ -1099,11 +1099,19 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
         return e ? std::max<int64_t>(16, atoll(e)) : int64_t(16 << 10);
       }();
       // multi-hop trees signal every chunk (flags + a store drain): keep
-      // their chunks larger (BLINK_MIN_CHUNK_DEEP)
-      static const int64_t min_chunk_deep = [] {
+      // their chunks larger, but a small tree needs enough chunks to
+      // pipeline over its hops ((c+h-1)/c): the floor grows with
+      // the tree's range, bytes/16 (Broadcast) or bytes/8 (AllReduce: twice
+      // the signals per chunk) clamped to [16 KiB, 64 KiB] (A/B in
+      // profiles/README.md; BLINK_MIN_CHUNK_DEEP fixes it)
+      static const int64_t min_chunk_deep_env = [] {
         const char* e = getenv("BLINK_MIN_CHUNK_DEEP");
-        return e ? std::max<int64_t>(16, atoll(e)) : int64_t(64 << 10);
+        return e ? std::max<int64_t>(16, atoll(e)) : int64_t(0);
       }();
+      const int64_t min_chunk_deep =
+          min_chunk_deep_env ? min_chunk_deep_env
+                             : std::min<int64_t>(64 << 10, std::max<int64_t>(16 << 10,
+                                                                             bytes / (p.coll == kBroadcast ? 16 : 8)));
       cb = std::max<int64_t>(cb, p.trees[i].depth >= 2 ? std::max(min_chunk, min_chunk_deep) : min_chunk);
       cb = std::min<int64_t>(cb, 4 << 20);
     }

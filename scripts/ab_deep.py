@@ -2,6 +2,7 @@
 """Device time (graph replay) of the multi-hop configs at mid/large sizes."""
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.environ.get("AB_ROOT", os.getcwd()))
 import paper_1910_04940_b200 as B
 from oracle import graphs as OG
 
@@ -16,13 +17,14 @@ def run(comms, coll, S, root=0):
     for _ in range(3): fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g): fn()
+    with torch.cuda.graph(g):
+        for _ in range(10): fn()
     g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(10): g.replay()
     e1.record(); torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / 10 * 1e3
+    return e0.elapsed_time(e1) / 100 * 1e3
 
 g = OG.dgx1v()
 tri, _ = OG.induced(OG.dgx1p(), [0, 1, 3])
@@ -34,6 +36,6 @@ cases = [("c1-bc", B.init_all([0]*3, graph=B.Graph.from_pairs(3, tri[1])), "bc")
 cases[2] = ("c2-ar", cases[1][1], "ar")
 line = []
 for name, comms, coll in cases:
-    for S in (4 << 20, 16 << 20, 64 << 20, 256 << 20):
+    for S in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20):
         line.append(f"{name}/{S>>20}M:{run(comms, coll, S):.0f}")
 print(os.environ.get("BLINK_MIN_CHUNK_DEEP", "default"), " ".join(line), flush=True)
