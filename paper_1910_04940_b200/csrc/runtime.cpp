@@ -316,10 +316,19 @@ bool alloc_channels(const Plan& plan, const std::vector<std::vector<uint32_t>>& 
   double tot = 0;
   for (auto& c : chans) tot += c.work;
   int used = 0;
-  for (auto& c : chans) {
-    c.ctas = std::max(1, int(std::floor(avail * c.work / tot)));
+  std::vector<std::pair<double, int>> rem;  // (fractional share, channel)
+  for (size_t j = 0; j < chans.size(); ++j) {
+    Channel& c = chans[j];
+    const double share = avail * c.work / tot;
+    c.ctas = std::max(1, int(std::floor(share)));
+    rem.push_back({share - std::floor(share), int(j)});
     used += c.ctas;
   }
+  // largest remainders get the CTAs the floors left over (every SM works);
+  // ties by channel order, so every launch group computes the same split
+  std::stable_sort(rem.begin(), rem.end(),
+                   [](const std::pair<double, int>& a, const std::pair<double, int>& b) { return a.first > b.first; });
+  for (size_t j = 0; used < avail && j < rem.size(); ++j, ++used) ++chans[rem[j].second].ctas;
   while (used > avail) {  // trim the largest
     auto it = std::max_element(chans.begin(), chans.end(),
                                [](const Channel& a, const Channel& b) { return a.ctas < b.ctas; });
