@@ -196,9 +196,9 @@ struct LLArgs {
 };
 
 // exec.cu
-cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative);
+cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative, bool pdl);
 cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,
-                        bool cooperative);
+                        bool cooperative, bool pdl);
 constexpr int kMaxSmemBytes = 224 * 1024;  // + static smem <= 227 KB opt-in
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream);
 int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll, int smem_bytes);

@@ -1,7 +1,8 @@
 // Device executor for tree-packed collectives on sm_100a (Broadcast,
 // AllReduce; ReduceScatter / AllGather / Gather on one-hop trees).
 //
-// One persistent, cooperative launch per device per collective.  Every CTA
+// One persistent launch per device per collective (PDL-chained to the
+// previous kernel in the stream).  Every CTA
 // runs one slice of a "channel" = (rank v, tree i, role).  A channel's CTAs
 // take its chunks in increasing order -- from a per-channel atomic counter
 // (dynamic balancing) or a static stride -- so chunks of all trees and all
@@ -740,6 +741,11 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
   // launch) reads and writes no flag: it needs no epoch, and its last CTA just
   // advances the counter -- no dependent load before the first TMA load.
   const bool no_flags = a.merged_all && !a.exit_wait;
+  // Programmatic dependent launch: everything above reads only kernel
+  // parameters and the host-written task table; every access to memory the
+  // previous kernel in the stream may touch (epoch, counters, flags, user
+  // buffers, trace) comes after this wait.  A no-op without the attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
     if (a.trace)
       for (int k = 1; k < kTraceSlots; ++k) a.trace[size_t(blockIdx.x) * kTraceSlots + k] = 0;
@@ -1037,6 +1043,7 @@ template <int DT, int OP>
 __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
   const int v = a.ranks[blockIdx.x / a.ctas_per_rank];
   const int cta = blockIdx.x % a.ctas_per_rank;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: see exec_kernel
   if (threadIdx.x == 0) ll_trace(a, 0);
   const int m = a.nranks;
   const int64_t T = int64_t(a.ctas_per_rank) * blockDim.x;
@@ -1182,6 +1189,27 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
 
 typedef void (*ExecFn)(const LaunchArgs);
 
+// Launch attributes: cooperative (co-residency checked by the driver) and/or
+// programmatic stream serialization (PDL: the launch overlaps the previous
+// kernel's tail; the kernels wait with griddepcontrol.wait before touching
+// memory).  Eager launches gain from PDL only without the cooperative
+// attribute (scripts/pdl_probe.cu), so the runtime sets one or the other.
+void set_launch_attrs(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr, bool cooperative, bool pdl) {
+  int n = 0;
+  if (cooperative) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+}
+
 template <int DT, bool VEC>
 ExecFn pick_op(int op) {
   switch (op) {
@@ -1207,7 +1235,7 @@ ExecFn pick(int coll, int dtype, int op, bool vec) {
 }  // namespace
 
 cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,
-                        bool cooperative) {
+                        bool cooperative, bool pdl) {
   ExecFn fn = pick(a.coll, a.dtype, a.op, vec);
   if (!fn) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -1223,11 +1251,8 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
     done = true;
   }
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = cooperative ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute attr[2];
+  set_launch_attrs(cfg, attr, cooperative, pdl);
   return cudaLaunchKernelEx(&cfg, fn, a);
 }
 
@@ -1243,7 +1268,7 @@ LLFn ll_pick_op(int op) {
   return nullptr;
 }
 
-cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative) {
+cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative, bool pdl) {
   LLFn fn = nullptr;
   if (a.coll == kBroadcast) {
     fn = ll_kernel<BLINK_FLOAT32, BLINK_SUM>;  // a byte copy
@@ -1259,11 +1284,8 @@ cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative)
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kLLThreads);
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = cooperative ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute attr[2];
+  set_launch_attrs(cfg, attr, cooperative, pdl);
   return cudaLaunchKernelEx(&cfg, fn, a);
 }
 

@@ -633,12 +633,25 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
 
 // Data path: BLINK_TMA=0 register/LSU loads and stores, 1 TMA loads + LSU
 // stores, 2 TMA loads + TMA bulk stores (default).
-// BLINK_COOP=0 launches without the cooperative attribute (co-residency then
-// relies on grid <= occupancy x SMs and an otherwise idle device).
+// Launch attributes.  Default: programmatic dependent launch (PDL) -- a
+// call's kernel is launched while the previous kernel in the stream drains,
+// and waits (griddepcontrol.wait) before touching memory: 1.2-2.6 us less per
+// back-to-back eager call (scripts/pdl_probe.cu).  PDL gains nothing on a
+// cooperative launch, so co-residency then rests on the grid sizing (grid <=
+// occupancy x SMs, co_resident_budget) as it does for per-rank launches and
+// NCCL's kernels.  BLINK_PDL=0 launches cooperatively instead (the driver
+// checks co-residency); BLINK_COOP=0 with BLINK_PDL=0 sets neither.
+bool use_pdl() {
+  static bool v = [] {
+    const char* e = getenv("BLINK_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 bool use_coop() {
   static bool v = [] {
     const char* e = getenv("BLINK_COOP");
-    return !(e && e[0] == '0');
+    return !use_pdl() && !(e && e[0] == '0');
   }();
   return v;
 }
@@ -901,7 +914,7 @@ blink_result_t clique_launch(Clique* q) {
         evs.push_back(e);
       }
       const int grid = a.nlocal * a.ctas_per_rank;
-      cudaError_t le = launch_ll(a, grid, ls, use_coop() && !q->per_rank);
+      cudaError_t le = launch_ll(a, grid, ls, use_coop() && !q->per_rank, use_pdl());
       if (le != cudaSuccess)
         return fail(cd, BLINK_ERR_CUDA, std::string("LL launch: ") + cudaGetErrorString(le));
       if (q->per_rank) CUDA_TRY(cd, cudaEventRecord(q->rjoin[lead], ls));
@@ -1025,7 +1038,7 @@ blink_result_t clique_launch(Clique* q) {
     // per-rank launches rely on every group's grid fitting the device at once
     // (each takes 1/m of the co-resident CTAs); the cooperative attribute
     // cannot promise co-residency across launches
-    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, use_coop() && !q->per_rank);
+    cudaError_t le = launch_exec(a, s.ctas, cd->cfg.threads, vec, ls, use_coop() && !q->per_rank, use_pdl());
     if (le != cudaSuccess)
       return fail(cd, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
     if (q->per_rank) CUDA_TRY(cd, cudaEventRecord(q->rjoin[lead], ls));
@@ -1206,7 +1219,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     if (coll == kReduceScatter && a.recv[u]) a.recv[u] -= size_t(u) * bytes;
     if ((coll == kAllGather || coll == kGather) && a.send[u]) a.send[u] -= size_t(u) * bytes;
   }
-  cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, use_coop());
+  cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, use_coop(), use_pdl());
   if (le != cudaSuccess)
     return fail(comm, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
   comm->stats.launches++;
@@ -1298,7 +1311,7 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
       a.recv[comm->rank] = static_cast<char*>(recvbuf);
       for (int u = 0; u < comm->nranks; ++u)
         a.ll[u] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(comm->peer_flags[u]) + kFlagBytes);
-      cudaError_t le = launch_ll(a, a.ctas_per_rank, stream, false);
+      cudaError_t le = launch_ll(a, a.ctas_per_rank, stream, false, use_pdl());
       if (le != cudaSuccess)
         return fail(comm, BLINK_ERR_CUDA, std::string("LL launch: ") + cudaGetErrorString(le));
       comm->stats.launches++;
