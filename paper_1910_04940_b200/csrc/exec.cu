@@ -492,7 +492,12 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
   const int ncons = reduce ? (blockDim.x >> 5) - 2 : 0;
   const int nsrc = sh.nsrc, ndst = sh.ndst;
   const int ns = reduce ? nsrc : 1;
-  int tile = ns == 1 ? 32768 : (ns <= 8 ? 8192 : 4096);
+  // tile per source: the stage ring holds <= kMaxStages x ns tiles; two or
+  // three sources (m = 2, 3 roots) take 16 KB tiles -- half as many stage
+  // and output hand-offs per byte (A/B, virtual ranks, 64 MiB: m = 2 f32
+  // 0.86 -> 0.89, bf16 0.64 -> 0.76; m = 3 bf16 0.83 -> 0.92 of the HBM
+  // peak; neutral at m = 4; 7-20% slower at m = 8)
+  int tile = ns == 1 ? 32768 : (ns <= 3 ? 16384 : (ns <= 8 ? 8192 : 4096));
   if (a.tile_bytes > 0) tile = ns == 1 ? 4 * a.tile_bytes : a.tile_bytes;
   const int avail = a.smem_bytes - (reduce ? kOutBufs * tile : 0);
   const int stages = max(1, min(kMaxStages, avail / (tile * ns)));

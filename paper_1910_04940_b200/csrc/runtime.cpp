@@ -601,6 +601,13 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   }
   s->ctas = int(s->tasks.size());
   s->plan = &plan;
+  if (getenv("BLINK_DEBUG_TASKS")) {  // CTA -> channel map (scripts/trace_tree.py)
+    for (size_t j = 0; j < s->tasks.size(); ++j) {
+      const DevTask& t = s->tasks[j];
+      fprintf(stderr, "[blink] cta %zu rank %d tree %d role %d parent %d children %x chunks %d\n", j,
+              int(t.rank), int(t.tree), int(t.role), int(t.parent), t.children, t.c1);
+    }
+  }
   return BLINK_SUCCESS;
 }
 

@@ -31,3 +31,6 @@ firsts = sorted(((t[3] - t0) / 1e3, i) for i, t in enumerate(tr) if t[3])
 print("first-load: min/med/max", firsts[0][0], statistics.median(x for x, _ in firsts), firsts[-1][0])
 print("stores-done: min/med/max", ends[0][0], statistics.median(x for x, _ in ends), ends[-1][0])
 print("kernel end max", max((t[7] - t0) / 1e3 for t in tr))
+if os.environ.get("PER_CTA"):
+    for i, t in enumerate(tr):
+        print(f"cta {i}: " + " ".join(f"{(x - t0) / 1e3:.1f}" if x else "-" for x in t[:8]))
