@@ -118,7 +118,15 @@ typedef struct {
  *                  Default 256 KiB (64 KiB when one launch holds every rank,
  *                  which has no handshake to save).
  *                  Costs 64 * m * (ll_max_bytes / (8 m) + 8) bytes of device
- *                  memory per rank.  Must agree across ranks */
+ *                  memory per rank.  Must agree across ranks
+ *   shallow_max_bytes  link graphs (not switches, not multi-server): Broadcast
+ *                  and AllReduce calls of at most this many bytes per rank run
+ *                  on ONE minimum-depth (BFS) tree -- from the root, or from
+ *                  the graph's centre for AllReduce -- instead of the packed
+ *                  trees: small calls are latency-bound and every hop waits
+ *                  for a whole chunk (depth-1 trees on the
+ *                  switch).  Default 256 KiB; 0 = always packed.
+ *                  Must agree across ranks */
 typedef struct {
   double mwu_eps;
   double ilp_gap;
@@ -131,6 +139,7 @@ typedef struct {
   int autotune;
   int launch_per_rank;
   size_t ll_max_bytes;
+  size_t shallow_max_bytes;
 } blink_config_t;
 
 /* MIAD controller: "initialize the chunk size with a small value

@@ -465,6 +465,52 @@ def plan_switch_broadcast(m, r, onehop=False):
     return dict(trees=trees, rate=Fraction(m - 1))
 
 
+def plan_shallow(g, allreduce, r=0):
+    """Latency plan for small calls on link graphs (R#27): ONE minimum-depth
+    tree.  The paper: a chunk waits for the whole chunk at every hop, so depth
+    adds latency, and on the switch it uses depth-1 trees
+    (P:440-444).  Level sets L_0 = {root}, L_{k+1} = vertices not yet reached
+    with a link from L_k (Broadcast: directed u -> v; AllReduce: both
+    directions present); parent(v) = the lowest-rank u in the previous level
+    with a link u -> v.  AllReduce roots the tree at the graph centre: the
+    vertex whose level sets end soonest (minimum eccentricity), ties -> the
+    lowest rank (R#9's rule)."""
+    n, cap = g
+
+    def link(u, v):
+        return cap.get((u, v), 0) > 0 and (not allreduce or cap.get((v, u), 0) > 0)
+
+    def levels(src):
+        seen, lev, out = {src}, [src], [[src]]
+        while True:
+            nxt = sorted({v for u in lev for v in range(n) if v not in seen and link(u, v)})
+            if not nxt:
+                return out, seen
+            seen |= set(nxt)
+            out.append(nxt)
+            lev = nxt
+
+    if allreduce:
+        best = None
+        for s in range(n):
+            lv, seen = levels(s)
+            if len(seen) == n and (best is None or len(lv) < best[0]):
+                best = (len(lv), s)
+        if best is None:
+            raise ValueError("graph not connected over bidirectional links")
+        r = best[1]
+    lv, seen = levels(r)
+    if len(seen) != n:
+        raise ValueError("rank unreachable from the root")
+    parent = [-1] * n
+    for k in range(1, len(lv)):
+        for v in lv[k]:
+            parent[v] = min(u for u in lv[k - 1] if link(u, v))
+    edges = [(min(u, v), max(u, v)) if allreduce else (u, v) for v, u in enumerate(parent) if u >= 0]
+    tree = dict(parent=tuple(parent), root=r, weight=Fraction(1), edges=edges, depth=len(lv) - 1)
+    return dict(trees=[tree], rate=Fraction(1))
+
+
 def split_bytes(S, weights):
     """Weight-proportional split (R#11): G = floor(S/16) grains,
     b_i = floor(G * sum_{j<i} w_j / sum w); tree i gets bytes

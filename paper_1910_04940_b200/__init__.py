@@ -48,7 +48,8 @@ class _Config(ctypes.Structure):
                 ("chunk_bytes", ctypes.c_size_t), ("ctas", ctypes.c_int), ("threads", ctypes.c_int),
                 ("timeout_s", ctypes.c_double), ("onehop_bcast_max_bytes", ctypes.c_size_t),
                 ("staging_bytes", ctypes.c_size_t), ("autotune", ctypes.c_int),
-                ("launch_per_rank", ctypes.c_int), ("ll_max_bytes", ctypes.c_size_t)]
+                ("launch_per_rank", ctypes.c_int), ("ll_max_bytes", ctypes.c_size_t),
+                ("shallow_max_bytes", ctypes.c_size_t)]
 
 
 class Miad(ctypes.Structure):

@@ -218,6 +218,9 @@ struct Graph {
 blink_result_t build_graph(const blink_graph_t* g, int nranks, Graph* out, std::string* err);
 blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_t& cfg, Plan* out,
                          std::string* err);
+// R#27 latency plan: one minimum-depth (BFS) tree for small calls on link graphs.
+bool use_shallow_plan(const Graph& g, int coll, size_t bytes, const blink_config_t& cfg);
+blink_result_t make_shallow_plan(const Graph& g, int coll, int root, Plan* out, std::string* err);
 // Split (R#11) + chunking (a8).  ctas_for_tree: CTA count expected per tree channel.
 blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
                          int ctas_hint, std::vector<TreeRange>* out, std::string* err);

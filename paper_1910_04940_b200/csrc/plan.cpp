@@ -1043,6 +1043,99 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
   return BLINK_SUCCESS;
 }
 
+// ============================================================== latency plan
+// R#27: calls at or below cfg.shallow_max_bytes on a link graph run on ONE
+// minimum-depth tree.  Small calls are latency-bound: a chunk waits for the
+// whole chunk at every hop, so time grows with depth, and
+// the paper's answer on the switch is the depth-1 tree.  The
+// tree: BFS distances d(v) from the root over links of positive capacity
+// (Broadcast: directed u -> v; AllReduce: both directions present), and
+// parent(v) = the lowest-rank u with d(u) = d(v) - 1 and a link u -> v.
+// AllReduce roots it at the graph centre (minimum BFS eccentricity, ties ->
+// lowest rank, as R#9 does per tree).
+namespace {
+std::vector<int> bfs_dist(const Graph& g, int src, bool undirected) {
+  std::vector<int> d(g.n, -1);
+  std::vector<int> q{src};
+  d[src] = 0;
+  for (size_t h = 0; h < q.size(); ++h) {
+    const int u = q[h];
+    for (int v = 0; v < g.n; ++v) {
+      const bool link = g.cap[u][v] > 0 && (!undirected || g.cap[v][u] > 0);
+      if (link && d[v] < 0) {
+        d[v] = d[u] + 1;
+        q.push_back(v);
+      }
+    }
+  }
+  return d;
+}
+}  // namespace
+
+bool use_shallow_plan(const Graph& g, int coll, size_t bytes, const blink_config_t& cfg) {
+  // bytes == 0: plan introspection (blink_get_plan / blink_plan_json with
+  // count 0) shows the size-independent packed plan
+  return !g.switch_model && !g.multi_server && g.n > 2 && bytes > 0 && bytes <= cfg.shallow_max_bytes &&
+         (coll == kBroadcast || coll == kAllReduce);
+}
+
+blink_result_t make_shallow_plan(const Graph& g, int coll, int root, Plan* out, std::string* err) {
+  const int n = g.n;
+  const bool und = coll == kAllReduce;
+  *out = Plan();
+  out->coll = coll;
+  out->root = coll == kBroadcast ? root : -1;
+  out->nranks = n;
+  if (coll == kBroadcast && (root < 0 || root >= n)) {
+    *err = "root " + std::to_string(root) + " out of range [0," + std::to_string(n) + ")";
+    return BLINK_ERR_INVALID_ARGUMENT;
+  }
+  if (und)  // every link needs its reverse, as for the packed plan
+    for (int u = 0; u < n; ++u)
+      for (int v = u + 1; v < n; ++v)
+        if ((g.cap[u][v] > 0) != (g.cap[v][u] > 0)) {
+          const bool f = g.cap[u][v] > 0;
+          *err = "link " + std::to_string(f ? u : v) + "->" + std::to_string(f ? v : u) +
+                 " has no reverse edge (AllReduce needs bidirectional links, P:397)";
+          return BLINK_ERR_TOPOLOGY;
+        }
+  int r = root;
+  if (und) {  // centre: minimum eccentricity, ties -> lowest rank
+    int best = 1 << 30;
+    for (int s = 0; s < n; ++s) {
+      const std::vector<int> d = bfs_dist(g, s, true);
+      int ecc = 0;
+      for (int v = 0; v < n; ++v) ecc = d[v] < 0 ? (1 << 29) : std::max(ecc, d[v]);
+      if (ecc < best) {
+        best = ecc;
+        r = s;
+      }
+    }
+  }
+  const std::vector<int> d = bfs_dist(g, r, und);
+  Tree t;
+  t.root = r;
+  t.parent.assign(n, -1);
+  for (int v = 0; v < n; ++v) {
+    if (d[v] < 0) {
+      *err = "rank " + std::to_string(v) + " is not reachable from rank " + std::to_string(r) +
+             (und ? " over bidirectional links" : "");
+      return BLINK_ERR_TOPOLOGY;
+    }
+    if (v == r) continue;
+    for (int u = 0; u < n; ++u)
+      if (d[u] == d[v] - 1 && g.cap[u][v] > 0 && (!und || g.cap[v][u] > 0)) {
+        t.parent[v] = u;
+        break;
+      }
+    t.depth = std::max(t.depth, d[v]);
+  }
+  out->trees.push_back(t);
+  out->rate_num = 1;
+  out->rate_den = 1;
+  return BLINK_SUCCESS;
+}
+
 // ============================================================== split + chunks
 blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
                          int ctas_hint, std::vector<TreeRange>* out, std::string* err) {

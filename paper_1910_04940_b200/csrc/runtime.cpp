@@ -193,6 +193,7 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
   if (const char* e = getenv("BLINK_MIAD")) r.autotune = atoi(e);
   if (const char* e = getenv("BLINK_PER_RANK")) r.launch_per_rank = atoi(e);
   if (const char* e = getenv("BLINK_LL_MAX")) r.ll_max_bytes = size_t(atoll(e));
+  if (const char* e = getenv("BLINK_SHALLOW_MAX")) r.shallow_max_bytes = size_t(atoll(e));
   if (r.ll_max_bytes > (size_t(16) << 20)) r.ll_max_bytes = size_t(16) << 20;
   r.ll_max_bytes = r.ll_max_bytes / kGrain * kGrain;
   if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
@@ -207,8 +208,9 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
   return r;
 }
 
-// Plan cache: key (coll, root) with root = -1 for AllReduce, and root + 1000
-// for the one-hop Broadcast star variant on switches.
+// Plan cache: key (coll, root) with root = -1 for AllReduce, root + 1000
+// for the one-hop Broadcast star variant on switches, root + 2000 for the
+// single minimum-depth tree of small calls on link graphs (R#27).
 blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, const Plan** out) {
   int key_root = (coll == kBroadcast || coll == kGather) ? root : -1;
   if (is_block_coll(coll) && !comm->graph.switch_model)
@@ -217,6 +219,8 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
   bool star = coll == kBroadcast && comm->graph.switch_model && comm->nranks > 2 &&
               bytes <= comm->cfg.onehop_bcast_max_bytes;
   if (star) key_root += 1000;
+  const bool shallow = !is_block_coll(coll) && use_shallow_plan(comm->graph, coll, bytes, comm->cfg);
+  if (shallow) key_root += 2000;
   auto k = std::make_pair(coll, key_root);
   auto it = comm->plans.find(k);
   if (it != comm->plans.end()) {
@@ -239,6 +243,8 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
     p->trees.push_back(t);
     p->rate_num = 1;
     r = BLINK_SUCCESS;
+  } else if (shallow) {
+    r = make_shallow_plan(comm->graph, coll, root, p.get(), &err);
   } else {
     r = make_plan(comm->graph, is_block_coll(coll) ? kAllReduce : coll, root, comm->cfg, p.get(),
                   &err);
@@ -1375,6 +1381,7 @@ void blink_config_default(blink_config_t* c) {
   c->autotune = 0;
   c->launch_per_rank = 0;
   c->ll_max_bytes = 256 << 10;
+  c->shallow_max_bytes = 256 << 10;
 }
 
 void blink_miad_init(blink_miad_t* st, size_t init, size_t min_chunk, size_t max_chunk) {
@@ -1457,7 +1464,11 @@ blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const bli
   blink_result_t r = build_graph(graph, nranks, &g, &err);
   if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
   Plan p;
-  r = make_plan(g, is_allreduce ? kAllReduce : kBroadcast, root, cfg, &p, &err);
+  const int coll = is_allreduce ? kAllReduce : kBroadcast;
+  if (use_shallow_plan(g, coll, count * size_t(es), cfg))
+    r = make_shallow_plan(g, coll, root, &p, &err);
+  else
+    r = make_plan(g, coll, root, cfg, &p, &err);
   if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
   std::vector<TreeRange> ranges;
   int hint = std::max(1, (cfg.ctas > 0 ? cfg.ctas : 296) / int(p.trees.size()));

@@ -230,14 +230,15 @@ def test_random_graph_plans_satisfy_the_oracle_invariants(B, seed):
             break
     G = B.Graph.from_pairs(n, cap)
     root = rng.randrange(n)
-    pb = B.plan_json(n, False, root, 123457, "f32", graph=G)
+    packed = B.config(shallow_max_bytes=0)  # the packed plan at every size (not R#27's small-call tree)
+    pb = B.plan_json(n, False, root, 123457, "f32", graph=G, cfg=packed)
     _check_plan(pb, (n, cap), False)
     for t in pb["trees"]:
         par = t["parent"]
         assert par[root] == -1 and all((par[v], v) in cap for v in range(n) if v != root)
     unit = min(cap.values())
     assert Fraction(*pb["rate"]) * unit <= bounds.edmonds_rate((n, cap), root) + Fraction(1, 10**9)
-    pa = B.plan_json(n, True, 0, 123457, "bf16", graph=G)
+    pa = B.plan_json(n, True, 0, 123457, "bf16", graph=G, cfg=packed)
     _check_plan(pa, (n, cap), True)
     pairs = graphs.undirected_pairs((n, cap))
     assert float(Fraction(*pa["rate"]) * unit) <= bounds.nash_williams_rate(pairs, n) + 1e-9
@@ -279,3 +280,84 @@ def test_library_plans_move_the_bytes_of_the_message_bound(B, name):
         assert sum(b for (_, w), b in lb.items() if w == v) == (0 if v == m - 1 else S)
     pa = _oracle_plan(B.plan_json(m, True, 0, count, "f32", graph=G))
     assert sum(model.link_bytes(pa, m, S, True).values()) == 2 * (m - 1) * S
+
+
+# ------------------------------------------------------------ R#27 latency plan
+def _bfs_dist_fw(n, cap, allreduce):
+    """All-pairs hop distances by Floyd-Warshall (independent of the BFS)."""
+    INF = 10**9
+    d = [[0 if u == v else INF for v in range(n)] for u in range(n)]
+    for (u, v), c in cap.items():
+        if c > 0 and (not allreduce or cap.get((v, u), 0) > 0):
+            d[u][v] = 1
+    for k in range(n):
+        for i in range(n):
+            for j in range(n):
+                if d[i][k] + d[k][j] < d[i][j]:
+                    d[i][j] = d[i][k] + d[k][j]
+    return d
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_small_calls_take_the_oracle_shallow_tree(B, seed):
+    """Calls <= shallow_max_bytes on link graphs run on one minimum-depth tree
+    (R#27): the C++ plan equals the oracle's plan_shallow, and every vertex
+    sits at its shortest-path distance (Floyd-Warshall) from the root; the
+    AllReduce root has the minimum eccentricity.  Above the threshold the
+    packed plan returns."""
+    import random
+    from oracle import graphs, packing
+    rng = random.Random(7000 + seed)
+    n = rng.randint(3, 8)
+    while True:
+        cap = {}
+        for u in range(n):
+            for v in range(u + 1, n):
+                if rng.random() < 0.45:
+                    cap[(u, v)] = cap[(v, u)] = rng.randint(1, 3)
+        if graphs.is_connected((n, cap)):
+            break
+    G = B.Graph.from_pairs(n, cap)
+    root = rng.randrange(n)
+    for allreduce in (False, True):
+        p = B.plan_json(n, allreduce, root, 1000, "f32", graph=G)
+        want = packing.plan_shallow((n, cap), allreduce, root)["trees"][0]
+        assert len(p["trees"]) == 1
+        t = p["trees"][0]
+        assert tuple(t["parent"]) == want["parent"] and t["root"] == want["root"]
+        d = _bfs_dist_fw(n, cap, allreduce)
+        r = t["root"]
+        if allreduce:
+            assert max(d[r]) == min(max(row) for row in d)
+        else:
+            assert r == root
+        assert t["depth"] == max(d[r][v] for v in range(n))
+        for v in range(n):  # parent one level up, over a real link
+            u = t["parent"][v]
+            if v == r:
+                assert u == -1
+            else:
+                assert d[r][u] + 1 == d[r][v] and cap.get((u, v), 0) > 0
+        assert t["lo"] == 0 and t["hi"] == 1000
+        # above the threshold: the packed plan (the size-independent count-0 plan)
+        big = B.plan_json(n, allreduce, root, (256 << 10) // 4 + 1, "f32", graph=G)
+        packed = B.plan_json(n, allreduce, root, 0, "f32", graph=G)
+        assert [x["parent"] for x in big["trees"]] == [x["parent"] for x in packed["trees"]]
+
+
+def test_dgx1v_small_broadcast_tree_golden(B):
+    """App. B DGX-1V, root 0: neighbours 1, 2, 3, 4 at depth 1; 5, 6, 7 hang
+    off their lowest-rank neighbour at depth 1 (1, 2, 3) -- derived by hand
+    from the link list (P:56-61 reconstruction)."""
+    from oracle import graphs, packing
+    g = graphs.dgx1v()
+    want = (-1, 0, 0, 0, 0, 1, 2, 3)
+    assert packing.plan_shallow(g, False, 0)["trees"][0]["parent"] == want
+    assert packing.plan_shallow(g, True)["trees"][0]["parent"] == want  # centre: rank 0 (all ecc 2)
+    assert packing.plan_shallow(g, False, 5)["trees"][0]["parent"] == (1, 5, 1, 1, 5, -1, 5, 5)
+    G = B.Graph.from_pairs(8, g[1])
+    assert tuple(B.plan_json(8, False, 0, 4096, "f32", graph=G)["trees"][0]["parent"]) == want
+    assert len(B.plan_json(8, False, 0, 1 << 20, "f32", graph=G)["trees"]) == 6
+    assert len(B.plan_json(8, False, 0, 0, "f32", graph=G)["trees"]) == 6  # count 0: packed plan
+    off = B.config(shallow_max_bytes=0)
+    assert len(B.plan_json(8, False, 0, 4096, "f32", graph=G, cfg=off)["trees"]) == 6

@@ -211,8 +211,43 @@ def test_config2_dgx1v_broadcast(B, root, count):
     for x in recvs:
         assert_bitwise(x.cpu().numpy(), send)
     p = comms[0].plan(False, root, count)
-    assert len(p["trees"]) == 6
-    assert comms[0].stats()["last_trees"] == 6
+    if count * 4 <= (256 << 10):  # R#27: small calls run on the one BFS tree
+        assert len(p["trees"]) == 1
+        assert tuple(p["trees"][0]["parent"]) == OP.plan_shallow(g, False, root)["trees"][0]["parent"]
+        assert comms[0].stats()["last_trees"] == 1
+    else:
+        assert len(p["trees"]) == 6
+        assert comms[0].stats()["last_trees"] == 6
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+@pytest.mark.parametrize("count", [1, 4099, 65536])
+def test_small_calls_on_link_graphs_shallow_tree(B, dtype, count):
+    """R#27: small AllReduce / Broadcast on link graphs (DGX-1V, a 6-GPU
+    fragment) run on one minimum-depth tree; fp32/bf16 AllReduce is bit-exact
+    against the oracle's OWN plan_shallow (its reduction order), Broadcast is
+    the root's bytes."""
+    g8 = OG.dgx1v()
+    frag, _ = OG.induced(g8, [0, 1, 3, 4, 5, 7])
+    for g in (g8, frag):
+        m = g[0]
+        comms = make_comms(B, m, graph=B.Graph.from_pairs(m, g[1]))
+        sends = synth.inputs(41 + m, m, count, dtype)
+        got = run_allreduce(B, comms, sends, dtype, "sum")
+        want = OC.allreduce(OP.plan_shallow(g, True), sends, dtype, "sum")
+        for x in got:
+            assert_bitwise(x, want)
+        assert comms[0].stats()["last_trees"] == 1
+        root = m - 1
+        dsend = to_dev(sends[root], dtype)
+        recvs = [sentinel(count, dtype) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.broadcast(dsend if r == root else None, recvs[r], root=root, count=count, dtype=dtype)
+        torch.cuda.synchronize()
+        for x in recvs:
+            assert_bitwise(to_host(x, dtype), sends[root])
+        for c in comms:
+            c.destroy()
 
 
 def test_config2_dgx1v_broadcast_bf16_inplace(B):
