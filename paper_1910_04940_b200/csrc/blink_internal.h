@@ -181,7 +181,7 @@ struct LLArgs {
   int root;                    // Broadcast root
   int nlocal;                  // ranks run by this launch: ranks[0 .. nlocal)
   int ctas_per_rank;
-  int pad;
+  int scope_sys;               // 1: peers on other devices / processes (.sys flags)
   int8_t ranks[kMaxRanks];
   int64_t bytes;               // S per rank
   int64_t cap;                 // lines per slice area (ll_cap_lines)

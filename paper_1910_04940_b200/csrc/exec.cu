@@ -1060,6 +1060,29 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
   const uint32_t f = uint32_t(e);
   const size_t p = size_t(e & 1u);
   uint4* const my = a.ll[v];
+  // Ranks in other launches (per-rank launches, processes): publish entry(e)
+  // -- this rank finished call e-1, so it no longer reads the LL lines of
+  // parity p^1 -- in every peer's flag words (they precede the LL area).  A
+  // Broadcast root waits for every leaf's entry(e-1) before it overwrites
+  // their parity-p lines: nothing else stops a root that only pushes from
+  // running two calls ahead of a leaf (AllReduce results depend on every
+  // rank's previous call, so its roots cannot).
+  const bool multi = a.nlocal < m;
+  auto flags_of = [&](int u) {
+    return reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(a.ll[u]) - kFlagBytes);
+  };
+  if (multi && cta == 0 && threadIdx.x < m && int(threadIdx.x) != v)
+    st_relaxed(flags_of(threadIdx.x) + entry_idx(v), e, a.scope_sys != 0);
+  __shared__ int s_root_ok;
+  if (multi && a.coll == kBroadcast && v == a.root) {
+    if (threadIdx.x < 32) {
+      const Ctl ctl{e - 1, a.timeout_ns, a.err, a.scope_sys != 0};
+      const uint32_t leaves = ((m >= 32 ? 0u : (1u << m)) - 1u) & ~(1u << v);
+      const bool ok = warp_wait(leaves, [&](int u) { return flags_of(v) + entry_idx(u); }, ctl);
+      if (threadIdx.x == 0) s_root_ok = ok;  // timeout: error word set, no pushes
+    }
+    __syncthreads();
+  }
   auto in_area = [&](uint4* base, int src) { return base + (p * m + src) * cap; };
   auto out_area = [&](uint4* base, int j) { return base + ((2 + p) * m + j) * cap; };
   bool ok = true;
@@ -1154,7 +1177,8 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
     const int r = a.root;
     const int64_t len = a.bytes, nl = (len + 7) >> 3;
     if (v == r) {
-      for (int64_t k = t0; k < nl; k += T) {
+      const int64_t kend = (multi && !s_root_ok) ? 0 : nl;
+      for (int64_t k = t0; k < kend; k += T) {
         const int valid = int(min(int64_t(8), len - 8 * k));
         const uint2 x = ld8(a.send[r] + 8 * k, valid);
         if (a.recv[r] != a.send[r]) st8(a.recv[r] + 8 * k, x, valid);

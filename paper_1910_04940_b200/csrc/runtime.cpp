@@ -905,6 +905,7 @@ blink_result_t clique_launch(Clique* q) {
         if (g2.device == grp.device) share += __builtin_popcountll(g2.mask);
       fill_ll_args(cd, q->coll, q->dtype, q->op, q->root, bytes, ll_lo, q->ctrl[grp.key],
                    q->err_dev[grp.key], share, &a);
+      a.scope_sys = q->devices.size() > 1 ? 1 : 0;
       for (int v = 0; v < n; ++v) {
         a.send[v] = static_cast<const char*>(q->pending[v].send);
         a.recv[v] = static_cast<char*>(q->pending[v].recv);
@@ -1320,6 +1321,7 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
       LLArgs a{};
       a.ranks[a.nlocal++] = int8_t(comm->rank);
       fill_ll_args(comm, coll, dtype, op, root, bytes, lo, comm->ctrl, comm->err_dev, 1, &a);
+      a.scope_sys = 1;
       a.send[comm->rank] = static_cast<const char*>(sendbuf);
       a.recv[comm->rank] = static_cast<char*>(recvbuf);
       for (int u = 0; u < comm->nranks; ++u)

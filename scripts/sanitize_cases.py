@@ -81,6 +81,17 @@ def main():
     torch.cuda.synchronize()
     for y in iy:
         check(y, OC.naive_reduce(isends, "i32", "sum"), "dgx1v allreduce")
+    # small calls: the single minimum-depth tree (R#27)
+    ns = 4099
+    for r, c in enumerate(comms):
+        c.allreduce(ix[r][:ns], iy[r][:ns])
+    for r, c in enumerate(comms):
+        c.broadcast(dsrc[:ns] if r == 3 else None, out[r][:ns], root=3)
+    torch.cuda.synchronize()
+    for r in range(8):
+        check(iy[r][:ns], OC.naive_reduce([s[:ns] for s in isends], "i32", "sum"), "dgx1v shallow allreduce")
+        check(out[r][:ns], src[:ns], "dgx1v shallow broadcast")
+    assert comms[0].stats()["last_trees"] == 1
     for c in comms:
         c.destroy()
     # LL protocol (batched and per-rank launches) and the per-rank tree path

@@ -153,3 +153,32 @@ def test_ll_off_uses_the_tree_executor(B):
     assert comms[0].stats()["last_chunks"] > 0
     for c in comms:
         c.destroy()
+
+
+def test_ll_broadcast_root_runs_ahead(B):
+    """Per-rank launches, every rank on its own stream; one leaf's stream is
+    held back by a long kernel while the root issues several LL Broadcasts.
+    The root must not overwrite the leaf's LL lines of a call the leaf has
+    not read yet (parity areas alternate, so a root two calls ahead would
+    reuse them): it waits for the leaf's entry of the previous call.  (On
+    one GPU the per-rank launches of successive calls happen to serialize
+    behind the held-back leaf, so this mostly checks that the guard is
+    transparent; across processes / GPUs nothing else orders them.)"""
+    m, count, calls = 4, 1001, 5
+    comms = comms_for(B, m, 1, timeout_s=10.0)
+    streams = [torch.cuda.Stream() for _ in range(m)]
+    srcs = [synth.rank_input(300 + k, 0, count, "f32") for k in range(calls)]
+    dsrc = [to_dev(s, "f32") for s in srcs]
+    outs = [[sentinel(count, "f32") for _ in range(m)] for _ in range(calls)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(streams[3]):
+        torch.cuda._sleep(200_000_000)  # ~0.1 s on the held-back leaf's stream
+    for k in range(calls):
+        for r, c in enumerate(comms):
+            c.broadcast(dsrc[k] if r == 0 else None, outs[k][r], root=0, stream=streams[r])
+    torch.cuda.synchronize()
+    for k in range(calls):
+        for r in range(m):
+            assert_bitwise(to_host(outs[k][r], "f32"), srcs[k])
+    for c in comms:
+        c.destroy()
