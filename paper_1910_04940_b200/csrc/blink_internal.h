@@ -182,6 +182,9 @@ struct LLArgs {
   int nlocal;                  // ranks run by this launch: ranks[0 .. nlocal)
   int ctas_per_rank;
   int scope_sys;               // 1: peers on other devices / processes (.sys flags)
+  int tree;                    // 1: one multi-level tree (R#27 shallow plan), parent[] below
+  int tree_root;               // its root (AllReduce: the graph centre)
+  int8_t parent[kMaxRanks];    // tree: parent rank, -1 at the root
   int8_t ranks[kMaxRanks];
   int64_t bytes;               // S per rank
   int64_t cap;                 // lines per slice area (ll_cap_lines)

@@ -1086,7 +1086,85 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
   auto in_area = [&](uint4* base, int src) { return base + (p * m + src) * cap; };
   auto out_area = [&](uint4* base, int j) { return base + ((2 + p) * m + j) * cap; };
   bool ok = true;
-  if (a.coll == kAllReduce) {
+  // rank v: poll its OUT[p][0] lines (the final value from its parent),
+  // write them to recv and forward them to its children's OUT[p][0]
+  auto tree_down = [&](uint32_t kids) {
+    const int64_t len = a.bytes, nl = (len + 7) >> 3;
+    const uint4* src = out_area(my, 0);
+    for (int64_t k0 = t0; k0 < nl; k0 += kLLU * T) {
+      uint2 d[kLLU];
+      uint32_t act = 0;
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u)
+        if (k0 + u * T < nl) act |= 1u << u;
+      if (!ll_poll_n<kLLU>([&](int u) { return src + k0 + u * T; }, act, f, d, a)) return false;
+#pragma unroll
+      for (int u = 0; u < kLLU; ++u)
+        if ((act >> u) & 1u) {
+          const int64_t k = k0 + u * T;
+          st8(a.recv[v] + 8 * k, d[u], int(min(int64_t(8), len - 8 * k)));
+          for (int c = 0; c < m; ++c)
+            if ((kids >> c) & 1u) ll_store(out_area(a.ll[c], 0) + k, d[u], f);
+        }
+    }
+    return true;
+  };
+  if (a.tree) {
+    // One multi-level tree (R#27): child u's partial lines go to its
+    // parent's IN[p][u]; final lines travel down through OUT[p][0].  Every
+    // node combines {own send} + children in ascending rank order with the
+    // executor's arithmetic (one rounding per node, R#12/R#13), like the
+    // tree executor and the oracle.
+    const int rt = a.tree_root;
+    uint32_t kids = 0;
+    for (int u = 0; u < m; ++u)
+      if (a.parent[u] == v) kids |= 1u << u;
+    const int64_t len = a.bytes, nl = (len + 7) >> 3;
+    if (a.coll == kAllReduce) {
+      for (int64_t k = t0; k < nl; k += T) {
+        const int valid = int(min(int64_t(8), len - 8 * k));
+        const uint2 own = ld8(a.send[v] + 8 * k, valid);
+        uint2 d[kMaxRanks];
+        if (kids && !ll_poll_n<kMaxRanks>([&](int u) { return in_area(my, u) + k; }, kids, f, d, a)) {
+          ok = false;
+          break;
+        }
+        Acc8<DT, OP> acc;
+        bool first = true;
+#pragma unroll
+        for (int u = 0; u < kMaxRanks; ++u) {
+          if (u >= m) break;
+          if (u != v && !((kids >> u) & 1u)) continue;
+          const uint2 x = u == v ? own : d[u];
+          if (first)
+            acc.init(x);
+          else
+            acc.add(x);
+          first = false;
+        }
+        const uint2 r = acc.out();
+        if (v == rt) {
+          st8(a.recv[v] + 8 * k, r, valid);
+          for (int c = 0; c < m; ++c)
+            if ((kids >> c) & 1u) ll_store(out_area(a.ll[c], 0) + k, r, f);
+        } else {
+          ll_store(in_area(a.ll[a.parent[v]], v) + k, r, f);
+        }
+      }
+      if (ok && v != rt) ok = tree_down(kids);
+    } else if (v == rt) {  // Broadcast root
+      const int64_t kend = (multi && !s_root_ok) ? 0 : nl;
+      for (int64_t k = t0; k < kend; k += T) {
+        const int valid = int(min(int64_t(8), len - 8 * k));
+        const uint2 x = ld8(a.send[v] + 8 * k, valid);
+        if (a.recv[v] != a.send[v]) st8(a.recv[v] + 8 * k, x, valid);
+        for (int c = 0; c < m; ++c)
+          if ((kids >> c) & 1u) ll_store(out_area(a.ll[c], 0) + k, x, f);
+      }
+    } else {
+      ok = tree_down(kids);
+    }
+  } else if (a.coll == kAllReduce) {
     int64_t lmax = 0;
     for (int j = 0; j < m; ++j) lmax = max(lmax, a.lo[j + 1] - a.lo[j]);
     const int64_t nlmax = (lmax + 7) >> 3;

@@ -806,6 +806,24 @@ bool ll_slices(blink_comm_t c, const Plan& plan, int coll, size_t count, int es,
   return true;
 }
 
+// Small calls on a link graph's single minimum-depth tree (R#27) take the
+// LL protocol too when every rank's whole buffer fits one LL slot
+// (ll_cap_lines - 8 lines of 8 payload bytes: ll_max_bytes / m).
+bool ll_tree(blink_comm_t c, const Plan& plan, int coll, size_t bytes) {
+  const int m = c->nranks;
+  if (c->ll_bytes == 0 || m < 3 || bytes == 0 || bytes > c->cfg.ll_max_bytes || plan.switch_model ||
+      plan.trees.size() != 1 || (coll != kBroadcast && coll != kAllReduce))
+    return false;
+  if (getenv("BLINK_LL_TREE") && getenv("BLINK_LL_TREE")[0] == '0') return false;
+  return bytes <= 8 * (ll_cap_lines(c->cfg.ll_max_bytes, m) - 8);
+}
+
+void set_ll_tree(const Plan& plan, LLArgs* a) {
+  a->tree = 1;
+  a->tree_root = plan.trees[0].root;
+  for (int u = 0; u < a->nranks; ++u) a->parent[u] = int8_t(plan.trees[0].parent[u]);
+}
+
 // Everything but the per-rank buffers.  `share` = ranks whose launches share
 // this device (their CTAs split the SMs).
 void fill_ll_args(blink_comm_t c, int coll, int dtype, int op, int root, size_t bytes,
@@ -861,9 +879,10 @@ blink_result_t clique_launch(Clique* q) {
   size_t chunk_override = 0;
   // one launch holding every rank has no handshake for LL to save; there it
   // pays only below kLLOneLaunchMax (A/B: scripts/per_rank_trace.py)
-  int64_t ll_lo[kMaxRanks + 1];
-  const bool ll = (q->groups.size() > 1 || bytes <= kLLOneLaunchMax) &&
-                  ll_slices(c0, *plan, q->coll, q->count, es, ll_lo);
+  int64_t ll_lo[kMaxRanks + 1] = {};
+  const bool lltree = ll_tree(c0, *plan, q->coll, bytes);
+  const bool ll = lltree || ((q->groups.size() > 1 || bytes <= kLLOneLaunchMax) &&
+                             ll_slices(c0, *plan, q->coll, q->count, es, ll_lo));
   if (c0->cfg.autotune && !ll) {
     auto mk = std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count);
     auto mit = q->miad.find(mk);
@@ -917,6 +936,7 @@ blink_result_t clique_launch(Clique* q) {
       fill_ll_args(cd, q->coll, q->dtype, q->op, q->root, bytes, ll_lo, q->ctrl[grp.key],
                    q->err_dev[grp.key], share, &a);
       a.scope_sys = q->devices.size() > 1 ? 1 : 0;
+      if (lltree) set_ll_tree(*plan, &a);
       for (int v = 0; v < n; ++v) {
         a.send[v] = static_cast<const char*>(q->pending[v].send);
         a.recv[v] = static_cast<char*>(q->pending[v].recv);
@@ -1326,13 +1346,15 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
     const Plan* plan = nullptr;
     blink_result_t r = get_plan(comm, coll, root, bytes, &plan);
     if (r != BLINK_SUCCESS) return r;
-    int64_t lo[kMaxRanks + 1];
-    if (ll_slices(comm, *plan, coll, count, es, lo)) {
+    int64_t lo[kMaxRanks + 1] = {};
+    const bool lltree = ll_tree(comm, *plan, coll, bytes);
+    if (lltree || ll_slices(comm, *plan, coll, count, es, lo)) {
       comm->calls++;
       LLArgs a{};
       a.ranks[a.nlocal++] = int8_t(comm->rank);
       fill_ll_args(comm, coll, dtype, op, root, bytes, lo, comm->ctrl, comm->err_dev, 1, &a);
       a.scope_sys = 1;
+      if (lltree) set_ll_tree(*plan, &a);
       a.send[comm->rank] = static_cast<const char*>(sendbuf);
       a.recv[comm->rank] = static_cast<char*>(recvbuf);
       for (int u = 0; u < comm->nranks; ++u)

@@ -250,6 +250,42 @@ def test_small_calls_on_link_graphs_shallow_tree(B, dtype, count):
             c.destroy()
 
 
+@pytest.mark.parametrize("per_rank", [0, 1])
+def test_small_calls_on_link_graphs_tree_ll(B, per_rank):
+    """R#27 + LL: calls that fit one LL slot (ll_max_bytes / m) on the single
+    shallow tree take the low-latency protocol (no chunks, no flags): bit-exact
+    against the oracle's plan_shallow for f32 / bf16 / i32 AllReduce and every
+    Broadcast root, in one launch and in per-rank launches, interleaved with
+    tree-executor calls and in place."""
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), launch_per_rank=per_rank)
+    for dtype, count in (("f32", 1001), ("bf16", 3), ("i32", 4096)):
+        sends = synth.inputs(77, 8, count, dtype)
+        got = run_allreduce(B, comms, sends, dtype, "sum", inplace=(dtype == "i32"))
+        assert comms[0].stats()["last_chunks"] == 0, "expected the LL protocol"
+        want = OC.allreduce(OP.plan_shallow(g, True), sends, dtype, "sum")
+        for x in got:
+            assert_bitwise(x, want)
+    count = 2049
+    for root in range(8):
+        src = synth.rank_input(78, root, count, "f32")
+        bufs = [to_dev(src, "f32") if r == root else sentinel(count, "f32") for r in range(8)]
+        for r, c in enumerate(comms):
+            c.broadcast(bufs[r], bufs[r], root=root)
+        torch.cuda.synchronize()
+        assert comms[0].stats()["last_chunks"] == 0
+        for x in bufs:
+            assert_bitwise(to_host(x, "f32"), src)
+        # a tree-executor call in between (shared epochs, alternating LL parity)
+        big = synth.inputs(79, 8, 70001, "i32")
+        gb = run_allreduce(B, comms, big, "i32", "sum")
+        assert comms[0].stats()["last_chunks"] > 0
+        for x in gb:
+            assert_bitwise(x, OC.naive_reduce(big, "i32", "sum"))
+    for c in comms:
+        c.destroy()
+
+
 def test_config2_dgx1v_broadcast_bf16_inplace(B):
     g = OG.dgx1v()
     comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]))
