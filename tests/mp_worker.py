@@ -20,6 +20,7 @@ import torch.distributed as dist  # noqa: E402
 import synth  # noqa: E402
 from oracle import collectives as OC  # noqa: E402
 from oracle import graphs as OG  # noqa: E402
+from oracle import packing as OP  # noqa: E402
 
 
 def cpu_mode(rank, world):
@@ -172,6 +173,53 @@ def gpu_mode(rank, world):
     print(f"rank {rank}: gpu ok launches={st['launches']} ctas={st['last_ctas']}")
 
 
+def chain_mode(rank, world):
+    """3 processes on the link graph 0 - 1 - 2 (R#27 shallow tree rooted at
+    the centre, rank 1): small calls take the tree LL protocol across
+    processes; five Broadcasts back to back from rank 0 (the root may run
+    ahead of the leaves: the entry guard must hold it back); a packed-plan
+    call in between."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    dev = 0 if os.environ.get("BLINK_SAME_GPU") == "1" else rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    G = B.Graph(3, [(0, 1, 1.0, 1), (1, 2, 1.0, 1)])
+    comm = BD.init(graph=G, cfg=B.config(timeout_s=60.0, staging_bytes=1 << 20), device=dev)
+
+    def check(got, want, what):
+        gb = got.cpu().numpy().view(np.uint32)
+        bad = np.nonzero(gb != np.asarray(want).view(np.uint32))[0]
+        if bad.size:
+            raise SystemExit(f"rank {rank}: {what}: {bad.size} mismatches, first {bad[:4]}")
+
+    tree = OP.plan_shallow((3, {(0, 1): 1, (1, 0): 1, (1, 2): 1, (2, 1): 1}), True)
+    assert tree["trees"][0]["root"] == 1
+    for cnt in (1, 1001, 5003):
+        ls = synth.inputs(48, world, cnt, "f32")
+        lx = torch.from_numpy(ls[rank]).cuda()
+        ly = torch.empty_like(lx)
+        comm.allreduce(lx, ly, op="sum")
+        torch.cuda.synchronize()
+        assert comm.stats()["last_chunks"] == 0, "expected the LL protocol"
+        check(ly, OC.allreduce(tree, ls, "f32", "sum"), f"tree LL allreduce {cnt}")
+    srcs = [synth.rank_input(49 + k, 0, 2001, "f32") for k in range(5)]
+    outs = [torch.from_numpy(srcs[k]).cuda() if rank == 0 else torch.zeros(2001, device="cuda")
+            for k in range(5)]
+    if rank != 0:
+        torch.cuda._sleep(100_000_000)  # the leaves start late; the root must not overwrite
+    for k in range(5):
+        comm.broadcast(outs[k], outs[k], root=0)
+    big = synth.inputs(50, world, 300001, "f32")
+    bx = torch.from_numpy(big[rank]).cuda()
+    by = torch.empty_like(bx)
+    comm.allreduce(bx, by, op="sum")  # packed plan, tree executor
+    torch.cuda.synchronize()
+    for k in range(5):
+        check(outs[k], srcs[k], f"tree LL broadcast {k}")
+    comm.destroy()
+    print(f"rank {rank}: chain ok")
+
+
 def timeout_mode(rank, world):
     """Failure detection: rank 1 never joins the collective; rank 0's flag
     waits time out (cfg.timeout_s), the launch aborts instead of hanging, and
@@ -209,6 +257,8 @@ def main():
             cpu_mode(rank, world)
         elif mode == "timeout":
             timeout_mode(rank, world)
+        elif mode == "chain":
+            chain_mode(rank, world)
         else:
             gpu_mode(rank, world)
     finally:

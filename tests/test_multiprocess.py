@@ -49,6 +49,12 @@ def test_two_processes_share_one_gpu():
 
 
 @pytest.mark.gpu
+def test_three_processes_shallow_tree_ll():
+    out = launch(3, "chain", {"BLINK_SAME_GPU": "1"}, timeout=900)
+    assert out.count("chain ok") == 3
+
+
+@pytest.mark.gpu
 def test_missing_rank_times_out_instead_of_hanging():
     out = launch(2, "timeout", {"BLINK_SAME_GPU": "1"}, timeout=300)
     assert "rank 0: tree timeout ok" in out
