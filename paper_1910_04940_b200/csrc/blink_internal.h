@@ -132,7 +132,7 @@ struct LaunchArgs {
   int pad3;
   uint64_t* trace;           // BLINK_TRACE: kTraceSlots globaltimer stamps per CTA, else NULL
   int nctr;                  // chunk counters ctrl[2 .. 2 + nctr) zeroed by the last CTA
-  int pad4;
+  int split_ring;            // 1: signalling copies alternate chunks over two store threads
   uint64_t epoch;            // set by the kernel from ctrl[0] + 1
   uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
                              // [1] CTAs finished in the current launch (graph-safe epochs)

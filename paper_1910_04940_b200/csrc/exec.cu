@@ -506,10 +506,22 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
   // does anybody wait for this channel's per-chunk signals?
   const bool need_signal = (reduce && !is_root) || a.exit_wait || ((t.children & ~t.leafmask) != 0u);
   unsigned int* ctr = t.ctr >= 0 ? reinterpret_cast<unsigned int*>(a.ctrl + 2) + t.ctr : nullptr;
+  // A copy that signals every chunk drains its bulk stores (wait_group 0)
+  // before the flag store, which stalls the next chunk's stores.  Split the
+  // stage ring into two halves, chunks alternating between them, each drained
+  // by its own store thread in its own warp (bulk groups are per thread; a
+  // blocked wait stalls the whole warp): one half's drain overlaps the other
+  // half's stores, and no signal is delayed.
+  // Only when a chunk fits half the ring: longer chunks would leave the
+  // other half idle (A/B: DGX-1V Broadcast 256 MiB, 4 MiB chunks, 30% slower).
+  const bool short_chunks = !t.merged && (tr.chunk + tile - 1) / tile <= int64_t(NS / 2);
+  const uint32_t R = (!reduce && need_signal && NS >= 2 && a.split_ring && short_chunks) ? 2u : 1u;
+  const uint32_t H = NS / R;
 
   if (warp == 0) {
     // ------------------------------------------------ producer
-    uint32_t g = 0;
+    uint32_t gq[2] = {0u, 0u};  // tiles issued per sub-ring
+    uint32_t nord = 0;          // chunks taken so far (sub-ring = nord % R)
     int cs = t.c0;  // static sequence
     // dynamic tasks: the first chunk is the CTA's own index (no atomic round
     // trip on the critical path); later chunks come from the counter, offset
@@ -567,11 +579,13 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
       if (lane == 0) {
         if (wmask) fence_proxy_async();  // acquired flags order the TMA reads below
-        if (c == t.c0 || (ctr && g == 0)) trace(a, 3);
+        if (c == t.c0 || (ctr && nord == 0)) trace(a, 3);
+        const uint32_t r = nord % R;
+        uint32_t& g = gq[r];
         const int ntiles = body > 0 ? int((body + tile - 1) / tile) : 1;
         for (int k = 0; k < ntiles; ++k, ++g) {
-          const uint32_t s = g % NS;
-          if (!mbar_wait_or_abort(&sh.empty[s], ((g / NS) & 1u) ^ 1u, sh)) break;
+          const uint32_t s = r * H + g % H;
+          if (!mbar_wait_or_abort(&sh.empty[s], ((g / H) & 1u) ^ 1u, sh)) break;
           const int64_t off = int64_t(k) * tile;
           const uint32_t tb = uint32_t(max(int64_t(0), min(int64_t(tile), body - off)));
           TileMeta& mt = sh.smeta[s];
@@ -595,23 +609,26 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         }
       }
       __syncwarp();
+      ++nord;
     }
-    if (lane == 0) {  // end of stream
-      const uint32_t s = g % NS;
-      if (mbar_wait_or_abort(&sh.empty[s], ((g / NS) & 1u) ^ 1u, sh)) {
-        sh.smeta[s].c = -1;
-        mbar_arrive(&sh.full[s]);
+    if (lane == 0)  // end of stream, in every sub-ring
+      for (uint32_t r = 0; r < R; ++r) {
+        const uint32_t s = r * H + gq[r] % H;
+        if (mbar_wait_or_abort(&sh.empty[s], ((gq[r] / H) & 1u) ^ 1u, sh)) {
+          sh.smeta[s].c = -1;
+          mbar_arrive(&sh.full[s]);
+        }
       }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------ store
+  } else if (warp >= 1 && uint32_t(warp) <= R && lane == 0) {
+    // ------------------------------------------------ store (warp 1 + r: sub-ring r)
+    const uint32_t r = uint32_t(warp) - 1u;
     const int Dwant = a.store_depth >= 0 ? a.store_depth : 2;
-    const int D = min(Dwant, (reduce ? int(K) : int(NS)) - 1);
+    const int D = min(Dwant, (reduce ? int(K) : int(H)) - 1);
     auto release = [&](uint32_t gt) {
       if (reduce)
         mbar_arrive(&sh.oempty[gt % K]);
       else
-        mbar_arrive(&sh.empty[gt % NS]);
+        mbar_arrive(&sh.empty[r * H + gt % H]);
     };
     int kept = 0;
     bool first = true;
@@ -624,8 +641,8 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         mt = sh.ometa[o];
         src = out + size_t(o) * tile;
       } else {
-        const uint32_t s = g % NS;
-        if (!mbar_wait_or_abort(&sh.full[s], (g / NS) & 1u, sh)) break;
+        const uint32_t s = r * H + g % H;
+        if (!mbar_wait_or_abort(&sh.full[s], (g / H) & 1u, sh)) break;
         mt = sh.smeta[s];
         src = ring + size_t(s) * tile;
       }

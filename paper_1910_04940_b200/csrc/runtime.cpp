@@ -707,6 +707,13 @@ int store_depth() {
   }();
   return v;
 }
+int split_ring() {
+  static int v = [] {
+    const char* e = getenv("BLINK_SPLIT_RING");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
 int l2_hint() {
   static int v = [] {
     const char* e = getenv("BLINK_L2HINT");
@@ -1034,6 +1041,7 @@ blink_result_t clique_launch(Clique* q) {
     a.smem_bytes = smem_bytes();
     a.tile_bytes = tile_bytes();
     a.store_depth = store_depth();
+    a.split_ring = split_ring();
     a.l2_hint = l2_hint();
     a.nctr = s.nctr;
     a.ctrl = q->ctrl[grp.key];
@@ -1252,6 +1260,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.smem_bytes = smem_bytes();
   a.tile_bytes = tile_bytes();
   a.store_depth = store_depth();
+    a.split_ring = split_ring();
   a.l2_hint = l2_hint();
   a.nctr = s.nctr;
   a.ctrl = comm->ctrl;

@@ -64,7 +64,9 @@ def main():
         c.destroy()
     # emulated DGX-1V Broadcast + multi-level AllReduce (int: exact under any tree)
     g = OG.dgx1v()
-    comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]), cfg=cfg)
+    # packed trees at this size (R#27's single shallow tree is checked below)
+    packed = B.config(timeout_s=120.0, chunk_bytes=8192, shallow_max_bytes=0)
+    comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]), cfg=packed)
     src = synth.rank_input(202, 3, n, "f32")
     out = [torch.empty(n, device="cuda") for _ in range(8)]
     dsrc = torch.from_numpy(src).cuda()
@@ -81,7 +83,22 @@ def main():
     torch.cuda.synchronize()
     for y in iy:
         check(y, OC.naive_reduce(isends, "i32", "sum"), "dgx1v allreduce")
-    # small calls: the single minimum-depth tree (R#27)
+    assert comms[0].stats()["last_trees"] > 1
+    for c in comms:
+        c.destroy()
+    # small calls: the single minimum-depth tree (R#27), tree executor (64 KiB)
+    # and tree LL protocol (16 KiB)
+    comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]), cfg=B.config(timeout_s=120.0))
+    ns = 16001
+    for r, c in enumerate(comms):
+        c.allreduce(ix[r][:ns], iy[r][:ns])
+    for r, c in enumerate(comms):
+        c.broadcast(dsrc[:ns] if r == 3 else None, out[r][:ns], root=3)
+    torch.cuda.synchronize()
+    assert comms[0].stats()["last_chunks"] > 0
+    for r in range(8):
+        check(iy[r][:ns], OC.naive_reduce([s[:ns] for s in isends], "i32", "sum"), "dgx1v shallow allreduce")
+        check(out[r][:ns], src[:ns], "dgx1v shallow broadcast")
     ns = 4099
     for r, c in enumerate(comms):
         c.allreduce(ix[r][:ns], iy[r][:ns])

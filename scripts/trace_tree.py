@@ -11,7 +11,7 @@ from oracle import graphs as OG
 g = OG.dgx1v()
 coll = sys.argv[1] if len(sys.argv) > 1 else "ar"
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 256 << 20
-comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]))
+comms = B.init_all([0] * 8, graph=None if os.environ.get("SWITCH") else B.Graph.from_pairs(8, g[1]))
 cnt = S // 4
 xs = [torch.randn(cnt, device="cuda") for _ in range(8)]
 ys = [torch.empty_like(x) for x in xs]
