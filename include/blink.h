@@ -117,8 +117,13 @@ typedef struct {
  *                  lines, no handshake; NEXT-2); 0 = off.
  *                  Default 256 KiB (64 KiB when one launch holds every rank,
  *                  which has no handshake to save).
- *                  Costs 64 * m * (ll_max_bytes / (8 m) + 8) bytes of device
- *                  memory per rank.  Must agree across ranks
+ *                  On link graphs, calls of at most min(ll_max_bytes / 2,
+ *                  128 KiB) on R#27's single shallow tree (see
+ *                  shallow_max_bytes) run the LL protocol up and down that
+ *                  tree.  Costs 64 * m * (cap) bytes of device memory per
+ *                  rank, cap = ll_max_bytes / (8 m) + 8 lines (link graphs:
+ *                  at least min(ll_max_bytes / 2, 128 KiB) / 8 + 8).  Must
+ *                  agree across ranks
  *   shallow_max_bytes  link graphs (not switches, not multi-server): Broadcast
  *                  and AllReduce calls of at most this many bytes per rank run
  *                  on ONE minimum-depth (BFS) tree -- from the root, or from

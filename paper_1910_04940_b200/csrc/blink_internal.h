@@ -170,11 +170,21 @@ static_assert(sizeof(LaunchArgs) <= 4096, "kernel parameter space");
 //   OUT[p][j][cap]     result lines of root j's slice (Broadcast: one
 //                      contiguous run of the whole buffer from OUT[p][0])
 constexpr int kLLThreads = 256;
-inline size_t ll_cap_lines(size_t ll_max_bytes, int m) {
-  return ll_max_bytes / (8 * size_t(m)) + 8;
+// Link graphs (R#27) also run small calls on one tree in the LL protocol
+// (LLArgs::tree): a child's whole buffer goes into one IN slot, so their slots
+// hold ll_tree_max(ll_max) bytes (<= 128 KiB: A/B on DGX-1V, the tree
+// executor wins beyond it for AllReduce).
+inline size_t ll_tree_max(size_t ll_max_bytes) {
+  const size_t t = ll_max_bytes / 2;
+  return (t < (size_t(128) << 10) ? t : (size_t(128) << 10)) / 16 * 16;
 }
-inline size_t ll_area_bytes(size_t ll_max_bytes, int m) {
-  return ll_max_bytes ? 4 * size_t(m) * ll_cap_lines(ll_max_bytes, m) * 16 : 0;
+inline size_t ll_cap_lines(size_t ll_max_bytes, int m, bool link_graph = false) {
+  size_t cap = ll_max_bytes / (8 * size_t(m)) + 8;
+  if (link_graph && ll_tree_max(ll_max_bytes) / 8 + 8 > cap) cap = ll_tree_max(ll_max_bytes) / 8 + 8;
+  return cap;
+}
+inline size_t ll_area_bytes(size_t ll_max_bytes, int m, bool link_graph = false) {
+  return ll_max_bytes ? 4 * size_t(m) * ll_cap_lines(ll_max_bytes, m, link_graph) * 16 : 0;
 }
 struct LLArgs {
   int nranks, coll, dtype, op;

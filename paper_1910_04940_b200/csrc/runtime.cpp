@@ -813,16 +813,19 @@ bool ll_slices(blink_comm_t c, const Plan& plan, int coll, size_t count, int es,
   return true;
 }
 
+bool link_graph(blink_comm_t c) { return !c->graph.switch_model && !c->graph.multi_server; }
+
 // Small calls on a link graph's single minimum-depth tree (R#27) take the
 // LL protocol too when every rank's whole buffer fits one LL slot
-// (ll_cap_lines - 8 lines of 8 payload bytes: ll_max_bytes / m).
+// (ll_tree_max: 128 KiB by default).
 bool ll_tree(blink_comm_t c, const Plan& plan, int coll, size_t bytes) {
   const int m = c->nranks;
   if (c->ll_bytes == 0 || m < 3 || bytes == 0 || bytes > c->cfg.ll_max_bytes || plan.switch_model ||
       plan.trees.size() != 1 || (coll != kBroadcast && coll != kAllReduce))
     return false;
   if (getenv("BLINK_LL_TREE") && getenv("BLINK_LL_TREE")[0] == '0') return false;
-  return bytes <= 8 * (ll_cap_lines(c->cfg.ll_max_bytes, m) - 8);
+  return bytes <= ll_tree_max(c->cfg.ll_max_bytes) &&
+         bytes <= 8 * (ll_cap_lines(c->cfg.ll_max_bytes, m, link_graph(c)) - 8);
 }
 
 void set_ll_tree(const Plan& plan, LLArgs* a) {
@@ -842,7 +845,7 @@ void fill_ll_args(blink_comm_t c, int coll, int dtype, int op, int root, size_t 
   a->op = op;
   a->root = root;
   a->bytes = int64_t(bytes);
-  a->cap = int64_t(ll_cap_lines(c->cfg.ll_max_bytes, m));
+  a->cap = int64_t(ll_cap_lines(c->cfg.ll_max_bytes, m, link_graph(c)));
   for (int j = 0; j <= m; ++j) a->lo[j] = lo[j];
   const int64_t lines = (int64_t(bytes) + 7) / 8;
   const int want = int((lines + kLLThreads - 1) / kLLThreads);
@@ -1532,7 +1535,7 @@ static blink_result_t alloc_comm_common(blink_comm_t c) {
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   // flag words, then the LL protocol's line areas (zero = no flag yet); one
   // allocation, so the flag mapping also maps the LL area to the peers
-  c->ll_bytes = c->nranks > 1 ? ll_area_bytes(c->cfg.ll_max_bytes, c->nranks) : 0;
+  c->ll_bytes = c->nranks > 1 ? ll_area_bytes(c->cfg.ll_max_bytes, c->nranks, link_graph(c)) : 0;
   CUDA_TRY(c, cudaMalloc(&c->flags, kFlagBytes + c->ll_bytes));
   CUDA_TRY(c, cudaMemset(c->flags, 0, kFlagBytes + c->ll_bytes));
   CUDA_TRY(c, cudaDeviceSynchronize());

@@ -221,7 +221,7 @@ def test_config2_dgx1v_broadcast(B, root, count):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
-@pytest.mark.parametrize("count", [1, 4099, 65536])
+@pytest.mark.parametrize("count", [1, 4099, 30000, 65536])
 def test_small_calls_on_link_graphs_shallow_tree(B, dtype, count):
     """R#27: small AllReduce / Broadcast on link graphs (DGX-1V, a 6-GPU
     fragment) run on one minimum-depth tree; fp32/bf16 AllReduce is bit-exact
