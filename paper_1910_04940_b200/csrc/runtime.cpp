@@ -1183,6 +1183,8 @@ struct Blob {
   uint64_t staging_bytes;
   uint64_t ll_bytes;
   uint64_t ll_max_bytes;  // the LL-or-tree decision must be the same on every rank
+  uint64_t shallow_max_bytes;       // so must the plan choices by size (R#27,
+  uint64_t onehop_bcast_max_bytes;  // the switch Broadcast star)
 };
 struct RegBlob {
   char magic[8];
@@ -1703,6 +1705,8 @@ blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_b
   b.staging_bytes = comm->staging_bytes;
   b.ll_bytes = comm->ll_bytes;
   b.ll_max_bytes = comm->ll_bytes ? comm->cfg.ll_max_bytes : 0;
+  b.shallow_max_bytes = comm->cfg.shallow_max_bytes;
+  b.onehop_bcast_max_bytes = comm->cfg.onehop_bcast_max_bytes;
   memcpy(blob, &b, sizeof b);
   return BLINK_SUCCESS;
 }
@@ -1724,6 +1728,10 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
     if (b.ll_bytes != comm->ll_bytes ||
         b.ll_max_bytes != (comm->ll_bytes ? comm->cfg.ll_max_bytes : 0))
       return fail(comm, BLINK_ERR_INVALID_USAGE, "ll_max_bytes differs across ranks");
+    if (b.shallow_max_bytes != comm->cfg.shallow_max_bytes ||
+        b.onehop_bcast_max_bytes != comm->cfg.onehop_bcast_max_bytes)
+      return fail(comm, BLINK_ERR_INVALID_USAGE,
+                  "shallow_max_bytes / onehop_bcast_max_bytes differ across ranks");
     if (u == comm->rank) {
       comm->peer_flags[u] = comm->flags;
       comm->peer_staging[u] = comm->staging;
