@@ -133,6 +133,7 @@ struct LaunchArgs {
   uint64_t* trace;           // BLINK_TRACE: kTraceSlots globaltimer stamps per CTA, else NULL
   int nctr;                  // chunk counters ctrl[2 .. 2 + nctr) zeroed by the last CTA
   int split_ring;            // 1: signalling copies alternate chunks over two store threads
+  int copy_stages;           // stage-ring depth of copies (0 = default 6; BLINK_COPY_STAGES)
   uint64_t epoch;            // set by the kernel from ctrl[0] + 1
   uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
                              // [1] CTAs finished in the current launch (graph-safe epochs)

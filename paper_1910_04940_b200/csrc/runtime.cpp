@@ -707,6 +707,13 @@ int store_depth() {
   }();
   return v;
 }
+int copy_stages() {
+  static int v = [] {
+    const char* e = getenv("BLINK_COPY_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 int split_ring() {
   static int v = [] {
     const char* e = getenv("BLINK_SPLIT_RING");
@@ -1045,6 +1052,7 @@ blink_result_t clique_launch(Clique* q) {
     a.tile_bytes = tile_bytes();
     a.store_depth = store_depth();
     a.split_ring = split_ring();
+    a.copy_stages = copy_stages();
     a.l2_hint = l2_hint();
     a.nctr = s.nctr;
     a.ctrl = q->ctrl[grp.key];
@@ -1266,6 +1274,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.tile_bytes = tile_bytes();
   a.store_depth = store_depth();
     a.split_ring = split_ring();
+    a.copy_stages = copy_stages();
   a.l2_hint = l2_hint();
   a.nctr = s.nctr;
   a.ctrl = comm->ctrl;
