@@ -64,7 +64,9 @@ typedef enum { BLINK_FLOAT32 = 0, BLINK_BFLOAT16 = 1, BLINK_INT32 = 2 } blink_dt
  * SUM/PROD on floats accumulate in fp32 (bf16 widened exactly, rounded RNE once
  * per tree node); int32 wraps modulo 2^32; MIN/MAX are exact (IEEE minNum /
  * maxNum, -0 < +0). */
-typedef enum { BLINK_SUM = 0, BLINK_PROD = 1, BLINK_MIN = 2, BLINK_MAX = 3 } blink_redop_t;
+/* AVG (R#28): the sum along the same tree, divided by nranks at the tree root
+ * before its one rounding (fp32 IEEE division; int32 truncating division). */
+typedef enum { BLINK_SUM = 0, BLINK_PROD = 1, BLINK_MIN = 2, BLINK_MAX = 3, BLINK_AVG = 4 } blink_redop_t;
 
 /* Link graph.  Nodes 0..nranks-1 are the ranks' GPUs, in rank order;
  * further nodes may be SWITCH nodes.  Each link is directed src->dst with a

@@ -94,18 +94,33 @@ def _narrow(acc, dtype):
     return acc
 
 
-def reduce_operands(operands, dtype, op):
-    """Node combine: operands already sorted by tag.  Returns the node output."""
+def avg_divide(acc, m):
+    """R#28 (AVG, "all the reduction functions supported by NCCL"): the
+    tree root divides its fp32 / int32 accumulator by m before its rounding:
+    IEEE fp32 division (RNE), or C integer division (truncation toward 0)."""
+    if acc.dtype == np.int32:
+        a = acc.astype(np.int64)
+        return (np.sign(a) * (np.abs(a) // m)).astype(np.int32)
+    return (acc / np.float32(m)).astype(np.float32)
+
+
+def reduce_operands(operands, dtype, op, div=0):
+    """Node combine: operands already sorted by tag.  Returns the node output.
+    AVG combines as a sum; div > 0 (the tree root) divides before the
+    rounding."""
+    cop = "sum" if op == "avg" else op
     acc = _widen(operands[0], dtype).copy()
     for x in operands[1:]:
-        acc = combine(op, acc, _widen(x, dtype))
+        acc = combine(cop, acc, _widen(x, dtype))
+    if op == "avg" and div:
+        acc = avg_divide(acc, div)
     return _narrow(acc, dtype)
 
 
 def naive_reduce(sends, dtype, op):
     """sum_{j=0}^{m-1} send_j left to right in fp32 (int32), one final rounding.
-    The tolerance reference of north_star (R#20)."""
-    return reduce_operands(list(sends), dtype, op)
+    The tolerance reference of north_star (R#20).  AVG: that sum divided by m."""
+    return reduce_operands(list(sends), dtype, op, div=len(sends))
 
 
 # ---------------------------------------------------------------------------
@@ -142,7 +157,7 @@ def allreduce(plan, sends, dtype, op):
         def partial(v):                      # post-order value at v
             ops = [(v, sends[v][lo:hi])] + [(c, partial(c)) for c in ch[v]]
             ops.sort(key=lambda kv: kv[0])
-            return reduce_operands([x for _, x in ops], dtype, op)
+            return reduce_operands([x for _, x in ops], dtype, op, div=m if v == t["root"] else 0)
 
         out[lo:hi] = partial(t["root"])
     return out
@@ -182,7 +197,7 @@ def reduce_scatter(sends, dtype, op):
     (rank j receives block j)."""
     m = len(sends)
     B = len(sends[0]) // m
-    return [reduce_operands([s[j * B:(j + 1) * B] for s in sends], dtype, op) for j in range(m)]
+    return [reduce_operands([s[j * B:(j + 1) * B] for s in sends], dtype, op, div=m) for j in range(m)]
 
 
 def allgather(sends):

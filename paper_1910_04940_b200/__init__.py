@@ -29,7 +29,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 DTYPES = {"f32": 0, "bf16": 1, "i32": 2}
 ESIZE = {"f32": 4, "bf16": 2, "i32": 4}
-OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3}
+OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "avg": 4}
 NODE_GPU, NODE_SWITCH = 0, 1
 
 

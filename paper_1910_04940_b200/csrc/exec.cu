@@ -82,7 +82,7 @@ __device__ __forceinline__ int ld_volatile_int(const int* p) {
 // with -0 < +0.
 template <int OP>
 __device__ __forceinline__ float fop(float a, float b) {
-  if (OP == BLINK_SUM) return __fadd_rn(a, b);
+  if (OP == BLINK_SUM || OP == BLINK_AVG) return __fadd_rn(a, b);  // AVG: a sum, divided at the root
   if (OP == BLINK_PROD) return __fmul_rn(a, b);
   if (OP == BLINK_MIN) {
     float r = (a < b) ? a : b;
@@ -99,7 +99,7 @@ __device__ __forceinline__ float fop(float a, float b) {
 }
 template <int OP>
 __device__ __forceinline__ int iop(int a, int b) {
-  if (OP == BLINK_SUM) return int(unsigned(a) + unsigned(b));
+  if (OP == BLINK_SUM || OP == BLINK_AVG) return int(unsigned(a) + unsigned(b));
   if (OP == BLINK_PROD) return int(unsigned(a) * unsigned(b));
   if (OP == BLINK_MIN) return a < b ? a : b;
   return a > b ? a : b;
@@ -164,6 +164,16 @@ __device__ __forceinline__ void combine(Acc<DT>& a, const uint4& x) {
   }
 }
 
+// R#28 AVG: the root divides its accumulator by m before its one rounding
+// (fp32: IEEE division, RNE; int32: C division, truncating toward zero).
+__device__ __forceinline__ float avg_div(float x, int m) { return __fdiv_rn(x, float(m)); }
+__device__ __forceinline__ int avg_div(int x, int m) { return x / m; }
+template <int DT>
+__device__ __forceinline__ void divide(Acc<DT>& a, int m) {
+#pragma unroll
+  for (int k = 0; k < int(sizeof(a.v) / sizeof(a.v[0])); ++k) a.v[k] = avg_div(a.v[k], m);
+}
+
 template <int DT>
 __device__ __forceinline__ uint4 narrow(const Acc<DT>& a);
 template <>
@@ -189,15 +199,18 @@ struct Scalar {
     if (DT == BLINK_BFLOAT16) return __uint_as_float(uint32_t(__ldcg((const unsigned short*)p)) << 16);
     return __ldcg((const float*)p);
   }
+  // div > 0: AVG at the root (divide by div before the rounding)
   __device__ static void reduce(const char* const* srcs, int nsrc, char* const* dsts, int ndst,
-                                int64_t off) {
+                                int64_t off, int div = 0) {
     if constexpr (DT == BLINK_INT32) {
       int acc = __ldcg((const int*)(srcs[0] + off));
       for (int s = 1; s < nsrc; ++s) acc = iop<OP>(acc, __ldcg((const int*)(srcs[s] + off)));
+      if (div > 0) acc = avg_div(acc, div);
       for (int d = 0; d < ndst; ++d) __stcg((int*)(dsts[d] + off), acc);
     } else {
       float acc = load_f(srcs[0] + off);
       for (int s = 1; s < nsrc; ++s) acc = fop<OP>(acc, load_f(srcs[s] + off));
+      if (div > 0) acc = avg_div(acc, div);
       if (DT == BLINK_BFLOAT16) {
         unsigned short h = (unsigned short)f2bf(acc);
         for (int d = 0; d < ndst; ++d) __stcg((unsigned short*)(dsts[d] + off), h);
@@ -215,7 +228,7 @@ constexpr int kG = 4;  // sources loaded before combining (memory-level parallel
 // reduce bytes [b0, b1) of the chunk: dst_d[x] = combine_s src_s[x]
 template <int DT, int OP, bool VEC>
 __device__ __forceinline__ void reduce_range(const char* const* srcs, int nsrc, char* const* dsts,
-                                             int ndst, int64_t b0, int64_t b1) {
+                                             int ndst, int64_t b0, int64_t b1, int div) {
   constexpr int es = Scalar<DT, OP>::es;
   const int T = blockDim.x;
   int64_t vb1 = b0;
@@ -247,7 +260,10 @@ __device__ __forceinline__ void reduce_range(const char* const* srcs, int nsrc, 
       }
       uint4 out[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) out[u] = narrow<DT>(acc[u]);
+      for (int u = 0; u < kU; ++u) {
+        if (OP == BLINK_AVG && div > 0) divide<DT>(acc[u], div);
+        out[u] = narrow<DT>(acc[u]);
+      }
       for (int d = 0; d < ndst; ++d) {
         uint4* q = reinterpret_cast<uint4*>(dsts[d]);
 #pragma unroll
@@ -259,13 +275,14 @@ __device__ __forceinline__ void reduce_range(const char* const* srcs, int nsrc, 
       widen<DT>(acc, __ldcg(reinterpret_cast<const uint4*>(srcs[0]) + j));
       for (int s = 1; s < nsrc; ++s)
         combine<DT, OP>(acc, __ldcg(reinterpret_cast<const uint4*>(srcs[s]) + j));
+      if (OP == BLINK_AVG && div > 0) divide<DT>(acc, div);
       uint4 o = narrow<DT>(acc);
       for (int d = 0; d < ndst; ++d) __stcg(reinterpret_cast<uint4*>(dsts[d]) + j, o);
     }
     vb1 = v1 << 4;
   }
   for (int64_t off = vb1 + int64_t(threadIdx.x) * es; off < b1; off += int64_t(T) * es)
-    Scalar<DT, OP>::reduce(srcs, nsrc, dsts, ndst, off);
+    Scalar<DT, OP>::reduce(srcs, nsrc, dsts, ndst, off, OP == BLINK_AVG ? div : 0);
 }
 
 // copy bytes [b0, b1) from src to every dst
@@ -490,6 +507,8 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
   const bool reduce = t.role == kRoleReduce;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncons = reduce ? (blockDim.x >> 5) - 2 : 0;
+  // AVG (R#28): the root of a reduce divides its result by m
+  const int avg_m = (OP == BLINK_AVG && reduce && is_root) ? a.nranks : 0;
   const int nsrc = sh.nsrc, ndst = sh.ndst;
   const int ns = reduce ? nsrc : 1;
   // tile per source: the stage ring holds <= kMaxStages x ns tiles; two or
@@ -573,7 +592,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         if (reduce) {
           const int es = DT == BLINK_BFLOAT16 ? 2 : 4;
           for (int64_t off = b0 + body + int64_t(lane) * es; off < b1; off += 32 * es)
-            Scalar<DT, OP>::reduce(sh.srcs, nsrc, sh.dsts, ndst, off);
+            Scalar<DT, OP>::reduce(sh.srcs, nsrc, sh.dsts, ndst, off, avg_m);
         } else {
           for (int64_t off = b0 + body + lane; off < b1; off += 32) {
             const char ch = __ldcg(sh.srcs[0] + off);
@@ -701,6 +720,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
           Acc<DT> acc;
           widen<DT>(acc, st[vv]);
           for (int j = 1; j < nsrc; ++j) combine<DT, OP>(acc, st[j * vstride + vv]);
+          if (OP == BLINK_AVG && avg_m) divide<DT>(acc, avg_m);
           ob[vv] = narrow<DT>(acc);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -736,7 +756,8 @@ __device__ void run_lsu(const LaunchArgs& a, const DevTask& t, const DevTree& tr
         b1 = min(a.mbytes, b0 + a.mchunk);
       }
       if (t.role == kRoleReduce)
-        reduce_range<DT, OP, VEC>(sh.srcs, sh.nsrc, sh.dsts, sh.ndst, b0, b1);
+        reduce_range<DT, OP, VEC>(sh.srcs, sh.nsrc, sh.dsts, sh.ndst, b0, b1,
+                                  (OP == BLINK_AVG && is_root) ? a.nranks : 0);
       else
         copy_range<VEC>(sh.srcs[0], sh.dsts, sh.ndst, b0, b1);
     }
@@ -991,6 +1012,15 @@ struct Acc8 {
         f[k] = fop<OP>(f[k], g[k]);
     }
   }
+  __device__ __forceinline__ void divide(int m) {  // AVG at the root (R#28)
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if constexpr (DT == BLINK_INT32)
+        i[k] = avg_div(i[k], m);
+      else
+        f[k] = avg_div(f[k], m);
+    }
+  }
   __device__ __forceinline__ uint2 out() const {
     if constexpr (DT == BLINK_BFLOAT16)
       return make_uint2(f2bf(f[0]) | (f2bf(f[1]) << 16), f2bf(f[2]) | (f2bf(f[3]) << 16));
@@ -1164,6 +1194,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
             acc.add(x);
           first = false;
         }
+        if (OP == BLINK_AVG && v == rt) acc.divide(m);
         const uint2 r = acc.out();
         if (v == rt) {
           st8(a.recv[v] + 8 * k, r, valid);
@@ -1237,6 +1268,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
           else
             acc.add(x);
         }
+        if (OP == BLINK_AVG) acc.divide(m);
         const uint2 r = acc.out();
         st8(a.recv[v] + lo + 8 * k, r, valid);
         for (int u = 0; u < m; ++u)
@@ -1346,6 +1378,7 @@ ExecFn pick_op(int op) {
     case BLINK_PROD: return exec_kernel<DT, BLINK_PROD, VEC>;
     case BLINK_MIN: return exec_kernel<DT, BLINK_MIN, VEC>;
     case BLINK_MAX: return exec_kernel<DT, BLINK_MAX, VEC>;
+    case BLINK_AVG: return exec_kernel<DT, BLINK_AVG, VEC>;
   }
   return nullptr;
 }
@@ -1371,7 +1404,7 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = vec ? a.smem_bytes : 0;
-  static bool attr_set[5][3][4][2] = {};
+  static bool attr_set[5][3][5][2] = {};
   bool& done = attr_set[a.coll][a.dtype][a.op][vec];
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1393,6 +1426,7 @@ LLFn ll_pick_op(int op) {
     case BLINK_PROD: return ll_kernel<DT, BLINK_PROD>;
     case BLINK_MIN: return ll_kernel<DT, BLINK_MIN>;
     case BLINK_MAX: return ll_kernel<DT, BLINK_MAX>;
+    case BLINK_AVG: return ll_kernel<DT, BLINK_AVG>;
   }
   return nullptr;
 }

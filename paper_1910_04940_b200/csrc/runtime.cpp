@@ -755,7 +755,7 @@ blink_result_t validate_call(blink_comm_t comm, size_t count, blink_dtype_t dtyp
   if (!comm) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "comm is NULL");
   if (esize_of(dtype) == 0)
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported dtype " + std::to_string(dtype));
-  if ((coll == kAllReduce || coll == kReduceScatter) && (op < BLINK_SUM || op > BLINK_MAX))
+  if ((coll == kAllReduce || coll == kReduceScatter) && (op < BLINK_SUM || op > BLINK_AVG))
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "unsupported op " + std::to_string(op));
   if ((coll == kBroadcast || coll == kGather) && (root < 0 || root >= comm->nranks))
     return fail(comm, BLINK_ERR_INVALID_ARGUMENT,

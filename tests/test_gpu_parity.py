@@ -92,7 +92,7 @@ def make_comms(B, m, graph=None, **cfg):
 # ----------------------------------------------------------------- config 3/4: switch one-hop
 @pytest.mark.parametrize("m", [2, 3, 5, 8])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
-@pytest.mark.parametrize("op", ["sum", "min", "max", "prod"])
+@pytest.mark.parametrize("op", ["sum", "min", "max", "prod", "avg"])
 def test_onehop_allreduce_bitexact(B, m, dtype, op):
     count = 2048 * m + 13          # several tiles + a ragged, sub-16-byte tail
     sends = synth.inputs(30 + m, m, count, dtype)
@@ -654,3 +654,58 @@ def test_sixteen_ranks_max(B, dtype):
     want = OC.allreduce(OP.plan_switch_allreduce(m), sends, dtype, "sum")
     for g in got:
         assert_bitwise(g, want)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_avg_multilevel_ll_and_reduce_scatter(B, dtype):
+    """R#28 AVG: bit-exact vs the oracle (sum along the tree, one division at
+    the root before its rounding) on DGX-1V's multi-level trees (tree
+    executor, misaligned LSU path), the shallow tree in the LL protocol, the
+    one-hop LL protocol, and ReduceScatter."""
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=16384)
+    for count in (200003, 1001):
+        sends = synth.inputs(91, 8, count, dtype)
+        got = run_allreduce(B, comms, sends, dtype, "avg")
+        plan = oracle_plan_from_json(comms[0].plan(True, 0, count, dtype))
+        want = OC.allreduce(plan, sends, dtype, "avg")
+        for x in got:
+            assert_bitwise(x, want)
+    # misaligned buffers take the LSU path (reduce_range / Scalar)
+    count = 50001
+    sends = synth.inputs(92, 8, count, dtype)
+    es = OC.ESIZE[dtype]
+    dsend = []
+    for s_ in sends:
+        raw = torch.zeros(count * es + 16, dtype=torch.uint8, device="cuda")
+        v = raw[es:es + count * es].view(TORCH_DT[dtype])
+        v.copy_(to_dev(s_, dtype))
+        dsend.append(v)
+    drecv = [sentinel(count, dtype, offset=es) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.allreduce(dsend[r], drecv[r], op="avg", count=count, dtype=dtype)
+    torch.cuda.synchronize()
+    want = OC.allreduce(oracle_plan_from_json(comms[0].plan(True, 0, count, dtype)), sends, dtype, "avg")
+    for x in drecv:
+        assert_bitwise(to_host(x, dtype), want)
+    for c in comms:
+        c.destroy()
+    comms = make_comms(B, 8)
+    for count in (1001, 70001):   # one-hop LL, then the merged tree executor
+        sends = synth.inputs(93, 8, count, dtype)
+        got = run_allreduce(B, comms, sends, dtype, "avg")
+        want = OC.allreduce(OP.plan_switch_allreduce(8), sends, dtype, "avg")
+        for x in got:
+            assert_bitwise(x, want)
+    Bk = 4099
+    rs = synth.inputs(94, 8, 8 * Bk, dtype)
+    full = [to_dev(x, dtype) for x in rs]
+    outs = [sentinel(Bk, dtype) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.reduce_scatter(full[r], outs[r], op="avg")
+    torch.cuda.synchronize()
+    blocks = OC.reduce_scatter(rs, dtype, "avg")
+    for r in range(8):
+        assert_bitwise(to_host(outs[r], dtype), blocks[r])
+    for c in comms:
+        c.destroy()

@@ -214,3 +214,44 @@ def test_gather_is_allgather_at_the_root_only():
     # inverse of Broadcast: block j of the root's result is exactly rank j's send
     for j in range(m):
         assert g[2][j * B:(j + 1) * B].tobytes() == sends[j].tobytes()
+
+
+# ------------------------------------------------------------------ AVG (R#28)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_avg_of_identical_inputs_is_the_input(dtype):
+    """Every rank sends the same x (values whose m-fold sums are exact): the
+    average is x exactly, on the one-hop plan and on a multi-level tree."""
+    from oracle import graphs
+    vals = np.array([0.75, -1.5, 3.0, 0.0, 96.0, -0.125], dtype=np.float32)
+    x = C.f32_to_bf16(vals) if dtype == "bf16" else vals
+    for m, plan in ((8, packing.plan_switch_allreduce(8)),
+                    (8, packing.plan_allreduce_graph(graphs.dgx1v())),
+                    (5, packing.plan_switch_allreduce(5))):
+        got = C.allreduce(plan, [x] * m, dtype, "avg")
+        assert np.array_equal(np.asarray(got).view(np.uint16 if dtype == "bf16" else np.uint32),
+                              np.asarray(x).view(np.uint16 if dtype == "bf16" else np.uint32))
+
+
+def test_avg_int32_truncates_toward_zero():
+    """C integer division: (sum) / m truncates toward 0 (-7 / 2 = -3); the sum
+    is exact (wraparound arithmetic under any tree)."""
+    m = 4
+    sends = [np.array([1, -1, 2, -2, 10, -10, 0], dtype=np.int32) * (r + 1) for r in range(m)]
+    # sum over r of (r + 1) = 10  ->  10 * base / 4
+    base = np.array([1, -1, 2, -2, 10, -10, 0])
+    want = np.array([int(v * 10 / 4) for v in base], dtype=np.int32)   # trunc toward 0
+    for plan in (packing.plan_switch_allreduce(m),):
+        assert np.array_equal(C.allreduce(plan, sends, "i32", "avg"), want)
+    assert list(C.naive_reduce(sends, "i32", "avg")) == [2, -2, 5, -5, 25, -25, 0]
+
+
+def test_avg_fp32_root_divides_once():
+    """Hand-computed: one-hop, m = 3, inputs 1, 2, 4: sum 7 then 7 / 3 rounded
+    once (RNE) = 2.3333333 (0x40155555); dividing each input first would
+    give a different last bit (1/3 + 2/3 + 4/3 = 0x40155556)."""
+    sends = [np.array([v], dtype=np.float32) for v in (1.0, 2.0, 4.0)]
+    got = C.allreduce(packing.plan_switch_allreduce(3), sends, "f32", "avg")
+    assert got.view(np.uint32)[0] == 0x40155555
+    pre = np.float32(np.float32(np.float32(1.0) / np.float32(3)) + np.float32(np.float32(2.0) / np.float32(3)))
+    pre = np.float32(pre + np.float32(np.float32(4.0) / np.float32(3)))
+    assert pre.view(np.uint32) != 0x40155555
