@@ -7,8 +7,9 @@
  * m virtual ranks on device 0 (blink_init_all with a repeated device, the
  * single-process mode), then on the emulated DGX-1V link graph: an int32
  * SUM AllReduce (exact under any tree, so the expected value is a closed
- * form: sum_r (r * 1000 + i) = 1000 m(m-1)/2 + m i), a Broadcast from the
- * last rank, and the error path of a bad root.  Prints "c api ok".
+ * form: sum_r (r * 1000 + i) = 1000 m(m-1)/2 + m i), AVG (500 (m-1) + i), a
+ * Broadcast from the last rank, and the error path of a bad root.  Prints
+ * "c api ok".
  */
 #include <cuda_runtime_api.h>
 #include <stdio.h>
@@ -65,6 +66,18 @@ static int run(int m, size_t count, const blink_graph_t* graph, const char* what
         return 1;
       }
     }
+  }
+  /* AVG (R#28): the same sum divided by m at the tree root = 500 (m-1) + i */
+  for (int r = 0; r < m; ++r)
+    CK(blink_allreduce(comms[r], send[r], recv[r], count, BLINK_INT32, BLINK_AVG, NULL));
+  CU(cudaDeviceSynchronize());
+  for (int r = 0; r < m; ++r) {
+    CU(cudaMemcpy(host, recv[r], count * sizeof(int), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < count; ++i)
+      if (host[i] != 500 * (m - 1) + (int)i) {
+        fprintf(stderr, "%s: avg rank %d [%zu] = %d\n", what, r, i, host[i]);
+        return 1;
+      }
   }
   for (int r = 0; r < m; ++r)
     CK(blink_broadcast(comms[r], r == m - 1 ? send[r] : NULL, recv[r], count, BLINK_INT32, m - 1, NULL));

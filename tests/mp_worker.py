@@ -147,9 +147,12 @@ def gpu_mode(rank, world):
         ls = synth.inputs(45, world, cnt, dt)
         lx = to_dev(ls[rank], dt)
         ly = torch.empty_like(lx)
+        la = torch.empty_like(lx)
+        comm.allreduce(lx, la, op="avg")
         comm.allreduce(lx, ly, op="sum")
         comm.allreduce(lx, lx, op="max")
         torch.cuda.synchronize()
+        check(la, OC.naive_reduce(ls, dt, "avg"), f"LL allreduce avg {dt} {cnt}")
         check(ly, OC.naive_reduce(ls, dt, "sum"), f"LL allreduce {dt} {cnt}")
         check(lx, OC.naive_reduce(ls, dt, "max"), f"LL in-place max {dt} {cnt}")
     bsrc = synth.rank_input(46, 0, 3333, "f32")
