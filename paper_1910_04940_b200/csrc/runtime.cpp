@@ -820,6 +820,11 @@ bool ll_slices(blink_comm_t c, const Plan& plan, int coll, size_t count, int es,
   return true;
 }
 
+bool trace_on() {  // BLINK_TRACE, read once (checked on every launch)
+  static const bool v = getenv("BLINK_TRACE") != nullptr;
+  return v;
+}
+
 bool link_graph(blink_comm_t c) { return !c->graph.switch_model && !c->graph.multi_server; }
 
 // Small calls on a link graph's single minimum-depth tree (R#27) take the
@@ -830,7 +835,8 @@ bool ll_tree(blink_comm_t c, const Plan& plan, int coll, size_t bytes) {
   if (c->ll_bytes == 0 || m < 3 || bytes == 0 || bytes > c->cfg.ll_max_bytes || plan.switch_model ||
       plan.trees.size() != 1 || (coll != kBroadcast && coll != kAllReduce))
     return false;
-  if (getenv("BLINK_LL_TREE") && getenv("BLINK_LL_TREE")[0] == '0') return false;
+  static const bool off = getenv("BLINK_LL_TREE") && getenv("BLINK_LL_TREE")[0] == '0';
+  if (off) return false;
   return bytes <= ll_tree_max(c->cfg.ll_max_bytes) &&
          bytes <= 8 * (ll_cap_lines(c->cfg.ll_max_bytes, m, link_graph(c)) - 8);
 }
@@ -959,7 +965,7 @@ blink_result_t clique_launch(Clique* q) {
         a.recv[v] = static_cast<char*>(q->pending[v].recv);
         a.ll[v] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(q->comms[v]->flags) + kFlagBytes);
       }
-      if (getenv("BLINK_TRACE")) {
+      if (trace_on()) {
         uint64_t*& tb = q->trace[grp.key];
         if (!tb) CUDA_TRY(cd, cudaMalloc(&tb, sizeof(uint64_t) * kTraceSlots * 4096));
         a.trace = tb;
@@ -1056,7 +1062,7 @@ blink_result_t clique_launch(Clique* q) {
     a.l2_hint = l2_hint();
     a.nctr = s.nctr;
     a.ctrl = q->ctrl[grp.key];
-    if (getenv("BLINK_TRACE")) {
+    if (trace_on()) {
       uint64_t*& tb = q->trace[grp.key];
       if (!tb) CUDA_TRY(cd, cudaMalloc(&tb, sizeof(uint64_t) * kTraceSlots * 4096));
       a.trace = tb;
