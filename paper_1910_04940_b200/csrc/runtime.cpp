@@ -820,9 +820,8 @@ bool ll_slices(blink_comm_t c, const Plan& plan, int coll, size_t count, int es,
   return true;
 }
 
-bool trace_on() {  // BLINK_TRACE, read once (checked on every launch)
-  static const bool v = getenv("BLINK_TRACE") != nullptr;
-  return v;
+bool trace_on() {  // BLINK_TRACE (read per launch: tests toggle it at run time)
+  return getenv("BLINK_TRACE") != nullptr;
 }
 
 bool link_graph(blink_comm_t c) { return !c->graph.switch_model && !c->graph.multi_server; }
