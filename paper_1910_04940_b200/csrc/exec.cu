@@ -181,10 +181,23 @@ __device__ __forceinline__ uint4 narrow<BLINK_FLOAT32>(const Acc<BLINK_FLOAT32>&
   return make_uint4(__float_as_uint(a.v[0]), __float_as_uint(a.v[1]), __float_as_uint(a.v[2]),
                     __float_as_uint(a.v[3]));
 }
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {  // RNE; NaN -> 0x7fff
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 template <>
 __device__ __forceinline__ uint4 narrow<BLINK_BFLOAT16>(const Acc<BLINK_BFLOAT16>& a) {
-  return make_uint4(f2bf(a.v[0]) | (f2bf(a.v[1]) << 16), f2bf(a.v[2]) | (f2bf(a.v[3]) << 16),
-                    f2bf(a.v[4]) | (f2bf(a.v[5]) << 16), f2bf(a.v[6]) | (f2bf(a.v[7]) << 16));
+  // the hardware conversion rounds like f2bf (RNE) but returns the canonical
+  // NaN; a NaN keeps its sign and payload (oracle f32_to_bf16) on the rare path
+  bool nan = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) nan |= a.v[k] != a.v[k];
+  if (__builtin_expect(nan, 0))
+    return make_uint4(f2bf(a.v[0]) | (f2bf(a.v[1]) << 16), f2bf(a.v[2]) | (f2bf(a.v[3]) << 16),
+                      f2bf(a.v[4]) | (f2bf(a.v[5]) << 16), f2bf(a.v[6]) | (f2bf(a.v[7]) << 16));
+  return make_uint4(cvt_bf16x2(a.v[0], a.v[1]), cvt_bf16x2(a.v[2], a.v[3]), cvt_bf16x2(a.v[4], a.v[5]),
+                    cvt_bf16x2(a.v[6], a.v[7]));
 }
 template <>
 __device__ __forceinline__ uint4 narrow<BLINK_INT32>(const Acc<BLINK_INT32>& a) {
