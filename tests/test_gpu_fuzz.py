@@ -5,6 +5,7 @@ Values: int32 and MIN/MAX must be exact under any plan; fp32/bf16 SUM must be
 bit-exact against the oracle's tree-order evaluation of the library's plan and
 within R#20's tolerance of the naive sum; Broadcast / AllGather are bitwise
 copies."""
+import os
 import random
 from fractions import Fraction
 
@@ -81,19 +82,22 @@ def oracle_plan(p):
                             weight=Fraction(*t["weight"])) for t in p["trees"]])
 
 
-@pytest.mark.parametrize("seed", range(128))
+# FUZZ_N / FUZZ_BASE widen or move the seed set for one-off runs (default: 128 from 7000)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FUZZ_N", "128"))))
 def test_random_configuration(B, seed):
-    rng = random.Random(7000 + seed)
+    rng = random.Random(int(os.environ.get("FUZZ_BASE", "7000")) + seed)
     m, graph, kind = random_graph(B, rng)
     coll = "allreduce" if kind == "multiserver" else rng.choice(["allreduce", "allreduce", "broadcast"] +
                       (["reduce_scatter", "allgather", "gather"] if kind == "switch" else []))
     dtype = rng.choice(["f32", "bf16", "i32"])
-    op = rng.choice(["sum", "min", "max"] + (["prod"] if dtype == "i32" else []))
+    op = rng.choice(["sum", "min", "max", "avg"] + (["prod"] if dtype == "i32" else []))
     count = rng.choice([1, 7, 255, 4096, 65537, 300001, rng.randint(1, 200000)])
     inplace = rng.random() < 0.25 and coll in ("allreduce", "broadcast")
     misalign = rng.random() < 0.15 and not inplace
     chunk = rng.choice([0, 4096, 65536])
-    comms = B.init_all([0] * m, graph=graph, cfg=B.config(timeout_s=30.0, chunk_bytes=chunk))
+    per_rank = int(rng.random() < 0.2)
+    comms = B.init_all([0] * m, graph=graph, cfg=B.config(timeout_s=30.0, chunk_bytes=chunk,
+                                                          launch_per_rank=per_rank))
     es = OC.ESIZE[dtype]
     if coll == "reduce_scatter":
         sends = synth.inputs(seed, m, m * count, dtype)
@@ -138,7 +142,8 @@ def test_random_configuration(B, seed):
             c.allgather(ds[r], rs[r], sendcount=count, dtype=dtype)
     torch.cuda.synchronize()
     got = [to_host(x, dtype) if x is not None else None for x in rs]
-    what = f"{kind} m={m} {coll} {dtype} {op} n={count} inplace={inplace} misalign={misalign} chunk={chunk}"
+    what = (f"{kind} m={m} {coll} {dtype} {op} n={count} inplace={inplace} misalign={misalign} "
+            f"chunk={chunk} per_rank={per_rank}")
     if coll == "broadcast":
         for g in got:
             assert np.array_equal(bits(g), bits(sends[root])), what
