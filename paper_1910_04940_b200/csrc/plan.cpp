@@ -1195,15 +1195,24 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
       // their chunks larger, but a small tree needs enough chunks to
       // pipeline over its hops ((c+h-1)/c): the floor grows with
       // the tree's range, bytes/16 (Broadcast) or bytes/8 (AllReduce: twice
-      // the signals per chunk) clamped to [16 KiB, 64 KiB] (A/B in
+      // the signals per chunk) clamped to [16 KiB, cap] (A/B in
       // profiles/README.md; BLINK_MIN_CHUNK_DEEP fixes it)
       static const int64_t min_chunk_deep_env = [] {
         const char* e = getenv("BLINK_MIN_CHUNK_DEEP");
         return e ? std::max<int64_t>(16, atoll(e)) : int64_t(0);
       }();
+      // cap of that floor: 96 KiB on link graphs, 64 KiB on the switch's
+      // two-level Broadcast trees (A/B per call, 64 MiB: 3-GPU chains 69.6
+      // -> 64.5 us, DGX-1V Broadcast 173.5 -> 159.5 us, DGX-1V AllReduce
+      // 396 -> 358 us; switch Broadcast 2% slower with 96 KiB)
+      static const int64_t deep_cap_env = [] {
+        const char* e = getenv("BLINK_DEEP_CAP");
+        return e ? std::max<int64_t>(16 << 10, atoll(e)) : int64_t(0);
+      }();
+      const int64_t deep_cap = deep_cap_env ? deep_cap_env : (p.switch_model ? (64 << 10) : (96 << 10));
       const int64_t min_chunk_deep =
           min_chunk_deep_env ? min_chunk_deep_env
-                             : std::min<int64_t>(64 << 10, std::max<int64_t>(16 << 10,
+                             : std::min<int64_t>(deep_cap, std::max<int64_t>(16 << 10,
                                                                              bytes / (p.coll == kBroadcast ? 16 : 8)));
       cb = std::max<int64_t>(cb, p.trees[i].depth >= 2 ? std::max(min_chunk, min_chunk_deep) : min_chunk);
       cb = std::min<int64_t>(cb, 4 << 20);
