@@ -35,6 +35,11 @@
 // Epochs live in device memory (CUDA-graph safe).  Misaligned buffers run a
 // 128-bit / scalar LSU path with ld.global.cg.  Timeouts (globaltimer) abort
 // the launch through a host-mapped error word instead of hanging.
+// Signalling copies with short chunks split the stage ring over two store
+// warps (one half drains while the other stores).  AVG (R#28) is a SUM whose
+// tree root divides by m before its rounding.  Small calls run ll_kernel
+// (flag-in-data lines): the one-hop trees / star on a switch, or R#27's
+// single shallow tree on a link graph (LLArgs::tree).
 #include <cuda_runtime.h>
 
 #include <cstdint>
