@@ -192,7 +192,10 @@ def run_virtual(args):
     recv2 = [recvs, [torch.empty_like(s) for s in sends]]
     d2h = torch.cuda.Stream()
     ev_free = [None, None]
-    e2e_steps = max(2, min(args.steps, 6))
+    # 20 steps (or K if fewer): the first step's H2D and the last step's D2H
+    # run alone (pipeline fill / drain), every other step overlaps them
+    # (scripts/pcie_probe.py: 2.15 GB each way concurrently in 43 ms)
+    e2e_steps = max(2, min(args.steps, 20))
 
     def e2e_step(k):
         i = k % 2
@@ -245,6 +248,7 @@ def run_virtual(args):
         "e2e": {"value": round(S / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                 "h2d_bytes_per_step": m * S, "d2h_bytes_per_step": m * S,
                 "ms_per_step": round(e2e_ms, 3),
+                "steps": e2e_steps,
                 "note": "every rank's input H2D and result D2H (pinned) per step; D2H of step k overlaps H2D of step k+1"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
