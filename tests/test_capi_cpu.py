@@ -361,3 +361,32 @@ def test_dgx1v_small_broadcast_tree_golden(B):
     assert len(B.plan_json(8, False, 0, 0, "f32", graph=G)["trees"]) == 6  # count 0: packed plan
     off = B.config(shallow_max_bytes=0)
     assert len(B.plan_json(8, False, 0, 4096, "f32", graph=G, cfg=off)["trees"]) == 6
+
+
+def test_chunk_policy_deep_trees_and_merged_medium_calls(B):
+    """a8 static table as documented in DESIGN §1: multi-hop Broadcast trees
+    get a chunk floor of bytes/16 clamped to [16 KiB, 96 KiB] on link graphs
+    and [16 KiB, 64 KiB] on the switch's two-level trees; chunk sizes are
+    16-byte grains and the chunks cover every tree's range."""
+    from oracle import graphs
+    g = graphs.dgx1v()
+    G = B.Graph.from_pairs(8, g[1])
+    count = (64 << 20) // 4
+    p = B.plan_json(8, False, 0, count, "f32", graph=G)
+    for t in p["trees"]:
+        nbytes = (t["hi"] - t["lo"]) * 4
+        assert t["depth"] >= 2
+        assert t["chunk"] * 4 >= min(96 << 10, max(16 << 10, nbytes // 16))
+        assert (t["chunk"] * 4) % 16 == 0 and t["nchunks"] * t["chunk"] >= t["hi"] - t["lo"]
+        assert t["chunk"] * 4 == 96 << 10   # ~11 MB trees: the cap binds (the per-CTA target is smaller)
+    p = B.plan_json(8, False, 0, count, "f32")  # switch: 7 two-level trees
+    assert len(p["trees"]) == 7
+    for t in p["trees"]:
+        nbytes = (t["hi"] - t["lo"]) * 4
+        assert min(64 << 10, max(16 << 10, nbytes // 16)) <= t["chunk"] * 4
+        assert t["chunk"] * 4 == 64 << 10
+    # small trees: the floor follows the range (bytes / 16), never below 16 KiB
+    p = B.plan_json(8, False, 0, (1 << 20) // 4, "f32", graph=G)
+    for t in p["trees"]:
+        nbytes = (t["hi"] - t["lo"]) * 4
+        assert t["chunk"] * 4 >= max(16 << 10, nbytes // 16)
