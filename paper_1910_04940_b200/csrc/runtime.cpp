@@ -414,9 +414,22 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
         // (1 MiB runs on all SMs instead of S / 16 KiB of them; no one-chunk
         // tail), in 1 KiB steps (tile-friendly sizes), not below 4 KiB.
         // A/B, m = 8 per call: 256 KiB 7.6 -> 6.0 us, 1 MiB 7.8 -> 6.8 us
-        int64_t c2 = (S + int64_t(B) * per - 1) / (int64_t(B) * per);
+        // up to 4 chunks per CTA (8 with <= 4 ranks): one larger chunk per
+        // CTA instead -- fewer chunk set-ups and drains, and the per-call
+        // ramp overlaps better (A/B per call: m = 8 3/4/6 MiB 10.7/11.6/17.4
+        // -> 9.4/10.7/16.7 us; m = 4 8 MiB 13.3 -> 11.7 us; m = 2 6/16 MiB
+        // 9.3/15.0 -> 7.4/11.7 us; beyond these limits, or above 192 KiB
+        // per chunk, it loses)
+        static const int one_env = [] {
+          const char* e = getenv("BLINK_ONE_CHUNK");
+          return e ? atoi(e) : -1;
+        }();
+        const int64_t one_max = one_env >= 0 ? one_env : (n <= 4 ? 8 : 4);
+        const int64_t one_bytes = (S + int64_t(B) - 1) / int64_t(B);  // <= 192 KiB (m = 2 48 MiB: 7% slower)
+        const int64_t per2 = (per >= 2 && per <= one_max && one_bytes <= (192 << 10)) ? 1 : per;
+        int64_t c2 = (S + int64_t(B) * per2 - 1) / (int64_t(B) * per2);
         c2 = (c2 + 1023) / 1024 * 1024;
-        cb = std::max<int64_t>(std::min<int64_t>(c2, cb), std::min<int64_t>(cb, 4 << 10));
+        cb = per2 < per ? c2 : std::max<int64_t>(std::min<int64_t>(c2, cb), std::min<int64_t>(cb, 4 << 10));
       }
       const int total = int((S + cb - 1) / cb);
       s->mchunk = cb;
