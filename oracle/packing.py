@@ -11,10 +11,15 @@ Follows the paper step by step:
   each minimum-tree call (without normalisation the raw lengths
   ~1e-34 lose the (1 - eps) guarantee).  Final uniform scaling to exact
   feasibility; identical trees merged.
-* Sec. 3.2.1 (Eqs. 4-7): binary ILP over the MWU candidates, then
+* Sec. 3.2.1 (Eqs. 4-7): binary ILP over the MWU candidates ("k
+  here is controlled by the number of trees returned by the MWU procedure",
+  P:390; the candidates are the trees of four MWU runs, R#21), then
   "iteratively relax the constraints (i.e. allowing w_i to take fractional
   values) until c_hat is within a configured threshold (e.g., 5%) of c*"
-  (R#5, R#6: grid w in {0, 1/g, ..., 1} for g = 1, 2, 4, 8, 16; gap 0.05).
+  (R#5, R#6: grid w in {0, 1/g, ..., 1} for g = 1, 2, 4, 8, 16; gap 0.05;
+  R#3: c* = the optimal rate, exact where computable).  No other candidates
+  and no weight above 1 (Eq. 6): the product's extra heuristics (R#21, R#26)
+  are not part of the oracle.
 * Sec. 3.3: AllReduce packs *undirected* spanning trees (a tree
   of weight w consumes w on the link in both directions); the per-tree root is
   the tree's centre (R#9).
@@ -33,15 +38,23 @@ GRAIN = 16  # bytes; R#11
 # --------------------------------------------------------------------------
 # Minimum-weight arborescence (Chu-Liu / Edmonds), the MWU inner oracle
 # --------------------------------------------------------------------------
-def min_arborescence(n, r, lengths):
+def _tie_key(e, tiebreak):
+    """Deterministic tie-break among equal lengths: lexicographic
+    (src, dst) ascending ("asc") or descending ("desc", the alternate run of
+    SURVEY 7 hard part 8)."""
+    return e if tiebreak == "asc" else (-e[0], -e[1])
+
+
+def min_arborescence(n, r, lengths, tiebreak="asc"):
     """Minimum-total-length arborescence rooted at r.
 
-    `lengths`: {(u, v): l}.  Ties: smallest (length, (u, v)) in-edge.
+    `lengths`: {(u, v): l}.  Ties: smallest (length, tie key) in-edge.
     Returns a parent tuple (parent[r] = -1).  Plain recursive contraction."""
-    edges = [(u, v, w, (u, v)) for (u, v), w in lengths.items() if u != v]
+    edges = [(u, v, w, _tie_key((u, v), tiebreak)) for (u, v), w in lengths.items() if u != v]
     chosen = _cle(n, r, edges)
     parent = [-1] * n
-    for (u, v) in chosen:
+    for key in chosen:
+        u, v = key if tiebreak == "asc" else (-key[0], -key[1])
         parent[v] = u
     return tuple(parent)
 
@@ -101,9 +114,9 @@ def _cle(n, r, edges):
     return {entered[v] if v in entered else inb[v][3] for v in range(n) if v != r}
 
 
-def min_spanning_tree(n, lengths):
-    """Kruskal over undirected {(u,v) u<v: l}; ties by (l, u, v).  Returns a
-    sorted tuple of (u, v) pairs."""
+def min_spanning_tree(n, lengths, tiebreak="asc"):
+    """Kruskal over undirected {(u,v) u<v: l}; ties by (l, tie key of (u, v)).
+    Returns a sorted tuple of (u, v) pairs."""
     parent = list(range(n))
 
     def find(x):
@@ -113,7 +126,7 @@ def min_spanning_tree(n, lengths):
         return x
 
     out = []
-    for (w, (u, v)) in sorted((w, e) for e, w in lengths.items()):
+    for (w, _, (u, v)) in sorted((w, _tie_key(e, tiebreak), e) for e, w in lengths.items()):
         a, b = find(u), find(v)
         if a != b:
             parent[a] = b
@@ -165,25 +178,25 @@ def _mwu(caps, tree_of, eps):
     return w, tree_edges, sum(w.values()), iters
 
 
-def mwu_broadcast(g, r, eps=0.1):
+def mwu_broadcast(g, r, eps=0.1, tiebreak="asc"):
     """MWU packing of arborescences rooted at r on the directed graph.
     Returns (weights {parent_tuple: w}, rate c*, iterations)."""
     n, cap = g
 
     def tree_of(lengths):
-        p = min_arborescence(n, r, lengths)
+        p = min_arborescence(n, r, lengths, tiebreak)
         return p, [(u, v) for v, u in enumerate(p) if u >= 0]
 
     w, _, rate, iters = _mwu(cap, tree_of, eps)
     return w, rate, iters
 
 
-def mwu_allreduce(pairs, n, eps=0.1):
+def mwu_allreduce(pairs, n, eps=0.1, tiebreak="asc"):
     """MWU packing of undirected spanning trees: Kruskal inner
     oracle, capacity per undirected link = per-direction capacity (R#9).
     Returns (weights {edge_tuple: w}, rate c*, iterations)."""
     def tree_of(lengths):
-        t = min_spanning_tree(n, lengths)
+        t = min_spanning_tree(n, lengths, tiebreak)
         return t, list(t)
 
     w, _, rate, iters = _mwu(pairs, tree_of, eps)
@@ -250,14 +263,16 @@ def root_tree(edges, n, root):
 # --------------------------------------------------------------------------
 # ILP refinement (Sec. 3.2.1)
 # --------------------------------------------------------------------------
-def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_limit=500,
-               multiplicity=False):
+def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_limit=500):
     """Eqs. 4-7 with the relaxation grid (R#5).
 
     `caps`: {edge: c_e}; `candidates`: list of (edge_list, depth, key) in a
-    fixed order.  For each g: maximise sum z_T s.t. sum_{T contains e} z_T <=
-    g c_e, z_T in {0..g}; tie-break fewest trees, then least total depth, then
-    (deterministic solver) whatever HiGHS returns.  Accept the first g with sum z / g >= (1 - gap) c*.
+    fixed order -- "k here is controlled by the number of trees returned by the
+    MWU procedure".  For each g: maximise sum z_T s.t.
+    sum_{T contains e} z_T <= g c_e, z_T in {0..g} (w_T = z_T / g <= 1, Eq. 6
+    relaxed to the grid).  Tie-breaks (R#21): fewest trees, then the smallest
+    maximum depth, then the least total depth (depth adds pipeline latency,
+    P:511-513).  Accept the first g with sum z / g >= (1 - gap) c*.
     Returns (list of (candidate index, Fraction weight), g, accepted).
     scipy.optimize.milp (HiGHS) is the library primitive; the lexicographic
     tie-breaks are sequential MILPs."""
@@ -274,27 +289,26 @@ def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_
     depth = np.array([d for (_, d, _) in candidates], dtype=float)
     best = None
     for g in grids:
-        # variables: z (k, integer 0..g*u_T), y (k, binary); z_T <= g u_T y_T with
-        # u_T = 1 (the paper's w_i <= 1) or, in the multiplicity fallback
-        # (R#26), the tree's bottleneck link count floor(min_{e in T} c_e)
-        ub = np.array([g * (int(min(caps[e] for e in te)) if multiplicity else 1)
-                       for (te, _, _) in candidates], dtype=float)
-        Z = np.hstack([A, np.zeros_like(A)])
-        link = np.hstack([np.eye(k), -np.diag(ub)])
-        cons = [LinearConstraint(Z, -np.inf, g * cvec), LinearConstraint(link, -np.inf, 0.0)]
-        integ = np.ones(2 * k)
-        bnds = Bounds(np.zeros(2 * k), np.concatenate([ub, np.ones(k)]))
-        ones_z = np.concatenate([np.ones(k), np.zeros(k)])
-        ones_y = np.concatenate([np.zeros(k), np.ones(k)])
-        dep_y = np.concatenate([np.zeros(k), depth])
+        # variables: z (k, integer 0..g), y (k, binary: tree used), D (max depth)
+        Z = np.hstack([A, np.zeros_like(A), np.zeros((len(edges), 1))])
+        link = np.hstack([np.eye(k), -g * np.eye(k), np.zeros((k, 1))])       # z_T <= g y_T
+        dmax = np.hstack([np.zeros((k, k)), np.diag(depth), -np.ones((k, 1))])  # depth_T y_T <= D
+        cons = [LinearConstraint(Z, -np.inf, g * cvec), LinearConstraint(link, -np.inf, 0.0),
+                LinearConstraint(dmax, -np.inf, 0.0)]
+        integ = np.concatenate([np.ones(2 * k), [0]])
+        bnds = Bounds(np.zeros(2 * k + 1), np.concatenate([np.full(k, g), np.ones(k), [np.inf]]))
+        ones_z = np.concatenate([np.ones(k), np.zeros(k), [0]])
+        ones_y = np.concatenate([np.zeros(k), np.ones(k), [0]])
+        d_max = np.concatenate([np.zeros(2 * k), [1]])
+        dep_y = np.concatenate([np.zeros(k), depth, [0]])
         r1 = milp(-ones_z, constraints=cons, integrality=integ, bounds=bnds)
         zstar = round(-r1.fun)
         x = r1.x
-        # tie-breaks (fewest trees, then least total depth) as sequential MILPs
-        # under a deterministic node limit; a limit-stopped stage keeps its
-        # best feasible point (the tie-break is a preference, not a pin).
+        # tie-breaks as sequential MILPs under a deterministic node limit; a
+        # limit-stopped stage keeps its best feasible point (the tie-break is
+        # a preference, not a pin).
         cons.append(LinearConstraint(ones_z[None, :], zstar, zstar))
-        for obj in (ones_y, dep_y):
+        for obj in (ones_y, d_max, dep_y):
             r = milp(obj, constraints=cons, integrality=integ, bounds=bnds,
                      options={"node_limit": node_limit})
             if r.x is None:
@@ -313,63 +327,37 @@ def ilp_refine(caps, candidates, c_star, gap=0.05, grids=(1, 2, 4, 8, 16), node_
 
 
 # --------------------------------------------------------------------------
-# Integral candidates (R#21): the ILP over MWU candidates alone can miss the
-# integral optimum (hard part 8); these enrich the candidate set.
+# MWU candidate sets: several MWU runs widen the candidates the ILP
+# chooses from (SURVEY 7 hard part 8: "a larger candidate set from several
+# eps/tie-break runs"); c* is the best MWU rate among them (R#3).
 # --------------------------------------------------------------------------
-def lovasz_arborescences(g, r):
-    """k = min_v lambda(r, v) edge-disjoint arborescences (integer capacities),
-    by Lovasz's constructive proof of Edmonds' theorem: grow each tree
-    from r one edge (u in tree, v not) at a time, taking an edge only if the
-    remaining graph keeps lambda(r, v) >= k - t; edges tried by (depth of u,
-    u, v).  Returns parent tuples."""
-    from .bounds import maxflow
-    n, cap0 = g
-    cap = {e: int(c) for e, c in cap0.items()}
-    k = min(maxflow(n, cap, r, v) for v in range(n) if v != r)
-    out = []
-    for t in range(1, k + 1):
-        parent = {r: -1}
-        depth = {r: 0}
-        while len(parent) < n:
-            cands = sorted((depth[u], u, v) for (u, v), c in cap.items()
-                           if c > 0 and u in parent and v not in parent)
-            for d, u, v in cands:
-                cap[(u, v)] -= 1
-                if maxflow(n, {e: c for e, c in cap.items() if c > 0}, r, v) >= k - t:
-                    parent[v] = u
-                    depth[v] = d + 1
-                    break
-                cap[(u, v)] += 1
-            else:
-                raise RuntimeError("Lovasz step found no edge (cannot happen)")
-        out.append(tuple(parent[v] for v in range(n)))
-    return out
+MWU_RUNS = ((0.1, "asc"), (0.1, "desc"), (0.05, "asc"), (0.05, "desc"))
 
 
-def peel_spanning_trees(pairs, n, scale):
-    """Greedy integral peeling at capacity scale `scale`: repeatedly take the
-    spanning tree that prefers links with the largest relative residual
-    capacity and remove one unit along it.  Returns {tree: multiplicity}."""
-    res = {e: scale * c for e, c in pairs.items()}
-    full = dict(res)
-    out = {}
-    while True:
-        lengths = {e: (full[e] / res[e] if res[e] > 0 else 1e30) for e in pairs}
-        try:
-            t = min_spanning_tree(n, lengths)
-        except ValueError:
-            break
-        if any(res[e] <= 0 for e in t):
-            break
-        for e in t:
-            res[e] -= 1
-        out[t] = out.get(t, 0) + 1
-    return out
+def optimal_rate(g, allreduce, r, c_star_mwu):
+    """The rate the ILP's relaxation is measured against ("within a
+    configured threshold ... of c*", c* = b* = "the optimal rate"; R#3).
+    MWU only approximates it from below ((1 - eps)), so where the
+    optimum is exactly computable it is used: Broadcast -- Edmonds' theorem,
+    min_v maxflow(r -> v); AllReduce -- the Nash-Williams partition
+    bound by enumeration for <= 8 GPUs (Bell(8) = 4140 partitions).  Larger
+    AllReduce allocations fall back to the best MWU rate."""
+    from . import bounds
+    from .graphs import undirected_pairs
+    n, _ = g
+    if not allreduce:
+        return float(bounds.edmonds_rate(g, r))
+    if n <= 8:
+        return float(bounds.nash_williams_rate(undirected_pairs(g), n))
+    return c_star_mwu
 
 
-# --------------------------------------------------------------------------
-# Plans
-# --------------------------------------------------------------------------
+def mwu_runs(eps):
+    """The MWU runs of one plan: the configured eps with both tie-breaks, then
+    eps / 2 with both (the defaults give MWU_RUNS)."""
+    return ((eps, "asc"), (eps, "desc"), (eps / 2, "asc"), (eps / 2, "desc"))
+
+
 def _order_trees(trees):
     """Split order (R#11): weight descending, then lexicographic edge list."""
     return sorted(trees, key=lambda t: (-t["weight"], sorted(t["edges"])))
@@ -377,50 +365,52 @@ def _order_trees(trees):
 
 def plan_broadcast_graph(g, r, eps=0.1, gap=0.05):
     """Broadcast plan on an explicit link graph: MWU then ILP (Secs. 3.2, 3.2.1).
-    Returns dict(trees=[{parent, root, weight(Fraction), edges, depth}], rate, c_star)."""
+    Candidates = the union of the trees of the MWU runs (`mwu_runs`); c* = the
+    best MWU rate.  Returns dict(trees=[{parent, root, weight(Fraction), edges,
+    depth}], rate, c_star, grid, accepted)."""
     n, cap = g
     if n == 1:
         return dict(trees=[dict(parent=(-1,), root=0, weight=Fraction(1), edges=[], depth=0)],
                     rate=Fraction(1), c_star=1.0)
-    w, c_star, _ = mwu_broadcast(g, r, eps)
-    cands = sorted(set(w) | set(lovasz_arborescences(g, r)))  # parent tuples (R#21)
+    cands, c_star = set(), 0.0
+    for e, tb in mwu_runs(eps):
+        w, rate, _ = mwu_broadcast(g, r, e, tb)
+        cands |= set(w)
+        c_star = max(c_star, rate)
+    cands = sorted(cands)                                  # parent tuples
     cand = [([(u, v) for v, u in enumerate(p) if u >= 0], parent_depth(p), p) for p in cands]
-    sol, gg, ok = ilp_refine(cap, cand, c_star, gap)
-    if not ok:  # R#26: let a tree carry up to its bottleneck link count
-        sol2, gg2, ok2 = ilp_refine(cap, cand, c_star, gap, multiplicity=True)
-        if sum(w for _, w in sol2) > sum(w for _, w in sol):
-            sol, gg, ok = sol2, gg2, ok2
+    opt = optimal_rate(g, False, r, c_star)
+    sol, gg, ok = ilp_refine(cap, cand, opt, gap)
     trees = []
     for j, wt in sol:
         p = cands[j]
         trees.append(dict(parent=p, root=r, weight=wt, edges=cand[j][0], depth=cand[j][1]))
     trees = _order_trees(trees)
-    return dict(trees=trees, rate=sum(t["weight"] for t in trees), c_star=c_star, grid=gg, accepted=ok)
+    return dict(trees=trees, rate=sum(t["weight"] for t in trees), c_star=c_star, opt=opt, grid=gg,
+                accepted=ok)
 
 
 def plan_allreduce_graph(g, eps=0.1, gap=0.05):
-    """AllReduce plan on an explicit link graph: undirected MWU then ILP; each
-    tree rooted at its centre (Sec. 3.3)."""
+    """AllReduce plan on an explicit link graph: undirected MWU runs then ILP;
+    each tree rooted at its centre (Sec. 3.3)."""
     from .graphs import undirected_pairs
     n, cap = g
     if n == 1:
         return dict(trees=[dict(parent=(-1,), root=0, weight=Fraction(1), edges=[], depth=0)],
                     rate=Fraction(1), c_star=1.0)
     pairs = undirected_pairs(g)
-    w, c_star, _ = mwu_allreduce(pairs, n, eps)
-    peeled = set()
-    for scale in (1, 2, 4, 8):                     # R#21
-        peeled |= set(peel_spanning_trees(pairs, n, scale))
-    cands = sorted(set(w) | peeled)
+    cands, c_star = set(), 0.0
+    for e, tb in mwu_runs(eps):
+        w, rate, _ = mwu_allreduce(pairs, n, e, tb)
+        cands |= set(w)
+        c_star = max(c_star, rate)
+    cands = sorted(cands)
     cand = []
     for t in cands:
         root = tree_centre(t, n)
         cand.append((list(t), parent_depth(root_tree(t, n, root)), t))
-    sol, gg, ok = ilp_refine(pairs, cand, c_star, gap)
-    if not ok:  # R#26
-        sol2, gg2, ok2 = ilp_refine(pairs, cand, c_star, gap, multiplicity=True)
-        if sum(w for _, w in sol2) > sum(w for _, w in sol):
-            sol, gg, ok = sol2, gg2, ok2
+    opt = optimal_rate(g, True, 0, c_star)
+    sol, gg, ok = ilp_refine(pairs, cand, opt, gap)
     trees = []
     for j, wt in sol:
         t = cands[j]
@@ -428,7 +418,8 @@ def plan_allreduce_graph(g, eps=0.1, gap=0.05):
         trees.append(dict(parent=root_tree(t, n, root), root=root, weight=wt,
                           edges=list(t), depth=cand[j][1]))
     trees = _order_trees(trees)
-    return dict(trees=trees, rate=sum(t["weight"] for t in trees), c_star=c_star, grid=gg, accepted=ok)
+    return dict(trees=trees, rate=sum(t["weight"] for t in trees), c_star=c_star, opt=opt, grid=gg,
+                accepted=ok)
 
 
 def plan_switch_allreduce(m):

@@ -52,15 +52,18 @@ def build(force=False, verbose=False):
 
 def _build(verbose):
     objs = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:          # the sources compile concurrently
         obj = os.path.join(CSRC, "build", src + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
         cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log = r.stdout + r.stderr
-        if verbose or r.returncode != 0:
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                                 text=True)))
+    for src, obj, pr in procs:
+        log, _ = pr.communicate()
+        if verbose or pr.returncode != 0:
             sys.stderr.write(log)
-        if r.returncode != 0:
+        if pr.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}")
         with open(obj + ".ptxas.txt", "w") as f:
             f.write(log)

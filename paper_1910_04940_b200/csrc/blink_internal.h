@@ -63,7 +63,9 @@ struct Plan {                // size-independent (TreeGen output)
   int nranks = 0;
   std::vector<Tree> trees;   // in split order (R#11)
   int64_t rate_num = 0, rate_den = 1;
-  double c_star = 0.0;       // MWU rate (0 for closed forms)
+  double c_star = 0.0;       // best MWU rate (0 for closed forms)
+  double opt = 0.0;          // optimal rate the ILP ladder is measured against (R#3)
+  bool accepted = true;      // the ladder reached (1 - gap) * opt
   int grid = 1;              // accepted relaxation level g
   bool switch_model = false;
   bool blocks = false;       // tree i covers block i = [i*count, (i+1)*count) (RS / AG)

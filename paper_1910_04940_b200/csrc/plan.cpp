@@ -266,14 +266,15 @@ std::vector<int> min_arborescence(int n, int root, const std::vector<WEdge>& edg
   return parent;
 }
 
-// Kruskal over undirected pairs (u < v); ties (w, u, v).  Returns pair indices.
+// Kruskal over undirected pairs (u < v); ties (w, u, v) ascending, or (w,
+// -u, -v) with `desc` (the alternate MWU run).  Returns pair indices.
 std::vector<int> min_spanning_tree(int n, const std::vector<std::pair<int, int>>& pairs,
-                                   const std::vector<double>& w) {
+                                   const std::vector<double>& w, bool desc = false) {
   std::vector<int> idx(pairs.size());
   std::iota(idx.begin(), idx.end(), 0);
   std::sort(idx.begin(), idx.end(), [&](int a, int b) {
     if (w[a] != w[b]) return w[a] < w[b];
-    return pairs[a] < pairs[b];
+    return desc ? pairs[b] < pairs[a] : pairs[a] < pairs[b];
   });
   std::vector<int> uf(n);
   std::iota(uf.begin(), uf.end(), 0);
@@ -342,8 +343,6 @@ bool run_mwu(const std::vector<double>& c, double eps,
 }
 
 // ============================================================== ILP (Eqs. 4-7)
-// Branch and bound over candidate trees: maximise sum z, then fewest trees,
-// then least total depth; z_T in {0..g}; sum_{T contains e} z_T <= g c_e.
 struct IlpCand {
   std::vector<int> res;  // resources used (each once)
   int depth;
@@ -351,145 +350,453 @@ struct IlpCand {
   int prio = 0;          // 1: exact/peeled integral candidate, tried first
   int lovasz = 0;        // from the exact integral arborescence packing
   int mult[5] = {0, 0, 0, 0, 0};  // peel multiplicity at grid 1, 2, 4, 8, 16
+  int paper = 1;         // 1: returned by an MWU run (P:390's candidate set)
 };
 struct IlpSol {
   std::vector<int> z;
   int64_t sumz = -1;
   int ntrees = 0;
+  int maxdepth = 0;
   int64_t sumdepth = 0;
 };
+// Lexicographic ILP objective: maximise sum z, then fewest trees, then the
+// smallest maximum depth, then the least total depth (R#21: depth adds
+// pipeline latency).
+bool sol_better(int64_t sz, int nt, int md, int64_t sd, const IlpSol& b) {
+  if (sz != b.sumz) return sz > b.sumz;
+  if (nt != b.ntrees) return nt < b.ntrees;
+  if (md != b.maxdepth) return md < b.maxdepth;
+  return sd < b.sumdepth;
+}
 
-// Branch and bound for Eqs. 4-7 on the relaxation grid g: maximise sum z,
-// then fewest trees, then least total depth; z_T in {0..g};
-// sum_{T contains e} z_T <= g c_e.  The incumbent is seeded with the rounded
-// MWU solution floor(g x_T) plus a greedy fill (always feasible); candidates
-// are searched heaviest-MWU-weight first; a node budget keeps it bounded and
-// deterministic.
-class Ilp {
- public:
-  Ilp(const std::vector<IlpCand>& cand, const std::vector<double>& c, int g,
-      const std::function<int64_t(const std::vector<int64_t>&)>& cut_bound, int64_t node_limit,
-      bool multiplicity = false)
-      : cand_(cand), g_(g), cut_bound_(cut_bound), node_limit_(node_limit) {
-    res_.resize(c.size());
-    for (size_t e = 0; e < c.size(); ++e) res_[e] = int64_t(std::floor(g * c[e] + 1e-9));
-    // z_T <= g u_T: u_T = 1 (the paper's w_i <= 1) or, in the multiplicity
-    // fallback (R#26), the tree's bottleneck link count
-    ub_.resize(cand.size());
-    for (size_t j = 0; j < cand.size(); ++j) {
-      int64_t u = 1;
-      if (multiplicity) {
-        double b = 1e30;
-        for (int e : cand[j].res) b = std::min(b, c[e]);
-        u = std::max<int64_t>(1, int64_t(std::floor(b + 1e-9)));
-      }
-      ub_[j] = g * u;
+// ------------------------------------------------------------ LP-based B&B
+// Bounded-variable primal simplex: max c^T x s.t. A x <= b, 0 <= x <= u, with
+// b >= 0 (the slack basis is feasible).  Dense tableau; the problems here are
+// tiny (rows = links, <= ~120; columns = candidate trees).  Dantzig pricing,
+// switching to Bland's rule after a run of degenerate pivots (no cycling).
+struct BoundedLp {
+  int m = 0, n = 0;
+  std::vector<double> A;  // m x n, row-major
+  std::vector<double> b, c, u;
+  // returns the optimum; x gets the primal solution
+  double solve(std::vector<double>* x) const {
+    const int N = n + m;
+    const double tol = 1e-9;
+    std::vector<double> T(size_t(m) * N, 0.0);
+    for (int i = 0; i < m; ++i) {
+      for (int j = 0; j < n; ++j) T[size_t(i) * N + j] = A[size_t(i) * n + j];
+      T[size_t(i) * N + n + i] = 1.0;
     }
-    order_.resize(cand.size());
-    std::iota(order_.begin(), order_.end(), 0);
-    std::stable_sort(order_.begin(), order_.end(), [&](int a, int b) {
-      if (cand[a].prio != cand[b].prio) return cand[a].prio > cand[b].prio;
-      if (cand[a].x != cand[b].x) return cand[a].x > cand[b].x;
-      return cand[a].depth < cand[b].depth;
-    });
-    z_.assign(cand.size(), 0);
+    std::vector<double> beta(b), rc(N, 0.0), ub(N, INFINITY);
+    for (int j = 0; j < n; ++j) {
+      rc[j] = c[j];
+      ub[j] = u[j];
+    }
+    std::vector<int> basis(m), at_upper(N, 0), row_of(N, -1);
+    for (int i = 0; i < m; ++i) {
+      basis[i] = n + i;
+      row_of[n + i] = i;
+    }
+    int degenerate = 0;
+    for (int it = 0; it < 50000; ++it) {
+      int e = -1;
+      double bestrc = tol;
+      const bool bland = degenerate > 50;
+      for (int j = 0; j < N; ++j) {
+        if (row_of[j] >= 0 || ub[j] <= 0) continue;
+        const double d = at_upper[j] ? -rc[j] : rc[j];
+        if (d > bestrc) {
+          bestrc = d;
+          e = j;
+          if (bland) break;
+        }
+      }
+      if (e < 0) break;
+      const double dir = at_upper[e] ? -1.0 : 1.0;
+      double t = ub[e];
+      int r = -1;
+      bool leave_upper = false;
+      for (int i = 0; i < m; ++i) {
+        const double al = dir * T[size_t(i) * N + e];
+        if (al > tol) {
+          const double lim = std::max(0.0, beta[i]) / al;
+          if (lim < t - 1e-12 || (r >= 0 && lim <= t + 1e-12 && basis[i] < basis[r])) {
+            t = lim;
+            r = i;
+            leave_upper = false;
+          }
+        } else if (al < -tol && std::isfinite(ub[basis[i]])) {
+          const double lim = std::max(0.0, ub[basis[i]] - beta[i]) / -al;
+          if (lim < t - 1e-12 || (r >= 0 && lim <= t + 1e-12 && basis[i] < basis[r])) {
+            t = lim;
+            r = i;
+            leave_upper = true;
+          }
+        }
+      }
+      if (!std::isfinite(t)) break;  // unbounded (cannot happen: A >= 0, x bounded)
+      degenerate = t < 1e-12 ? degenerate + 1 : 0;
+      for (int i = 0; i < m; ++i) beta[i] -= dir * t * T[size_t(i) * N + e];
+      if (r < 0) {  // bound flip
+        at_upper[e] ^= 1;
+        continue;
+      }
+      const double enter_val = (at_upper[e] ? ub[e] : 0.0) + dir * t;
+      const int lv = basis[r];
+      row_of[lv] = -1;
+      at_upper[lv] = leave_upper ? 1 : 0;
+      basis[r] = e;
+      row_of[e] = r;
+      at_upper[e] = 0;
+      beta[r] = enter_val;
+      const double piv = T[size_t(r) * N + e];
+      double* R = &T[size_t(r) * N];
+      for (int j = 0; j < N; ++j) R[j] /= piv;
+      for (int i = 0; i < m; ++i) {
+        if (i == r) continue;
+        const double f = T[size_t(i) * N + e];
+        if (f == 0.0) continue;
+        double* Ri = &T[size_t(i) * N];
+        for (int j = 0; j < N; ++j) Ri[j] -= f * R[j];
+      }
+      const double f = rc[e];
+      for (int j = 0; j < N; ++j) rc[j] -= f * R[j];
+    }
+    x->assign(n, 0.0);
+    for (int j = 0; j < n; ++j)
+      (*x)[j] = row_of[j] >= 0 ? beta[row_of[j]] : (at_upper[j] ? ub[j] : 0.0);
+    double v = 0;
+    for (int j = 0; j < n; ++j) v += c[j] * (*x)[j];
+    return v;
   }
-  IlpSol solve() {
-    seed();
-    dfs(0, 0, 0, 0);
-    return best_;
+};
+
+// Eqs. 4-7 on one relaxation grid g by LP-based branch and bound: maximise
+// sum z (z_T in {0..g u_T}, sum_{T contains e} z_T <= g c_e), then -- among
+// solutions of that sum -- the tie-breaks of sol_better.  The LP relaxation
+// bounds every node; integral LP vertices have at most |E| trees, so the
+// search also finds few-tree solutions.  Minimum depth: the search is rerun
+// with the candidates restricted to depth <= D for each D; fewer trees: a
+// local search drops one used tree at a time and re-solves.
+class IlpBB {
+ public:
+  const int kDives = [] {
+    const char* e = getenv("BLINK_ILP_DIVES");
+    return e ? std::max(2, atoi(e)) : 18;
+  }();
+  IlpBB(const std::vector<IlpCand>& cand, const std::vector<double>& c, int g, bool multiplicity,
+        int64_t node_limit)
+      : cand_(cand), g_(g), node_limit_(node_limit) {
+    K_ = int(cand.size());
+    E_ = int(c.size());
+    cap_.resize(E_);
+    for (int e = 0; e < E_; ++e) cap_[e] = int64_t(std::floor(g * c[e] + 1e-9));
+    ub_.resize(K_);
+    for (int j = 0; j < K_; ++j) {
+      int64_t uu = 1;
+      if (multiplicity) {
+        double bmin = 1e30;
+        for (int e : cand[j].res) bmin = std::min(bmin, c[e]);
+        uu = std::max<int64_t>(1, int64_t(std::floor(bmin + 1e-9)));
+      }
+      ub_[j] = g * uu;
+    }
+  }
+  int64_t nodes() const { return nodes_; }
+  // max sum z (the paper's ILP objective) by LP-based branch and bound
+  IlpSol solve_sum() {
+    std::vector<int> all(K_);
+    std::iota(all.begin(), all.end(), 0);
+    return max_sum(all);
+  }
+  // tie-breaks at that sum: few and shallow trees.  LP diving under every
+  // depth bound D (the candidates restricted to depth <= D), then a local
+  // search that bans one used tree at a time and dives again; best by
+  // sol_better.
+  IlpSol refine(IlpSol best) {
+    if (best.sumz <= 0) return best;
+    const int64_t zstar = best.sumz;
+    std::set<int> depths;
+    for (int j = 0; j < K_; ++j) depths.insert(cand_[j].depth);
+    for (int D : depths) {
+      if (D > best.maxdepth) break;
+      std::vector<int> sub;
+      for (int j = 0; j < K_; ++j)
+        if (cand_[j].depth <= D) sub.push_back(j);
+      for (int variant = 0; variant < kDives; ++variant) {
+        IlpSol s = dive(sub, zstar, variant);
+        if (s.sumz == zstar && sol_better(s.sumz, s.ntrees, s.maxdepth, s.sumdepth, best)) best = s;
+      }
+    }
+    for (int round = 0; round < 16; ++round) {
+      std::vector<std::pair<int, int>> used;
+      for (int j = 0; j < K_; ++j)
+        if (best.z[j] > 0) used.push_back({best.z[j], j});
+      std::sort(used.begin(), used.end());
+      bool improved = false;
+      for (auto& uj : used) {
+        std::vector<int> sub;
+        for (int j = 0; j < K_; ++j)
+          if (j != uj.second && cand_[j].depth <= best.maxdepth) sub.push_back(j);
+        for (int variant = 0; variant < kDives && !improved; ++variant) {
+          IlpSol s = dive(sub, zstar, variant);
+          if (s.sumz == zstar && sol_better(s.sumz, s.ntrees, s.maxdepth, s.sumdepth, best)) {
+            best = s;
+            improved = true;
+          }
+        }
+        if (improved) break;
+      }
+      if (!improved) break;
+    }
+    return best;
   }
 
  private:
-  void seed() {
-    std::vector<int64_t> res = res_;
-    std::vector<int> z(cand_.size(), 0);
-    for (int pass = 0; pass < 2; ++pass)
-      for (int j : order_) {
-        int64_t want = pass == 0 ? int64_t(std::floor(g_ * cand_[j].x + 1e-9)) : ub_[j];
-        int64_t m = std::min<int64_t>(want, ub_[j]) - z[j];
-        for (int e : cand_[j].res) m = std::min(m, res[e]);
-        if (m <= 0) continue;
-        z[j] += int(m);
-        for (int e : cand_[j].res) res[e] -= m;
-      }
+  // max sum z over the candidates in `sub` (others fixed at 0).  `target` > 0:
+  // stop at the first solution reaching it.
+  IlpSol max_sum(const std::vector<int>& sub, int64_t target = -1) {
+    best_ = IlpSol();
+    best_.z.assign(K_, 0);
+    best_.sumz = 0;
+    sub_ = sub;
+    target_ = target;
+    nodes_ = 0;
+    // greedy incumbent (heaviest MWU weight first)
+    std::vector<int> ord = sub;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cand_[a].x > cand_[b].x; });
+    std::vector<int64_t> res = cap_;
+    std::vector<int> z(K_, 0);
+    for (int j : ord) {
+      int64_t m = ub_[j];
+      for (int e : cand_[j].res) m = std::min(m, res[e]);
+      if (m <= 0) continue;
+      z[j] = int(m);
+      for (int e : cand_[j].res) res[e] -= m;
+    }
     consider(z);
+    std::vector<int64_t> lo(K_, 0), hi(K_, 0);
+    for (int j : sub) hi[j] = ub_[j];
+    node(lo, hi);
+    return best_;
+  }
+  // LP diving toward few trees: repeatedly solve the LP over the free
+  // candidates and fix the one with the largest LP value at its rounded value
+  // (variant 1: rounded down), until the LP vertex is integral.  Stops
+  // without a solution if the target sum becomes unreachable.
+  IlpSol dive(const std::vector<int>& sub, int64_t zstar, int variant) {
+    IlpSol out;
+    // variants >= 2 perturb the LP objective (deterministic hash noise of
+    // 1e-4 per unit) so that different vertices, hence tree sets, come out
+    std::vector<double> cost(K_, 1.0);
+    if (variant >= 2)
+      for (int j = 0; j < K_; ++j) {
+        uint64_t h = uint64_t(j + 1) * 0x9E3779B97F4A7C15ull ^ uint64_t(variant) * 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 31;
+        h *= 0x94D049BB133111EBull;
+        h ^= h >> 29;
+        cost[j] = 1.0 + 1e-4 * double(h >> 11) / double(1ull << 53);
+      }
+    std::vector<int64_t> lo(K_, 0), hi(K_, 0);
+    for (int j : sub) hi[j] = ub_[j];
+    for (int step = 0; step <= K_; ++step) {
+      std::vector<int64_t> res = cap_;
+      int64_t base = 0;
+      for (int j : sub)
+        if (lo[j] > 0) {
+          base += lo[j];
+          for (int e : cand_[j].res) res[e] -= lo[j];
+        }
+      std::vector<int> cols;
+      for (int j : sub)
+        if (hi[j] > lo[j]) cols.push_back(j);
+      std::vector<double> x;
+      lp_over(cols, res, lo, hi, &x, &cost);
+      double v = 0;
+      for (double xq : x) v += xq;
+      if (base + int64_t(std::floor(v + 1e-7)) < zstar) return out;
+      int pick = -1;
+      bool integral = true;
+      for (size_t q = 0; q < cols.size(); ++q) {
+        const double f = x[q] - std::floor(x[q] + 1e-9);
+        if (std::min(f, 1.0 - f) > 1e-6) integral = false;
+        if (x[q] > 1e-6 && lo[cols[q]] == 0 &&
+            (pick < 0 || x[q] > x[pick] + 1e-9 ||
+             (x[q] > x[pick] - 1e-9 && cand_[cols[q]].depth < cand_[cols[pick]].depth)))
+          pick = int(q);
+      }
+      if (integral) {
+        std::vector<int> z(K_, 0);
+        int64_t sz = 0, sd = 0;
+        int nt = 0, md = 0;
+        for (int j : sub) z[j] = int(lo[j]);
+        for (size_t q = 0; q < cols.size(); ++q) z[cols[q]] += int(std::llround(x[q]));
+        for (int j = 0; j < K_; ++j)
+          if (z[j] > 0) {
+            sz += z[j];
+            ++nt;
+            sd += cand_[j].depth;
+            md = std::max(md, cand_[j].depth);
+          }
+        if (sz < zstar) return out;
+        out.z = z;
+        out.sumz = sz;
+        out.ntrees = nt;
+        out.maxdepth = md;
+        out.sumdepth = sd;
+        return out;
+      }
+      if (pick < 0) return out;
+      const int j = cols[pick];
+      int64_t val = variant == 1 ? int64_t(std::floor(x[pick] + 1e-9)) : int64_t(std::llround(x[pick]));
+      val = std::max<int64_t>(1, std::min<int64_t>(val, hi[j]));
+      lo[j] = hi[j] = val;  // fixed
+      // every other candidate the LP already puts at a positive integer stays
+      // there (fewer LP solves per dive)
+      for (size_t q = 0; q < cols.size(); ++q) {
+        const int jj = cols[q];
+        if (jj == j || lo[jj] > 0 || x[q] < 1.0 - 1e-6) continue;
+        const double f = x[q] - std::floor(x[q] + 1e-9);
+        if (std::min(f, 1.0 - f) > 1e-6) continue;
+        lo[jj] = hi[jj] = int64_t(std::llround(x[q]));
+      }
+    }
+    return out;
+  }
+  double lp_over(const std::vector<int>& cols, const std::vector<int64_t>& res,
+                 const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
+                 std::vector<double>* x, const std::vector<double>* cost = nullptr) const {
+    BoundedLp L;
+    L.m = E_;
+    L.n = int(cols.size());
+    if (L.n == 0) {
+      x->clear();
+      return 0.0;
+    }
+    L.A.assign(size_t(L.m) * L.n, 0.0);
+    L.b.resize(E_);
+    for (int e = 0; e < E_; ++e) L.b[e] = double(std::max<int64_t>(res[e], 0));
+    L.c.assign(L.n, 1.0);
+    L.u.resize(L.n);
+    for (int q = 0; q < L.n; ++q) {
+      const int j = cols[q];
+      for (int e : cand_[j].res) L.A[size_t(e) * L.n + q] += 1.0;
+      L.u[q] = double(hi[j] - lo[j]);
+      if (cost) L.c[q] = (*cost)[j];
+    }
+    return L.solve(x);
   }
   void consider(const std::vector<int>& z) {
     int64_t sz = 0, sd = 0;
-    int nt = 0;
-    for (size_t j = 0; j < z.size(); ++j)
+    int nt = 0, md = 0;
+    for (int j = 0; j < K_; ++j)
       if (z[j] > 0) {
         sz += z[j];
         ++nt;
         sd += cand_[j].depth;
+        md = std::max(md, cand_[j].depth);
       }
-    if (better(sz, nt, sd)) {
+    if (sol_better(sz, nt, md, sd, best_)) {
       best_.z = z;
       best_.sumz = sz;
       best_.ntrees = nt;
+      best_.maxdepth = md;
       best_.sumdepth = sd;
     }
   }
-  int64_t cap_of(int j) const {
-    int64_t m = ub_[j];
-    for (int e : cand_[j].res) m = std::min(m, res_[e]);
-    return std::max<int64_t>(m, 0);
-  }
-  int64_t upper(size_t k) const {
-    int64_t s = 0;
-    for (size_t t = k; t < order_.size(); ++t) s += cap_of(order_[t]);
-    return std::min(s, cut_bound_(res_));
-  }
-  bool better(int64_t sz, int nt, int64_t sd) const {
-    if (sz != best_.sumz) return sz > best_.sumz;
-    if (nt != best_.ntrees) return nt < best_.ntrees;
-    return sd < best_.sumdepth;
-  }
-  void dfs(size_t k, int64_t sz, int nt, int64_t sd) {
-    if (++nodes_ > node_limit_) return;
-    if (better(sz, nt, sd)) {
-      best_.z = z_;
-      best_.sumz = sz;
-      best_.ntrees = nt;
-      best_.sumdepth = sd;
-    }
-    if (k == order_.size()) return;
-    int64_t ub = upper(k);
-    if (sz + ub < best_.sumz) return;
-    if (sz + ub == best_.sumz || sz >= best_.sumz) {
-      // only a tie on sum z is reachable: it must use fewer trees or less depth
-      int64_t need = best_.sumz - sz;
-      int64_t more = need > 0 ? (need + g_ - 1) / g_ : 0;
-      if (sz + ub == best_.sumz && nt + more > best_.ntrees) return;
-      if (sz >= best_.sumz) return;  // adding trees can only worsen the tie-breaks
-    }
-    int j = order_[k];
-    int64_t cmax = cap_of(j);
-    for (int64_t zz = cmax; zz >= 0; --zz) {
-      if (zz > 0) {
-        for (int e : cand_[j].res) res_[e] -= zz;
-        z_[j] = int(zz);
-        dfs(k + 1, sz + zz, nt + 1, sd + cand_[j].depth);
-        z_[j] = 0;
-        for (int e : cand_[j].res) res_[e] += zz;
-      } else {
-        dfs(k + 1, sz, nt, sd);
+  bool done() const { return nodes_ > node_limit_ || (target_ > 0 && best_.sumz >= target_); }
+  void node(std::vector<int64_t>& lo, std::vector<int64_t>& hi) {
+    if (done()) return;
+    ++nodes_;
+    std::vector<int64_t> res = cap_;
+    int64_t base = 0;
+    for (int j : sub_)
+      if (lo[j] > 0) {
+        base += lo[j];
+        for (int e : cand_[j].res) res[e] -= lo[j];
       }
-      if (nodes_ > node_limit_) return;
+    for (int e = 0; e < E_; ++e)
+      if (res[e] < 0) return;  // infeasible
+    // LP over the free parts x' = z - lo
+    std::vector<int> cols;
+    for (int j : sub_)
+      if (hi[j] > lo[j]) cols.push_back(j);
+    std::vector<double> x;
+    const double v = lp_over(cols, res, lo, hi, &x);
+    const int64_t bound = base + int64_t(std::floor(v + 1e-7));
+    if (bound <= best_.sumz) return;  // ties are the business of refine()
+    // integral?
+    int br = -1;
+    double bfrac = 0;
+    for (int q = 0; q < int(cols.size()); ++q) {
+      const double f = x[q] - std::floor(x[q] + 1e-9);
+      const double d = std::min(f, 1.0 - f);
+      if (d > 1e-6 && d > bfrac) {
+        bfrac = d;
+        br = q;
+      }
     }
+    if (br < 0) {
+      std::vector<int> z(K_, 0);
+      for (int j : sub_) z[j] = int(lo[j]);
+      for (size_t q = 0; q < cols.size(); ++q) z[cols[q]] += int(std::llround(x[q]));
+      consider(z);
+      return;
+    }
+    const int j = cols[br];
+    const int64_t fl = lo[j] + int64_t(std::floor(x[br] + 1e-9));
+    const int64_t olo = lo[j], ohi = hi[j];
+    lo[j] = fl + 1;  // up branch first
+    node(lo, hi);
+    lo[j] = olo;
+    if (done()) return;
+    hi[j] = fl;
+    node(lo, hi);
+    hi[j] = ohi;
   }
   const std::vector<IlpCand>& cand_;
-  int g_;
-  std::function<int64_t(const std::vector<int64_t>&)> cut_bound_;
-  int64_t node_limit_;
-  int64_t nodes_ = 0;
-  std::vector<int64_t> res_;
-  std::vector<int64_t> ub_;
-  std::vector<int> order_;
-  std::vector<int> z_;
+  int g_, K_ = 0, E_ = 0;
+  int64_t node_limit_, nodes_ = 0, target_ = -1;
+  std::vector<int64_t> cap_, ub_;
+  std::vector<int> sub_;
   IlpSol best_;
 };
+
+// The relaxation ladder of P:390 over one candidate set: g = 1, 2, 4, 8, 16,
+// accept the first g whose rate sum z / g reaches (1 - gap) * opt; otherwise
+// the best rate seen (not accepted).
+struct Ladder {
+  IlpSol sol;
+  int g = 1;
+  bool accepted = false;
+  double rate() const { return sol.sumz < 0 ? -1.0 : double(sol.sumz) / g; }
+};
+Ladder run_ladder(const std::vector<IlpCand>& cands, const std::vector<double>& caps, double threshold,
+                  bool multiplicity, bool integral_first) {
+  Ladder best;
+  for (int gi = 0; gi < 5; ++gi) {
+    const int gg = 1 << gi;
+    std::vector<IlpCand> cg = cands;
+    if (integral_first)  // the exact packing (Broadcast) or this grid's peeling seed the incumbent
+      for (auto& c : cg) {
+        if (c.lovasz) c.x = 2.0;
+        if (c.mult[gi] > 0) c.x = 1.0 + double(c.mult[gi]) / gg;
+      }
+    IlpBB bb(cg, caps, gg, multiplicity, 2000);
+    IlpSol s = bb.solve_sum();
+    const double r = double(s.sumz) / gg;
+    if (getenv("BLINK_PLAN_DEBUG"))
+      fprintf(stderr, "ladder g=%d cands=%zu sum=%lld trees=%d nodes=%lld\n", gg, cands.size(),
+              (long long)s.sumz, s.ntrees, (long long)bb.nodes());
+    if (r >= threshold - 1e-12) return Ladder{bb.refine(s), gg, true};
+    if (r > best.rate() + 1e-12) best = Ladder{s, gg, false};
+  }
+  if (best.sol.sumz > 0) {
+    std::vector<IlpCand> cg = cands;
+    best.sol = IlpBB(cg, caps, best.g, multiplicity, 2000).refine(best.sol);
+  }
+  return best;
+}
 
 // Max flow (Edmonds-Karp) on a small dense integer capacity matrix.
 int64_t maxflow(std::vector<std::vector<int64_t>> c, int s, int t) {
@@ -513,6 +820,58 @@ int64_t maxflow(std::vector<std::vector<int64_t>> c, int s, int t) {
       c[v][prev[v]] += b;
     }
     flow += b;
+  }
+}
+
+// Max flow over real capacities (Edmonds-Karp on the directed edge list):
+// Edmonds' theorem gives the optimal Broadcast rate.
+double maxflow_real(const std::vector<double>& caps, const std::vector<WEdge>& edges, int n, int s,
+                    int t) {
+  std::vector<std::vector<double>> c(n, std::vector<double>(n, 0.0));
+  for (size_t j = 0; j < edges.size(); ++j) c[edges[j].u][edges[j].v] += caps[j];
+  double flow = 0;
+  while (true) {
+    std::vector<int> prev(n, -1);
+    prev[s] = s;
+    std::vector<int> q{s};
+    for (size_t h = 0; h < q.size() && prev[t] < 0; ++h)
+      for (int v = 0; v < n; ++v)
+        if (prev[v] < 0 && c[q[h]][v] > 1e-12) {
+          prev[v] = q[h];
+          q.push_back(v);
+        }
+    if (prev[t] < 0) return flow;
+    double b = INFINITY;
+    for (int v = t; v != s; v = prev[v]) b = std::min(b, c[prev[v]][v]);
+    for (int v = t; v != s; v = prev[v]) {
+      c[prev[v]][v] -= b;
+      c[v][prev[v]] += b;
+    }
+    flow += b;
+  }
+}
+
+// Nash-Williams / Tutte: the optimal fractional spanning-tree packing of an
+// undirected graph is min over partitions P (|P| >= 2) of cross(P) / (|P| - 1).
+// Partitions enumerated as restricted growth strings (Bell(8) = 4140).
+double nash_williams(int n, const std::vector<std::pair<int, int>>& pairs,
+                     const std::vector<double>& caps) {
+  std::vector<int> a(n, 0), mx(n, 0);
+  double best = INFINITY;
+  while (true) {
+    const int k = *std::max_element(a.begin(), a.end()) + 1;
+    if (k >= 2) {
+      double cross = 0;
+      for (size_t j = 0; j < pairs.size(); ++j)
+        if (a[pairs[j].first] != a[pairs[j].second]) cross += caps[j];
+      best = std::min(best, cross / (k - 1));
+    }
+    int i = n - 1;  // next restricted growth string
+    while (i > 0 && a[i] == mx[i - 1] + 1) --i;
+    if (i == 0) return best;
+    ++a[i];
+    for (int j = i + 1; j < n; ++j) a[j] = 0;
+    for (int j = i; j < n; ++j) mx[j] = std::max(mx[j - 1], a[j]);
   }
 }
 
@@ -802,19 +1161,35 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
     return make_multiserver_plan(g, cfg, out, err);
   }
 
-  // ---------------- explicit link graph: MWU then ILP
+  // ---------------- explicit link graph: MWU runs, then the ILP ladder
   double cmin = INFINITY;
   for (int u = 0; u < n; ++u)
     for (int v = 0; v < n; ++v)
       if (g.cap[u][v] > 0) cmin = std::min(cmin, g.cap[u][v]);
   const double eps = cfg.mwu_eps > 0 ? cfg.mwu_eps : 0.1;
   const double gap = cfg.ilp_gap > 0 ? cfg.ilp_gap : 0.05;
+  // P:390's candidates: the trees of several MWU runs (the configured eps and
+  // eps / 2, each with ascending and descending tie-breaks; SURVEY 7 hard
+  // part 8); c* = the best MWU rate.  Same runs as oracle/packing.py mwu_runs.
+  const double run_eps[4] = {eps, eps, eps / 2, eps / 2};
+  const bool run_desc[4] = {false, true, false, true};
 
   std::vector<IlpCand> cands;
   std::vector<std::vector<int>> cand_parent;
   std::vector<double> caps;
-  std::function<int64_t(const std::vector<int64_t>&)> cut;
-  double c_star = 0;
+  double c_star = 0, opt = 0;
+  std::map<std::vector<int>, int> cand_of;  // resource list -> candidate index
+  auto add_cand = [&](const std::vector<int>& res, const std::vector<int>& par, double x) -> int {
+    auto it = cand_of.find(res);
+    if (it != cand_of.end()) {
+      cands[it->second].x = std::max(cands[it->second].x, x);
+      return it->second;
+    }
+    cand_of[res] = int(cands.size());
+    cands.push_back({res, tree_depth(par), x});
+    cand_parent.push_back(par);
+    return int(cands.size()) - 1;
+  };
   if (coll == kBroadcast) {
     // resources = directed edges, capacities in units of the smallest link
     std::vector<WEdge> edges;
@@ -843,30 +1218,36 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
         return BLINK_ERR_TOPOLOGY;
       }
     std::map<int, int> key_to_res;
-    for (size_t j = 0; j < edges.size(); ++j) key_to_res[edges[j].key] = int(j);
-    MwuResult mr;
-    auto tree_of = [&](const std::vector<double>& len) {
-      for (size_t j = 0; j < edges.size(); ++j) edges[j].w = len[j];
-      std::vector<int> par = min_arborescence(n, root, edges);
-      std::vector<int> res;
-      if (par.empty()) return res;
-      for (int v = 0; v < n; ++v)
-        if (par[v] >= 0) res.push_back(key_to_res[par[v] * n + v]);
-      std::sort(res.begin(), res.end());
-      return res;
-    };
-    if (!run_mwu(caps, eps, tree_of, &mr)) {
-      *err = "MWU failed to converge";
-      return BLINK_ERR_INTERNAL;
+    for (size_t j = 0; j < edges.size(); ++j) key_to_res[edges[j].u * n + edges[j].v] = int(j);
+    for (int run = 0; run < 4; ++run) {
+      for (auto& e : edges) e.key = run_desc[run] ? n * n - (e.u * n + e.v) : e.u * n + e.v;
+      MwuResult mr;
+      auto tree_of = [&](const std::vector<double>& len) {
+        for (size_t j = 0; j < edges.size(); ++j) edges[j].w = len[j];
+        std::vector<int> par = min_arborescence(n, root, edges);
+        std::vector<int> res;
+        if (par.empty()) return res;
+        for (int v = 0; v < n; ++v)
+          if (par[v] >= 0) res.push_back(key_to_res[par[v] * n + v]);
+        std::sort(res.begin(), res.end());
+        return res;
+      };
+      if (!run_mwu(caps, run_eps[run], tree_of, &mr)) {
+        *err = "MWU failed to converge";
+        return BLINK_ERR_INTERNAL;
+      }
+      c_star = std::max(c_star, mr.rate);
+      for (auto& kv : mr.x) {
+        std::vector<int> par(n, -1);
+        for (int e : kv.first) par[edges[e].v] = edges[e].u;
+        add_cand(kv.first, par, kv.second);
+      }
     }
-    c_star = mr.rate;
-    for (auto& kv : mr.x) {
-      std::vector<int> par(n, -1);
-      for (int e : kv.first) par[edges[e].v] = edges[e].u;
-      cands.push_back({kv.first, tree_depth(par), kv.second});
-      cand_parent.push_back(par);
-    }
-    // exact integral candidates (Lovasz), weight 1 each
+    // Edmonds' theorem: the optimal rate is min_v maxflow(root -> v)
+    opt = INFINITY;
+    for (int v = 0; v < n; ++v)
+      if (v != root) opt = std::min(opt, maxflow_real(caps, edges, n, root, v));
+    // product extra: exact integral candidates (Lovasz), weight 1 each
     {
       std::vector<std::vector<int64_t>> ic(n, std::vector<int64_t>(n, 0));
       for (size_t j = 0; j < edges.size(); ++j)
@@ -876,24 +1257,12 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
         for (int v = 0; v < n; ++v)
           if (par[v] >= 0) res.push_back(key_to_res[par[v] * n + v]);
         std::sort(res.begin(), res.end());
-        IlpCand c{res, tree_depth(par), 0.0};
-        c.lovasz = 1;
-        cands.push_back(c);
-        cand_parent.push_back(par);
+        const bool known = cand_of.count(res) > 0;
+        const int j = add_cand(res, par, 0.0);
+        cands[j].lovasz = 1;
+        if (!known) cands[j].paper = 0;
       }
     }
-    // every arborescence enters each non-root vertex once: sum z <= min_v in-capacity
-    cut = [n, root, edges](const std::vector<int64_t>& res) {
-      int64_t b = INT64_MAX;
-      for (int v = 0; v < n; ++v) {
-        if (v == root) continue;
-        int64_t s = 0;
-        for (size_t j = 0; j < edges.size(); ++j)
-          if (edges[j].v == v) s += std::max<int64_t>(res[j], 0);
-        b = std::min(b, s);
-      }
-      return b;
-    };
   } else {
     // undirected pairs; every link needs its reverse
     std::vector<std::pair<int, int>> pairs;
@@ -910,22 +1279,25 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
           caps.push_back(std::min(g.cap[u][v], g.cap[v][u]) / cmin);
         }
       }
-    MwuResult mr;
-    auto tree_of = [&](const std::vector<double>& len) { return min_spanning_tree(n, pairs, len); };
-    if (!run_mwu(caps, eps, tree_of, &mr)) {
-      *err = "MWU failed (graph disconnected?)";
-      return BLINK_ERR_TOPOLOGY;
+    for (int run = 0; run < 4; ++run) {
+      MwuResult mr;
+      const bool desc = run_desc[run];
+      auto tree_of = [&](const std::vector<double>& len) { return min_spanning_tree(n, pairs, len, desc); };
+      if (!run_mwu(caps, run_eps[run], tree_of, &mr)) {
+        *err = "MWU failed (graph disconnected?)";
+        return BLINK_ERR_TOPOLOGY;
+      }
+      c_star = std::max(c_star, mr.rate);
+      for (auto& kv : mr.x) {
+        std::vector<std::pair<int, int>> te;
+        for (int e : kv.first) te.push_back(pairs[e]);
+        add_cand(kv.first, orient(n, te, centre(n, te)), kv.second);
+      }
     }
-    c_star = mr.rate;
-    for (auto& kv : mr.x) {
-      std::vector<std::pair<int, int>> te;
-      for (int e : kv.first) te.push_back(pairs[e]);
-      int r = centre(n, te);
-      std::vector<int> par = orient(n, te, r);
-      cands.push_back({kv.first, tree_depth(par), kv.second});
-      cand_parent.push_back(par);
-    }
-    // greedy integral peelings at the grid scales (multiplicity / g each)
+    // Nash-Williams: the optimal undirected packing rate, by partition
+    // enumeration up to 8 GPUs; larger allocations use the MWU rate
+    opt = n <= 8 ? nash_williams(n, pairs, caps) : c_star;
+    // product extra: greedy integral peelings at the grid scales
     for (int gi = 0; gi < 4; ++gi) {
       const int gg = 1 << gi;
       std::vector<int64_t> res(caps.size());
@@ -935,72 +1307,63 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
       for (auto& kv : mult) {
         std::vector<std::pair<int, int>> te;
         for (int e : kv.first) te.push_back(pairs[e]);
-        int r = centre(n, te);
-        std::vector<int> par = orient(n, te, r);
-        IlpCand c{kv.first, tree_depth(par), 0.0};
-        c.mult[gi] = kv.second;
-        cands.push_back(c);
-        cand_parent.push_back(par);
+        const bool known = cand_of.count(kv.first) > 0;
+        const int j = add_cand(kv.first, orient(n, te, centre(n, te)), 0.0);
+        cands[j].mult[gi] += kv.second;
+        if (!known) cands[j].paper = 0;
       }
     }
-    // every spanning tree uses n-1 links: sum z <= sum res / (n-1)
-    cut = [n](const std::vector<int64_t>& res) {
-      int64_t s = 0;
-      for (int64_t r : res) s += std::max<int64_t>(r, 0);
-      return s / (n - 1);
-    };
   }
   out->c_star = c_star;
-  {
-    std::map<std::vector<int>, int> seen;
-    std::vector<IlpCand> c2;
-    std::vector<std::vector<int>> p2;
-    for (size_t j = 0; j < cands.size(); ++j) {
-      auto it = seen.find(cands[j].res);
-      if (it != seen.end()) {
-        IlpCand& d = c2[it->second];
-        d.x = std::max(d.x, cands[j].x);
-        d.lovasz |= cands[j].lovasz;
-        for (int q = 0; q < 5; ++q) d.mult[q] += cands[j].mult[q];
-        continue;
-      }
-      seen[cands[j].res] = int(c2.size());
-      c2.push_back(cands[j]);
-      p2.push_back(cand_parent[j]);
-    }
-    cands.swap(c2);
-    cand_parent.swap(p2);
-  }
+  out->opt = opt;
 
-  // ILP with the relaxation grid g = 1, 2, 4, 8, 16 (R#5)
+  // the ILP over the MWU candidates with the relaxation ladder,
+  // accepted within `gap` of the optimal rate (R#3).  Product heuristics
+  // (R#21: Lovasz / peeled candidates; R#26: multiplicity) run afterwards and
+  // replace the paper's plan only when it missed the threshold or when they
+  // reach it with fewer trees / shallower trees.
+  const double threshold = (1.0 - gap) * opt;
+  std::vector<IlpCand> paper_cands;
+  std::vector<int> paper_idx;
+  for (size_t j = 0; j < cands.size(); ++j)
+    if (cands[j].paper) {
+      paper_cands.push_back(cands[j]);
+      paper_idx.push_back(int(j));
+    }
+  Ladder lp = run_ladder(paper_cands, caps, threshold, false, false);
+  // map the paper solution onto the full candidate list
   IlpSol best;
-  int bestg = 1;
-  bool accepted = false;
-  for (int pass = 0; pass < 2 && !accepted; ++pass) {  // pass 1: multiplicity fallback (R#26)
-    for (int gi = 0; gi < 5; ++gi) {
-      const int gg = 1 << gi;
-      // integral candidates first: the exact packing (Broadcast) or the peeling
-      // at this grid scale, seeded with their multiplicity
-      std::vector<IlpCand> cg = cands;
-      for (auto& c : cg) {
-        c.prio = (c.lovasz || c.mult[gi] > 0) ? 1 : 0;
-        if (c.lovasz) c.x = 1.0;
-        if (c.mult[gi] > 0) c.x = double(c.mult[gi]) / gg;
-      }
-      Ilp ilp(cg, caps, gg, cut, 200000, pass == 1);
-      IlpSol s = ilp.solve();
-      if (best.sumz < 0 || double(s.sumz) / gg > double(best.sumz) / bestg + 1e-12) {
-        best = s;
-        bestg = gg;
-      }
-      if (double(s.sumz) / gg >= (1.0 - gap) * c_star - 1e-12) {
-        best = s;
-        bestg = gg;
-        accepted = true;
-        break;
-      }
+  best.z.assign(cands.size(), 0);
+  for (size_t q = 0; q < paper_idx.size(); ++q)
+    if (!lp.sol.z.empty()) best.z[paper_idx[q]] = lp.sol.z[q];
+  best.sumz = lp.sol.sumz;
+  best.ntrees = lp.sol.ntrees;
+  best.maxdepth = lp.sol.maxdepth;
+  best.sumdepth = lp.sol.sumdepth;
+  int bestg = lp.g;
+  bool accepted = lp.accepted;
+  for (int pass = 0; pass < 2; ++pass) {  // pass 1: multiplicity fallback (R#26)
+    if (pass == 1 && accepted) break;
+    Ladder lx = run_ladder(cands, caps, threshold, pass == 1, true);
+    bool take;
+    if (lx.accepted != accepted) {
+      take = lx.accepted;
+    } else if (!accepted) {
+      take = lx.rate() > double(best.sumz) / bestg + 1e-12;
+    } else {  // both accepted: fewer trees, then shallower, then higher rate
+      const IlpSol& a = lx.sol;
+      if (a.ntrees != best.ntrees) take = a.ntrees < best.ntrees;
+      else if (a.maxdepth != best.maxdepth) take = a.maxdepth < best.maxdepth;
+      else if (a.sumdepth != best.sumdepth) take = a.sumdepth < best.sumdepth;
+      else take = lx.rate() > double(best.sumz) / bestg + 1e-12;
+    }
+    if (take) {
+      best = lx.sol;
+      bestg = lx.g;
+      accepted = lx.accepted;
     }
   }
+  out->accepted = accepted;
   std::vector<std::vector<std::pair<int, int>>> keys;
   for (size_t j = 0; j < cands.size(); ++j) {
     if (best.z.empty() || best.z[j] == 0) continue;
@@ -1238,11 +1601,13 @@ blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_con
 std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vector<TreeRange>& r,
                          int ctas) {
   std::ostringstream o;
+  o.precision(17);
   static const char* names[] = {"broadcast", "allreduce", "reduce_scatter", "allgather", "gather"};
   o << "{\"coll\":\"" << names[p.coll] << "\",\"root\":"
     << p.root << ",\"nranks\":" << p.nranks << ",\"count\":" << count << ",\"esize\":" << esize
     << ",\"switch\":" << (p.switch_model ? "true" : "false") << ",\"rate\":[" << p.rate_num << ","
-    << p.rate_den << "],\"c_star\":" << p.c_star << ",\"grid\":" << p.grid << ",\"ctas\":" << ctas
+    << p.rate_den << "],\"c_star\":" << p.c_star << ",\"opt\":" << p.opt
+    << ",\"accepted\":" << (p.accepted ? "true" : "false") << ",\"grid\":" << p.grid << ",\"ctas\":" << ctas
     << ",\"trees\":[";
   for (size_t i = 0; i < p.trees.size(); ++i) {
     const Tree& t = p.trees[i];

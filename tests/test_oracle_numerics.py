@@ -225,7 +225,7 @@ def test_avg_of_identical_inputs_is_the_input(dtype):
     vals = np.array([0.75, -1.5, 3.0, 0.0, 96.0, -0.125], dtype=np.float32)
     x = C.f32_to_bf16(vals) if dtype == "bf16" else vals
     for m, plan in ((8, packing.plan_switch_allreduce(8)),
-                    (8, packing.plan_allreduce_graph(graphs.dgx1v())),
+                    (8, packing.plan_allreduce_graph(graphs.dgx1p())),
                     (5, packing.plan_switch_allreduce(5))):
         got = C.allreduce(plan, [x] * m, dtype, "avg")
         assert np.array_equal(np.asarray(got).view(np.uint16 if dtype == "bf16" else np.uint32),
