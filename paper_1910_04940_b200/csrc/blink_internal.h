@@ -131,7 +131,7 @@ struct LaunchArgs {
   int scope_sys;             // 1: flags cross devices/processes (.sys), 0: one device (.gpu)
   int store_depth;           // bulk-store groups kept in flight (-1 = default)
   int l2_hint;               // 1: TMA loads/stores carry an L2 evict-first policy
-  int pad3;
+  int defer_signal;          // 1: chunk signals wait for their own bulk group only (no drain)
   uint64_t* trace;           // BLINK_TRACE: kTraceSlots globaltimer stamps per CTA, else NULL
   int nctr;                  // chunk counters ctrl[2 .. 2 + nctr) zeroed by the last CTA
   int split_ring;            // 1: signalling copies alternate chunks over two store threads

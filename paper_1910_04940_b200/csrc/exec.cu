@@ -392,6 +392,10 @@ __device__ __forceinline__ void tma_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_group() {  // all but the N newest groups complete (writes done)
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
@@ -459,6 +463,16 @@ __device__ __forceinline__ bool mbar_wait_or_abort(uint64_t* bar, uint32_t phase
     if (done) return true;
     if ((spin & 63) == 63 && sh.abort) return false;
   }
+}
+// Non-blocking probe of an mbarrier phase.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t done;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return done != 0;
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -674,20 +688,54 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
     };
     int kept = 0;
     bool first = true;
+    // Deferred chunk signals (a5): a finished chunk is published once its
+    // bulk-store group has completed, without draining the stores behind it.
+    // Groups complete in order, so after wait_group<kSigDepth> every chunk
+    // whose last group is at least kSigDepth groups old is complete.  When
+    // the next tile is not ready yet the store thread drains instead (nothing
+    // to overlap, and a deep tree's next hop waits on this signal).
+    constexpr int kSigDepth = 3;
+    constexpr int kPend = 8;
+    int pend_c[kPend];
+    uint32_t pend_g[kPend];
+    int npend = 0;
+    uint32_t groups = 0;  // bulk groups committed so far
+    auto publish_upto = [&](uint32_t done_groups) {  // groups [0, done_groups) are complete
+      int k = 0;
+      while (k < npend && pend_g[k] <= done_groups) ++k;
+      if (k == 0) return;
+      fence_proxy_async();
+      for (int q = 0; q < k; ++q) signal_chunk(a, t, pend_c[q], is_root, ctl);
+      for (int q = k; q < npend; ++q) {
+        pend_c[q - k] = pend_c[q];
+        pend_g[q - k] = pend_g[q];
+      }
+      npend -= k;
+    };
     for (uint32_t g = 0;; ++g) {
       TileMeta mt;
       const char* src;
+      uint64_t* fb;
+      uint32_t par;
       if (reduce) {
         const uint32_t o = g % K;
-        if (!mbar_wait_or_abort(&sh.ofull[o], (g / K) & 1u, sh)) break;
-        mt = sh.ometa[o];
+        fb = &sh.ofull[o];
+        par = (g / K) & 1u;
         src = out + size_t(o) * tile;
       } else {
         const uint32_t s = r * H + g % H;
-        if (!mbar_wait_or_abort(&sh.full[s], (g / H) & 1u, sh)) break;
-        mt = sh.smeta[s];
+        fb = &sh.full[s];
+        par = (g / H) & 1u;
         src = ring + size_t(s) * tile;
       }
+      if (npend > 0 && !mbar_test(fb, par)) {  // idle: publish everything now
+        tma_wait_all();
+        for (int j = kept - 1; j >= 0; --j) release(g - 1u - uint32_t(j));
+        kept = 0;
+        publish_upto(groups);
+      }
+      if (!mbar_wait_or_abort(fb, par, sh)) break;
+      mt = reduce ? sh.ometa[g % K] : sh.smeta[r * H + g % H];
       if (mt.c < 0) break;
       if (a.l2_hint) {
         const uint64_t pol = l2_evict_first_policy();
@@ -696,6 +744,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         for (int d = 0; d < ndst && mt.tb > 0; ++d) tma_store(sh.dsts[d] + mt.off, src, uint32_t(mt.tb));
       }
       tma_commit();
+      ++groups;
       if (first) {
         trace(a, 4);
         first = false;
@@ -710,16 +759,28 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         release(g - uint32_t(D));
         --kept;
       }
-      if (mt.last && need_signal) {  // chunk complete: drain, publish
-        tma_wait_all();
-        fence_proxy_async();
-        for (int j = kept - 1; j >= 0; --j) release(g - uint32_t(j));
-        kept = 0;
-        signal_chunk(a, t, mt.c, is_root, ctl);
+      if (need_signal) {
+        if (mt.last) {
+          if (npend == kPend) {  // full: drain the oldest first
+            tma_wait_all();
+            publish_upto(groups);
+          }
+          pend_c[npend] = mt.c;
+          pend_g[npend] = groups;
+          ++npend;
+        }
+        if (npend > 0 && !a.defer_signal) {  // BLINK_DEFER_SIGNAL=0: drain per chunk
+          tma_wait_all();
+          publish_upto(groups);
+        } else if (npend > 0 && groups >= uint32_t(kSigDepth) && pend_g[0] <= groups - kSigDepth) {
+          tma_wait_group<kSigDepth>();
+          publish_upto(groups - kSigDepth);
+        }
       }
     }
     tma_wait_all();
     fence_proxy_async();
+    if (npend > 0) publish_upto(groups);
     trace(a, 5);
   } else if (reduce && warp >= 2) {
     // ------------------------------------------------ consumers
@@ -1422,8 +1483,13 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = vec ? a.smem_bytes : 0;
-  static bool attr_set[5][3][5][2] = {};
-  bool& done = attr_set[a.coll][a.dtype][a.op][vec];
+  // cudaFuncSetAttribute is per device: remember it per (device, kernel)
+  constexpr int kDevs = 64;
+  static bool attr_set[kDevs][5][3][5][2] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) dev = -1;
+  bool unknown_dev = false;
+  bool& done = dev >= 0 ? attr_set[dev][a.coll][a.dtype][a.op][vec] : unknown_dev;
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          vec ? kMaxSmemBytes : 0);

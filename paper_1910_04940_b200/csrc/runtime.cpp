@@ -741,6 +741,14 @@ int l2_hint() {
   }();
   return v;
 }
+// deferred chunk signals (exec.cu run_ws); BLINK_DEFER_SIGNAL=0 drains per chunk
+int defer_signal() {
+  static int v = [] {
+    const char* e = getenv("BLINK_DEFER_SIGNAL");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
 int tile_bytes() {
   static int v = [] {
     const char* e = getenv("BLINK_TILE");
@@ -1072,6 +1080,7 @@ blink_result_t clique_launch(Clique* q) {
     a.split_ring = split_ring();
     a.copy_stages = copy_stages();
     a.l2_hint = l2_hint();
+    a.defer_signal = defer_signal();
     a.nctr = s.nctr;
     a.ctrl = q->ctrl[grp.key];
     if (trace_on()) {
@@ -1211,7 +1220,45 @@ struct Blob {
   uint64_t ll_max_bytes;  // the LL-or-tree decision must be the same on every rank
   uint64_t shallow_max_bytes;       // so must the plan choices by size (R#27,
   uint64_t onehop_bcast_max_bytes;  // the switch Broadcast star)
+  uint64_t chunk_fp;                // and every input of the chunk table (a chunk's flags name bytes)
 };
+
+// Fingerprint of everything the chunk table (size_plan / build_sized) reads:
+// config fields, the SM count and the environment overrides.  Ranks whose
+// chunking differs would consume each other's flags for different byte
+// ranges, so blink_connect refuses to mix them.
+uint64_t chunking_fingerprint(blink_comm_t comm) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  mix(comm->cfg.chunk_bytes);
+  mix(uint64_t(comm->cfg.ctas));
+  mix(uint64_t(comm->cfg.threads));
+  mix(uint64_t(comm->cfg.autotune));
+  uint64_t d;
+  memcpy(&d, &comm->cfg.mwu_eps, sizeof d);  // the plan's trees (MWU / ILP settings)
+  mix(d);
+  memcpy(&d, &comm->cfg.ilp_gap, sizeof d);
+  mix(d);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
+  mix(uint64_t(sms));
+  static const char* envs[] = {"BLINK_CHUNK_BYTES", "BLINK_CTAS", "BLINK_MIN_CHUNK", "BLINK_MIN_CHUNK_DEEP",
+                               "BLINK_DEEP_CAP", "BLINK_CHUNKS_PER_CTA", "BLINK_SMEM_KB", "BLINK_TILE",
+                               "BLINK_TMA", "BLINK_ONE_CHUNK", "BLINK_MERGE", "BLINK_DYNAMIC",
+                               "BLINK_PACK", "BLINK_THREADS", "BLINK_MIAD", "BLINK_ILP_DIVES",
+                               "BLINK_LL_TREE"};
+  for (const char* name : envs) {
+    const char* e = getenv(name);
+    mix(0x5eedull);
+    for (const char* q = e ? e : ""; *q; ++q) mix(uint64_t(uint8_t(*q)));
+  }
+  return h;
+}
 struct RegBlob {
   char magic[8];
   int32_t rank, pad;
@@ -1294,6 +1341,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     a.split_ring = split_ring();
     a.copy_stages = copy_stages();
   a.l2_hint = l2_hint();
+  a.defer_signal = defer_signal();
   a.nctr = s.nctr;
   a.ctrl = comm->ctrl;
   a.timeout_ns = uint64_t(comm->cfg.timeout_s * 1e9);
@@ -1335,7 +1383,10 @@ blink_result_t mp_block_collective(blink_comm_t comm, int coll, const void* send
       return mp_run(comm, coll, sp, rp, count, dtype, op, -1, stream);
   } else {
     sp[me] = const_cast<char*>(sb);
-    if (recvbuf && resolve(comm, recvbuf, size_t(m) * count * es, rp))
+    // Every rank must take the same path (the flags name the same bytes).
+    // Gather's non-roots may pass recvbuf = NULL, so Gather always stages;
+    // AllGather's registration is collective (symmetric on every rank).
+    if (coll == kAllGather && recvbuf && resolve(comm, recvbuf, size_t(m) * count * es, rp))
       return mp_run(comm, coll, sp, rp, count, dtype, op, root, stream);
   }
   const size_t P = std::max<size_t>(1, comm->staging_bytes / (size_t(m) * es));
@@ -1734,6 +1785,7 @@ blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_b
   b.ll_max_bytes = comm->ll_bytes ? comm->cfg.ll_max_bytes : 0;
   b.shallow_max_bytes = comm->cfg.shallow_max_bytes;
   b.onehop_bcast_max_bytes = comm->cfg.onehop_bcast_max_bytes;
+  b.chunk_fp = chunking_fingerprint(comm);
   memcpy(blob, &b, sizeof b);
   return BLINK_SUCCESS;
 }
@@ -1759,6 +1811,11 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
         b.onehop_bcast_max_bytes != comm->cfg.onehop_bcast_max_bytes)
       return fail(comm, BLINK_ERR_INVALID_USAGE,
                   "shallow_max_bytes / onehop_bcast_max_bytes differ across ranks");
+    if (b.chunk_fp != chunking_fingerprint(comm))
+      return fail(comm, BLINK_ERR_INVALID_USAGE,
+                  "rank " + std::to_string(u) +
+                      " chunks differently (cfg.chunk_bytes / ctas / threads / autotune, SM count or "
+                      "BLINK_* chunking overrides differ)");
     if (u == comm->rank) {
       comm->peer_flags[u] = comm->flags;
       comm->peer_staging[u] = comm->staging;

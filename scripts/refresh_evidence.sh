@@ -15,8 +15,10 @@ python scripts/sweep.py --out $O/sweep.json > $O/sweep.log 2>&1
 python scripts/trace_probe.py 8 > $O/trace.txt 2>&1
 BLINK_LL_MAX=0 python scripts/trace_probe.py 8 >> $O/trace.txt 2>&1
 python scripts/per_rank_sweep.py --out $O/per_rank_sweep.json > $O/per_rank_sweep.log 2>&1 || true
+# full logs (no tail: the round-1 logs hid a failing script behind `tail -3`)
 for t in memcheck synccheck racecheck; do
   echo "=== compute-sanitizer --tool $t python scripts/sanitize_cases.py"
-  timeout 900 compute-sanitizer --tool $t python scripts/sanitize_cases.py 2>&1 | tail -3
+  timeout 1200 compute-sanitizer --tool $t python scripts/sanitize_cases.py 2>&1
+  echo "=== exit $?"
 done > $O/sanitizer.txt
 echo done

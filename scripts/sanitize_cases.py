@@ -1,10 +1,18 @@
 #!/usr/bin/env python
-"""Small collectives for compute-sanitizer (memcheck / synccheck / racecheck):
-one-hop AllReduce (TMA and LSU paths), emulated DGX-1V Broadcast and
-multi-level AllReduce, ReduceScatter / AllGather, misaligned buffers, the LL
-protocol (batched and per-rank launches) and a per-rank tree AllReduce.
-Every result is checked against the oracle so a clean sanitizer run is also a
-correct run."""
+"""Small collectives for compute-sanitizer (memcheck / synccheck / racecheck).
+
+One section per executor path, each with its thresholds pinned in its own
+config so a later change of a default cannot silently move a case onto another
+path (the round-1 script broke that way).  Every section checks which path ran
+(`stats()`: LL calls report 0 chunks) and checks every result against the
+oracle, so a clean sanitizer run is also a correct run.  It prints
+"ok <section>" per section and "sanitize cases ok" at the end.
+
+Sections: one-hop tree executor (TMA aligned, LSU misaligned), bf16, AVG,
+ReduceScatter / AllGather, DGX-1V packed Broadcast and multi-level AllReduce,
+the R#27 shallow tree on the tree executor, the shallow tree in the LL
+protocol, switch LL (batched and per-rank launches), per-rank tree AllReduce.
+"""
 import os
 import sys
 
@@ -16,125 +24,189 @@ import paper_1910_04940_b200 as B  # noqa: E402
 import synth  # noqa: E402
 from oracle import collectives as OC  # noqa: E402
 from oracle import graphs as OG  # noqa: E402
+from oracle import packing as OP  # noqa: E402
+
+T = 120.0  # flag-wait timeout: the sanitizers slow kernels down by 100x and more
+
+
+def dev(a, dtype="f32"):
+    a = np.ascontiguousarray(a)
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
 
 
 def check(got, want, what):
-    g = got.cpu().numpy().view(np.uint32)
-    if not np.array_equal(g, np.asarray(want).view(np.uint32)):
+    g = got.contiguous().view(torch.uint8).cpu().numpy().tobytes()
+    if g != np.ascontiguousarray(want).tobytes():
         raise SystemExit(f"MISMATCH {what}")
 
 
-def main():
-    cfg = B.config(timeout_s=120.0, chunk_bytes=8192)
-    # one-hop AllReduce, aligned (TMA pipeline) and misaligned (LSU)
+def expect_path(comm, tree_executor, what):
+    chunks = comm.stats()["last_chunks"]
+    if tree_executor != (chunks > 0):
+        raise SystemExit(f"WRONG PATH {what}: last_chunks={chunks}")
+
+
+def allreduce(comms, xs, ys, op="sum"):
+    for r, c in enumerate(comms):
+        c.allreduce(xs[r], ys[r], op=op)
+    torch.cuda.synchronize()
+
+
+def onehop_sections():
     m, n = 4, 20000 + 3
+    cfg = B.config(timeout_s=T, chunk_bytes=8192, ll_max_bytes=0)
     comms = B.init_all([0] * m, cfg=cfg)
     sends = synth.inputs(200, m, n, "f32")
-    xs = [torch.from_numpy(s).cuda() for s in sends]
+    xs = [dev(s) for s in sends]
     ys = [torch.empty_like(x) for x in xs]
-    for r, c in enumerate(comms):
-        c.allreduce(xs[r], ys[r])
-    torch.cuda.synchronize()
+    allreduce(comms, xs, ys)
     want = OC.naive_reduce(sends, "f32", "sum")
     for y in ys:
-        check(y, want, "onehop")
+        check(y, want, "onehop tma")
+    expect_path(comms[0], True, "onehop tma")
+    print("ok onehop TMA", flush=True)
     xm = []
     for s in sends:
         b = torch.empty(n + 1, device="cuda")
         b[1:] = torch.from_numpy(s).cuda()
         xm.append(b[1:])
-    for r, c in enumerate(comms):
-        c.allreduce(xm[r], ys[r])
-    torch.cuda.synchronize()
+    allreduce(comms, xm, ys)
     for y in ys:
-        check(y, want, "misaligned")
-    # RS / AG
+        check(y, want, "onehop lsu")
+    print("ok onehop LSU (misaligned)", flush=True)
+    bs = synth.inputs(205, m, n, "bf16")
+    bx = [dev(s, "bf16") for s in bs]
+    by = [torch.empty_like(x) for x in bx]
+    allreduce(comms, bx, by)
+    for y in by:
+        check(y, OC.allreduce(OP.plan_switch_allreduce(m), bs, "bf16", "sum"), "bf16")
+    print("ok onehop bf16", flush=True)
+    allreduce(comms, xs, ys, op="avg")
+    for y in ys:
+        check(y, OC.allreduce(OP.plan_switch_allreduce(m), sends, "f32", "avg"), "avg")
+    print("ok onehop AVG", flush=True)
     rs = [torch.empty(n, device="cuda") for _ in range(m)]
     big = synth.inputs(201, m, m * n, "f32")
-    bx = [torch.from_numpy(s).cuda() for s in big]
+    bxs = [dev(s) for s in big]
     for r, c in enumerate(comms):
-        c.reduce_scatter(bx[r], rs[r])
+        c.reduce_scatter(bxs[r], rs[r])
     ag = [torch.empty(m * n, device="cuda") for _ in range(m)]
     for r, c in enumerate(comms):
         c.allgather(rs[r], ag[r])
     torch.cuda.synchronize()
     for y in ag:
         check(y, OC.naive_reduce(big, "f32", "sum"), "rs+ag")
+    print("ok ReduceScatter + AllGather", flush=True)
     for c in comms:
         c.destroy()
-    # emulated DGX-1V Broadcast + multi-level AllReduce (int: exact under any tree)
+    return sends, want
+
+
+def dgx1v_sections(n=20000 + 3):
     g = OG.dgx1v()
-    # packed trees at this size (R#27's single shallow tree is checked below)
-    packed = B.config(timeout_s=120.0, chunk_bytes=8192, shallow_max_bytes=0)
-    comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]), cfg=packed)
+    G = B.Graph.from_pairs(8, g[1])
     src = synth.rank_input(202, 3, n, "f32")
+    dsrc = dev(src)
     out = [torch.empty(n, device="cuda") for _ in range(8)]
-    dsrc = torch.from_numpy(src).cuda()
+    isends = synth.inputs(203, 8, n, "i32")
+    ix = [dev(s) for s in isends]
+    iy = [torch.empty_like(x) for x in ix]
+    # packed trees (R#27's single tree off), tree executor
+    packed = B.config(timeout_s=T, chunk_bytes=8192, shallow_max_bytes=0, ll_max_bytes=0)
+    comms = B.init_all([0] * 8, graph=G, cfg=packed)
     for r, c in enumerate(comms):
         c.broadcast(dsrc if r == 3 else None, out[r], root=3)
     torch.cuda.synchronize()
     for y in out:
         check(y, src, "dgx1v broadcast")
-    isends = synth.inputs(203, 8, n, "i32")
-    ix = [torch.from_numpy(s).cuda() for s in isends]
-    iy = [torch.empty_like(x) for x in ix]
-    for r, c in enumerate(comms):
-        c.allreduce(ix[r], iy[r])
-    torch.cuda.synchronize()
+    expect_path(comms[0], True, "dgx1v broadcast")
+    if comms[0].stats()["last_trees"] != 6:
+        raise SystemExit("dgx1v broadcast: expected the 6 packed trees")
+    allreduce(comms, ix, iy)
     for y in iy:
         check(y, OC.naive_reduce(isends, "i32", "sum"), "dgx1v allreduce")
-    assert comms[0].stats()["last_trees"] > 1
+    if comms[0].stats()["last_trees"] <= 1:
+        raise SystemExit("dgx1v allreduce: expected packed trees")
+    print("ok DGX-1V packed Broadcast + multi-level AllReduce", flush=True)
     for c in comms:
         c.destroy()
-    # small calls: the single minimum-depth tree (R#27), tree executor (64 KiB)
-    # and tree LL protocol (16 KiB)
-    comms = B.init_all([0] * 8, graph=B.Graph.from_pairs(8, g[1]), cfg=B.config(timeout_s=120.0))
+    # R#27 shallow tree on the tree executor (LL off), 64 KiB
+    shallow = B.config(timeout_s=T, shallow_max_bytes=256 << 10, ll_max_bytes=0)
+    comms = B.init_all([0] * 8, graph=G, cfg=shallow)
     ns = 16001
-    for r, c in enumerate(comms):
-        c.allreduce(ix[r][:ns], iy[r][:ns])
-    for r, c in enumerate(comms):
-        c.broadcast(dsrc[:ns] if r == 3 else None, out[r][:ns], root=3)
-    torch.cuda.synchronize()
-    assert comms[0].stats()["last_chunks"] > 0
-    for r in range(8):
-        check(iy[r][:ns], OC.naive_reduce([s[:ns] for s in isends], "i32", "sum"), "dgx1v shallow allreduce")
-        check(out[r][:ns], src[:ns], "dgx1v shallow broadcast")
-    ns = 4099
-    for r, c in enumerate(comms):
-        c.allreduce(ix[r][:ns], iy[r][:ns])
+    allreduce(comms, [x[:ns] for x in ix], [y[:ns] for y in iy])
+    expect_path(comms[0], True, "shallow allreduce")
     for r, c in enumerate(comms):
         c.broadcast(dsrc[:ns] if r == 3 else None, out[r][:ns], root=3)
     torch.cuda.synchronize()
+    expect_path(comms[0], True, "shallow broadcast")
+    if comms[0].stats()["last_trees"] != 1:
+        raise SystemExit("shallow: expected one tree")
     for r in range(8):
-        check(iy[r][:ns], OC.naive_reduce([s[:ns] for s in isends], "i32", "sum"), "dgx1v shallow allreduce")
-        check(out[r][:ns], src[:ns], "dgx1v shallow broadcast")
-    assert comms[0].stats()["last_trees"] == 1
+        check(iy[r][:ns], OC.naive_reduce([s[:ns] for s in isends], "i32", "sum"), "shallow allreduce")
+        check(out[r][:ns], src[:ns], "shallow broadcast")
+    print("ok DGX-1V shallow tree (tree executor)", flush=True)
     for c in comms:
         c.destroy()
-    # LL protocol (batched and per-rank launches) and the per-rank tree path
+    # the shallow tree in the LL protocol, 16 KiB
+    lltree = B.config(timeout_s=T, shallow_max_bytes=256 << 10, ll_max_bytes=256 << 10)
+    comms = B.init_all([0] * 8, graph=G, cfg=lltree)
+    ns = 4099
+    allreduce(comms, [x[:ns] for x in ix], [y[:ns] for y in iy])
+    expect_path(comms[0], False, "LL tree allreduce")
+    for r, c in enumerate(comms):
+        c.broadcast(dsrc[:ns] if r == 3 else None, out[r][:ns], root=3)
+    torch.cuda.synchronize()
+    expect_path(comms[0], False, "LL tree broadcast")
+    for r in range(8):
+        check(iy[r][:ns], OC.naive_reduce([s[:ns] for s in isends], "i32", "sum"), "LL tree allreduce")
+        check(out[r][:ns], src[:ns], "LL tree broadcast")
+    print("ok DGX-1V shallow tree (LL protocol)", flush=True)
+    for c in comms:
+        c.destroy()
+
+
+def ll_and_per_rank_sections(sends, want):
     for per_rank in (0, 1):
-        comms = B.init_all([0] * 4, cfg=B.config(timeout_s=120.0, launch_per_rank=per_rank))
+        comms = B.init_all([0] * 4, cfg=B.config(timeout_s=T, launch_per_rank=per_rank,
+                                                 ll_max_bytes=256 << 10))
         for cnt in (1, 1001):
             ls = synth.inputs(204, 4, cnt, "f32")
-            lx = [torch.from_numpy(s).cuda() for s in ls]
+            lx = [dev(s) for s in ls]
             ly = [torch.empty_like(x) for x in lx]
-            for r, c in enumerate(comms):
-                c.allreduce(lx[r], ly[r])
+            allreduce(comms, lx, ly)
+            expect_path(comms[0], False, f"LL allreduce pr={per_rank}")
             for r, c in enumerate(comms):
                 c.broadcast(lx[r] if r == 2 else None, lx[r], root=2)
             torch.cuda.synchronize()
+            expect_path(comms[0], False, f"LL broadcast pr={per_rank}")
             for r in range(4):
                 check(ly[r], OC.naive_reduce(ls, "f32", "sum"), f"LL allreduce pr={per_rank}")
                 check(lx[r], ls[2], f"LL broadcast pr={per_rank}")
-        if per_rank:
-            for r, c in enumerate(comms):
-                c.allreduce(xs[r], ys[r])
-            torch.cuda.synchronize()
-            for y in ys:
-                check(y, want, "per-rank tree allreduce")
+        print(f"ok switch LL ({'per-rank' if per_rank else 'batched'} launches)", flush=True)
         for c in comms:
             c.destroy()
-    print("sanitize cases ok")
+    # the multi-process protocol's tree executor: per-rank launches, LL off
+    comms = B.init_all([0] * 4, cfg=B.config(timeout_s=T, launch_per_rank=1, ll_max_bytes=0,
+                                             chunk_bytes=8192))
+    xs = [dev(s) for s in sends]
+    ys = [torch.empty_like(x) for x in xs]
+    allreduce(comms, xs, ys)
+    expect_path(comms[0], True, "per-rank tree allreduce")
+    for y in ys:
+        check(y, want, "per-rank tree allreduce")
+    print("ok per-rank tree AllReduce", flush=True)
+    for c in comms:
+        c.destroy()
+
+
+def main():
+    sends, want = onehop_sections()
+    dgx1v_sections()
+    ll_and_per_rank_sections(sends, want)
+    print("sanitize cases ok", flush=True)
 
 
 if __name__ == "__main__":
