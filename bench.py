@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 DEFAULT_M = 8
 DEFAULT_COUNT = 64 << 20           # 256 MiB fp32 per rank
 METRIC = "AllReduce/Broadcast algBW GB/s vs size, 2/4/8 B200, % NVLink peak vs NCCL"
+REF_SAMPLE_COUNT = 4 << 20         # oracle samples (cpu_baseline and --impl reference): 16 MiB fp32 per rank
 UNIT = "GB/s"
 
 
@@ -253,10 +254,156 @@ def run_virtual(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_oracle_baseline(m, min(count, 16 << 20))
+    if not args.no_cpu_baseline:   # the same sample as the reference arm: 16 MiB per rank
+        out["cpu_baseline"] = cpu_oracle_baseline(m, min(count, REF_SAMPLE_COUNT))
     for c in comms:
         c.destroy()
+    return out
+
+
+NVLINK_GBS = 900.0   # NVLink 5 per direction per B200 (busBW / 900)
+
+
+class Nccl:
+    """NCCL 2.28 (torch's bundled libnccl) called directly through ctypes: the
+    comparison the metric names, on the SAME device buffers and stream as
+    Blink, out of place, AllReduce and Broadcast, eager and CUDA-graph
+    captured; optionally with symmetric-window registration (ncclMemAlloc +
+    ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC).  NCCL is never on
+    Blink's data path."""
+    FLOAT32, SUM = 7, 0
+
+    def __init__(self, rank, world):
+        import ctypes
+        import glob
+        import torch.distributed as dist
+        import nvidia
+        base = os.path.dirname(list(nvidia.__path__)[0])
+        cands = glob.glob(os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so*"))
+        if not cands:
+            raise RuntimeError("libnccl.so not found")
+        self.lib = ctypes.CDLL(cands[0])
+        self.ct = ctypes
+
+        class UID(ctypes.Structure):
+            _fields_ = [("internal", ctypes.c_char * 128)]
+        uid = UID()
+        if rank == 0:
+            self._ok(self.lib.ncclGetUniqueId(ctypes.byref(uid)), "ncclGetUniqueId")
+        obj = [bytes(uid.internal) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid.internal = obj[0]
+        self.comm = ctypes.c_void_p()
+        self._ok(self.lib.ncclCommInitRank(ctypes.byref(self.comm), world, uid, rank), "ncclCommInitRank")
+        v = ctypes.c_int()
+        self.lib.ncclGetVersion(ctypes.byref(v))
+        self.version = v.value
+
+    def _ok(self, r, what):
+        if r != 0:
+            raise RuntimeError(f"{what} returned {r}")
+
+    def allreduce(self, send, recv, count, stream):
+        self._ok(self.lib.ncclAllReduce(self.ct.c_void_p(send), self.ct.c_void_p(recv), self.ct.c_size_t(count),
+                                        self.FLOAT32, self.SUM, self.comm, self.ct.c_void_p(stream)),
+                 "ncclAllReduce")
+
+    def broadcast(self, send, recv, count, root, stream):
+        self._ok(self.lib.ncclBroadcast(self.ct.c_void_p(send), self.ct.c_void_p(recv), self.ct.c_size_t(count),
+                                        self.FLOAT32, root, self.comm, self.ct.c_void_p(stream)),
+                 "ncclBroadcast")
+
+    def mem_alloc(self, nbytes):
+        p = self.ct.c_void_p()
+        self._ok(self.lib.ncclMemAlloc(self.ct.byref(p), self.ct.c_size_t(nbytes)), "ncclMemAlloc")
+        return p.value
+
+    def window(self, ptr, nbytes):
+        w = self.ct.c_void_p()
+        self._ok(self.lib.ncclCommWindowRegister(self.comm, self.ct.c_void_p(ptr), self.ct.c_size_t(nbytes),
+                                                 self.ct.byref(w), 1), "ncclCommWindowRegister")
+        return w
+
+    def close(self):
+        self.lib.ncclCommDestroy(self.comm)
+
+
+def tuning_lines(path):
+    """NCCL's algorithm/protocol choices from its NCCL_DEBUG=INFO TUNING log."""
+    out = []
+    try:
+        for line in open(path):
+            low = line.lower()
+            if ("algo" in low or "protocol" in low or "proto" in low) and ("allreduce" in low or "broadcast" in low):
+                txt = line.strip().split("NCCL INFO", 1)[-1].strip()
+                if txt not in out:
+                    out.append(txt)
+            if len(out) >= 6:
+                break
+    except OSError:
+        pass
+    return out
+
+
+def time_device(fn, steps, stream, graph=False):
+    """Mean ms per call over `steps` calls with CUDA events on `stream`
+    (eager), or of one CUDA graph holding `steps` calls, replayed once."""
+    import torch
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(steps):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        g.replay()
+        t1.record(stream)
+    else:
+        t0.record(stream)
+        for _ in range(steps):
+            fn()
+        t1.record(stream)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / steps
+
+
+def multiprocess_line(args, m, S, ms, bc_ms, graph, e2e_ms, n_e2e, launches, clocks, nccl):
+    """Rank 0's JSON line at N > 1 (pure: tested on the CPU with given times).
+    AllReduce is the headline (`value` = algBW); busBW = algBW * 2(m-1)/m is
+    measured against NVLink's 900 GB/s per direction; the
+    Broadcast arm (busBW = algBW) and NCCL's numbers ride along."""
+    workload = f"c3-onehop-allreduce-m{m}-nvswitch-f32-{S >> 20}MiB"
+    algbw = S / (ms * 1e-3) / 1e9
+    bus = algbw * 2 * (m - 1) / m
+    bc_alg = S / (bc_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(algbw, 3), "unit": UNIT, "n_gpus": m,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded N(0,1)*1e-2 gradients, generated on device)",
+        "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
+                   "ranks_kind": "one process per GPU", "bytes_per_rank": S,
+                   "bus_bw_gbs": round(bus, 3),
+                   "l2": f"{2 * S >> 20} MiB send+recv per rank per step"
+                         + (" > 126 MB L2" if 2 * S > (126 << 20) else " (fits L2)")},
+        "roofline": {"bound": "nvlink", "achieved": round(bus, 2), "peak": NVLINK_GBS, "unit": "GB/s",
+                     "frac": round(bus / NVLINK_GBS, 4),
+                     "traffic": traffic_from_profiles(workload),
+                     "peak_source": "NVLink 5 nominal per direction (SURVEY 8(d): busBW / 900); "
+                                    "traffic: ncu nvltx+nvlrx bytes per launch from profiles/traffic.json "
+                                    "(scripts/nvlink_traffic.sh), null until measured"},
+        "broadcast": {"root": 0, "ms": round(bc_ms, 4), "alg_bw_gbs": round(bc_alg, 3),
+                      "bus_bw_gbs": round(bc_alg, 3), "frac": round(bc_alg / NVLINK_GBS, 4)},
+        "graph": graph,
+        "e2e": {"value": round(S / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
+                "h2d_bytes_per_step": S, "d2h_bytes_per_step": S, "steps": n_e2e,
+                "note": "per rank: input H2D and result D2H (pinned); D2H of step k overlaps H2D of step k+1"},
+        "gpu_launches": launches, "clocks": clocks,
+        "nccl": nccl,
+    }
     return out
 
 
@@ -269,8 +416,17 @@ def run_multiprocess(args):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    if os.environ.get("BENCH_SAME_GPU") == "1":   # test harness: all ranks share cuda:0
+    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"   # test harness: all ranks share cuda:0
+    if same_gpu:
         local = 0
+    # NCCL reads its environment once, at its first communicator: set the
+    # comparison's knobs before anything initialises it
+    tune_log = os.path.join(tempfile.gettempdir(), f"bench_nccl_tuning.{os.getpid()}.log")
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "TUNING")
+    os.environ["NCCL_DEBUG_FILE"] = tune_log
+    if args.nccl_nvls is not None:
+        os.environ["NCCL_NVLS_ENABLE"] = str(args.nccl_nvls)
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     ex = B.torch_exchange()
@@ -282,28 +438,43 @@ def run_multiprocess(args):
     comm.register(send, S, ex)
     comm.register(recv, S, ex)
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    sp = stream.cuda_stream
+
+    def blink_ar():
         comm.allreduce(send, recv, op="sum", stream=stream)
+
+    def blink_bc():
+        comm.broadcast(send if rank == 0 else None, recv, root=0, count=count, dtype="f32", stream=stream)
+
+    def max_ms(ms):
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        blink_ar()
+        blink_bc()
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = comm.stats()["launches"]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         dist.barrier()
-        t0.record(stream)
-        for _ in range(args.steps):
-            comm.allreduce(send, recv, op="sum", stream=stream)
-        t1.record(stream)
-        torch.cuda.synchronize()
+        ms = time_device(blink_ar, args.steps, stream)
         dist.barrier()
-    ms = t0.elapsed_time(t1) / args.steps
-    tt = torch.tensor([ms], dtype=torch.float64)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms = float(tt.item())
+    ms = max_ms(ms)
     launches = comm.stats()["launches"] - launches0
-    algbw = S / (ms * 1e-3) / 1e9
+    dist.barrier()
+    bc_ms = max_ms(time_device(blink_bc, args.steps, stream))
+    dist.barrier()
+    graph = {}
+    try:
+        graph["blink_allreduce_ms"] = round(max_ms(time_device(blink_ar, args.steps, stream, graph=True)), 4)
+        dist.barrier()
+        graph["blink_broadcast_ms"] = round(max_ms(time_device(blink_bc, args.steps, stream, graph=True)), 4)
+    except Exception as e:  # pragma: no cover - depends on the box
+        graph["blink_unavailable"] = f"{type(e).__name__}: {e}"[:160]
+    m = world
     # e2e through host buffers (pinned): H2D input, collective, D2H result.
     # Results are double-buffered (a second registered recv) so step k's D2H
     # (copy stream) overlaps step k+1's H2D, as in the N = 1 line.
@@ -341,72 +512,75 @@ def run_multiprocess(args):
     stream.wait_stream(d2h)
     e1.record(stream)
     torch.cuda.synchronize()
-    et = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64)
-    dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    nccl = nccl_same_buffers(args, send, recv, stream) if os.environ.get("BENCH_SAME_GPU") != "1" else \
-        {"unavailable": "all ranks share one GPU (NCCL needs one GPU per rank)"}
-    m = world
-    peak_nvl = 770.0   # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+    e2e_ms = max_ms(e0.elapsed_time(e1) / n_e2e)
+    nccl = nccl_compare(args, send, recv, count, stream, rank, world, same_gpu, tune_log)
     out = None
     if rank == 0:
-        workload = f"c3-onehop-allreduce-m{m}-nvswitch-f32-{S >> 20}MiB"
-        out = {
-            "metric": METRIC, "value": round(algbw, 3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded N(0,1)*1e-2 gradients, generated on device)",
-            "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
-                       "ranks_kind": "one process per GPU", "bytes_per_rank": S,
-                       "bus_bw_gbs": round(algbw * 2 * (m - 1) / m, 3),
-                       "l2": f"{2 * S >> 20} MiB send+recv per rank per step"
-                             + (" > 126 MB L2" if 2 * S > (126 << 20) else " (fits L2)")},
-            "roofline": {"bound": "nvlink", "achieved": round(algbw * 2 * (m - 1) / m, 2),
-                         "peak": peak_nvl, "unit": "GB/s",
-                         "frac": round(algbw * 2 * (m - 1) / m / peak_nvl, 4),
-                         "traffic": None,
-                         "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"},
-            "e2e": {"value": round(S / (float(et.item()) * 1e-3) / 1e9, 3), "unit": UNIT,
-                    "h2d_bytes_per_step": S, "d2h_bytes_per_step": S, "steps": n_e2e,
-                    "note": "per rank: input H2D and result D2H (pinned); D2H of step k overlaps H2D of step k+1"},
-            "gpu_launches": launches, "clocks": clk.summary(),
-            "nccl": nccl,
-        }
+        out = multiprocess_line(args, m, S, ms, bc_ms, graph, e2e_ms, n_e2e, launches, clk.summary(), nccl)
     comm.destroy()
     dist.barrier()
     dist.destroy_process_group()
     return out
 
 
-def nccl_same_buffers(args, send, recv, stream):
-    """NCCL AllReduce (torch.distributed nccl group) on the same buffers,
-    stream and step count: the comparison the metric names.  Max over ranks."""
+def nccl_compare(args, send, recv, count, stream, rank, world, same_gpu, tune_log):
+    """NCCL on the same buffers, stream and step count, out of place, max over
+    ranks: AllReduce and Broadcast, eager and CUDA-graph captured, and the
+    symmetric-window variant; plus the algorithm / protocol NCCL chose."""
     import torch
     import torch.distributed as dist
+    if same_gpu:
+        return {"unavailable": "all ranks share one GPU (NCCL needs one GPU per rank)"}
+    out = {}
     try:
-        g = dist.new_group(backend="nccl")
-        S = send.numel() * send.element_size()
-        recv.copy_(send)
-        for _ in range(args.warmup):
-            dist.all_reduce(recv, group=g)
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.steps):
-            dist.all_reduce(recv, group=g)
-        t1.record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-        world = dist.get_world_size()
-        alg = S / (ms * 1e-3) / 1e9
-        return {"value": round(alg, 3), "unit": UNIT, "ms_per_step": round(ms, 4),
-                "bus_bw_gbs": round(alg * 2 * (world - 1) / world, 3),
-                "impl": f"NCCL {'.'.join(map(str, torch.cuda.nccl.version()))} via torch.distributed, in place"}
+        nc = Nccl(rank, world)
     except Exception as e:  # pragma: no cover - depends on the box
         return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    S = count * 4
+    sp = stream.cuda_stream
+
+    def max_ms(ms):
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def arm(name, fn, f_bus):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ms = max_ms(time_device(fn, args.steps, stream))
+        alg = S / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 4), "alg_bw_gbs": round(alg, 3), "bus_bw_gbs": round(alg * f_bus, 3)}
+        try:
+            dist.barrier()
+            gms = max_ms(time_device(fn, args.steps, stream, graph=True))
+            out[name]["graph_ms"] = round(gms, 4)
+        except Exception as e:  # pragma: no cover
+            out[name]["graph"] = f"{type(e).__name__}"[:80]
+
+    f_ar = 2 * (world - 1) / world
+    sptr, rptr = send.data_ptr(), recv.data_ptr()
+    try:
+        arm("allreduce", lambda: nc.allreduce(sptr, rptr, count, sp), f_ar)
+        arm("broadcast", lambda: nc.broadcast(sptr, rptr, count, 0, sp), 1.0)
+        try:   # symmetric windows (NCCL 2.27+): buffers from ncclMemAlloc
+            a = nc.mem_alloc(S)
+            b = nc.mem_alloc(S)
+            torch.cuda.synchronize()
+            nc.window(a, S)
+            nc.window(b, S)
+            arm("allreduce_symmetric", lambda: nc.allreduce(a, b, count, sp), f_ar)
+        except Exception as e:  # pragma: no cover
+            out["allreduce_symmetric"] = {"unavailable": f"{type(e).__name__}: {e}"[:160]}
+    except Exception as e:  # pragma: no cover - depends on the box
+        out["error"] = f"{type(e).__name__}: {e}"[:200]
+    torch.cuda.synchronize()
+    out["impl"] = f"NCCL {nc.version} (ctypes, torch's libnccl), out of place, same buffers and stream"
+    out["env"] = {k: os.environ[k] for k in ("NCCL_NVLS_ENABLE", "NCCL_ALGO", "NCCL_PROTO") if k in os.environ}
+    out["tuning"] = tuning_lines(tune_log)
+    nc.close()
+    return out
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -420,7 +594,7 @@ def run_reference(args):
     from oracle import collectives as OC
     from oracle import packing as OP
     m = args.ranks if int(os.environ.get("WORLD_SIZE", "1")) == 1 else int(os.environ["WORLD_SIZE"])
-    count = min(args.count, 4 << 20)
+    count = min(args.count, REF_SAMPLE_COUNT)
     plan = OP.plan_switch_allreduce(m)
     sends = synth.inputs(3, m, count, "f32")
     for _ in range(args.warmup):
@@ -452,6 +626,8 @@ def main():
     ap.add_argument("--ranks", type=int, default=DEFAULT_M, help="virtual ranks at N=1")
     ap.add_argument("--count", type=int, default=DEFAULT_COUNT, help="fp32 elements per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl-nvls", type=int, default=None, choices=[0, 1],
+                    help="N>1: NCCL_NVLS_ENABLE for the NCCL comparison (set before NCCL initialises)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

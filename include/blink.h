@@ -177,7 +177,9 @@ typedef struct blink_comm* blink_comm_t;
  * "weight":[num,den],"depth","lo","hi","chunk","nchunks"}]} (lo/hi/chunk in
  * elements).  *json_bytes is in/out: capacity in, required size (incl. NUL)
  * out; BLINK_ERR_INVALID_ARGUMENT if the capacity is too small.
- * graph == NULL means the NVSwitch model (all ranks behind one switch). */
+ * graph == NULL means the NVSwitch model (all ranks behind one switch).
+ * `is_allreduce` selects the collective: 0 Broadcast, 1 AllReduce, and (NEXT-3)
+ * 2 ReduceScatter, 3 AllGather, 4 Gather, whose trees cover one block each. */
 blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const blink_config_t* cfg,
                                int is_allreduce, int root, size_t count, blink_dtype_t dtype,
                                char* json, size_t* json_bytes);
@@ -237,15 +239,20 @@ blink_result_t blink_reduce_scatter(blink_comm_t comm, const void* sendbuf, void
 /* AllGather (NEXT-3: "AllReduce without using a reduction function").
  * Every rank's sendcount elements land at block `rank` of every recvbuf
  * (nranks*sendcount elements).  In place iff sendbuf == recvbuf + rank*sendcount.
- * Switch (one-hop) topologies only. */
+ * Switch: block j is pushed by root j along its one-hop star.  Link graphs:
+ * block j is broadcast down a minimum-depth arborescence rooted at j (the m
+ * arborescences spread over the links); multi-server graphs are unsupported. */
 blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
                                size_t sendcount, blink_dtype_t dtype, void* stream);
 
 /* Gather (NEXT-3: "Gather is the inverse of Broadcast").  Every rank's
  * sendcount elements land at block `rank` of the root's recvbuf
  * (nranks*sendcount elements); recvbuf is unused (may be NULL) on other
- * ranks.  One-hop trees: rank j's block travels the single edge j -> root.
- * Switch (one-hop) topologies only. */
+ * ranks.  Switch: rank j's block travels the single edge j -> root (one-hop
+ * trees).  Link graphs: block j travels j's path to the root in the root's
+ * minimum-depth Broadcast tree, reversed (intermediate ranks forward it; in
+ * single-process comms a rank with recvbuf == NULL forwards through a
+ * library-owned scratch buffer). */
 blink_result_t blink_gather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
                             size_t sendcount, blink_dtype_t dtype, int root, void* stream);
 

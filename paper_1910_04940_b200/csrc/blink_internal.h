@@ -28,10 +28,14 @@ constexpr int kMaxCounters = 4096;  // dynamic chunk counters per launch (ctrl[2
 //                         (written by u into its parent's region)
 //   bflag[i][c]           the final value of tree i / chunk c has been
 //                         written into this rank's recv (written by parent)
+//   miad[s]               (multi-process MIAD, NEXT-2) rank 0's chunk decision for
+//                         autotuned call s: {s + 1, chunk | phase << 56}, slot s % kMiadSlots
 constexpr size_t kEntryWords = kMaxRanks;
 constexpr size_t kPflagWords = size_t(kMaxTrees) * kMaxRanks * kMaxChunks;
 constexpr size_t kBflagWords = size_t(kMaxTrees) * kMaxChunks;
-constexpr size_t kFlagWords = kEntryWords + kPflagWords + kBflagWords;
+constexpr size_t kMiadSlots = 64;
+constexpr size_t kMiadWords = 2 * kMiadSlots;
+constexpr size_t kFlagWords = kEntryWords + kPflagWords + kBflagWords + kMiadWords;
 constexpr size_t kFlagBytes = kFlagWords * sizeof(uint64_t);
 __host__ __device__ inline size_t entry_idx(int u) { return size_t(u); }
 __host__ __device__ inline size_t pflag_idx(int tree, int child, int chunk) {
@@ -39,6 +43,9 @@ __host__ __device__ inline size_t pflag_idx(int tree, int child, int chunk) {
 }
 __host__ __device__ inline size_t bflag_idx(int tree, int chunk) {
   return kEntryWords + kPflagWords + size_t(tree) * kMaxChunks + chunk;
+}
+__host__ __device__ inline size_t miad_idx(uint64_t seq) {
+  return kEntryWords + kPflagWords + kBflagWords + 2 * size_t(seq % kMiadSlots);
 }
 
 enum Coll : int { kBroadcast = 0, kAllReduce = 1, kReduceScatter = 2, kAllGather = 3, kGather = 4 };
@@ -217,6 +224,8 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
                         bool cooperative, bool pdl);
 constexpr int kMaxSmemBytes = 224 * 1024;  // + static smem <= 227 KB opt-in
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream);
+// two u64 stores by one thread, stream-ordered (values travel as kernel parameters)
+cudaError_t launch_store2(uint64_t* dst, uint64_t v0, uint64_t v1, void* stream);
 int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll, int smem_bytes);
 
 // plan.cpp -------------------------------------------------------------
@@ -237,6 +246,8 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
 // R#27 latency plan: one minimum-depth (BFS) tree for small calls on link graphs.
 bool use_shallow_plan(const Graph& g, int coll, size_t bytes, const blink_config_t& cfg);
 blink_result_t make_shallow_plan(const Graph& g, int coll, int root, Plan* out, std::string* err);
+// NEXT-3 on link graphs: AllGather / Gather block plans (tree j covers block j).
+blink_result_t make_block_plan(const Graph& g, int coll, int root, Plan* out, std::string* err);
 // Split (R#11) + chunking (a8).  ctas_for_tree: CTA count expected per tree channel.
 blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
                          int ctas_hint, std::vector<TreeRange>* out, std::string* err);

@@ -1546,6 +1546,17 @@ int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll, int
   return n;
 }
 
+__global__ void store2_kernel(uint64_t* dst, uint64_t v0, uint64_t v1) {
+  dst[1] = v1;
+  __threadfence_system();
+  dst[0] = v0;  // the tag last: a reader that sees it sees the value
+}
+
+cudaError_t launch_store2(uint64_t* dst, uint64_t v0, uint64_t v1, void* stream) {
+  store2_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst, v0, v1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0 || dst == src) return cudaSuccess;
   bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;

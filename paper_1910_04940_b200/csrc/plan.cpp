@@ -1499,6 +1499,122 @@ blink_result_t make_shallow_plan(const Graph& g, int coll, int root, Plan* out, 
   return BLINK_SUCCESS;
 }
 
+// ============================================================== NEXT-3 on link graphs
+// "Gather is the inverse of Broadcast, and AllGather is AllReduce
+// without using a reduction function."  Block plans (Plan::blocks): tree j
+// covers block j of the m-block buffer.
+//  AllGather: block j is broadcast from rank j down one spanning arborescence
+//    rooted at j -- the AllReduce pattern (every rank's contribution reaches
+//    every rank) with concatenation instead of a combine.  Each arborescence
+//    is a minimum-depth (BFS) tree, as R#27's small-call tree; among the
+//    vertices one level up with a link to v, v's parent is the one whose link
+//    is least loaded relative to its capacity after the roots before j
+//    (ties: lowest rank), so the m trees spread over the links.
+//  Gather to r: the minimum-depth Broadcast tree of r, reversed ("the inverse
+//    of Broadcast").  Block j travels along j's path to r; tree j is that
+//    chain rooted at j, and ranks off the chain are not members (-2).  Tree r
+//    is r alone (its own block).  Parents are chosen deepest level first so
+//    that subtree sizes are known: v joins the candidate whose resulting
+//    subtree, over the capacity of the link that carries it on toward r,
+//    is smallest (ties: lowest rank).
+blink_result_t make_block_plan(const Graph& g, int coll, int root, Plan* out, std::string* err) {
+  const int n = g.n;
+  *out = Plan();
+  out->coll = coll;
+  out->root = coll == kGather ? root : -1;
+  out->nranks = n;
+  out->blocks = true;
+  if (coll != kAllGather && coll != kGather) {
+    *err = "ReduceScatter runs on one-hop trees: switch topologies only";
+    return BLINK_ERR_UNSUPPORTED;
+  }
+  auto cap = [&](int u, int v) { return g.cap[u][v]; };
+  if (coll == kAllGather) {
+    std::vector<std::vector<double>> load(n, std::vector<double>(n, 0.0));
+    for (int j = 0; j < n; ++j) {
+      const std::vector<int> d = bfs_dist(g, j, false);
+      Tree t;
+      t.root = j;
+      t.parent.assign(n, -1);
+      int maxd = 0;
+      for (int v = 0; v < n; ++v) maxd = std::max(maxd, d[v]);
+      for (int v = 0; v < n; ++v) {
+        if (d[v] < 0) {
+          *err = "rank " + std::to_string(v) + " is not reachable from rank " + std::to_string(j);
+          return BLINK_ERR_TOPOLOGY;
+        }
+      }
+      for (int lvl = 1; lvl <= maxd; ++lvl)
+        for (int v = 0; v < n; ++v) {
+          if (d[v] != lvl) continue;
+          int best = -1;
+          double bs = INFINITY;
+          for (int u = 0; u < n; ++u)
+            if (d[u] == lvl - 1 && cap(u, v) > 0) {
+              const double sc = (load[u][v] + 1.0) / cap(u, v);
+              if (sc < bs - 1e-12) {
+                bs = sc;
+                best = u;
+              }
+            }
+          t.parent[v] = best;
+          load[best][v] += 1.0;
+        }
+      t.depth = maxd;
+      out->trees.push_back(t);
+    }
+  } else {
+    if (root < 0 || root >= n) {
+      *err = "root " + std::to_string(root) + " out of range [0," + std::to_string(n) + ")";
+      return BLINK_ERR_INVALID_ARGUMENT;
+    }
+    // distances TO the root over links v -> u (the reversed Broadcast tree)
+    Graph rg = g;
+    for (int u = 0; u < n; ++u)
+      for (int v = 0; v < n; ++v) rg.cap[u][v] = g.cap[v][u];
+    const std::vector<int> d = bfs_dist(rg, root, false);
+    int maxd = 0;
+    for (int v = 0; v < n; ++v) {
+      if (d[v] < 0) {
+        *err = "rank " + std::to_string(v) + " cannot reach the gather root " + std::to_string(root);
+        return BLINK_ERR_TOPOLOGY;
+      }
+      maxd = std::max(maxd, d[v]);
+    }
+    std::vector<int> up(n, -1), sub(n, 1);  // next hop toward the root, subtree size
+    for (int lvl = maxd; lvl >= 1; --lvl)
+      for (int v = 0; v < n; ++v) {
+        if (d[v] != lvl) continue;
+        int best = -1;
+        double bs = INFINITY;
+        for (int u = 0; u < n; ++u)
+          if (d[u] == lvl - 1 && cap(v, u) > 0) {
+            const double c = lvl == 1 ? cap(v, u) : (d[u] == 1 ? cap(u, root) : cap(v, u));
+            const double sc = double(sub[u] + sub[v]) / c;
+            if (sc < bs - 1e-12) {
+              bs = sc;
+              best = u;
+            }
+          }
+        up[v] = best;
+        sub[best] += sub[v];
+      }
+    for (int j = 0; j < n; ++j) {
+      Tree t;
+      t.root = j;
+      t.parent.assign(n, -2);
+      t.parent[j] = -1;
+      int hops = 0;
+      for (int v = j; v != root; v = up[v], ++hops) t.parent[up[v]] = v;
+      t.depth = hops;
+      out->trees.push_back(t);
+    }
+  }
+  out->rate_num = 1;
+  out->rate_den = 1;
+  return BLINK_SUCCESS;
+}
+
 // ============================================================== split + chunks
 blink_result_t size_plan(const Plan& p, size_t count, int esize, const blink_config_t& cfg,
                          int ctas_hint, std::vector<TreeRange>* out, std::string* err) {

@@ -22,6 +22,8 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
+#include <chrono>
 #include <numeric>
 #include <tuple>
 #include <string>
@@ -118,8 +120,23 @@ struct blink_comm {
   char* staging = nullptr;
   size_t staging_bytes = 0;
   char* peer_staging[kMaxRanks] = {};
+  char* scratch = nullptr;    // single-process Gather on link graphs: forwarding buffer of a
+  size_t scratch_bytes = 0;   // rank that passed recvbuf == NULL but relays other blocks
   std::string last_error;
   blink_stats_t stats{};
+  // multi-process MIAD (NEXT-2): rank 0 decides each autotuned call's chunk
+  // size and publishes it in its flag words; the other ranks read it there
+  struct MpMiad {
+    blink_miad_t st{};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool pending = false;  // rank 0: ev0/ev1 bracket a launch not yet folded into st
+    bool done = false;     // converged (phase 2) and published: no more slots
+    size_t chunk = 0;
+    int calls = 0;
+  };
+  std::map<std::tuple<int, int, int, size_t>, MpMiad> mp_miad;  // (coll, root, dtype, count)
+  uint64_t miad_seq = 0;                // autotuned calls so far (same sequence on every rank)
+  cudaStream_t miad_stream = nullptr;   // non-blocking stream for reading rank 0's slots
 };
 
 namespace {
@@ -213,9 +230,11 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
 // single minimum-depth tree of small calls on link graphs (R#27).
 blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, const Plan** out) {
   int key_root = (coll == kBroadcast || coll == kGather) ? root : -1;
-  if (is_block_coll(coll) && !comm->graph.switch_model)
-    return fail(comm, BLINK_ERR_UNSUPPORTED,
-                "ReduceScatter/AllGather run on one-hop trees: switch topologies only");
+  if (coll == kReduceScatter && !comm->graph.switch_model)
+    return fail(comm, BLINK_ERR_UNSUPPORTED, "ReduceScatter runs on one-hop trees: switch topologies only");
+  if (is_block_coll(coll) && comm->graph.multi_server)
+    return fail(comm, BLINK_ERR_UNSUPPORTED, "multi-server graphs support AllReduce only");
+  const bool link_blocks = is_block_coll(coll) && !comm->graph.switch_model;  // NEXT-3 on link graphs
   bool star = coll == kBroadcast && comm->graph.switch_model && comm->nranks > 2 &&
               bytes <= comm->cfg.onehop_bcast_max_bytes;
   if (star) key_root += 1000;
@@ -245,6 +264,8 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
     r = BLINK_SUCCESS;
   } else if (shallow) {
     r = make_shallow_plan(comm->graph, coll, root, p.get(), &err);
+  } else if (link_blocks) {
+    r = make_block_plan(comm->graph, coll, root, p.get(), &err);
   } else {
     r = make_plan(comm->graph, is_block_coll(coll) ? kAllReduce : coll, root, comm->cfg, p.get(),
                   &err);
@@ -1095,6 +1116,23 @@ blink_result_t clique_launch(Clique* q) {
       a.send[v] = const_cast<char*>(static_cast<const char*>(q->pending[v].send));
       a.recv[v] = static_cast<char*>(q->pending[v].recv);
       a.flags[v] = q->comms[v]->flags;
+      if (q->coll == kGather && !a.recv[v]) {  // a relay on a link-graph Gather chain
+        bool relay = false;
+        for (const Tree& t : plan->trees) relay = relay || (t.parent[v] >= 0 && t.root != v);
+        if (relay) {
+          blink_comm* cv = q->comms[v];
+          const size_t need = size_t(n) * bytes;
+          if (cv->scratch_bytes < need) {
+            DeviceGuard gv(cv->device);
+            if (cv->scratch) cudaFree(cv->scratch);
+            cv->scratch = nullptr;
+            cv->scratch_bytes = 0;
+            CUDA_TRY(cd, cudaMalloc(&cv->scratch, need));
+            cv->scratch_bytes = need;
+          }
+          a.recv[v] = cv->scratch;
+        }
+      }
       // block collectives address rank v's short buffer through tree v's range
       if (q->coll == kReduceScatter) a.recv[v] -= size_t(v) * bytes;
       if ((q->coll == kAllGather || q->coll == kGather) && a.send[v]) a.send[v] -= size_t(v) * bytes;
@@ -1292,6 +1330,84 @@ bool resolve(blink_comm_t comm, const void* ptr, size_t bytes, char* out[kMaxRan
   return false;
 }
 
+// MIAD across processes (NEXT-2).  Every rank makes the same
+// sequence of autotuned calls, numbered by comm->miad_seq.  Rank 0 runs the
+// MIAD controller on its own CUDA-event time of the previous call (its kernel
+// waits for every peer through the flags, so that time is the collective's,
+// i.e. the slowest rank's) and publishes call s's chunk size in its flag
+// words, slot s % kMiadSlots, with a stream-ordered store before its launch.
+// Every other rank reads that slot (through its IPC mapping of rank 0's flags)
+// until the slot carries tag s + 1: all ranks chunk call s identically.  Once
+// rank 0 publishes a converged size (phase 2), both sides stop for that key.
+// Slot reuse is safe: rank 0 overwrites slot s at call s + kMiadSlots, after
+// its kernel for call s + kMiadSlots - 1, which needs every rank's entry for
+// that call -- so every reader has long read slot s.
+blink_result_t mp_miad_chunk(blink_comm_t comm, int coll, int root, blink_dtype_t dtype, size_t count,
+                             const Plan& plan, cudaStream_t stream, size_t* chunk,
+                             blink_comm::MpMiad** out) {
+  const auto key = std::make_tuple(coll, coll == kBroadcast ? root : -1, int(dtype), count);
+  blink_comm::MpMiad& m = comm->mp_miad[key];
+  *out = &m;
+  if (m.done) {
+    *chunk = m.chunk;
+    return BLINK_SUCCESS;
+  }
+  const uint64_t seq = comm->miad_seq++;
+  const int es = esize_of(dtype);
+  size_t c = 0;
+  bool conv = false;
+  if (comm->rank == 0) {
+    if (m.calls == 0) {  // start from the static table's chunk (R#15)
+      std::vector<TreeRange> rr;
+      std::string err;
+      const int hint = std::max(1, co_resident_budget(comm, comm->device, dtype, BLINK_SUM, coll) /
+                                       std::max<int>(1, int(plan.trees.size())));
+      size_t init = size_t(1) << 20;
+      if (size_plan(plan, count, es, comm->cfg, hint, &rr, &err) == BLINK_SUCCESS && !rr.empty())
+        init = size_t(rr[0].chunk) * es;
+      blink_miad_init(&m.st, init, 16 << 10, size_t(64) << 20);
+      CUDA_TRY(comm, cudaEventCreate(&m.ev0));
+      CUDA_TRY(comm, cudaEventCreate(&m.ev1));
+    } else if (m.pending && cudaEventQuery(m.ev1) == cudaSuccess) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, m.ev0, m.ev1);
+      if (ms > 0.f) blink_miad_step(&m.st, double(count * es) / (double(ms) * 1e-3));
+      m.pending = false;
+    }
+    conv = m.st.phase == 2;
+    c = conv ? m.st.best : m.st.chunk;
+    cudaError_t e = launch_store2(comm->flags + miad_idx(seq), seq + 1, uint64_t(c) | (uint64_t(conv) << 56),
+                                  stream);
+    if (e != cudaSuccess) return fail(comm, BLINK_ERR_CUDA, std::string("MIAD publish: ") + cudaGetErrorString(e));
+  } else {
+    if (!comm->miad_stream) CUDA_TRY(comm, cudaStreamCreateWithFlags(&comm->miad_stream, cudaStreamNonBlocking));
+    const uint64_t* src = comm->peer_flags[0] + miad_idx(seq);
+    uint64_t v[2] = {0, 0};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int pass = 0;; ++pass) {
+      CUDA_TRY(comm, cudaMemcpyAsync(v, src, sizeof v, cudaMemcpyDeviceToHost, comm->miad_stream));
+      CUDA_TRY(comm, cudaStreamSynchronize(comm->miad_stream));
+      if (v[0] == seq + 1) break;
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > comm->cfg.timeout_s)
+        return fail(comm, BLINK_ERR_TIMEOUT,
+                    "MIAD: rank 0 did not publish the chunk size of autotuned call " + std::to_string(seq));
+      if (pass > 8) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    // the tag is stored after the value (with a fence): read the value again
+    CUDA_TRY(comm, cudaMemcpyAsync(v, src, sizeof v, cudaMemcpyDeviceToHost, comm->miad_stream));
+    CUDA_TRY(comm, cudaStreamSynchronize(comm->miad_stream));
+    c = size_t(v[1] & ((uint64_t(1) << 56) - 1));
+    conv = (v[1] >> 56) != 0;
+  }
+  if (conv) {
+    m.done = true;
+    m.chunk = c;
+  }
+  m.calls++;
+  *chunk = c;
+  return BLINK_SUCCESS;
+}
+
 blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* recv[kMaxRanks],
                       size_t count, blink_dtype_t dtype, int op, int root, cudaStream_t stream) {
   const int n = comm->nranks;
@@ -1302,15 +1418,21 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   blink_result_t r = get_plan(comm, coll, root, bytes, &plan);
   if (r != BLINK_SUCCESS) return r;
   uint64_t mask = uint64_t(1) << comm->rank;
+  size_t chunk_override = 0;
+  blink_comm::MpMiad* mm = nullptr;
+  if (comm->cfg.autotune && (coll == kBroadcast || coll == kAllReduce)) {
+    r = mp_miad_chunk(comm, coll, root, dtype, count, *plan, stream, &chunk_override, &mm);
+    if (r != BLINK_SUCCESS) return r;
+  }
   SizedKey key{coll, (coll == kBroadcast || coll == kGather) ? root : -1, int(dtype), count,
-               mask | (uint64_t(plan->trees.size()) << 32)};
+               mask | (uint64_t(plan->trees.size()) << 32), chunk_override};
   auto it = comm->sized.find(key);
   if (it == comm->sized.end()) {
     Sized s;
     int budget = co_resident_budget(comm, comm->device, dtype, op, coll);
     std::vector<uint64_t> gm;  // one group per process
     for (int u = 0; u < n; ++u) gm.push_back(uint64_t(1) << u);
-    r = build_sized(comm, *plan, count, es, mask, gm, budget, &s);
+    r = build_sized(comm, *plan, count, es, mask, gm, budget, &s, chunk_override);
     if (r != BLINK_SUCCESS) return r;
     r = finalize_tables(comm, comm->device, es, &s);
     if (r != BLINK_SUCCESS) return r;
@@ -1353,9 +1475,15 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     if (coll == kReduceScatter && a.recv[u]) a.recv[u] -= size_t(u) * bytes;
     if ((coll == kAllGather || coll == kGather) && a.send[u]) a.send[u] -= size_t(u) * bytes;
   }
+  const bool time_it = mm && mm->ev0 && !mm->pending && !mm->done;  // rank 0 only
+  if (time_it) CUDA_TRY(comm, cudaEventRecord(mm->ev0, stream));
   cudaError_t le = launch_exec(a, s.ctas, comm->cfg.threads, vec, stream, use_coop(), use_pdl());
   if (le != cudaSuccess)
     return fail(comm, BLINK_ERR_CUDA, std::string("exec launch: ") + cudaGetErrorString(le));
+  if (time_it) {
+    CUDA_TRY(comm, cudaEventRecord(mm->ev1, stream));
+    mm->pending = true;
+  }
   comm->stats.launches++;
   comm->stats.last_ctas = s.ctas;
   comm->stats.last_chunks = s.chunks;
@@ -1591,11 +1719,28 @@ blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const bli
   blink_result_t r = build_graph(graph, nranks, &g, &err);
   if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
   Plan p;
-  const int coll = is_allreduce ? kAllReduce : kBroadcast;
-  if (use_shallow_plan(g, coll, count * size_t(es), cfg))
+  // is_allreduce: 0 Broadcast, 1 AllReduce, 2 ReduceScatter, 3 AllGather, 4 Gather
+  if (is_allreduce < 0 || is_allreduce > kGather)
+    return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "collective code must be 0..4");
+  const int coll = is_allreduce;
+  if (is_block_coll(coll) && g.multi_server) {
+    r = BLINK_ERR_UNSUPPORTED;
+    err = "multi-server graphs support AllReduce only";
+  } else if (is_block_coll(coll) && !g.switch_model) {
+    r = make_block_plan(g, coll, root, &p, &err);
+  } else if (is_block_coll(coll)) {  // one-hop stars, tree j owns block j (as get_plan)
+    r = make_plan(g, kAllReduce, root, cfg, &p, &err);
+    p.coll = coll;
+    p.blocks = true;
+    if (coll == kGather)
+      for (Tree& t : p.trees)
+        for (int v = 0; v < int(t.parent.size()); ++v)
+          if (t.parent[v] >= 0 && v != root) t.parent[v] = -2;
+  } else if (use_shallow_plan(g, coll, count * size_t(es), cfg)) {
     r = make_shallow_plan(g, coll, root, &p, &err);
-  else
+  } else {
     r = make_plan(g, coll, root, cfg, &p, &err);
+  }
   if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
   std::vector<TreeRange> ranges;
   int hint = std::max(1, (cfg.ctas > 0 ? cfg.ctas : 296) / int(p.trees.size()));
@@ -2059,10 +2204,16 @@ blink_result_t blink_destroy(blink_comm_t comm) {
       }
       for (auto& kv : comm->opened) cudaIpcCloseMemHandle(kv.second);
       if (comm->staging) cudaFree(comm->staging);
+      for (auto& kv : comm->mp_miad) {
+        if (kv.second.ev0) cudaEventDestroy(kv.second.ev0);
+        if (kv.second.ev1) cudaEventDestroy(kv.second.ev1);
+      }
+      if (comm->miad_stream) cudaStreamDestroy(comm->miad_stream);
       if (comm->err_host) cudaFreeHost(comm->err_host);
       if (comm->ctrl) cudaFree(comm->ctrl);
     }
     if (comm->flags) cudaFree(comm->flags);
+    if (comm->scratch) cudaFree(comm->scratch);
   }
   Clique* q = comm->clique;
   if (q) {

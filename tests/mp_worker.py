@@ -140,6 +140,14 @@ def gpu_mode(rank, world):
     torch.cuda.synchronize()
     if rank == groot:
         check(gout, OC.gather(gsends, groot)[groot], "staged gather")
+    # 6b) Gather whose root recv IS registered while the other ranks pass
+    # NULL: every rank must still take the same (staged) path
+    greg = torch.full((world * 9001,), float("nan"), device="cuda")
+    comm.register(greg, greg.numel() * 4, ex)          # collective: same size on every rank
+    comm.gather(gx, greg if rank == groot else None, root=groot)
+    torch.cuda.synchronize()
+    if rank == groot:
+        check(greg, OC.gather(gsends, groot)[groot], "gather into a registered root recv")
     # 7) low-latency protocol (small calls, unregistered buffers, no handshake):
     # AllReduce f32/bf16 (ragged), in place, Broadcast; then LL and tree calls
     # interleaved back to back (the epochs they share stay in step)
@@ -219,8 +227,79 @@ def chain_mode(rank, world):
     torch.cuda.synchronize()
     for k in range(5):
         check(outs[k], srcs[k], f"tree LL broadcast {k}")
+    # NEXT-3 on the chain: rank 1 relays; Gather to 0 (block 2 goes
+    # 2 -> 1 -> 0 through the staging buffers) and AllGather
+    gs = synth.inputs(52, world, 20001, "f32")
+    gx = torch.from_numpy(gs[rank]).cuda()
+    gout = torch.full((world * 20001,), float("nan"), device="cuda") if rank == 0 else None
+    comm.gather(gx, gout, root=0)
+    agout = torch.full((world * 20001,), float("nan"), device="cuda")
+    comm.allgather(gx, agout)
+    torch.cuda.synchronize()
+    if rank == 0:
+        check(gout, OC.gather(gs, 0)[0], "chain gather")
+    check(agout, OC.allgather(gs), "chain allgather")
     comm.destroy()
     print(f"rank {rank}: chain ok")
+
+
+def miad_mode(rank, world):
+    """MIAD across processes (NEXT-2): rank 0 picks every
+    autotuned call's chunk size and publishes it; every rank must chunk each
+    call identically (same last_chunk_bytes), the size must change across
+    calls, and every result stays bit-exact.  AllReduce and Broadcast calls
+    interleave (one numbered sequence of autotuned calls across keys)."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    dev = 0 if os.environ.get("BLINK_SAME_GPU") == "1" else rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    comm = BD.init(cfg=B.config(timeout_s=60.0, autotune=1, staging_bytes=1 << 20), device=dev)
+    ex = BD.exchange()
+    count = 4 << 20
+    sends = synth.inputs(51, world, count, "f32")
+    x = torch.from_numpy(sends[rank]).cuda()
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    comm.register(x, count * 4, ex)
+    comm.register(y, count * 4, ex)
+    comm.register(z, count * 4, ex)
+    want = OC.naive_reduce(sends, "f32", "sum")
+    chunks, bchunks = [], []
+    for k in range(14):
+        y.fill_(float("nan"))
+        comm.allreduce(x, y, op="sum")
+        chunks.append(comm.stats()["last_chunk_bytes"])
+        comm.broadcast(x if rank == 1 else None, z, root=1)
+        bchunks.append(comm.stats()["last_chunk_bytes"])
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()
+        if not np.array_equal(got.view(np.uint32), want.view(np.uint32)):
+            raise SystemExit(f"rank {rank}: MIAD call {k}: allreduce mismatch")
+        if not np.array_equal(z.cpu().numpy().view(np.uint32), sends[1].view(np.uint32)):
+            raise SystemExit(f"rank {rank}: MIAD call {k}: broadcast mismatch")
+    allc = [None] * world
+    dist.all_gather_object(allc, (chunks, bchunks))
+    assert all(c == allc[0] for c in allc), allc
+    assert len(set(chunks)) >= 2, chunks
+    comm.destroy()
+    print(f"rank {rank}: miad ok {chunks} {bchunks}")
+
+
+def fingerprint_mode(rank, world):
+    """Ranks whose chunk tables differ (here BLINK_CHUNKS_PER_CTA on rank 1)
+    would consume each other's flags for different byte ranges: blink_connect
+    refuses the mix on every rank with BLINK_ERR_INVALID_USAGE."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    torch.cuda.set_device(0)
+    if rank == 1:
+        os.environ["BLINK_CHUNKS_PER_CTA"] = "7"
+    try:
+        BD.init(cfg=B.config(timeout_s=5.0), device=0)
+        raise SystemExit(f"rank {rank}: connect accepted mismatched chunking")
+    except B.BlinkError as e:
+        assert e.code == 5 and "chunks differently" in str(e), e
+    print(f"rank {rank}: fingerprint ok")
 
 
 def timeout_mode(rank, world):
@@ -262,6 +341,10 @@ def main():
             timeout_mode(rank, world)
         elif mode == "chain":
             chain_mode(rank, world)
+        elif mode == "fingerprint":
+            fingerprint_mode(rank, world)
+        elif mode == "miad":
+            miad_mode(rank, world)
         else:
             gpu_mode(rank, world)
     finally:

@@ -42,3 +42,39 @@ def test_reference_arm_under_torchrun_prints_once():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["config"]["ranks"] == 2
+
+
+def test_multiprocess_line_fields():
+    """The N > 1 line (rank 0): busBW against NVLink's 900 GB/s per direction
+    (SURVEY 8(d)), the Broadcast arm, graph timings, e2e and NCCL blocks."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    args = argparse.Namespace(steps=20, warmup=5)
+    S = 256 << 20
+    m = 8
+    ms = 0.5
+    d = bench.multiprocess_line(args, m, S, ms, 0.4, {"blink_allreduce_ms": 0.49}, 40.0, 20, 20,
+                                None, {"allreduce": {"ms": 0.6}})
+    alg = S / (ms * 1e-3) / 1e9
+    assert d["value"] == round(alg, 3) and d["n_gpus"] == 8
+    r = d["roofline"]
+    assert r["peak"] == 900.0 and r["bound"] == "nvlink"
+    assert abs(r["frac"] - alg * 2 * 7 / 8 / 900.0) < 1e-3
+    assert d["broadcast"]["root"] == 0 and abs(d["broadcast"]["frac"] - S / 0.4e-3 / 1e9 / 900.0) < 1e-3
+    assert d["nccl"]["allreduce"]["ms"] == 0.6 and d["graph"]["blink_allreduce_ms"] == 0.49
+    for k in ("metric", "unit", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "dtype", "config", "e2e", "gpu_launches"):
+        assert k in d
+
+
+def test_nccl_tuning_lines_parser(tmp_path):
+    sys.path.insert(0, ROOT)
+    import bench
+    log = tmp_path / "nccl.log"
+    log.write_text("host:1:2 [0] NCCL INFO AllReduce: opCount 0 sendbuff 0x1 count 67108864 Algo RING proto SIMPLE\n"
+                   "host:1:2 [0] NCCL INFO Broadcast: opCount 1 Algo NVLS proto SIMPLE channels 16\n"
+                   "host:1:2 [0] NCCL INFO Channel 00/16 : 0 1 2\n")
+    got = bench.tuning_lines(str(log))
+    assert len(got) == 2 and "RING" in got[0] and "NVLS" in got[1]
+    assert bench.tuning_lines(str(tmp_path / "missing.log")) == []

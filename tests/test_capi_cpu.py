@@ -462,3 +462,71 @@ def test_chunk_policy_deep_trees_and_merged_medium_calls(B):
     for t in p["trees"]:
         nbytes = (t["hi"] - t["lo"]) * 4
         assert t["chunk"] * 4 >= max(16 << 10, nbytes // 16)
+
+
+# ------------------------------------------------------------ NEXT-3 on link graphs
+def _random_link_graph(seed, lo=3, hi=8, p=0.45):
+    import random
+    from oracle import graphs
+    rng = random.Random(seed)
+    n = rng.randint(lo, hi)
+    while True:
+        cap = {}
+        for u in range(n):
+            for v in range(u + 1, n):
+                if rng.random() < p:
+                    cap[(u, v)] = cap[(v, u)] = rng.randint(1, 3)
+        if graphs.is_connected((n, cap)):
+            return n, cap, rng
+
+
+@pytest.mark.parametrize("seed", list(range(10)) + ["dgx1v", "dgx1p"])
+def test_link_graph_allgather_and_gather_plans(B, seed):
+    """NEXT-3 on packed link graphs.  AllGather: tree j is a spanning
+    arborescence rooted at j over real links with every rank at its shortest
+    distance from j (Floyd-Warshall) and covers block j.  Gather to r: tree j
+    is a chain from j to r over real links of length dist(j, r), ranks off
+    the chain are not members; tree r is r alone."""
+    from oracle import graphs
+    if seed in ("dgx1v", "dgx1p"):
+        g = graphs.dgx1v() if seed == "dgx1v" else graphs.dgx1p()
+        n, cap = g
+        roots = range(n)
+    else:
+        n, cap, rng = _random_link_graph(9000 + seed)
+        roots = [rng.randrange(n)]
+    G = B.Graph.from_pairs(n, cap)
+    d = _bfs_dist_fw(n, cap, False)
+    count = 1001
+    ag = B.plan_json(n, 3, 0, count, "f32", graph=G)
+    assert len(ag["trees"]) == n
+    for j, t in enumerate(ag["trees"]):
+        par = t["parent"]
+        assert t["root"] == j and par[j] == -1
+        assert (t["lo"], t["hi"]) == (j * count, (j + 1) * count)
+        for v in range(n):
+            if v != j:
+                assert cap.get((par[v], v), 0) > 0 and d[j][par[v]] + 1 == d[j][v]
+        assert t["depth"] == max(d[j])
+    for r in roots:
+        ga = B.plan_json(n, 4, r, count, "f32", graph=G)
+        assert len(ga["trees"]) == n
+        for j, t in enumerate(ga["trees"]):
+            par = t["parent"]
+            assert t["root"] == j and par[j] == -1
+            assert (t["lo"], t["hi"]) == (j * count, (j + 1) * count)
+            members = [v for v in range(n) if par[v] != -2]
+            assert len(members) == d[j][r] + 1 and t["depth"] == d[j][r]
+            v = r
+            while v != j:                      # walk back from the gather root
+                u = par[v]
+                assert cap.get((u, v), 0) > 0 and d[u][r] == d[v][r] + 1
+                v = u
+
+
+def test_link_graph_reduce_scatter_stays_switch_only(B):
+    from oracle import graphs
+    g = graphs.dgx1v()
+    with pytest.raises(B.BlinkError) as e:
+        B.plan_json(8, 2, 0, 1000, "f32", graph=B.Graph.from_pairs(8, g[1]))
+    assert e.value.code == 9

@@ -741,3 +741,62 @@ def test_avg_multilevel_ll_and_reduce_scatter(B, dtype):
         assert_bitwise(to_host(outs[r], dtype), blocks[r])
     for c in comms:
         c.destroy()
+
+
+# ----------------------------------------------------------------- NEXT-3 on link graphs
+LINK_GRAPHS = [("dgx1v", list(range(8))), ("dgx1v", [0, 1, 3, 4, 5, 7]), ("dgx1p", [1, 4, 5, 6]),
+               ("dgx1p", [0, 1, 4])]
+
+
+@pytest.mark.parametrize("machine,ids", LINK_GRAPHS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_link_graph_allgather_and_gather(B, machine, ids, dtype):
+    """AllGather ("AllReduce without a reduction function") and Gather ("the
+    inverse of Broadcast") on packed link graphs: multi-level trees,
+    relays forwarding other ranks' blocks (Gather relays with recv = NULL go
+    through the library's scratch).  Exact against the oracle's definitions."""
+    full = OG.dgx1v() if machine == "dgx1v" else OG.dgx1p()
+    g, _ = OG.induced(full, ids)
+    m = len(ids)
+    comms = make_comms(B, m, graph=B.Graph.from_pairs(m, g[1]), chunk_bytes=8192)
+    for B_ in (1, 4099, 65536):
+        sends = synth.inputs(150 + B_ % 7, m, B_, dtype)
+        ds = [to_dev(s, dtype) for s in sends]
+        outs = [sentinel(m * B_, dtype) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.allgather(ds[r], outs[r], sendcount=B_, dtype=dtype)
+        torch.cuda.synchronize()
+        want = OC.allgather(sends)
+        for o in outs:
+            assert_bitwise(to_host(o, dtype), want)
+        for root in sorted({0, m - 1}):
+            out = sentinel(m * B_, dtype)
+            for r, c in enumerate(comms):
+                c.gather(ds[r], out if r == root else None, root=root, sendcount=B_, dtype=dtype)
+            torch.cuda.synchronize()
+            assert_bitwise(to_host(out, dtype), OC.gather(sends, root)[root])
+    assert comms[0].stats()["last_trees"] == m
+    for c in comms:
+        c.destroy()
+
+
+def test_link_graph_allgather_in_place_and_depth(B):
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]))
+    B_ = (1 << 20) + 3
+    sends = synth.inputs(160, 8, B_, "f32")
+    bufs = []
+    for r in range(8):
+        b = sentinel(8 * B_, "f32")
+        b[r * B_:(r + 1) * B_] = to_dev(sends[r], "f32")
+        bufs.append(b)
+    for r, c in enumerate(comms):
+        c.allgather(bufs[r][r * B_:(r + 1) * B_], bufs[r], sendcount=B_, dtype="f32")
+    torch.cuda.synchronize()
+    want = OC.allgather(sends)
+    for b in bufs:
+        assert_bitwise(to_host(b, "f32"), want)
+    p = B.plan_json(8, 3, 0, B_, "f32", graph=B.Graph.from_pairs(8, g[1]))
+    assert max(t["depth"] for t in p["trees"]) == 2          # DGX-1V: every rank within 2 hops
+    for c in comms:
+        c.destroy()

@@ -215,3 +215,54 @@ def test_per_rank_large_multilevel_allreduce_int_exact(B):
         assert torch.equal(y, want)
     for c in comms:
         c.destroy()
+
+
+def test_per_rank_miad_autotune(B):
+    """NEXT-2 with per-rank launches (the multi-process protocol's kernels):
+    MIAD moves the chunk size across calls, every rank's launch chunks each
+    call identically, and every call stays bit-exact."""
+    m, count = 4, (2 << 20) + 7
+    comms = per_rank_comms(B, m, autotune=1)
+    sends = synth.inputs(121, m, count, "f32")
+    want = OC.naive_reduce(sends, "f32", "sum")
+    ds = [to_dev(s, "f32") for s in sends]
+    out = [torch.empty_like(d) for d in ds]
+    chunks = []
+    for it in range(14):
+        for r, c in enumerate(comms):
+            c.allreduce(ds[r], out[r])
+        torch.cuda.synchronize()
+        per = {c.stats()["last_chunk_bytes"] for c in comms}
+        assert len(per) == 1, per
+        chunks.append(per.pop())
+        for x in out:
+            assert_bitwise(x.cpu().numpy(), want)
+    assert len(set(chunks)) >= 2, chunks
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "i32"])
+def test_per_rank_link_graph_allgather_and_gather(B, dtype):
+    """NEXT-3 on DGX-1V with per-rank launches: relays wait for their chain
+    parent's per-chunk flags across launches, exit waits cover every block a
+    rank receives."""
+    g = OG.dgx1v()
+    comms = per_rank_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=8192)
+    B_ = 70001
+    sends = synth.inputs(170, 8, B_, dtype)
+    ds = [to_dev(s, dtype) for s in sends]
+    outs = [sentinel(8 * B_, dtype) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.allgather(ds[r], outs[r], sendcount=B_, dtype=dtype)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert_bitwise(to_host(o, dtype), OC.allgather(sends))
+    for root in (0, 6):
+        out = sentinel(8 * B_, dtype)
+        for r, c in enumerate(comms):
+            c.gather(ds[r], out if r == root else None, root=root, sendcount=B_, dtype=dtype)
+        torch.cuda.synchronize()
+        assert_bitwise(to_host(out, dtype), OC.gather(sends, root)[root])
+    for c in comms:
+        c.destroy()

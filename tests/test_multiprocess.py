@@ -59,3 +59,38 @@ def test_missing_rank_times_out_instead_of_hanging():
     out = launch(2, "timeout", {"BLINK_SAME_GPU": "1"}, timeout=300)
     assert "rank 0: tree timeout ok" in out
     assert "rank 0: LL timeout ok" in out
+
+
+@pytest.mark.gpu
+def test_connect_rejects_ranks_that_chunk_differently():
+    out = launch(2, "fingerprint", {"BLINK_SAME_GPU": "1"}, timeout=300)
+    assert out.count("fingerprint ok") == 2
+
+
+@pytest.mark.gpu
+def test_miad_across_processes_chunks_identically():
+    """NEXT-2 across processes: rank 0 decides, every rank chunks each call
+    the same way, the chunk size changes, results stay bit-exact."""
+    out = launch(2, "miad", {"BLINK_SAME_GPU": "1"}, timeout=600)
+    assert out.count("miad ok") == 2
+
+
+def _devices():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_devices() < 2, reason="needs >= 2 GPUs (distinct devices: .sys flags, TMA over NVLink)")
+@pytest.mark.parametrize("mode,n", [("gpu", 2), ("chain", 3), ("miad", 2)])
+def test_processes_on_distinct_gpus(mode, n):
+    """The multi-process suite with one process per GPU: .sys-scope flags,
+    cp.async.bulk loads/stores to IPC-mapped peer-GPU memory, cross-device
+    IPC.  Skipped on the 1-GPU box (readiness for the first multi-GPU lease)."""
+    if _devices() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = launch(n, mode, {}, timeout=900)
+    assert out.count(f"{mode} ok") == n
