@@ -256,6 +256,23 @@ blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* rec
 blink_result_t blink_gather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
                             size_t sendcount, blink_dtype_t dtype, int root, void* stream);
 
+/* ---------------------------------------------------------------- topology probe
+ * "Blink probes the set of links available ... and builds a topology with
+ * appropriate link capacities" (Sec. 1; Sec. 2.3).  For the GPUs
+ * named by their PCI bus ids (cudaDeviceGetPCIBusId format), reads every
+ * active NVLink port from NVML (loaded at run time) and writes
+ * {"kind": "virtual"|"nvswitch"|"nvlink"|"pcie", "switch_ports": [per GPU],
+ *  "links": [[u, v, ports], ...], "note": "..."}.  "nvlink" graphs (direct
+ * GPU-GPU links; capacity = parallel links) are packed (Sec. 3.2); the other
+ * kinds use the one-hop switch model.  blink_init / blink_init_all run this
+ * probe when graph == NULL, and blink_get_plan reports it under "topology".
+ * Host only; BLINK_FAKE_NVML=<file> substitutes a port table ("<bus id>
+ * <port> <remote bus id | switch>" per line).  json/json_bytes as for
+ * blink_plan_json.  Errors: INVALID_ARGUMENT (NULL, bad bus id, small
+ * buffer), UNSUPPORTED (ndev outside 1..16), SYSTEM (unreadable fake table).
+ * Without NVML the kind is "pcie" and "note" says why. */
+blink_result_t blink_topology_json(int ndev, const char* const* bus_ids, char* json, size_t* json_bytes);
+
 /* ---------------------------------------------------------------- introspection
  * Same JSON as blink_plan_json, for the plan this comm would run, plus "ctas"
  * (CTAs of this rank's launch). */

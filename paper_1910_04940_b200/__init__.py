@@ -91,6 +91,7 @@ _SIGS = {
     "blink_destroy": (_i, [_vp]),
     "blink_miad_init": (None, [ctypes.POINTER(Miad), _sz, _sz, _sz]),
     "blink_miad_step": (_sz, [ctypes.POINTER(Miad), ctypes.c_double]),
+    "blink_topology_json": (_i, [_i, ctypes.POINTER(_cp), _cp, ctypes.POINTER(_sz)]),
     "blink_result_string": (_cp, [_i]),
     "blink_last_error": (_cp, [_vp]),
 }
@@ -176,6 +177,12 @@ def _json_call(fn, *args, comm=None):
         code = fn(*args, buf, ctypes.byref(n))
     _check(code, comm)
     return json.loads(buf.value.decode())
+
+
+def topology_json(bus_ids):
+    """Host-only topology probe of the GPUs with these PCI bus ids."""
+    arr = (ctypes.c_char_p * len(bus_ids))(*[b.encode() for b in bus_ids])
+    return _json_call(_lib.blink_topology_json, len(bus_ids), arr)
 
 
 def plan_json(nranks, is_allreduce, root=0, count=0, dtype="f32", graph=None, cfg=None):

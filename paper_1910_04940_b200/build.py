@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libblink.so")
-SOURCES = ["exec.cu", "plan.cpp", "runtime.cpp"]
+SOURCES = ["exec.cu", "plan.cpp", "runtime.cpp", "probe.cpp"]
 HEADERS = ["blink_internal.h", os.path.join("..", "..", "include", "blink.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -70,7 +70,7 @@ def _build(verbose):
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-           "-o", tmp] + objs
+           "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -255,4 +255,16 @@ std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vect
                          int ctas);
 int esize_of(blink_dtype_t d);
 
+// probe.cpp -------------------------------------------------------------
+// Topology probe: NVLink ports of the ranks' GPUs from NVML.
+struct Probe {
+  std::string kind = "virtual";            // virtual | nvswitch | nvlink | pcie
+  std::string note;
+  std::vector<std::vector<int>> links;     // links[u][v]: NVLink ports of u ending at v
+  std::vector<int> switch_ports;           // NVLink ports of u ending at an NVSwitch
+};
+blink_result_t probe_topology(const std::vector<std::string>& bus_ids, Probe* out, std::string* err);
+void apply_probe(const Probe& p, Graph* g);  // "nvlink" -> the link graph (if connected)
+std::string probe_to_json(const Probe& p);
+
 }  // namespace blink

@@ -120,6 +120,8 @@ struct blink_comm {
   char* staging = nullptr;
   size_t staging_bytes = 0;
   char* peer_staging[kMaxRanks] = {};
+  Probe probe;                // topology probe result (graph == NULL at init)
+  bool probe_at_connect = false;  // multi-process: graph == NULL, probed from the peers' bus ids
   char* scratch = nullptr;    // single-process Gather on link graphs: forwarding buffer of a
   size_t scratch_bytes = 0;   // rank that passed recvbuf == NULL but relays other blocks
   std::string last_error;
@@ -1755,12 +1757,34 @@ blink_result_t blink_plan_json(const blink_graph_t* graph, int nranks, const bli
   return BLINK_SUCCESS;
 }
 
+blink_result_t blink_topology_json(int ndev, const char* const* bus_ids, char* json, size_t* json_bytes) {
+  if (!json_bytes || (ndev > 0 && !bus_ids)) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (ndev < 1 || ndev > kMaxRanks) return fail(nullptr, BLINK_ERR_UNSUPPORTED, "ndev out of range");
+  std::vector<std::string> bus;
+  for (int i = 0; i < ndev; ++i) {
+    if (!bus_ids[i]) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "NULL bus id");
+    bus.push_back(bus_ids[i]);
+  }
+  Probe p;
+  std::string err;
+  blink_result_t r = probe_topology(bus, &p, &err);
+  if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
+  std::string s = probe_to_json(p);
+  const size_t need = s.size() + 1, cap = *json_bytes;
+  *json_bytes = need;
+  if (!json || cap < need) return fail(nullptr, BLINK_ERR_INVALID_ARGUMENT, "json buffer too small");
+  memcpy(json, s.c_str(), need);
+  return BLINK_SUCCESS;
+}
+
 static blink_result_t alloc_comm_common(blink_comm_t c) {
   DeviceGuard g(c->device);
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   // flag words, then the LL protocol's line areas (zero = no flag yet); one
   // allocation, so the flag mapping also maps the LL area to the peers
-  c->ll_bytes = c->nranks > 1 ? ll_area_bytes(c->cfg.ll_max_bytes, c->nranks, link_graph(c)) : 0;
+  c->ll_bytes = c->nranks > 1 ? ll_area_bytes(c->cfg.ll_max_bytes, c->nranks,
+                                               link_graph(c) || c->probe_at_connect)
+                              : 0;
   CUDA_TRY(c, cudaMalloc(&c->flags, kFlagBytes + c->ll_bytes));
   CUDA_TRY(c, cudaMemset(c->flags, 0, kFlagBytes + c->ll_bytes));
   CUDA_TRY(c, cudaDeviceSynchronize());
@@ -1805,6 +1829,20 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
         return fail(nullptr, BLINK_ERR_CUDA, std::string("enable peer access: ") + cudaGetErrorString(e));
       cudaGetLastError();
     }
+  // topology probe when the caller gave no graph
+  Probe probe;
+  if (!graph) {
+    std::vector<std::string> bus(ndev);
+    for (int i = 0; i < ndev; ++i) {
+      char b[32] = {};
+      if (cudaDeviceGetPCIBusId(b, sizeof b, devs[i]) != cudaSuccess)
+        return fail(nullptr, BLINK_ERR_CUDA, "cudaDeviceGetPCIBusId failed");
+      bus[i] = b;
+    }
+    r = probe_topology(bus, &probe, &err);
+    if (r != BLINK_SUCCESS) return fail(nullptr, r, err);
+    apply_probe(probe, &gr);
+  }
   Clique* q = new Clique();
   q->nranks = ndev;
   q->devices = distinct;
@@ -1816,6 +1854,7 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
     c->device = devs[i];
     c->cfg = cfg;
     c->graph = gr;
+    c->probe = probe;
     c->clique = q;
     c->connected = true;
     r = alloc_comm_common(c);
@@ -1889,6 +1928,7 @@ blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_dev
     delete c;
     return fail(nullptr, r, err);
   }
+  c->probe_at_connect = graph == nullptr && nranks > 1;
   r = alloc_comm_common(c);
   if (r != BLINK_SUCCESS) {
     g_last_error = c->last_error;
@@ -1983,6 +2023,19 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
     r = open_handle(comm, b.staging_h, &p);
     if (r != BLINK_SUCCESS) return r;
     comm->peer_staging[u] = p;
+  }
+  if (comm->probe_at_connect) {  // topology probe over every rank's GPU
+    std::vector<std::string> bus(comm->nranks);
+    for (int u = 0; u < comm->nranks; ++u) {
+      Blob b;
+      memcpy(&b, base + size_t(u) * blob_bytes, sizeof b);
+      bus[u] = b.bus_id;
+    }
+    std::string perr;
+    blink_result_t pr = probe_topology(bus, &comm->probe, &perr);
+    if (pr != BLINK_SUCCESS) return fail(comm, pr, perr);
+    apply_probe(comm->probe, &comm->graph);
+    comm->plans.clear();
   }
   Reg st;
   st.buf = comm->staging;
@@ -2154,6 +2207,7 @@ blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, siz
   r = build_sized(comm, *plan, count, es, mask, gm, budget, &s);
   if (r != BLINK_SUCCESS) return r;
   std::string j = plan_to_json(*plan, count, es, s.ranges, s.ctas);
+  j.insert(j.size() - 1, ",\"topology\":" + probe_to_json(comm->probe));
   size_t need = j.size() + 1, cap = *json_bytes;
   *json_bytes = need;
   if (!json || cap < need) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "json buffer too small");

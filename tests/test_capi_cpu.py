@@ -530,3 +530,59 @@ def test_link_graph_reduce_scatter_stays_switch_only(B):
     with pytest.raises(B.BlinkError) as e:
         B.plan_json(8, 2, 0, 1000, "f32", graph=B.Graph.from_pairs(8, g[1]))
     assert e.value.code == 9
+
+
+# ------------------------------------------------------------ topology probe
+def _bus(i):
+    return f"0000:{0x10 + 0x10 * i:02X}:00.0"
+
+
+def _fake_table(path, ports):
+    with open(path, "w") as f:
+        for gpu, port, remote in ports:
+            f.write(f"{gpu} {port} {remote}\n")
+
+
+def test_probe_builds_the_dgx1v_graph_from_a_port_table(B, tmp_path, monkeypatch):
+    """An injected NVML port table with DGX-1V's cabling (App. B: every GPU 6
+    ports, 8 pairs doubled) must probe as kind "nvlink" with exactly the
+    DGX-1V link multiplicities; NVML's bus-id spelling (8-digit domain) must
+    match CUDA's."""
+    from oracle import graphs
+    n, cap = graphs.dgx1v()
+    ports = []
+    nxt = [0] * n
+    for (u, v), c in sorted(cap.items()):
+        for _ in range(c):
+            ports.append((_bus(u).replace("0000:", "00000000:"), nxt[u], _bus(v)))
+            nxt[u] += 1
+    assert all(k == 6 for k in nxt)
+    _fake_table(tmp_path / "t.txt", ports)
+    monkeypatch.setenv("BLINK_FAKE_NVML", str(tmp_path / "t.txt"))
+    d = B.topology_json([_bus(i) for i in range(n)])
+    assert d["kind"] == "nvlink" and d["switch_ports"] == [0] * n
+    got = {(u, v): c for u, v, c in d["links"]}
+    assert got == dict(cap)
+
+
+def test_probe_nvswitch_virtual_and_outside_gpus(B, tmp_path, monkeypatch):
+    # 4 B200-like GPUs, 18 ports each, all ending at NVSwitches
+    ports = [(_bus(i), p, "switch") for i in range(4) for p in range(18)]
+    _fake_table(tmp_path / "s.txt", ports)
+    monkeypatch.setenv("BLINK_FAKE_NVML", str(tmp_path / "s.txt"))
+    d = B.topology_json([_bus(i) for i in range(4)])
+    assert d["kind"] == "nvswitch" and d["switch_ports"] == [18] * 4 and d["links"] == []
+    # one device repeated (virtual ranks): no NVML needed
+    assert B.topology_json([_bus(0)] * 3)["kind"] == "virtual"
+    # links to a GPU outside the allocation do not count (P:320); a pair
+    # with ports only in one direction table still counts per direction
+    ports = [(_bus(0), 0, _bus(1)), (_bus(1), 0, _bus(0)), (_bus(1), 1, _bus(2)), (_bus(2), 0, _bus(1)),
+             (_bus(2), 1, _bus(7))]
+    _fake_table(tmp_path / "c.txt", ports)
+    monkeypatch.setenv("BLINK_FAKE_NVML", str(tmp_path / "c.txt"))
+    d = B.topology_json([_bus(i) for i in range(3)])
+    assert d["kind"] == "nvlink"
+    assert sorted(tuple(x) for x in d["links"]) == [(0, 1, 1), (1, 0, 1), (1, 2, 1), (2, 1, 1)]
+    with pytest.raises(B.BlinkError) as e:
+        B.topology_json(["not-a-bus-id", _bus(1)])
+    assert e.value.code == 4
