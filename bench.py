@@ -353,7 +353,9 @@ def time_device(fn, steps, stream, graph=False):
     t1 = torch.cuda.Event(enable_timing=True)
     if graph:
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
+        cs = torch.cuda.Stream()           # captures need a non-default stream
+        cs.wait_stream(stream)
+        with torch.cuda.graph(g, stream=cs):
             for _ in range(steps):
                 fn()
         g.replay()
@@ -438,13 +440,15 @@ def run_multiprocess(args):
     comm.register(send, S, ex)
     comm.register(recv, S, ex)
     stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
 
+    # calls enqueue on the current stream: `stream` eagerly, the capture
+    # stream inside a CUDA-graph capture
     def blink_ar():
-        comm.allreduce(send, recv, op="sum", stream=stream)
+        comm.allreduce(send, recv, op="sum", stream=torch.cuda.current_stream())
 
     def blink_bc():
-        comm.broadcast(send if rank == 0 else None, recv, root=0, count=count, dtype="f32", stream=stream)
+        comm.broadcast(send if rank == 0 else None, recv, root=0, count=count, dtype="f32",
+                       stream=torch.cuda.current_stream())
 
     def max_ms(ms):
         t = torch.tensor([ms], dtype=torch.float64)
@@ -537,7 +541,6 @@ def nccl_compare(args, send, recv, count, stream, rank, world, same_gpu, tune_lo
     except Exception as e:  # pragma: no cover - depends on the box
         return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
     S = count * 4
-    sp = stream.cuda_stream
 
     def max_ms(ms):
         t = torch.tensor([ms], dtype=torch.float64)
@@ -561,16 +564,20 @@ def nccl_compare(args, send, recv, count, stream, rank, world, same_gpu, tune_lo
 
     f_ar = 2 * (world - 1) / world
     sptr, rptr = send.data_ptr(), recv.data_ptr()
+
+    def cur():
+        return torch.cuda.current_stream().cuda_stream
+
     try:
-        arm("allreduce", lambda: nc.allreduce(sptr, rptr, count, sp), f_ar)
-        arm("broadcast", lambda: nc.broadcast(sptr, rptr, count, 0, sp), 1.0)
+        arm("allreduce", lambda: nc.allreduce(sptr, rptr, count, cur()), f_ar)
+        arm("broadcast", lambda: nc.broadcast(sptr, rptr, count, 0, cur()), 1.0)
         try:   # symmetric windows (NCCL 2.27+): buffers from ncclMemAlloc
             a = nc.mem_alloc(S)
             b = nc.mem_alloc(S)
             torch.cuda.synchronize()
             nc.window(a, S)
             nc.window(b, S)
-            arm("allreduce_symmetric", lambda: nc.allreduce(a, b, count, sp), f_ar)
+            arm("allreduce_symmetric", lambda: nc.allreduce(a, b, count, cur()), f_ar)
         except Exception as e:  # pragma: no cover
             out["allreduce_symmetric"] = {"unavailable": f"{type(e).__name__}: {e}"[:160]}
     except Exception as e:  # pragma: no cover - depends on the box

@@ -35,7 +35,9 @@ constexpr size_t kPflagWords = size_t(kMaxTrees) * kMaxRanks * kMaxChunks;
 constexpr size_t kBflagWords = size_t(kMaxTrees) * kMaxChunks;
 constexpr size_t kMiadSlots = 64;
 constexpr size_t kMiadWords = 2 * kMiadSlots;
-constexpr size_t kFlagWords = kEntryWords + kPflagWords + kBflagWords + kMiadWords;
+//   setup[2][u]           NVLS set-up barriers at blink_connect (1 = ok, 9 = failed)
+constexpr size_t kSetupWords = 2 * kMaxRanks;
+constexpr size_t kFlagWords = kEntryWords + kPflagWords + kBflagWords + kMiadWords + kSetupWords;
 constexpr size_t kFlagBytes = kFlagWords * sizeof(uint64_t);
 __host__ __device__ inline size_t entry_idx(int u) { return size_t(u); }
 __host__ __device__ inline size_t pflag_idx(int tree, int child, int chunk) {
@@ -46,6 +48,9 @@ __host__ __device__ inline size_t bflag_idx(int tree, int chunk) {
 }
 __host__ __device__ inline size_t miad_idx(uint64_t seq) {
   return kEntryWords + kPflagWords + kBflagWords + 2 * size_t(seq % kMiadSlots);
+}
+__host__ __device__ inline size_t setup_idx(int round, int u) {
+  return kEntryWords + kPflagWords + kBflagWords + kMiadWords + size_t(round) * kMaxRanks + u;
 }
 
 enum Coll : int { kBroadcast = 0, kAllReduce = 1, kReduceScatter = 2, kAllGather = 3, kGather = 4 };
@@ -217,6 +222,24 @@ struct LLArgs {
   char* recv[kMaxRanks];
   uint4* ll[kMaxRanks];        // rank u's LL area (peer-mapped)
 };
+
+// NEXT-1 (nvls.cu): one call / piece of an NVLS AllReduce (SUM) or Broadcast
+// over the multicast-bound buffers uc (unicast) / mc (multicast) of `bytes`
+// (a multiple of 16), for rank `rank`.
+struct NvlsArgs {
+  int nranks, rank, coll, dtype, root;
+  int pad;
+  int64_t bytes;
+  const char* send;
+  char* recv;
+  char* uc;
+  char* mc;
+  uint64_t* flags[kMaxRanks];  // every rank's flag words (peer mappings)
+  uint64_t* ctrl;              // this launch's epoch / counter words
+  int* err;
+  uint64_t timeout_ns;
+};
+cudaError_t launch_nvls(const NvlsArgs& a, int grid, void* stream);
 
 // exec.cu
 cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative, bool pdl);

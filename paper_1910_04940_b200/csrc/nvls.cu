@@ -1,0 +1,244 @@
+// NEXT-1: the one-hop trees of Sec. 3.5 realised inside the
+// NVSwitch (NVLS multicast objects).
+//
+// "each GPU acts as a root for 1/m of the data chunks and each root is
+// directly connected to (m - 1) leaf nodes".  On NVSwitch the star's two
+// halves become switch operations:
+//   reduce toward root j   multimem.ld_reduce on slice j of the multicast
+//                          address: the switch reads slice j from every
+//                          rank's buffer and adds (leaves -> root, in-fabric)
+//   broadcast back          multimem.st of the result to the multicast address:
+//                          the switch writes it into every rank's buffer
+// Per-GPU NVLink traffic is about (1 + 1/m) S each way instead of the P2P
+// stars' 2 (m - 1) / m S.  Broadcast: the root's multimem.st of the whole
+// buffer (the one-hop star r -> all, replicated in the switch).
+//
+// Buffers: every rank owns `nvls_bytes` of physical memory bound to one
+// multicast object (unicast mapping `uc[v]`, multicast mapping `mc[v]`).  A
+// call copies the rank's send into its uc (local HBM), runs the switch
+// operations on the mc addresses, and copies its uc out to recv (local).
+// Calls larger than the region run in pieces.
+//
+// Synchronisation (epoch flags in the tree executor's flag words, same
+// release/acquire pattern):
+//   entry[v] = e   in every peer: v's uc holds its send for call e, and v is
+//                  done with call e - 1 (its copy-out finished), so the switch
+//                  may read and overwrite it
+//   bflag[j][0] = e  in every peer: root j's reduced slice has been stored
+//                  through the switch into every uc (Broadcast: the root's
+//                  whole buffer, as bflag[root][0])
+// A rank copies out only after every root's bflag, i.e. after every switch
+// read of its uc for call e, so the next call's copy-in is safe.
+//
+// Numerics: the switch's reduction order is not the oracle's ascending-rank
+// order, so float results are compared with the north_star tolerance
+// (R#29); bf16 accumulates in fp32 (.acc::f32) and rounds once (R#13's one
+// rounding per node); int32 sums are exact.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "blink_internal.h"
+
+namespace blink {
+namespace {
+
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// spin until *p >= e; false on timeout (sets the host-mapped error word)
+__device__ bool nv_wait(const uint64_t* p, uint64_t e, uint64_t timeout_ns, int* err) {
+  const uint64_t t0 = gtimer();
+  for (int spin = 0;; ++spin) {
+    if (ld_relaxed_sys(p) >= e) return true;
+    if ((spin & 255) == 255) {
+      if (*reinterpret_cast<volatile int*>(err) != 0) return false;
+      if (gtimer() - t0 > timeout_ns) {
+        *reinterpret_cast<volatile int*>(err) = int(BLINK_ERR_TIMEOUT);
+        return false;
+      }
+    }
+  }
+}
+
+// grid-wide arrival on a device counter (CTAs are co-resident: grid <= SMs)
+__device__ void grid_sync(unsigned int* ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (atomicAdd(ctr, 0u) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int DT>
+__device__ __forceinline__ uint4 mm_ld_reduce(const uint4* mc) {
+  uint4 r;
+  if (DT == BLINK_FLOAT32) {
+    float x, y, z, w;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
+                 : "l"(mc)
+                 : "memory");
+    r = make_uint4(__float_as_uint(x), __float_as_uint(y), __float_as_uint(z), __float_as_uint(w));
+  } else if (DT == BLINK_BFLOAT16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(mc)
+                 : "memory");
+  } else {  // int32: scalar lanes (wraparound sum, exact)
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(mc);
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 1) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 2) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 3) : "memory");
+  }
+  return r;
+}
+// a 16-byte store through the switch into every rank's buffer (bit moves only)
+__device__ __forceinline__ void mm_st(uint4* mc, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc),
+               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+               "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+// One call (or piece) of an NVLS AllReduce / Broadcast for the ranks this
+// launch runs (one per launch in multi-process comms, one per device in
+// single-process comms).  Every CTA copies a stripe in, the rank publishes
+// entry, roots reduce+store their slice through the switch, publish bflag,
+// and every CTA copies a stripe out once all slices have arrived.
+template <int DT>
+__global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
+  __shared__ uint64_t s_epoch;
+  __shared__ int s_ok;
+  const int v = a.rank;
+  const int64_t T = int64_t(gridDim.x) * blockDim.x;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) {
+    s_epoch = *reinterpret_cast<volatile uint64_t*>(a.ctrl) + 1;
+    s_ok = 1;
+  }
+  __syncthreads();
+  const uint64_t e = s_epoch;
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(a.ctrl + 2);
+  const uint4* src = reinterpret_cast<const uint4*>(a.send);
+  uint4* uc = reinterpret_cast<uint4*>(a.uc);
+  uint4* mc = reinterpret_cast<uint4*>(a.mc);
+  const int64_t nvec = a.bytes >> 4;
+  const bool bcast = a.coll == kBroadcast;
+  // 1. copy-in (AllReduce: every rank; Broadcast: nobody -- the root stores
+  //    straight through the switch)
+  if (!bcast)
+    for (int64_t i = tid; i < nvec; i += T) uc[i] = __ldcg(src + i);
+  grid_sync(ctr, gridDim.x);
+  // 2. entry: my uc holds call e's input and call e - 1's copy-out is done
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    fence_sys();
+    for (int u = 0; u < a.nranks; ++u)
+      if (u != v) st_relaxed_sys(a.flags[u] + entry_idx(v), e);
+  }
+  // 3. wait for the peers this rank's switch operations touch
+  if (threadIdx.x == 0) {
+    bool ok = true;
+    if (!bcast || v == a.root)
+      for (int u = 0; u < a.nranks && ok; ++u)
+        if (u != v) ok = nv_wait(a.flags[v] + entry_idx(u), e, a.timeout_ns, a.err);
+    fence_sys();
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  // 4. switch operations on my slice (Broadcast root: the whole buffer)
+  int64_t lo, hi;
+  if (bcast) {
+    lo = 0;
+    hi = v == a.root ? nvec : 0;
+  } else {
+    lo = (nvec * v) / a.nranks;
+    hi = (nvec * (v + 1)) / a.nranks;
+  }
+  for (int64_t i = lo + tid; i < hi; i += T) {
+    if (bcast)
+      mm_st(mc + i, __ldcg(src + i));
+    else
+      mm_st(mc + i, mm_ld_reduce<DT>(mc + i));
+  }
+  grid_sync(ctr + 1, gridDim.x);
+  // 5. publish my slice (bflag[v][0]) and wait for every root's
+  if (threadIdx.x == 0 && blockIdx.x == 0 && hi > lo) {
+    fence_sys();
+    for (int u = 0; u < a.nranks; ++u)
+      if (u != v) st_relaxed_sys(a.flags[u] + bflag_idx(v, 0), e);
+  }
+  if (threadIdx.x == 0) {
+    bool ok = true;
+    for (int j = 0; j < a.nranks && ok; ++j) {
+      if (j == v) continue;
+      const bool has = bcast ? (j == a.root) : ((nvec * (j + 1)) / a.nranks > (nvec * j) / a.nranks);
+      if (has) ok = nv_wait(a.flags[v] + bflag_idx(j, 0), e, a.timeout_ns, a.err);
+    }
+    fence_sys();
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  // 6. copy-out (Broadcast root: recv = send, copied locally)
+  char* dst = a.recv;
+  if (bcast && v == a.root) {
+    if (dst != a.send)
+      for (int64_t i = tid; i < nvec; i += T) reinterpret_cast<uint4*>(dst)[i] = __ldcg(src + i);
+  } else {
+    for (int64_t i = tid; i < nvec; i += T) reinterpret_cast<uint4*>(dst)[i] = __ldcg(uc + i);
+  }
+  // 7. the last CTA resets the counters and advances the epoch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long prev = atomicAdd(reinterpret_cast<unsigned long long*>(a.ctrl + 1), 1ull);
+    if (prev + 1 == gridDim.x) {
+      a.ctrl[1] = 0;
+      ctr[0] = 0;
+      ctr[1] = 0;
+      atomicExch(reinterpret_cast<unsigned long long*>(a.ctrl), (unsigned long long)e);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_nvls(const NvlsArgs& a, int grid, void* stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (a.dtype) {
+    case BLINK_FLOAT32: return cudaLaunchKernelEx(&cfg, nvls_kernel<BLINK_FLOAT32>, a);
+    case BLINK_BFLOAT16: return cudaLaunchKernelEx(&cfg, nvls_kernel<BLINK_BFLOAT16>, a);
+    case BLINK_INT32: return cudaLaunchKernelEx(&cfg, nvls_kernel<BLINK_INT32>, a);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace blink
