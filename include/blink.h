@@ -35,6 +35,22 @@
 #ifndef BLINK_H_
 #define BLINK_H_
 
+/* Boundary vs SURVEY.md §8(b) (the planned signatures), and why it differs:
+ *   blink_register                       -> blink_register_export + blink_register_connect:
+ *        registration maps the PEERS' buffers (CUDA IPC), so it needs the same
+ *        handle exchange as init (export/connect), not one local call.
+ *   blink_config_t.slots                 -> none: partials live in the node's own recv
+ *        (DESIGN §2), so there are no per-edge staging slots to size; the
+ *        TMA stage ring is sized from shared memory (BLINK_SMEM_KB).
+ *   blink_config_t.ctas_per_channel      -> ctas (the CTA budget per launch), split over
+ *        channels in proportion to bytes x operands (a6).
+ *   blink_config_t.oneshot_max_bytes     -> ll_max_bytes (the low-latency protocol), plus
+ *        shallow_max_bytes (R#27) and onehop_bcast_max_bytes.
+ *   cudaStream_t stream                  -> void* stream (no CUDA types in the ABI).
+ *   additions: blink_reduce_scatter / blink_allgather / blink_gather (NEXT-3),
+ *        blink_miad_* (NEXT-2), blink_plan_json / blink_topology_json (host-only),
+ *        blink_get_stats / blink_get_trace / blink_comm_info (introspection),
+ *        cfg.autotune, launch_per_rank, staging_bytes, nvls, nvls_bytes. */
 #include <stddef.h>
 #include <stdint.h>
 
@@ -133,7 +149,20 @@ typedef struct {
  *                  trees: small calls are latency-bound and every hop waits
  *                  for a whole chunk (depth-1 trees on the
  *                  switch).  Default 256 KiB; 0 = always packed.
- *                  Must agree across ranks */
+ *                  Must agree across ranks
+ *   nvls           NEXT-1: 1 = run the switch's one-hop trees inside the
+ *                  NVSwitch (multicast objects: multimem.ld_reduce reduces
+ *                  slice j of every rank in the switch, multimem.st writes the
+ *                  result to every rank; Broadcast = the root's multimem.st)
+ *                  for AllReduce SUM (f32, bf16, int32) and Broadcast above
+ *                  the LL sizes, 16-byte-aligned buffers.  Needs one rank per
+ *                  device on >= 2 multicast-capable GPUs (multi-process: FABRIC
+ *                  handles); otherwise the P2P stars run and blink_get_plan's
+ *                  "nvls" says why.  Float sums then follow the switch's
+ *                  order, not ascending ranks (within the north_star
+ *                  tolerance).  0 = off (default).  Must agree across ranks
+ *   nvls_bytes     multicast-bound buffer per rank (calls run in pieces of
+ *                  this size); default 64 MiB */
 typedef struct {
   double mwu_eps;
   double ilp_gap;
@@ -147,6 +176,8 @@ typedef struct {
   int launch_per_rank;
   size_t ll_max_bytes;
   size_t shallow_max_bytes;
+  int nvls;
+  size_t nvls_bytes;
 } blink_config_t;
 
 /* MIAD controller: "initialize the chunk size with a small value

@@ -49,7 +49,8 @@ class _Config(ctypes.Structure):
                 ("timeout_s", ctypes.c_double), ("onehop_bcast_max_bytes", ctypes.c_size_t),
                 ("staging_bytes", ctypes.c_size_t), ("autotune", ctypes.c_int),
                 ("launch_per_rank", ctypes.c_int), ("ll_max_bytes", ctypes.c_size_t),
-                ("shallow_max_bytes", ctypes.c_size_t)]
+                ("shallow_max_bytes", ctypes.c_size_t), ("nvls", ctypes.c_int),
+                ("nvls_bytes", ctypes.c_size_t)]
 
 
 class Miad(ctypes.Structure):

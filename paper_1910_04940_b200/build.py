@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libblink.so")
-SOURCES = ["exec.cu", "plan.cpp", "runtime.cpp", "probe.cpp", "nvls.cu"]
+SOURCES = ["exec.cu", "plan.cpp", "runtime.cpp", "probe.cpp", "nvls.cu", "nvls_host.cpp"]
 HEADERS = ["blink_internal.h", os.path.join("..", "..", "include", "blink.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -241,6 +241,24 @@ struct NvlsArgs {
 };
 cudaError_t launch_nvls(const NvlsArgs& a, int grid, void* stream);
 
+// nvls_host.cpp: multicast objects (driver handles as 64-bit integers)
+struct NvlsMem {
+  unsigned long long mc = 0, mem = 0;      // multicast object, bound physical memory
+  unsigned long long uc_va = 0, mc_va = 0; // unicast / multicast mappings
+  size_t size = 0;
+  int dev = -1;
+  bool owner = false, bound = false;
+};
+bool nvls_supported(int dev, bool fabric, std::string* err);
+size_t nvls_round(int ndev, size_t bytes);
+bool nvls_create(int ndev, size_t bytes, bool fabric, NvlsMem* m, std::string* err);
+bool nvls_export(const NvlsMem& m, void* fabric_handle, std::string* err);   // 64-byte FABRIC handle
+bool nvls_import(const void* fabric_handle, size_t bytes, NvlsMem* m, std::string* err);
+bool nvls_add_device(NvlsMem* m, int dev, std::string* err);
+bool nvls_bind_map(NvlsMem* m, int dev, bool fabric, std::string* err);
+void nvls_release(NvlsMem* m);
+bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<NvlsMem>* out, std::string* err);
+
 // exec.cu
 cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative, bool pdl);
 cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, void* stream,

@@ -118,6 +118,27 @@ __device__ __forceinline__ void mm_st(uint4* mc, const uint4& v) {
                : "memory");
 }
 
+// 16-byte vector i of a user buffer of `bytes` bytes: a vector load when the
+// buffer is 16-byte aligned and the vector is whole, else byte loads with
+// zero padding past the end (SUM over zero padding stays zero)
+__device__ __forceinline__ uint4 user_vec(const char* p, int64_t i, int64_t bytes, bool aligned) {
+  if (aligned && (i + 1) * 16 <= bytes) return __ldcg(reinterpret_cast<const uint4*>(p) + i);
+  uint4 r = make_uint4(0, 0, 0, 0);
+  unsigned char* rb = reinterpret_cast<unsigned char*>(&r);
+  for (int k = 0; k < 16; ++k)
+    if (i * 16 + k < bytes) rb[k] = static_cast<unsigned char>(p[i * 16 + k]);
+  return r;
+}
+__device__ __forceinline__ void user_store(char* p, int64_t i, int64_t bytes, bool aligned, const uint4& v) {
+  if (aligned && (i + 1) * 16 <= bytes) {
+    reinterpret_cast<uint4*>(p)[i] = v;
+    return;
+  }
+  const unsigned char* vb = reinterpret_cast<const unsigned char*>(&v);
+  for (int k = 0; k < 16; ++k)
+    if (i * 16 + k < bytes) p[i * 16 + k] = static_cast<char>(vb[k]);
+}
+
 // One call (or piece) of an NVLS AllReduce / Broadcast for the ranks this
 // launch runs (one per launch in multi-process comms, one per device in
 // single-process comms).  Every CTA copies a stripe in, the rank publishes
@@ -138,15 +159,16 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   __syncthreads();
   const uint64_t e = s_epoch;
   unsigned int* ctr = reinterpret_cast<unsigned int*>(a.ctrl + 2);
-  const uint4* src = reinterpret_cast<const uint4*>(a.send);
   uint4* uc = reinterpret_cast<uint4*>(a.uc);
   uint4* mc = reinterpret_cast<uint4*>(a.mc);
-  const int64_t nvec = a.bytes >> 4;
+  const int64_t nvec = (a.bytes + 15) >> 4;  // a ragged tail is zero-padded in uc
   const bool bcast = a.coll == kBroadcast;
+  const bool sal = (reinterpret_cast<uintptr_t>(a.send) & 15) == 0;
+  const bool ral = (reinterpret_cast<uintptr_t>(a.recv) & 15) == 0;
   // 1. copy-in (AllReduce: every rank; Broadcast: nobody -- the root stores
   //    straight through the switch)
   if (!bcast)
-    for (int64_t i = tid; i < nvec; i += T) uc[i] = __ldcg(src + i);
+    for (int64_t i = tid; i < nvec; i += T) uc[i] = user_vec(a.send, i, a.bytes, sal);
   grid_sync(ctr, gridDim.x);
   // 2. entry: my uc holds call e's input and call e - 1's copy-out is done
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -176,7 +198,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   }
   for (int64_t i = lo + tid; i < hi; i += T) {
     if (bcast)
-      mm_st(mc + i, __ldcg(src + i));
+      mm_st(mc + i, user_vec(a.send, i, a.bytes, sal));
     else
       mm_st(mc + i, mm_ld_reduce<DT>(mc + i));
   }
@@ -203,9 +225,9 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   char* dst = a.recv;
   if (bcast && v == a.root) {
     if (dst != a.send)
-      for (int64_t i = tid; i < nvec; i += T) reinterpret_cast<uint4*>(dst)[i] = __ldcg(src + i);
+      for (int64_t i = tid; i < nvec; i += T) user_store(dst, i, a.bytes, ral, user_vec(a.send, i, a.bytes, sal));
   } else {
-    for (int64_t i = tid; i < nvec; i += T) reinterpret_cast<uint4*>(dst)[i] = __ldcg(uc + i);
+    for (int64_t i = tid; i < nvec; i += T) user_store(dst, i, a.bytes, ral, __ldcg(uc + i));
   }
   // 7. the last CTA resets the counters and advances the epoch
   __syncthreads();

@@ -120,6 +120,10 @@ struct blink_comm {
   char* staging = nullptr;
   size_t staging_bytes = 0;
   char* peer_staging[kMaxRanks] = {};
+  // NEXT-1: multicast-bound buffer (uc/mc mappings) when NVLS is on
+  NvlsMem nvls;
+  bool nvls_on = false;
+  std::string nvls_note = "off (cfg.nvls = 0)";
   Probe probe;                // topology probe result (graph == NULL at init)
   bool probe_at_connect = false;  // multi-process: graph == NULL, probed from the peers' bus ids
   char* scratch = nullptr;    // single-process Gather on link graphs: forwarding buffer of a
@@ -146,6 +150,7 @@ namespace {
 struct Clique {
   std::mutex mu;
   int nranks = 0;
+  bool nvls = false;         // NEXT-1 active (one rank per device, multicast object bound)
   std::vector<blink_comm*> comms;
   std::vector<int> devices;  // distinct devices
   // launch groups: the ranks one launch runs.  One group per device (ranks
@@ -213,6 +218,9 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
   if (const char* e = getenv("BLINK_PER_RANK")) r.launch_per_rank = atoi(e);
   if (const char* e = getenv("BLINK_LL_MAX")) r.ll_max_bytes = size_t(atoll(e));
   if (const char* e = getenv("BLINK_SHALLOW_MAX")) r.shallow_max_bytes = size_t(atoll(e));
+  if (const char* e = getenv("BLINK_NVLS")) r.nvls = atoi(e);
+  if (r.nvls_bytes == 0) r.nvls_bytes = d.nvls_bytes;
+  r.nvls_bytes = (r.nvls_bytes + 15) / 16 * 16;
   if (r.ll_max_bytes > (size_t(16) << 20)) r.ll_max_bytes = size_t(16) << 20;
   r.ll_max_bytes = r.ll_max_bytes / kGrain * kGrain;
   if (!(r.mwu_eps > 0 && r.mwu_eps < 1)) r.mwu_eps = d.mwu_eps;
@@ -913,6 +921,60 @@ void fill_ll_args(blink_comm_t c, int coll, int dtype, int op, int root, size_t 
 }
 
 // ---------------------------------------------------------------- single-process launch
+// NEXT-1: which calls run in the switch (the same decision on every rank:
+// it depends only on the call, never on a rank's pointers)
+bool nvls_call(int coll, int op) { return coll == kBroadcast || (coll == kAllReduce && op == BLINK_SUM); }
+
+// Fill the NVLS launch of rank v for bytes [off, off + cnt) of the call.
+NvlsArgs nvls_args(blink_comm_t cv, int n, int v, int coll, int dtype, int root, const char* send, char* recv,
+                   size_t off, size_t cnt, uint64_t* const* flags, uint64_t* ctrl, int* err) {
+  NvlsArgs a{};
+  a.nranks = n;
+  a.rank = v;
+  a.coll = coll;
+  a.dtype = dtype;
+  a.root = root;
+  a.bytes = int64_t(cnt);
+  a.send = send ? send + off : nullptr;
+  a.recv = recv ? recv + off : nullptr;
+  a.uc = reinterpret_cast<char*>(cv->nvls.uc_va);
+  a.mc = reinterpret_cast<char*>(cv->nvls.mc_va);
+  for (int u = 0; u < n; ++u) a.flags[u] = flags[u];
+  a.ctrl = ctrl;
+  a.err = err;
+  a.timeout_ns = uint64_t(cv->cfg.timeout_s * 1e9);
+  return a;
+}
+
+// single process, one rank per device: one NVLS launch per rank and piece
+blink_result_t clique_nvls(Clique* q, size_t bytes) {
+  const int n = q->nranks;
+  blink_comm_t c0 = q->comms[0];
+  uint64_t* flags[kMaxRanks];
+  for (int u = 0; u < n; ++u) flags[u] = q->comms[u]->flags;
+  const size_t P = c0->nvls.size;
+  for (size_t off = 0; off < bytes; off += P) {
+    const size_t cnt = std::min(P, bytes - off);
+    for (const Clique::Group& grp : q->groups) {
+      const int v = __builtin_ctzll(grp.mask);
+      blink_comm_t cv = q->comms[v];
+      DeviceGuard g(cv->device);
+      NvlsArgs a = nvls_args(cv, n, v, q->coll, q->dtype, q->root, static_cast<const char*>(q->pending[v].send),
+                             static_cast<char*>(q->pending[v].recv), off, cnt, flags, q->ctrl[grp.key],
+                             q->err_dev[grp.key]);
+      cudaError_t e = launch_nvls(a, cv->sms, q->pending[v].stream);
+      if (e != cudaSuccess) return fail(cv, BLINK_ERR_CUDA, std::string("NVLS launch: ") + cudaGetErrorString(e));
+      cv->stats.launches++;
+      cv->stats.last_ctas = cv->sms;
+      cv->stats.last_chunks = 0;
+      cv->stats.last_trees = n;
+      cv->stats.last_chunk_bytes = int64_t(cnt);
+    }
+    q->launches++;
+  }
+  return BLINK_SUCCESS;
+}
+
 blink_result_t clique_launch(Clique* q) {
   const int n = q->nranks;
   const int es = esize_of(blink_dtype_t(q->dtype));
@@ -949,6 +1011,7 @@ blink_result_t clique_launch(Clique* q) {
   const bool lltree = ll_tree(c0, *plan, q->coll, bytes);
   const bool ll = lltree || ((q->groups.size() > 1 || bytes <= kLLOneLaunchMax) &&
                              ll_slices(c0, *plan, q->coll, q->count, es, ll_lo));
+  if (q->nvls && !ll && nvls_call(q->coll, q->op)) return clique_nvls(q, bytes);
   if (c0->cfg.autotune && !ll) {
     auto mk = std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count);
     auto mit = q->miad.find(mk);
@@ -1261,6 +1324,9 @@ struct Blob {
   uint64_t shallow_max_bytes;       // so must the plan choices by size (R#27,
   uint64_t onehop_bcast_max_bytes;  // the switch Broadcast star)
   uint64_t chunk_fp;                // and every input of the chunk table (a chunk's flags name bytes)
+  int32_t nvls_offer, pad2;         // rank 0: a multicast object for NEXT-1 (FABRIC handle below)
+  uint64_t nvls_size;
+  unsigned char nvls_handle[64];
 };
 
 // Fingerprint of everything the chunk table (size_plan / build_sized) reads:
@@ -1279,6 +1345,8 @@ uint64_t chunking_fingerprint(blink_comm_t comm) {
   mix(uint64_t(comm->cfg.ctas));
   mix(uint64_t(comm->cfg.threads));
   mix(uint64_t(comm->cfg.autotune));
+  mix(uint64_t(comm->cfg.nvls));
+  mix(uint64_t(comm->cfg.nvls_bytes));
   uint64_t d;
   memcpy(&d, &comm->cfg.mwu_eps, sizeof d);  // the plan's trees (MWU / ILP settings)
   mix(d);
@@ -1592,6 +1660,24 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
       return BLINK_SUCCESS;
     }
   }
+  if (comm->nvls_on && nvls_call(coll, op)) {  // NEXT-1: the one-hop trees in the switch
+    const size_t P = comm->nvls.size;
+    for (size_t off = 0; off < bytes; off += P) {
+      const size_t cnt = std::min(P, bytes - off);
+      NvlsArgs a = nvls_args(comm, comm->nranks, comm->rank, coll, dtype, root,
+                             static_cast<const char*>(sendbuf), static_cast<char*>(recvbuf), off, cnt,
+                             comm->peer_flags, comm->ctrl, comm->err_dev);
+      comm->calls++;
+      cudaError_t e = launch_nvls(a, comm->sms, stream);
+      if (e != cudaSuccess) return fail(comm, BLINK_ERR_CUDA, std::string("NVLS launch: ") + cudaGetErrorString(e));
+      comm->stats.launches++;
+      comm->stats.last_ctas = comm->sms;
+      comm->stats.last_chunks = 0;
+      comm->stats.last_trees = comm->nranks;
+      comm->stats.last_chunk_bytes = int64_t(cnt);
+    }
+    return BLINK_SUCCESS;
+  }
   char* sp[kMaxRanks] = {};
   char* rp[kMaxRanks] = {};
   const bool recv_ok = resolve(comm, recvbuf, bytes, rp);
@@ -1639,6 +1725,8 @@ void blink_config_default(blink_config_t* c) {
   c->launch_per_rank = 0;
   c->ll_max_bytes = 256 << 10;
   c->shallow_max_bytes = 256 << 10;
+  c->nvls = 0;
+  c->nvls_bytes = size_t(64) << 20;
 }
 
 void blink_miad_init(blink_miad_t* st, size_t init, size_t min_chunk, size_t max_chunk) {
@@ -1865,6 +1953,25 @@ blink_result_t blink_init_all(blink_comm_t* comms, int ndev, const int* devs,
     q->comms.push_back(c);
     comms[i] = c;
   }
+  // NEXT-1: one multicast object over the ranks' devices (one rank per device)
+  if (cfg.nvls) {
+    std::string nerr;
+    std::vector<NvlsMem> mems;
+    if (ndev < 2 || int(distinct.size()) != ndev) {
+      nerr = "needs one rank per device on >= 2 devices";
+    } else if (nvls_setup_single(std::vector<int>(devs, devs + ndev), cfg.nvls_bytes, &mems, &nerr)) {
+      for (int i = 0; i < ndev; ++i) {
+        q->comms[i]->nvls = mems[i];
+        q->comms[i]->nvls_on = true;
+        q->comms[i]->nvls_note = "on";
+      }
+      q->nvls = true;
+    } else {
+      for (auto& m : mems) nvls_release(&m);
+    }
+    if (!q->nvls)
+      for (blink_comm* c : q->comms) c->nvls_note = "off: " + nerr;
+  }
   q->per_rank = cfg.launch_per_rank != 0 && ndev > 1;
   for (int d : distinct) {
     uint64_t mask = 0;
@@ -1938,6 +2045,14 @@ blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_dev
   DeviceGuard g(c->device);
   CUDA_TRY(c, cudaMalloc(&c->staging, c->cfg.staging_bytes));
   c->staging_bytes = c->cfg.staging_bytes;
+  if (c->cfg.nvls && nranks >= 2 && rank == 0) {  // NEXT-1: the multicast object, shared at connect
+    std::string nerr;
+    const size_t size = nvls_round(nranks, c->cfg.nvls_bytes);
+    if (!nvls_supported(cuda_device, true, &nerr) || !nvls_create(nranks, size, true, &c->nvls, &nerr)) {
+      c->nvls_note = "off: " + nerr;
+      nvls_release(&c->nvls);
+    }
+  }
   CUDA_TRY(c, cudaHostAlloc(&c->err_host, sizeof(int), cudaHostAllocMapped));
   CUDA_TRY(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   *c->err_host = 0;
@@ -1946,6 +2061,60 @@ blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_dev
   CUDA_TRY(c, cudaMemset(c->ctrl, 0, cb));
   CUDA_TRY(c, cudaDeviceSynchronize());
   *comm = c;
+  return BLINK_SUCCESS;
+}
+
+// NEXT-1 across processes: every rank joins rank 0's multicast object, the
+// ranks meet (setup words in each other's flags: 1 = ok, 9 = failed), bind
+// their memory and map it, and meet again.  NVLS turns on only when every
+// rank reported ok in both rounds, so all ranks decide alike.
+blink_result_t setup_barrier(blink_comm_t comm, int round, bool ok, bool* all_ok) {
+  const uint64_t mine = ok ? 1 : 9;
+  for (int u = 0; u < comm->nranks; ++u)
+    CUDA_TRY(comm, cudaMemcpy(comm->peer_flags[u] + setup_idx(round, comm->rank), &mine, sizeof mine,
+                              cudaMemcpyHostToDevice));
+  std::vector<uint64_t> w(comm->nranks, 0);
+  const auto t0 = std::chrono::steady_clock::now();
+  while (true) {
+    CUDA_TRY(comm, cudaMemcpy(w.data(), comm->flags + setup_idx(round, 0), sizeof(uint64_t) * comm->nranks,
+                              cudaMemcpyDeviceToHost));
+    bool all = true;
+    for (uint64_t x : w) all = all && x != 0;
+    if (all) break;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > comm->cfg.timeout_s)
+      return fail(comm, BLINK_ERR_TIMEOUT, "NVLS set-up: a rank did not reach barrier " + std::to_string(round));
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
+  *all_ok = true;
+  for (uint64_t x : w) *all_ok = *all_ok && x == 1;
+  return BLINK_SUCCESS;
+}
+
+blink_result_t mp_nvls_connect(blink_comm_t comm, const Blob& b0) {
+  std::string nerr = "rank 0 offered no multicast object";
+  bool ok = b0.nvls_offer == 1;
+  if (ok && comm->rank != 0) {
+    ok = nvls_supported(comm->device, true, &nerr) &&
+         nvls_import(b0.nvls_handle, size_t(b0.nvls_size), &comm->nvls, &nerr);
+  }
+  if (ok) ok = nvls_add_device(&comm->nvls, comm->device, &nerr);
+  bool all = false;
+  blink_result_t r = setup_barrier(comm, 0, ok, &all);
+  if (r != BLINK_SUCCESS) return r;
+  bool ok2 = all && nvls_bind_map(&comm->nvls, comm->device, true, &nerr);
+  if (all && !ok2) nerr = "bind/map: " + nerr;
+  if (!all && ok) nerr = "another rank failed to join the multicast object";
+  bool all2 = false;
+  r = setup_barrier(comm, 1, ok2, &all2);
+  if (r != BLINK_SUCCESS) return r;
+  comm->nvls_on = all2;
+  if (all2) {
+    comm->nvls_note = "on";
+  } else {
+    if (!ok2 && all) nerr = "another rank failed to bind";
+    comm->nvls_note = "off: " + nerr;
+    nvls_release(&comm->nvls);
+  }
   return BLINK_SUCCESS;
 }
 
@@ -1971,6 +2140,15 @@ blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_b
   b.shallow_max_bytes = comm->cfg.shallow_max_bytes;
   b.onehop_bcast_max_bytes = comm->cfg.onehop_bcast_max_bytes;
   b.chunk_fp = chunking_fingerprint(comm);
+  if (comm->rank == 0 && comm->nvls.mc) {
+    std::string nerr;
+    if (nvls_export(comm->nvls, b.nvls_handle, &nerr)) {
+      b.nvls_offer = 1;
+      b.nvls_size = comm->nvls.size;
+    } else {
+      comm->nvls_note = "off: " + nerr;
+    }
+  }
   memcpy(blob, &b, sizeof b);
   return BLINK_SUCCESS;
 }
@@ -2023,6 +2201,12 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
     r = open_handle(comm, b.staging_h, &p);
     if (r != BLINK_SUCCESS) return r;
     comm->peer_staging[u] = p;
+  }
+  if (comm->cfg.nvls && comm->nranks >= 2) {  // NEXT-1 set-up: join, barrier, bind, barrier
+    Blob b0;
+    memcpy(&b0, base, sizeof b0);
+    blink_result_t nr = mp_nvls_connect(comm, b0);
+    if (nr != BLINK_SUCCESS) return nr;
   }
   if (comm->probe_at_connect) {  // topology probe over every rank's GPU
     std::vector<std::string> bus(comm->nranks);
@@ -2208,6 +2392,15 @@ blink_result_t blink_get_plan(blink_comm_t comm, int is_allreduce, int root, siz
   if (r != BLINK_SUCCESS) return r;
   std::string j = plan_to_json(*plan, count, es, s.ranges, s.ctas);
   j.insert(j.size() - 1, ",\"topology\":" + probe_to_json(comm->probe));
+  {
+    const bool would = comm->nvls_on && nvls_call(coll, BLINK_SUM) &&
+                       !ll_tree(comm, *plan, coll, count * es);
+    std::string note = comm->nvls_note;
+    for (char& ch : note)
+      if (ch == '"') ch = '\'';
+    j.insert(j.size() - 1, std::string(",\"nvls\":{\"active\":") + (comm->nvls_on ? "true" : "false") +
+                               ",\"this_call\":" + (would ? "true" : "false") + ",\"note\":\"" + note + "\"}");
+  }
   size_t need = j.size() + 1, cap = *json_bytes;
   *json_bytes = need;
   if (!json || cap < need) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "json buffer too small");
@@ -2268,6 +2461,7 @@ blink_result_t blink_destroy(blink_comm_t comm) {
     }
     if (comm->flags) cudaFree(comm->flags);
     if (comm->scratch) cudaFree(comm->scratch);
+    if (comm->nvls.mc) nvls_release(&comm->nvls);
   }
   Clique* q = comm->clique;
   if (q) {

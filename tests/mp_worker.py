@@ -285,6 +285,41 @@ def miad_mode(rank, world):
     print(f"rank {rank}: miad ok {chunks} {bchunks}")
 
 
+def nvls_mode(rank, world):
+    """NEXT-1 across processes on distinct GPUs: rank 0's multicast object is
+    joined by every rank at connect; AllReduce SUM within the north_star
+    tolerance (f32) / exact (int32), Broadcast bitwise."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    dev = rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    comm = BD.init(cfg=B.config(timeout_s=60.0, nvls=1, nvls_bytes=4 << 20), device=dev)
+    p = comm.plan(True, 0, 8 << 20, "f32")
+    assert p["nvls"]["active"], p["nvls"]
+    count = (3 << 20) + 7
+    fs = synth.inputs(53, world, count, "f32")
+    x = torch.from_numpy(fs[rank]).cuda()
+    y = torch.empty_like(x)
+    comm.allreduce(x, y, op="sum")
+    ints = synth.inputs(54, world, count, "i32")
+    xi = torch.from_numpy(ints[rank]).cuda()
+    yi = torch.empty_like(xi)
+    comm.allreduce(xi, yi, op="sum")
+    z = torch.zeros_like(x)
+    comm.broadcast(x if rank == 0 else None, z, root=0)
+    torch.cuda.synchronize()
+    naive = OC.naive_reduce(fs, "f32", "sum").astype(np.float64)
+    absum = sum(np.abs(f.astype(np.float64)) for f in fs)
+    if not np.all(np.abs(y.cpu().numpy().astype(np.float64) - naive) <= 1e-5 * absum + 1e-30):
+        raise SystemExit(f"rank {rank}: NVLS f32 allreduce outside tolerance")
+    if not np.array_equal(yi.cpu().numpy(), OC.naive_reduce(ints, "i32", "sum")):
+        raise SystemExit(f"rank {rank}: NVLS i32 allreduce mismatch")
+    if not np.array_equal(z.cpu().numpy().view(np.uint32), fs[0].view(np.uint32)):
+        raise SystemExit(f"rank {rank}: NVLS broadcast mismatch")
+    comm.destroy()
+    print(f"rank {rank}: nvls ok")
+
+
 def fingerprint_mode(rank, world):
     """Ranks whose chunk tables differ (here BLINK_CHUNKS_PER_CTA on rank 1)
     would consume each other's flags for different byte ranges: blink_connect
@@ -345,6 +380,8 @@ def main():
             fingerprint_mode(rank, world)
         elif mode == "miad":
             miad_mode(rank, world)
+        elif mode == "nvls":
+            nvls_mode(rank, world)
         else:
             gpu_mode(rank, world)
     finally:

@@ -47,6 +47,7 @@ def test_result_strings_and_defaults(B):
     assert lib.blink_result_string(10) == b"timeout"
     c = B.config()
     assert c.mwu_eps == 0.1 and c.ilp_gap == 0.05 and c.threads == 256
+    assert c.nvls == 0 and c.nvls_bytes == 64 << 20 and c.shallow_max_bytes == 256 << 10
 
 
 def _oracle_plan(p):

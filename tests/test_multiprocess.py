@@ -85,7 +85,7 @@ def _devices():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(_devices() < 2, reason="needs >= 2 GPUs (distinct devices: .sys flags, TMA over NVLink)")
-@pytest.mark.parametrize("mode,n", [("gpu", 2), ("chain", 3), ("miad", 2)])
+@pytest.mark.parametrize("mode,n", [("gpu", 2), ("chain", 3), ("miad", 2), ("nvls", 2)])
 def test_processes_on_distinct_gpus(mode, n):
     """The multi-process suite with one process per GPU: .sys-scope flags,
     cp.async.bulk loads/stores to IPC-mapped peer-GPU memory, cross-device
