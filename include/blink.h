@@ -287,6 +287,17 @@ blink_result_t blink_allgather(blink_comm_t comm, const void* sendbuf, void* rec
 blink_result_t blink_gather(blink_comm_t comm, const void* sendbuf, void* recvbuf,
                             size_t sendcount, blink_dtype_t dtype, int root, void* stream);
 
+/* Eq. 8 (Sec. 3.4 "Handling hybrid communication"): the data
+ * split between PCIe trees and NVLink trees that equalises
+ * T_PCIe + T_dpa = T_NVL:  D_PCIe = D_total BW_PCIe / (BW_PCIe + BW_NVL)
+ * - T_dpa BW_PCIe BW_NVL / (BW_PCIe + BW_NVL), D_NVL = D_total - D_PCIe.
+ * Bandwidths in bytes/s, T_dpa (cudaDeviceDisablePeerAccess latency) in s.
+ * D_PCIe is clamped to [0, D_total] and rounded down to 16 bytes.  Host-only
+ * planning (the hybrid data path is out of scope on B200).  Errors:
+ * INVALID_ARGUMENT for NULL outputs, nonpositive bandwidths, negative T_dpa. */
+blink_result_t blink_hybrid_split(size_t d_total, double bw_pcie, double bw_nvl, double t_dpa,
+                                  size_t* d_pcie, size_t* d_nvl);
+
 /* ---------------------------------------------------------------- topology probe
  * "Blink probes the set of links available ... and builds a topology with
  * appropriate link capacities" (Sec. 1; Sec. 2.3).  For the GPUs

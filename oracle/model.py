@@ -65,3 +65,19 @@ def link_bytes(plan, n, S, allreduce):
             if allreduce:
                 out[(v, p)] = out.get((v, p), 0) + b      # reduce direction
     return out
+
+
+def hybrid_split(d_total, bw_pcie, bw_nvl, t_dpa):
+    """Eq. 8 (P:425-432, Sec. 3.4 "Handling hybrid communication"): split
+    D_total between the PCIe trees and the NVLink trees so that
+    T_PCIe + T_dpa = T_NVL, i.e.
+        D_PCIe = D_total * BW_PCIe / (BW_PCIe + BW_NVL)
+                 - T_dpa * BW_PCIe * BW_NVL / (BW_PCIe + BW_NVL),
+        D_NVL  = D_total - D_PCIe.
+    The paper leaves the infeasible case silent; R#31: D_PCIe is clamped to
+    [0, D_total] (a large T_dpa sends everything over NVLink).  Exact
+    rationals in, exact rationals out."""
+    d_total, bw_pcie, bw_nvl, t_dpa = (Fraction(x) for x in (d_total, bw_pcie, bw_nvl, t_dpa))
+    d_pcie = d_total * bw_pcie / (bw_pcie + bw_nvl) - t_dpa * bw_pcie * bw_nvl / (bw_pcie + bw_nvl)
+    d_pcie = min(max(d_pcie, Fraction(0)), d_total)
+    return d_pcie, d_total - d_pcie

@@ -93,6 +93,8 @@ _SIGS = {
     "blink_miad_init": (None, [ctypes.POINTER(Miad), _sz, _sz, _sz]),
     "blink_miad_step": (_sz, [ctypes.POINTER(Miad), ctypes.c_double]),
     "blink_topology_json": (_i, [_i, ctypes.POINTER(_cp), _cp, ctypes.POINTER(_sz)]),
+    "blink_hybrid_split": (_i, [_sz, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),
     "blink_result_string": (_cp, [_i]),
     "blink_last_error": (_cp, [_vp]),
 }
@@ -178,6 +180,13 @@ def _json_call(fn, *args, comm=None):
         code = fn(*args, buf, ctypes.byref(n))
     _check(code, comm)
     return json.loads(buf.value.decode())
+
+
+def hybrid_split(d_total, bw_pcie, bw_nvl, t_dpa):
+    """Eq. 8: (D_PCIe, D_NVL) bytes for the PCIe / NVLink trees."""
+    a, b = _sz(), _sz()
+    _check(_lib.blink_hybrid_split(d_total, bw_pcie, bw_nvl, t_dpa, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def topology_json(bus_ids):

@@ -1740,3 +1740,22 @@ std::string plan_to_json(const Plan& p, size_t count, int esize, const std::vect
 }
 
 }  // namespace blink
+
+// Eq. 8 (Sec. 3.4): the PCIe / NVLink data split that makes
+// T_PCIe + T_dpa = T_NVL; D_PCIe clamped to [0, D_total] (R#31), rounded
+// down to the 16-byte grain (R#11).  Host-only planning: the hybrid data
+// path is out of scope on B200 (PCIe Gen5 << NVLink 5, DESIGN 7).
+extern "C" blink_result_t blink_hybrid_split(size_t d_total, double bw_pcie, double bw_nvl, double t_dpa,
+                                             size_t* d_pcie, size_t* d_nvl) {
+  if (!d_pcie || !d_nvl || !(bw_pcie > 0) || !(bw_nvl > 0) || !(t_dpa >= 0))
+    return BLINK_ERR_INVALID_ARGUMENT;
+  const double s = bw_pcie + bw_nvl;
+  double x = double(d_total) * bw_pcie / s - t_dpa * bw_pcie * bw_nvl / s;
+  if (!(x > 0)) x = 0;
+  if (x > double(d_total)) x = double(d_total);
+  size_t p = size_t(x);
+  p = p / blink::kGrain * blink::kGrain;
+  *d_pcie = p;
+  *d_nvl = d_total - p;
+  return BLINK_SUCCESS;
+}

@@ -587,3 +587,19 @@ def test_probe_nvswitch_virtual_and_outside_gpus(B, tmp_path, monkeypatch):
     with pytest.raises(B.BlinkError) as e:
         B.topology_json(["not-a-bus-id", _bus(1)])
     assert e.value.code == 4
+
+
+def test_hybrid_split_matches_the_oracle(B):
+    """blink_hybrid_split (Eq. 8) against oracle.model.hybrid_split, within the
+    16-byte rounding of R#11; errors for bad arguments."""
+    from fractions import Fraction
+    from oracle import model
+    for D, bp, bn, t in ((10**9, 32e9, 150e9, 1e-3), (3 * 10**8, 16e9, 50e9, 5e-4), (12345678, 25e9, 300e9, 0.0),
+                         (10**6, 32e9, 150e9, 1.0)):
+        dp, dn = B.hybrid_split(D, bp, bn, t)
+        wp, wn = model.hybrid_split(D, Fraction(bp), Fraction(bn), Fraction(t))
+        assert dp + dn == D and dp % 16 == 0
+        assert wp - 16 <= dp <= wp + 1e-6 * D / 1e6 + 1
+    with pytest.raises(B.BlinkError) as e:
+        B.hybrid_split(100, 0.0, 1.0, 0.0)
+    assert e.value.code == 4

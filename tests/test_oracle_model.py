@@ -104,3 +104,23 @@ def test_dgx1v_broadcast_respects_link_capacity_per_byte():
     cap = g[1]
     for (u, v), b in lb.items():
         assert b <= cap[(u, v)] * (S // 6 + 16)
+
+
+def test_hybrid_split_equalises_the_two_transfer_times():
+    """Eq. 8: the split satisfies its defining objective
+    T_PCIe + T_dpa = T_NVL exactly (checked as times, not by retyping the
+    closed form), conserves D_total, reduces to the bandwidth-proportional
+    split at T_dpa = 0, and clamps (R#31) when T_dpa exceeds T_NVL of the
+    whole buffer."""
+    from fractions import Fraction
+    from oracle import model
+    for D, bp, bn, t in ((10**9, 32 * 10**9, 150 * 10**9, Fraction(1, 10**3)),
+                         (3 * 10**8, 16 * 10**9, 50 * 10**9, Fraction(5, 10**4)),
+                         (12345678, 25 * 10**9, 300 * 10**9, Fraction(0))):
+        dp, dn = model.hybrid_split(D, bp, bn, t)
+        assert dp + dn == D and 0 <= dp <= D
+        assert dp / bp + t == dn / bn                      # T_PCIe + T_dpa = T_NVL
+        if t == 0:
+            assert dp * bn == dn * bp                      # proportional to bandwidth
+    dp, dn = model.hybrid_split(10**6, 32 * 10**9, 150 * 10**9, Fraction(1))   # T_dpa >> T_NVL
+    assert dp == 0 and dn == 10**6
