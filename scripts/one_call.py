@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """A few identical calls of one collective (for ncu captures):
-    python scripts/one_call.py M BYTES DTYPE [ar|bc] [calls]"""
+    python scripts/one_call.py M BYTES DTYPE [ar|bc] [calls]
+ONE_CALL_GRAPH=dgx1v plans on the emulated DGX-1V link graph (M = 8)."""
 import os
 import sys
 
@@ -13,7 +14,11 @@ m, nbytes = int(sys.argv[1]), int(sys.argv[2])
 dt = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}[sys.argv[3]]
 coll = sys.argv[4] if len(sys.argv) > 4 else "ar"
 calls = int(sys.argv[5]) if len(sys.argv) > 5 else 3
-comms = B.init_all([0] * m)
+graph = None
+if os.environ.get("ONE_CALL_GRAPH") == "dgx1v":
+    from oracle import graphs as OG  # topology preset only
+    graph = B.Graph.from_pairs(8, OG.dgx1v()[1])
+comms = B.init_all([0] * m, graph=graph)
 es = torch.empty((), dtype=dt).element_size()
 xs = [torch.randn(nbytes // es, device="cuda").to(dt) for _ in range(m)]
 ys = [torch.empty_like(x) for x in xs]
