@@ -254,6 +254,7 @@ def run_virtual(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    out["protocol_path"] = per_rank_protocol(B, m, sends, recvs, S, stream, max(3, min(args.steps, 20)))
     if not args.no_cpu_baseline:   # the same sample as the reference arm: 16 MiB per rank
         out["cpu_baseline"] = cpu_oracle_baseline(m, min(count, REF_SAMPLE_COUNT))
     for c in comms:
@@ -407,6 +408,41 @@ def multiprocess_line(args, m, S, ms, bc_ms, graph, e2e_ms, n_e2e, launches, clo
         "nccl": nccl,
     }
     return out
+
+
+def per_rank_protocol(B, m, sends, recvs, S, stream, steps):
+    """The same AllReduce with one launch per rank (cfg.launch_per_rank): the
+    kernels and cross-launch protocol a real one-process-per-GPU rank runs
+    (entry handshake, per-chunk flags between launches, exit waits), here with
+    1/m of the SMs per rank.  The headline `value` times the single launch
+    that holds every virtual rank (no flags); this shows what the protocol
+    costs on the same bytes."""
+    import torch
+    comms = B.init_all([0] * m, cfg=B.config(timeout_s=60.0, launch_per_rank=1))
+
+    def step():
+        for r, c in enumerate(comms):
+            c.allreduce(sends[r], recvs[r], op="sum", stream=stream)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    st = comms[0].stats()
+    for c in comms:
+        c.destroy()
+    return {"ms_per_step": round(ms, 4), "alg_bw_gbs": round(S / (ms * 1e-3) / 1e9, 3), "steps": steps,
+            "hbm_frac": round(2 * m * S / (ms * 1e-3) / 1e9 / float(load_peaks()[0]["hbm_gbs"]), 4),
+            "launches_per_step": m, "ctas_per_launch": st["last_ctas"],
+            "note": "launch_per_rank=1: one launch per rank with the multi-process protocol (entry "
+                    "handshake, per-chunk flags, exit waits), 1/m of the SMs each"}
 
 
 def run_multiprocess(args):

@@ -87,8 +87,9 @@ def oracle_plan(p):
 def test_random_configuration(B, seed):
     rng = random.Random(int(os.environ.get("FUZZ_BASE", "7000")) + seed)
     m, graph, kind = random_graph(B, rng)
+    # NEXT-3: ReduceScatter on the switch; AllGather / Gather on switches and link graphs
     coll = "allreduce" if kind == "multiserver" else rng.choice(["allreduce", "allreduce", "broadcast"] +
-                      (["reduce_scatter", "allgather", "gather"] if kind == "switch" else []))
+                      (["reduce_scatter"] if kind == "switch" else []) + ["allgather", "gather"])
     dtype = rng.choice(["f32", "bf16", "i32"])
     op = rng.choice(["sum", "min", "max", "avg"] + (["prod"] if dtype == "i32" else []))
     count = rng.choice([1, 7, 255, 4096, 65537, 300001, rng.randint(1, 200000)])
@@ -96,8 +97,9 @@ def test_random_configuration(B, seed):
     misalign = rng.random() < 0.15 and not inplace
     chunk = rng.choice([0, 4096, 65536])
     per_rank = int(rng.random() < 0.2)
+    autotune = int(coll in ("allreduce", "broadcast") and chunk == 0 and rng.random() < 0.2)  # NEXT-2
     comms = B.init_all([0] * m, graph=graph, cfg=B.config(timeout_s=30.0, chunk_bytes=chunk,
-                                                          launch_per_rank=per_rank))
+                                                          launch_per_rank=per_rank, autotune=autotune))
     es = OC.ESIZE[dtype]
     if coll == "reduce_scatter":
         sends = synth.inputs(seed, m, m * count, dtype)
@@ -143,7 +145,10 @@ def test_random_configuration(B, seed):
     torch.cuda.synchronize()
     got = [to_host(x, dtype) if x is not None else None for x in rs]
     what = (f"{kind} m={m} {coll} {dtype} {op} n={count} inplace={inplace} misalign={misalign} "
-            f"chunk={chunk} per_rank={per_rank}")
+            f"chunk={chunk} per_rank={per_rank} autotune={autotune}")
+    if coll != "allreduce":
+        for c in comms:
+            c.destroy()
     if coll == "broadcast":
         for g in got:
             assert np.array_equal(bits(g), bits(sends[root])), what
