@@ -116,8 +116,12 @@ typedef struct {
  *                  single one-hop star, above it the m-1 two-level trees
  *   staging_bytes  multi-process: size of the library-owned symmetric staging
  *                  buffer used for unregistered user buffers; default 64 MiB
- *   autotune       1 = MIAD chunk-size selection across calls (P:526-535,
- *                  single-process comms; chunking never changes results);
+ *   autotune       1 = MIAD chunk-size selection across calls (
+ *                  chunking never changes results).  Single process: one host
+ *                  decides for every rank.  One process per GPU: rank 0
+ *                  decides and publishes each call's size in its flag words,
+ *                  the other ranks read it before enqueueing the call (they
+ *                  wait for rank 0 to get that far).  Must agree across ranks.
  *                  0 = the static table (default)
  *   launch_per_rank  single-process comms only: 1 = every rank runs in its own
  *                  launch on a library-owned stream (forked from and joined
@@ -259,11 +263,15 @@ blink_result_t blink_broadcast(blink_comm_t comm, const void* sendbuf, void* rec
 blink_result_t blink_allreduce(blink_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
                                blink_dtype_t dtype, blink_redop_t op, void* stream);
 
-/* ReduceScatter (NEXT-3: the reduce half of the one-hop AllReduce).
+/* ReduceScatter (NEXT-3: the reduce half of AllReduce).
  * sendbuf holds nranks blocks of recvcount elements; rank j's recvbuf
- * (recvcount elements) receives block j reduced over all ranks in ascending
- * rank order.  Switch (one-hop) topologies only; BLINK_ERR_UNSUPPORTED on
- * explicit link graphs. */
+ * (recvcount elements) receives block j reduced over all ranks.  Switch: the
+ * one-hop star rooted at j, ascending rank order.  Link graphs: a
+ * minimum-depth spanning tree rooted at j over bidirectional links, each node
+ * combining its own block with its children's partials in ascending rank
+ * order (R#12); inner ranks relay partials through a library-owned area
+ * (single process: scratch; multi-process: the staging buffer's second
+ * half).  Multi-server graphs: BLINK_ERR_UNSUPPORTED. */
 blink_result_t blink_reduce_scatter(blink_comm_t comm, const void* sendbuf, void* recvbuf,
                                     size_t recvcount, blink_dtype_t dtype, blink_redop_t op,
                                     void* stream);

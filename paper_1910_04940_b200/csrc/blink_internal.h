@@ -162,6 +162,9 @@ struct LaunchArgs {
   DevTask mtask;
   char* send[kMaxArgRanks];
   char* recv[kMaxArgRanks];
+  // link-graph ReduceScatter: inner ranks keep their partials of other blocks
+  // in relay[v] (an m-block area, unshifted); roots write recv (NULL = unused)
+  char* relay[kMaxArgRanks];
   uint64_t* flags[kMaxArgRanks];
   // Per-call tables in the parameter space (constant bank): no dependent
   // global loads before a CTA's first TMA load.
@@ -265,6 +268,10 @@ cudaError_t launch_exec(const LaunchArgs& a, int grid, int threads, bool vec, vo
                         bool cooperative, bool pdl);
 constexpr int kMaxSmemBytes = 224 * 1024;  // + static smem <= 227 KB opt-in
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream);
+// force-load every kernel module on the current device (lazy loading would
+// otherwise load at a first launch that may wait for spinning kernels)
+cudaError_t preload_kernels();
+cudaError_t preload_nvls_kernels();
 // two u64 stores by one thread, stream-ordered (values travel as kernel parameters)
 cudaError_t launch_store2(uint64_t* dst, uint64_t v0, uint64_t v1, void* stream);
 int exec_max_ctas_per_sm(int threads, bool vec, int dtype, int op, int coll, int smem_bytes);

@@ -510,6 +510,11 @@ __device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask&
   fence_acqrel(sys);
   if (t.role == kRoleReduce && !is_root) {
     st_relaxed(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), ctl.epoch, sys);
+    // ReduceScatter on multi-level trees: this rank has consumed its
+    // children's chunk c -- ack them (their exit waits), as the root does
+    if (a.coll == kReduceScatter)
+      for (int u = 0; u < a.nranks; ++u)
+        if ((t.children >> u) & 1u) st_relaxed(a.flags[u] + bflag_idx(t.tree, c), ctl.epoch, sys);
   } else {
     for (int u = 0; u < a.nranks; ++u)
       if ((t.children >> u) & 1u) st_relaxed(a.flags[u] + bflag_idx(t.tree, c), ctl.epoch, sys);
@@ -942,6 +947,9 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
           from_send = ((t.leafmask | me) & bit) != 0u;
           // ReduceScatter keeps the result at the root
           is_dst = u == w || (is_root && a.coll == kAllReduce && (t.children & bit));
+          // link-graph ReduceScatter: partials of inner ranks live in the relay
+          // area (an internal child's source, a non-root's destination)
+          if (a.relay[u] && !(u == w && is_root)) ru = a.relay[u];
         } else {
           const bool src_root = is_push_coll(a.coll) && is_root;
           is_src = u == w;
@@ -1555,6 +1563,40 @@ __global__ void store2_kernel(uint64_t* dst, uint64_t v0, uint64_t v1) {
 cudaError_t launch_store2(uint64_t* dst, uint64_t v0, uint64_t v1, void* stream) {
   store2_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst, v0, v1);
   return cudaGetLastError();
+}
+
+// Load every kernel of the library on the current device now.  With lazy
+// module loading (CUDA 12's default) the first launch of a kernel loads its
+// module, which can wait for the device to go idle -- and a launch that
+// spins on flags set by a LATER launch (per-rank launches, multi-process
+// ranks sharing a GPU) would never let it.  Called once per device at comm
+// creation.
+cudaError_t preload_kernels() {
+  cudaFuncAttributes fa;
+  for (int coll = 0; coll <= kGather; ++coll)
+    for (int dt = 0; dt < 3; ++dt)
+      for (int op = 0; op <= BLINK_AVG; ++op)
+        for (int vec = 0; vec < 2; ++vec) {
+          ExecFn fn = pick(coll, dt, op, vec != 0);
+          if (fn) {
+            cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+            if (e != cudaSuccess) return e;
+          }
+        }
+  for (int dt = 0; dt < 3; ++dt)
+    for (int op = 0; op <= BLINK_AVG; ++op) {
+      LLFn fn = dt == 0 ? ll_pick_op<BLINK_FLOAT32>(op)
+                        : (dt == 1 ? ll_pick_op<BLINK_BFLOAT16>(op) : ll_pick_op<BLINK_INT32>(op));
+      if (fn) {
+        cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+        if (e != cudaSuccess) return e;
+      }
+    }
+  cudaError_t e = cudaFuncGetAttributes(&fa, copy_kernel<true>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, copy_kernel<false>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, store2_kernel);
+  if (e == cudaSuccess) e = preload_nvls_kernels();
+  return e;
 }
 
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, void* stream) {

@@ -244,6 +244,14 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
 
 }  // namespace
 
+cudaError_t preload_nvls_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, nvls_kernel<BLINK_FLOAT32>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, nvls_kernel<BLINK_BFLOAT16>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, nvls_kernel<BLINK_INT32>);
+  return e;
+}
+
 cudaError_t launch_nvls(const NvlsArgs& a, int grid, void* stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

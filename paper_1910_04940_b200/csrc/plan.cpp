@@ -918,6 +918,136 @@ std::vector<std::vector<int>> lovasz_packing(std::vector<std::vector<int64_t>> c
   return out;
 }
 
+int tree_depth(const std::vector<int>& parent);
+
+// hop distances from root over positive integer capacities
+std::vector<int> bfs_depths(int n, const std::vector<std::vector<int64_t>>& cap, int root) {
+  std::vector<int> d(n, 0), seen(n, 0), q{root};
+  seen[root] = 1;
+  for (size_t h = 0; h < q.size(); ++h)
+    for (int v = 0; v < n; ++v)
+      if (!seen[v] && cap[q[h]][v] > 0) {
+        seen[v] = 1;
+        d[v] = d[q[h]] + 1;
+        q.push_back(v);
+      }
+  return d;
+}
+
+// Shallow integral Broadcast packing (product heuristic, R#21): for depth
+// bounds D from the root's eccentricity up to below `cur_depth`, sample random
+// arborescences of depth <= D (random growth: an edge from the tree to a new
+// vertex, its tail at depth < D, chosen uniformly) and look for k of them
+// that fit the integer capacities (the ILP at grid 1 over the samples).
+// Returns the first (shallowest) such packing, or nothing.  Shallow trees
+// shorten every chunk's pipeline fill.  Graphs up to 16 ranks.
+std::vector<std::vector<int>> sample_shallow_packing(const std::vector<std::vector<int64_t>>& cap, int root,
+                                                     int64_t k, int cur_depth) {
+  const int n = int(cap.size());
+  if (k <= 0 || n > 16) return {};
+  std::vector<int> d0 = bfs_depths(n, cap, root);
+  int ecc = 0;
+  for (int x : d0) ecc = std::max(ecc, x);
+  std::vector<std::pair<int, int>> elist;
+  std::vector<double> ecap;
+  std::map<std::pair<int, int>, int> eid;
+  for (int u = 0; u < n; ++u)
+    for (int v = 0; v < n; ++v)
+      if (cap[u][v] > 0) {
+        eid[{u, v}] = int(elist.size());
+        elist.push_back({u, v});
+        ecap.push_back(double(cap[u][v]));
+      }
+  uint32_t st = 0x9e3779b9u;
+  auto rnd = [&]() {
+    st ^= st << 13;
+    st ^= st >> 17;
+    st ^= st << 5;
+    return st;
+  };
+  for (int D = ecc; D < cur_depth; ++D) {
+    std::map<std::vector<int>, int> seen;
+    std::vector<IlpCand> cands;
+    std::vector<std::vector<int>> pars;
+    for (int s = 0; s < 1500; ++s) {
+      std::vector<int> parent(n, -2), depth(n, 0);
+      parent[root] = -1;
+      int in_t = 1;
+      bool ok = true;
+      while (in_t < n && ok) {
+        std::vector<std::pair<int, int>> opts;
+        for (int u = 0; u < n; ++u)
+          if (parent[u] != -2 && depth[u] < D)
+            for (int v = 0; v < n; ++v)
+              if (parent[v] == -2 && cap[u][v] > 0) opts.push_back({u, v});
+        if (opts.empty()) {
+          ok = false;
+          break;
+        }
+        const auto e = opts[rnd() % opts.size()];
+        parent[e.second] = e.first;
+        depth[e.second] = depth[e.first] + 1;
+        ++in_t;
+      }
+      if (!ok) continue;
+      std::vector<int> res;
+      for (int v = 0; v < n; ++v)
+        if (parent[v] >= 0) res.push_back(eid[{parent[v], v}]);
+      std::sort(res.begin(), res.end());
+      if (seen.count(res)) continue;
+      seen[res] = 1;
+      IlpCand c{res, tree_depth(parent), 1.0};
+      cands.push_back(c);
+      pars.push_back(parent);
+    }
+    // plus the trees of MWU runs whose tree oracle is a depth-bounded greedy
+    // (Prim-like: the shortest edge from the tree to a new vertex whose tail
+    // has depth < D) -- the same Garg-Koenemann loop as the paper's MWU,
+    // restricted to shallow trees
+    for (double eps : {0.1, 0.05}) {
+      MwuResult mr;
+      auto tree_of = [&](const std::vector<double>& len) {
+        std::vector<int> parent(n, -2), depth(n, 0), res;
+        parent[root] = -1;
+        for (int step = 1; step < n; ++step) {
+          int be = -1;
+          for (size_t j = 0; j < elist.size(); ++j) {
+            const int u = elist[j].first, v = elist[j].second;
+            if (parent[u] == -2 || parent[v] != -2 || depth[u] >= D) continue;
+            if (be < 0 || len[j] < len[be]) be = int(j);
+          }
+          if (be < 0) return std::vector<int>();
+          parent[elist[be].second] = elist[be].first;
+          depth[elist[be].second] = depth[elist[be].first] + 1;
+          res.push_back(be);
+        }
+        std::sort(res.begin(), res.end());
+        return res;
+      };
+      if (!run_mwu(ecap, eps, tree_of, &mr)) continue;
+      for (auto& kv : mr.x) {
+        if (seen.count(kv.first)) continue;
+        seen[kv.first] = 1;
+        std::vector<int> parent(n, -1);
+        for (int e : kv.first) parent[elist[e].second] = elist[e].first;
+        IlpCand c{kv.first, tree_depth(parent), kv.second};
+        cands.push_back(c);
+        pars.push_back(parent);
+      }
+    }
+    if (int64_t(cands.size()) < k) continue;
+    IlpBB bb(cands, ecap, 1, false, 3000);
+    IlpSol sol = bb.solve_sum();
+    if (sol.sumz >= k) {
+      std::vector<std::vector<int>> out;
+      for (size_t j = 0; j < cands.size(); ++j)
+        if (sol.z[j] > 0) out.push_back(pars[j]);
+      return out;
+    }
+  }
+  return {};
+}
+
 // Greedy integral peeling of undirected spanning trees: Kruskal preferring
 // links with the largest RELATIVE residual capacity (balances single and
 // parallel links); candidates for the AllReduce ILP.
@@ -1247,12 +1377,19 @@ blink_result_t make_plan(const Graph& g, int coll, int root, const blink_config_
     opt = INFINITY;
     for (int v = 0; v < n; ++v)
       if (v != root) opt = std::min(opt, maxflow_real(caps, edges, n, root, v));
-    // product extra: exact integral candidates (Lovasz), weight 1 each
+    // product extra: exact integral candidates (Lovasz), weight 1 each, plus
+    // shallow integral packings (sample_shallow_packing)
     {
       std::vector<std::vector<int64_t>> ic(n, std::vector<int64_t>(n, 0));
       for (size_t j = 0; j < edges.size(); ++j)
         ic[edges[j].u][edges[j].v] = int64_t(std::floor(caps[j] + 1e-9));
-      for (auto& par : lovasz_packing(ic, root)) {
+      std::vector<std::vector<int>> lv = lovasz_packing(ic, root);
+      int cur_d = 0;
+      for (auto& par : lv) cur_d = std::max(cur_d, tree_depth(par));
+      for (auto& c : cands) cur_d = std::max(cur_d, c.depth);
+      std::vector<std::vector<int>> sh = sample_shallow_packing(ic, root, int64_t(lv.size()), cur_d);
+      lv.insert(lv.end(), sh.begin(), sh.end());
+      for (auto& par : lv) {
         std::vector<int> res;
         for (int v = 0; v < n; ++v)
           if (par[v] >= 0) res.push_back(key_to_res[par[v] * n + v]);
@@ -1510,6 +1647,9 @@ blink_result_t make_shallow_plan(const Graph& g, int coll, int root, Plan* out, 
 //    vertices one level up with a link to v, v's parent is the one whose link
 //    is least loaded relative to its capacity after the roots before j
 //    (ties: lowest rank), so the m trees spread over the links.
+//  ReduceScatter: block j reduces toward rank j along the same kind of tree
+//    over bidirectional links (the reduce half of AllReduce); inner
+//    ranks keep their partials in a block-sized relay area.
 //  Gather to r: the minimum-depth Broadcast tree of r, reversed ("the inverse
 //    of Broadcast").  Block j travels along j's path to r; tree j is that
 //    chain rooted at j, and ranks off the chain are not members (-2).  Tree r
@@ -1524,15 +1664,24 @@ blink_result_t make_block_plan(const Graph& g, int coll, int root, Plan* out, st
   out->root = coll == kGather ? root : -1;
   out->nranks = n;
   out->blocks = true;
-  if (coll != kAllGather && coll != kGather) {
-    *err = "ReduceScatter runs on one-hop trees: switch topologies only";
-    return BLINK_ERR_UNSUPPORTED;
-  }
   auto cap = [&](int u, int v) { return g.cap[u][v]; };
-  if (coll == kAllGather) {
+  const bool rs = coll == kReduceScatter;
+  if (rs)  // reduce toward root j and the acks back down need both directions
+    for (int u = 0; u < n; ++u)
+      for (int v = u + 1; v < n; ++v)
+        if ((g.cap[u][v] > 0) != (g.cap[v][u] > 0)) {
+          const bool f = g.cap[u][v] > 0;
+          *err = "link " + std::to_string(f ? u : v) + "->" + std::to_string(f ? v : u) +
+                 " has no reverse edge (ReduceScatter needs bidirectional links, P:397)";
+          return BLINK_ERR_TOPOLOGY;
+        }
+  if (coll == kAllGather || rs) {
+    // AllGather: block j broadcast down the arborescence rooted at j.
+    // ReduceScatter: block j reduced up the same shape of tree toward j (the
+    // reduce half of AllReduce), partials relayed by inner ranks.
     std::vector<std::vector<double>> load(n, std::vector<double>(n, 0.0));
     for (int j = 0; j < n; ++j) {
-      const std::vector<int> d = bfs_dist(g, j, false);
+      const std::vector<int> d = bfs_dist(g, j, rs);
       Tree t;
       t.root = j;
       t.parent.assign(n, -1);

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -240,8 +241,6 @@ blink_config_t resolve_cfg(const blink_config_t* c) {
 // single minimum-depth tree of small calls on link graphs (R#27).
 blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, const Plan** out) {
   int key_root = (coll == kBroadcast || coll == kGather) ? root : -1;
-  if (coll == kReduceScatter && !comm->graph.switch_model)
-    return fail(comm, BLINK_ERR_UNSUPPORTED, "ReduceScatter runs on one-hop trees: switch topologies only");
   if (is_block_coll(coll) && comm->graph.multi_server)
     return fail(comm, BLINK_ERR_UNSUPPORTED, "multi-server graphs support AllReduce only");
   const bool link_blocks = is_block_coll(coll) && !comm->graph.switch_model;  // NEXT-3 on link graphs
@@ -1198,6 +1197,22 @@ blink_result_t clique_launch(Clique* q) {
           a.recv[v] = cv->scratch;
         }
       }
+      if (q->coll == kReduceScatter && !plan->switch_model) {
+        // link-graph ReduceScatter: inner ranks relay partials of other
+        // blocks through an m-block relay area (library scratch); each root
+        // writes its own block straight into recv
+        blink_comm* cv = q->comms[v];
+        const size_t need = size_t(n) * bytes;
+        if (cv->scratch_bytes < need) {
+          DeviceGuard gv(cv->device);
+          if (cv->scratch) cudaFree(cv->scratch);
+          cv->scratch = nullptr;
+          cv->scratch_bytes = 0;
+          CUDA_TRY(cd, cudaMalloc(&cv->scratch, need));
+          cv->scratch_bytes = need;
+        }
+        a.relay[v] = cv->scratch;
+      }
       // block collectives address rank v's short buffer through tree v's range
       if (q->coll == kReduceScatter) a.recv[v] -= size_t(v) * bytes;
       if ((q->coll == kAllGather || q->coll == kGather) && a.send[v]) a.send[v] -= size_t(v) * bytes;
@@ -1276,6 +1291,22 @@ blink_result_t clique_post(blink_comm_t comm, int coll, const void* send, void* 
   std::lock_guard<std::mutex> lk(q->mu);
   for (auto& kv : q->err_host)
     if (*kv.second != 0) {
+      if (getenv("BLINK_DUMP_FLAGS")) {  // debugging aid: the flag words of chunk 0 of every tree
+        cudaDeviceSynchronize();
+        for (int v = 0; v < q->nranks; ++v) {
+          std::vector<uint64_t> w(kFlagWords);
+          cudaMemcpy(w.data(), q->comms[v]->flags, kFlagBytes, cudaMemcpyDeviceToHost);
+          fprintf(stderr, "[blink] rank %d entry:", v);
+          for (int u = 0; u < q->nranks; ++u) fprintf(stderr, " %llu", (unsigned long long)w[entry_idx(u)]);
+          fprintf(stderr, "  bflag[t][0]:");
+          for (int t = 0; t < q->nranks; ++t) fprintf(stderr, " %llu", (unsigned long long)w[bflag_idx(t, 0)]);
+          fprintf(stderr, "  pflag[t][child][0]:");
+          for (int t = 0; t < q->nranks; ++t)
+            for (int u = 0; u < q->nranks; ++u)
+              if (w[pflag_idx(t, u, 0)]) fprintf(stderr, " t%d/c%d=%llu", t, u, (unsigned long long)w[pflag_idx(t, u, 0)]);
+          fprintf(stderr, "\n");
+        }
+      }
       return fail(comm, blink_result_t(*kv.second),
                   "a previous launch aborted (flag wait timed out in launch group " +
                       std::to_string(kv.first) + ")");
@@ -1479,7 +1510,8 @@ blink_result_t mp_miad_chunk(blink_comm_t comm, int coll, int root, blink_dtype_
 }
 
 blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* recv[kMaxRanks],
-                      size_t count, blink_dtype_t dtype, int op, int root, cudaStream_t stream) {
+                      size_t count, blink_dtype_t dtype, int op, int root, cudaStream_t stream,
+                      char* const* relay = nullptr) {
   const int n = comm->nranks;
   const int es = esize_of(dtype);
   const size_t bytes = count * es;
@@ -1543,6 +1575,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
     a.recv[u] = recv[u];
     a.flags[u] = comm->peer_flags[u];
     if (coll == kReduceScatter && a.recv[u]) a.recv[u] -= size_t(u) * bytes;
+    if (relay) a.relay[u] = relay[u];
     if ((coll == kAllGather || coll == kGather) && a.send[u]) a.send[u] -= size_t(u) * bytes;
   }
   const bool time_it = mm && mm->ev0 && !mm->pending && !mm->done;  // rank 0 only
@@ -1575,6 +1608,30 @@ blink_result_t mp_block_collective(blink_comm_t comm, int coll, const void* send
   char* rb = static_cast<char*>(recvbuf);
   char* sp[kMaxRanks] = {};
   char* rp[kMaxRanks] = {};
+  if (coll == kReduceScatter && !comm->graph.switch_model) {
+    // link graphs: inner ranks relay partials of other blocks, so every rank
+    // needs a symmetric m-block relay area: the staging buffer's second half
+    // (the first half holds the send blocks).  Pieces of P elements per block.
+    const size_t P = std::max<size_t>(1, comm->staging_bytes / (2 * size_t(m) * es));
+    const size_t half = P * size_t(m) * es;
+    char* s2[kMaxRanks];
+    char* rl[kMaxRanks];
+    for (int u = 0; u < m; ++u) {
+      s2[u] = comm->peer_staging[u];
+      rl[u] = comm->peer_staging[u] + half;
+    }
+    for (size_t k0 = 0; k0 < count; k0 += P) {
+      const size_t cnt = std::min(P, count - k0);
+      for (int j = 0; j < m; ++j)
+        CUDA_TRY(comm, launch_copy(comm->staging + size_t(j) * cnt * es, sb + (size_t(j) * count + k0) * es,
+                                   cnt * es, stream));
+      char* r2[kMaxRanks] = {};
+      r2[me] = rb + k0 * es;  // only the root writes its recv: a local pointer suffices
+      blink_result_t r = mp_run(comm, coll, s2, r2, cnt, dtype, op, -1, stream, rl);
+      if (r != BLINK_SUCCESS) return r;
+    }
+    return BLINK_SUCCESS;
+  }
   if (coll == kReduceScatter) {
     rp[me] = rb;
     if (resolve(comm, sendbuf, size_t(m) * count * es, sp))
@@ -1867,6 +1924,15 @@ blink_result_t blink_topology_json(int ndev, const char* const* bus_ids, char* j
 
 static blink_result_t alloc_comm_common(blink_comm_t c) {
   DeviceGuard g(c->device);
+  {
+    static std::mutex mu;
+    static std::set<int> loaded;  // devices whose kernels are loaded
+    std::lock_guard<std::mutex> lk(mu);
+    if (!loaded.count(c->device)) {
+      CUDA_TRY(c, preload_kernels());
+      loaded.insert(c->device);
+    }
+  }
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   // flag words, then the LL protocol's line areas (zero = no flag yet); one
   // allocation, so the flag mapping also maps the LL area to the peers

@@ -239,6 +239,14 @@ def chain_mode(rank, world):
     if rank == 0:
         check(gout, OC.gather(gs, 0)[0], "chain gather")
     check(agout, OC.allgather(gs), "chain allgather")
+    # ReduceScatter on the chain: block 0's tree is 2 -> 1 -> 0 (rank 1 relays
+    # partials through its staging relay area); int32 is exact in any order
+    rsx = synth.inputs(55, world, world * 30001, "i32")
+    rx = torch.from_numpy(rsx[rank]).cuda()
+    ry = torch.zeros(30001, dtype=torch.int32, device="cuda")
+    comm.reduce_scatter(rx, ry, op="sum")
+    torch.cuda.synchronize()
+    check(ry, OC.reduce_scatter(rsx, "i32", "sum")[rank], "chain reduce_scatter")
     comm.destroy()
     print(f"rank {rank}: chain ok")
 

@@ -525,12 +525,31 @@ def test_link_graph_allgather_and_gather_plans(B, seed):
                 v = u
 
 
-def test_link_graph_reduce_scatter_stays_switch_only(B):
+@pytest.mark.parametrize("seed", list(range(6)) + ["dgx1v"])
+def test_link_graph_reduce_scatter_plans(B, seed):
+    """ReduceScatter on link graphs (NEXT-3): tree j is a spanning tree rooted
+    at j over bidirectional links, every rank at its shortest (undirected)
+    distance from j, covering block j; a link without its reverse is a
+    topology error."""
     from oracle import graphs
-    g = graphs.dgx1v()
+    if seed == "dgx1v":
+        n, cap = graphs.dgx1v()
+    else:
+        n, cap, _ = _random_link_graph(9100 + seed)
+    G = B.Graph.from_pairs(n, cap)
+    d = _bfs_dist_fw(n, cap, True)
+    p = B.plan_json(n, 2, 0, 777, "bf16", graph=G)
+    assert len(p["trees"]) == n
+    for j, t in enumerate(p["trees"]):
+        par = t["parent"]
+        assert t["root"] == j and par[j] == -1 and (t["lo"], t["hi"]) == (j * 777, (j + 1) * 777)
+        for v in range(n):
+            if v != j:
+                u = par[v]
+                assert cap.get((u, v), 0) > 0 and cap.get((v, u), 0) > 0 and d[j][u] + 1 == d[j][v]
     with pytest.raises(B.BlinkError) as e:
-        B.plan_json(8, 2, 0, 1000, "f32", graph=B.Graph.from_pairs(8, g[1]))
-    assert e.value.code == 9
+        B.plan_json(3, 2, 0, 16, graph=B.Graph(3, [(0, 1, 1, 1), (1, 2, 1, 0), (2, 0, 1, 1)]))
+    assert e.value.code == 8 and "reverse" in str(e.value)
 
 
 # ------------------------------------------------------------ topology probe (P:80, P:320)

@@ -87,9 +87,9 @@ def oracle_plan(p):
 def test_random_configuration(B, seed):
     rng = random.Random(int(os.environ.get("FUZZ_BASE", "7000")) + seed)
     m, graph, kind = random_graph(B, rng)
-    # NEXT-3: ReduceScatter on the switch; AllGather / Gather on switches and link graphs
-    coll = "allreduce" if kind == "multiserver" else rng.choice(["allreduce", "allreduce", "broadcast"] +
-                      (["reduce_scatter"] if kind == "switch" else []) + ["allgather", "gather"])
+    # NEXT-3: ReduceScatter / AllGather / Gather on switches and link graphs
+    coll = "allreduce" if kind == "multiserver" else rng.choice(["allreduce", "allreduce", "broadcast",
+                                                                 "reduce_scatter", "allgather", "gather"])
     dtype = rng.choice(["f32", "bf16", "i32"])
     op = rng.choice(["sum", "min", "max", "avg"] + (["prod"] if dtype == "i32" else []))
     count = rng.choice([1, 7, 255, 4096, 65537, 300001, rng.randint(1, 200000)])
@@ -161,7 +161,13 @@ def test_random_configuration(B, seed):
             assert np.array_equal(bits(g), bits(OC.allgather(sends))), what
         return
     if coll == "reduce_scatter":
-        want = OC.reduce_scatter(sends, dtype, op)
+        if kind == "switch" or dtype == "i32" or op in ("min", "max"):
+            want = OC.reduce_scatter(sends, dtype, op)   # one-hop order = ascending ranks, or exact
+        else:   # multi-level trees: the oracle's tree order of each block's tree
+            pj = B.plan_json(m, 2, 0, count, dtype, graph=graph)
+            want = [OC.allreduce(dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"], weight=1)]),
+                                 [s[j * count:(j + 1) * count] for s in sends], dtype, op)
+                    for j, t in enumerate(pj["trees"])]
         for r in range(m):
             assert np.array_equal(bits(got[r]), bits(want[r])), what
         return

@@ -522,13 +522,14 @@ def test_allgather_inplace_and_rs_max(B):
         assert_bitwise(out[r].cpu().numpy(), want[r])
 
 
-def test_block_collectives_need_a_switch(B):
-    tri = triangle()
-    comms = make_comms(B, 3, graph=B.Graph.from_pairs(3, tri[1]))
-    x = torch.zeros(48, device="cuda")
+def test_block_collectives_on_multiserver_graphs_are_unsupported(B):
+    g = OG.dgx1v()
+    servers = [[0, 1, 2, 3], [4, 5, 6, 7]]
+    comms = make_comms(B, 8, graph=B.Graph.multi_server(8, g[1], servers))
+    x = torch.zeros(8 * 16, device="cuda")
     y = torch.zeros(16, device="cuda")
     for r, c in enumerate(comms):
-        if r < 2:
+        if r < 7:
             c.reduce_scatter(x, y)
         else:
             with pytest.raises(B.BlinkError) as e:
@@ -776,6 +777,26 @@ def test_link_graph_allgather_and_gather(B, machine, ids, dtype):
             torch.cuda.synchronize()
             assert_bitwise(to_host(out, dtype), OC.gather(sends, root)[root])
     assert comms[0].stats()["last_trees"] == m
+    # ReduceScatter (the reduce half, inner ranks relaying partials): int32 and
+    # MIN/MAX exact; fp32/bf16 bit-exact against the oracle's tree-order
+    # evaluation of each block's tree
+    B_ = 20011
+    rsends = synth.inputs(155, m, m * B_, dtype)
+    dr = [to_dev(s, dtype) for s in rsends]
+    for op in ("sum", "max"):
+        outs = [sentinel(B_, dtype) for _ in range(m)]
+        for r, c in enumerate(comms):
+            c.reduce_scatter(dr[r], outs[r], op=op, recvcount=B_, dtype=dtype)
+        torch.cuda.synchronize()
+        if dtype == "i32" or op == "max":
+            want = OC.reduce_scatter(rsends, dtype, op)
+        else:
+            pj = B.plan_json(m, 2, 0, B_, dtype, graph=B.Graph.from_pairs(m, g[1]))
+            want = [OC.allreduce(dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"], weight=1)]),
+                                 [s[j * B_:(j + 1) * B_] for s in rsends], dtype, op)
+                    for j, t in enumerate(pj["trees"])]
+        for r in range(m):
+            assert_bitwise(to_host(outs[r], dtype), want[r])
     for c in comms:
         c.destroy()
 

@@ -264,5 +264,15 @@ def test_per_rank_link_graph_allgather_and_gather(B, dtype):
             c.gather(ds[r], out if r == root else None, root=root, sendcount=B_, dtype=dtype)
         torch.cuda.synchronize()
         assert_bitwise(to_host(out, dtype), OC.gather(sends, root)[root])
+    # ReduceScatter: inner ranks relay partials and ack their children
+    rs = synth.inputs(171, 8, 8 * B_, dtype)
+    dr = [to_dev(s, dtype) for s in rs]
+    outs = [sentinel(B_, dtype) for _ in range(8)]
+    for r, c in enumerate(comms):
+        c.reduce_scatter(dr[r], outs[r], op="max", recvcount=B_, dtype=dtype)
+    torch.cuda.synchronize()
+    want = OC.reduce_scatter(rs, dtype, "max")
+    for r in range(8):
+        assert_bitwise(to_host(outs[r], dtype), want[r])
     for c in comms:
         c.destroy()
