@@ -52,6 +52,9 @@ __device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// unicast and multicast mappings alias the same physical memory: order the
+// accesses made through one against those made through the other
+__device__ __forceinline__ void fence_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   grid_sync(ctr, gridDim.x);
   // 2. entry: my uc holds call e's input and call e - 1's copy-out is done
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    fence_alias();
     fence_sys();
     for (int u = 0; u < a.nranks; ++u)
       if (u != v) st_relaxed_sys(a.flags[u] + entry_idx(v), e);
@@ -183,6 +187,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
       for (int u = 0; u < a.nranks && ok; ++u)
         if (u != v) ok = nv_wait(a.flags[v] + entry_idx(u), e, a.timeout_ns, a.err);
     fence_sys();
+    fence_alias();
     s_ok = ok;
   }
   __syncthreads();
@@ -205,6 +210,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   grid_sync(ctr + 1, gridDim.x);
   // 5. publish my slice (bflag[v][0]) and wait for every root's
   if (threadIdx.x == 0 && blockIdx.x == 0 && hi > lo) {
+    fence_alias();
     fence_sys();
     for (int u = 0; u < a.nranks; ++u)
       if (u != v) st_relaxed_sys(a.flags[u] + bflag_idx(v, 0), e);
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
       if (has) ok = nv_wait(a.flags[v] + bflag_idx(j, 0), e, a.timeout_ns, a.err);
     }
     fence_sys();
+    fence_alias();
     s_ok = ok;
   }
   __syncthreads();

@@ -232,6 +232,12 @@ bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<N
   const int n = int(devs.size());
   for (int dv : devs)
     if (!nvls_supported(dv, false, err)) return false;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  struct Restore {
+    int d;
+    ~Restore() { cudaSetDevice(d); }
+  } restore{cur};
   const size_t size = nvls_round(n, bytes);
   NvlsMem base;
   if (!nvls_create(n, size, false, &base, err)) return false;
