@@ -554,12 +554,66 @@ def run_multiprocess(args):
     torch.cuda.synchronize()
     e2e_ms = max_ms(e0.elapsed_time(e1) / n_e2e)
     nccl = nccl_compare(args, send, recv, count, stream, rank, world, same_gpu, tune_log)
+    nvls = nvls_arm(args, B, ex, send, count, stream, rank, world, max_ms) if not same_gpu else \
+        {"unavailable": "all ranks share one GPU (a multicast team needs distinct GPUs)"}
     out = None
     if rank == 0:
         out = multiprocess_line(args, m, S, ms, bc_ms, graph, e2e_ms, n_e2e, launches, clk.summary(), nccl)
+        out["nvls"] = nvls
     comm.destroy()
     dist.barrier()
     dist.destroy_process_group()
+    return out
+
+
+def nvls_arm(args, B, ex, send, count, stream, rank, world, max_ms):
+    """NEXT-1 on the same workload: a second comm with cfg.nvls = 1 (the one-hop
+    trees inside the NVSwitch).  Reports whether multicast came up (and why
+    not), the AllReduce time, and the largest deviation from the P2P result
+    relative to sum|x| (the switch sums in its own order, R#29).  Any failure
+    is recorded, not raised: the P2P line stands on its own."""
+    import torch
+    import torch.distributed as dist
+    out = {}
+    comm = None
+    try:
+        comm = B.init_multiprocess(world, rank, torch.cuda.current_device(), ex,
+                                   cfg=B.config(timeout_s=10.0, nvls=1))
+        plan = comm.plan(True, 0, count, "f32")
+        out["active"] = plan["nvls"]["active"]
+        out["note"] = plan["nvls"]["note"]
+        if out["active"]:
+            ref = torch.empty_like(send)
+            comm2 = B.init_multiprocess(world, rank, torch.cuda.current_device(), ex,
+                                        cfg=B.config(timeout_s=10.0))
+            comm2.allreduce(send, ref, op="sum", stream=stream)
+            y = torch.empty_like(send)
+
+            def arm():
+                comm.allreduce(send, y, op="sum", stream=torch.cuda.current_stream())
+
+            for _ in range(args.warmup):
+                arm()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ms = max_ms(time_device(arm, args.steps, stream))
+            S = count * 4
+            alg = S / (ms * 1e-3) / 1e9
+            dev = float((y - ref).abs().max()) / max(1e-30, float(send.abs().max()) * world)
+            t = torch.tensor([dev], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out.update({"ms": round(ms, 4), "alg_bw_gbs": round(alg, 3),
+                        "bus_bw_gbs": round(alg * 2 * (world - 1) / world, 3),
+                        "max_dev_vs_p2p_rel": float(t.item())})
+            comm2.destroy()
+    except Exception as e:  # pragma: no cover - depends on the box
+        out["error"] = f"{type(e).__name__}: {e}"[:200]
+    finally:
+        if comm is not None:
+            try:
+                comm.destroy()
+            except Exception:
+                pass
     return out
 
 
