@@ -328,6 +328,100 @@ def nvls_mode(rank, world):
     print(f"rank {rank}: nvls ok")
 
 
+def fuzz_mode(rank, world):
+    """Randomized multi-process parity: every rank draws the same seeded
+    sequence of graphs and collectives (switch or link graph, every
+    collective, dtype and op, registered or staged buffers, LL and tree
+    sizes, MIAD on or off) and checks each result against the oracle --
+    the cross-process protocol (CUDA IPC, .sys flags, entry / exit waits,
+    staging relays) on random configurations."""
+    import random
+    from fractions import Fraction
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    torch.cuda.set_device(0)
+    ex = BD.exchange()
+    base = int(os.environ.get("MP_FUZZ_BASE", "500"))
+    n_cfg = int(os.environ.get("MP_FUZZ_N", "6"))
+    done = 0
+    for k in range(n_cfg):
+        rng = random.Random(base + k)
+        kind = rng.choice(["switch", "link"])
+        graph = None
+        pairs = None
+        if kind == "link":
+            while True:
+                cap = {}
+                for u in range(world):
+                    for v in range(u + 1, world):
+                        if rng.random() < 0.6:
+                            cap[(u, v)] = cap[(v, u)] = rng.randint(1, 2)
+                if OG.is_connected((world, cap)):
+                    break
+            graph = B.Graph.from_pairs(world, cap)
+            pairs = cap
+        comm = BD.init(graph=graph, cfg=B.config(timeout_s=60.0, staging_bytes=1 << 20,
+                                                  autotune=int(rng.random() < 0.3)), device=0)
+        for step in range(4):
+            coll = rng.choice(["allreduce", "allreduce", "broadcast", "reduce_scatter", "allgather", "gather"])
+            dtype = rng.choice(["f32", "bf16", "i32"])
+            op = rng.choice(["sum", "max", "min"] + (["avg"] if coll == "allreduce" else []))
+            count = rng.choice([1, 777, 65537, 300001])
+            reg = rng.random() < 0.4
+            root = rng.randrange(world)
+            n_in = world * count if coll == "reduce_scatter" else count
+            sends = synth.inputs(base + 100 * k + step, world, n_in, dtype)
+            x = to_dev(sends[rank], dtype)
+            n_out = count if coll == "reduce_scatter" else (world * count if coll in ("allgather", "gather") else count)
+            y = torch.zeros(n_out, dtype=x.dtype, device="cuda")
+            if reg and coll != "gather":
+                comm.register(x, x.numel() * x.element_size(), ex)
+                comm.register(y, y.numel() * y.element_size(), ex)
+            if coll == "allreduce":
+                comm.allreduce(x, y, op=op, count=count, dtype=dtype)
+            elif coll == "broadcast":
+                comm.broadcast(x if rank == root else None, y, root=root, count=count, dtype=dtype)
+            elif coll == "reduce_scatter":
+                comm.reduce_scatter(x, y, op=op, recvcount=count, dtype=dtype)
+            elif coll == "allgather":
+                comm.allgather(x, y, sendcount=count, dtype=dtype)
+            else:
+                comm.gather(x, y if rank == root else None, root=root, sendcount=count, dtype=dtype)
+            torch.cuda.synchronize()
+            got = y.view(torch.int16).cpu().numpy().view(np.uint16) if dtype == "bf16" else y.cpu().numpy()
+            what = f"cfg {k} step {step} {kind} {coll} {dtype} {op} n={count} reg={reg} root={root}"
+            if coll == "broadcast":
+                want = sends[root]
+            elif coll in ("allgather", "gather"):
+                if coll == "gather" and rank != root:
+                    continue
+                want = OC.allgather(sends)
+            elif coll == "reduce_scatter":
+                if kind == "switch" or dtype == "i32" or op in ("min", "max"):
+                    want = OC.reduce_scatter(sends, dtype, op)[rank]
+                else:
+                    pj = B.plan_json(world, 2, 0, count, dtype, graph=graph)
+                    t = pj["trees"][rank]
+                    want = OC.allreduce(dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"], weight=1)]),
+                                        [sv[rank * count:(rank + 1) * count] for sv in sends], dtype, op)
+            else:
+                if dtype == "i32" or op in ("min", "max"):
+                    want = OC.naive_reduce(sends, dtype, op)
+                else:
+                    p = comm.plan(True, 0, count, dtype)
+                    want = OC.allreduce(dict(trees=[dict(parent=tuple(t["parent"]), root=t["root"],
+                                                         weight=Fraction(*t["weight"])) for t in p["trees"]]),
+                                        sends, dtype, op)
+            gb = got.view(np.uint16 if got.dtype.itemsize == 2 else np.uint32)
+            wb = np.asarray(want).view(gb.dtype)
+            if not np.array_equal(gb, wb):
+                bad = np.nonzero(gb != wb)[0]
+                raise SystemExit(f"rank {rank}: {what}: {bad.size} mismatches, first {bad[:4]}")
+            done += 1
+        comm.destroy()
+    print(f"rank {rank}: fuzz ok {done}")
+
+
 def fingerprint_mode(rank, world):
     """Ranks whose chunk tables differ (here BLINK_CHUNKS_PER_CTA on rank 1)
     would consume each other's flags for different byte ranges: blink_connect
@@ -390,6 +484,8 @@ def main():
             miad_mode(rank, world)
         elif mode == "nvls":
             nvls_mode(rank, world)
+        elif mode == "fuzz":
+            fuzz_mode(rank, world)
         else:
             gpu_mode(rank, world)
     finally:

@@ -94,3 +94,12 @@ def test_processes_on_distinct_gpus(mode, n):
         pytest.skip(f"needs {n} GPUs")
     out = launch(n, mode, {}, timeout=900)
     assert out.count(f"{mode} ok") == n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,base", [(2, 500), (3, 600)])
+def test_multiprocess_fuzz(n, base):
+    """Seeded random configurations through the one-process-per-rank
+    protocol (processes time-sharing one GPU)."""
+    out = launch(n, "fuzz", {"BLINK_SAME_GPU": "1", "MP_FUZZ_BASE": str(base)}, timeout=900)
+    assert out.count("fuzz ok") == n
