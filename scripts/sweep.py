@@ -14,7 +14,9 @@ plus `plan_hbm_frac`: the HBM bytes the chosen plan must move (multi-hop
 trees re-read partials / forwarded chunks) over the same time -- the
 executor's efficiency on its plan.
 Config 5 replays the App. C DDP bucket sequences back to back on one stream.
-Times are device times of CUDA-graph replays (no host enqueue cost).
+Times are device times of CUDA-graph replays (no host enqueue cost): `ms` per
+call with up to 10 back-to-back calls per graph, `ms_one_call_per_graph` with
+one (that adds a graph launch, ~8 us, to every call).
 """
 import argparse
 import json
@@ -37,25 +39,35 @@ ES = {"f32": 4, "bf16": 2, "i32": 4}
 
 
 def time_calls(fn, nbytes):
-    """Device time per call: one call is captured into a CUDA graph (epochs are
-    device-resident, so replays are valid) and replayed `reps` times; the
-    host-side cost of m binding calls per collective is not in the number."""
-    reps = 50 if nbytes <= (1 << 20) else (20 if nbytes <= (64 << 20) else 5)
-    for _ in range(3):
-        fn()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        fn()
-    g.replay()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
+    """Device time per call of back-to-back calls: up to 10 calls are captured
+    in one CUDA graph (epochs are device-resident, so replays are valid) and
+    the graph is replayed; a graph launch has a fixed cost of its own
+    (~8 us on this box), which one call per graph would measure instead of the
+    collective (round 1's sweep did: every size up to 1 MiB read 8.3 us).
+    Returns (ms per call in a 10-call graph, ms per call with one call per
+    graph)."""
+    per_graph = 10 if nbytes <= (64 << 20) else 2
+    reps = 20 if nbytes <= (1 << 20) else (10 if nbytes <= (64 << 20) else 5)
+
+    def measure(k, r):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(k):
+                fn()
         g.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(r):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / (r * k)
+
+    return measure(per_graph, reps), measure(1, reps)
 
 
 def plan_traffic(plan, coll, esize):
@@ -102,12 +114,13 @@ def run_coll(comms, coll, S, dtype, root=0, tag=""):
                 c.broadcast(sends[root] if r == root else None, recvs[r], root=root)
         hbm = (m + 1) * cnt * ES[dtype]
         f = 1.0
-    ms = time_calls(fn, cnt * ES[dtype])
+    ms, ms1 = time_calls(fn, cnt * ES[dtype])
     Sb = cnt * ES[dtype]
     alg = Sb / (ms * 1e-3) / 1e9
     plan = comms[0].plan(coll == "allreduce", root, cnt, dtype)
     pt = plan_traffic(plan, coll, ES[dtype])
     return {"config": tag, "coll": coll, "m": m, "dtype": dtype, "bytes": Sb, "ms": round(ms, 5),
+            "ms_one_call_per_graph": round(ms1, 5),
             "algbw": round(alg, 2), "busbw": round(alg * f, 2),
             "hbm_gbs": round(hbm / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(hbm / (ms * 1e-3) / 1e9 / PEAK, 4),
             "plan_hbm_bytes": pt, "plan_hbm_frac": round(pt / (ms * 1e-3) / 1e9 / PEAK, 4),
@@ -131,10 +144,11 @@ def run_block(comms, coll, S, dtype, tag):
             for r, c in enumerate(comms):
                 c.allgather(part[r], full[r])
     Sb = m * B * ES[dtype]
-    ms = time_calls(fn, Sb)
+    ms, ms1 = time_calls(fn, Sb)
     hbm = (m + 1) * Sb
     alg = Sb / (ms * 1e-3) / 1e9
     return {"config": tag, "coll": coll, "m": m, "dtype": dtype, "bytes": Sb, "ms": round(ms, 5),
+            "ms_one_call_per_graph": round(ms1, 5),
             "algbw": round(alg, 2), "busbw": round(alg * (m - 1) / m, 2),
             "hbm_gbs": round(hbm / (ms * 1e-3) / 1e9, 1),
             "hbm_frac": round(hbm / (ms * 1e-3) / 1e9 / PEAK, 4)}
@@ -222,7 +236,7 @@ def main():
                     for r, c in enumerate(comms):
                         c.allreduce(bb[r], bb[r])
             tot = sum(buckets) * ES[dt]
-            ms = time_calls(seq, tot)
+            ms, _ = time_calls(seq, tot)
             alg = tot / (ms * 1e-3) / 1e9
             log({"config": f"c5-{model}-buckets", "coll": "allreduce", "m": m, "dtype": dt,
                  "bytes": tot, "buckets": len(buckets), "ms": round(ms, 4), "algbw": round(alg, 2),
