@@ -11,7 +11,9 @@ oracle, so a clean sanitizer run is also a correct run.  It prints
 Sections: one-hop tree executor (TMA aligned, LSU misaligned), bf16, AVG,
 ReduceScatter / AllGather, DGX-1V packed Broadcast and multi-level AllReduce,
 the R#27 shallow tree on the tree executor, the shallow tree in the LL
-protocol, switch LL (batched and per-rank launches), per-rank tree AllReduce.
+protocol, NEXT-3 on the DGX-1V link graph (AllGather, Gather with relays,
+ReduceScatter with relayed partials; batched and per-rank), switch LL (batched
+and per-rank launches), per-rank tree AllReduce.
 """
 import os
 import sys
@@ -168,6 +170,45 @@ def dgx1v_sections(n=20000 + 3):
         c.destroy()
 
 
+def link_block_sections():
+    """NEXT-3 on the DGX-1V link graph: AllGather (multi-level trees), Gather
+    (relays through scratch, recv = None off the root) and ReduceScatter
+    (inner ranks relay partials, roots write recv, acks), batched and per-rank."""
+    g = OG.dgx1v()
+    G = B.Graph.from_pairs(8, g[1])
+    n = 5003
+    for per_rank in (0, 1):
+        comms = B.init_all([0] * 8, graph=G, cfg=B.config(timeout_s=T, chunk_bytes=8192,
+                                                          launch_per_rank=per_rank, ll_max_bytes=0))
+        sends = synth.inputs(206, 8, n, "i32")
+        xs = [dev(s) for s in sends]
+        ag = [torch.zeros(8 * n, dtype=torch.int32, device="cuda") for _ in range(8)]
+        for r, c in enumerate(comms):
+            c.allgather(xs[r], ag[r])
+        torch.cuda.synchronize()
+        for y in ag:
+            check(y, OC.allgather(sends), "link allgather")
+        gout = torch.zeros(8 * n, dtype=torch.int32, device="cuda")
+        for r, c in enumerate(comms):
+            c.gather(xs[r], gout if r == 5 else None, root=5)
+        torch.cuda.synchronize()
+        check(gout, OC.gather(sends, 5)[5], "link gather")
+        rsend = synth.inputs(207, 8, 8 * n, "i32")
+        rx = [dev(s) for s in rsend]
+        ry = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(8)]
+        for r, c in enumerate(comms):
+            c.reduce_scatter(rx[r], ry[r], op="sum")
+        torch.cuda.synchronize()
+        want = OC.reduce_scatter(rsend, "i32", "sum")
+        for r in range(8):
+            check(ry[r], want[r], "link reduce_scatter")
+        expect_path(comms[0], True, "link reduce_scatter")
+        print(f"ok DGX-1V AllGather / Gather / ReduceScatter ({'per-rank' if per_rank else 'batched'})",
+              flush=True)
+        for c in comms:
+            c.destroy()
+
+
 def ll_and_per_rank_sections(sends, want):
     for per_rank in (0, 1):
         comms = B.init_all([0] * 4, cfg=B.config(timeout_s=T, launch_per_rank=per_rank,
@@ -205,6 +246,7 @@ def ll_and_per_rank_sections(sends, want):
 def main():
     sends, want = onehop_sections()
     dgx1v_sections()
+    link_block_sections()
     ll_and_per_rank_sections(sends, want)
     print("sanitize cases ok", flush=True)
 
