@@ -241,12 +241,20 @@ blink_result_t blink_connect(blink_comm_t comm, const void* all_blobs, size_t bl
 
 /* Symmetric buffer registration (multi-process zero-copy).  Collective: every
  * rank registers its own buffer of the same size in the same order, exports a
- * blob, all-gathers, and connects.  A registered buffer is used in place (the
- * kernels read and write peers' copies directly); collectives on it must use
- * the same byte offset into it on every rank.  Unregistered buffers go
- * through the staging buffer (local copy in/out).  In single-process comms
- * registration is unnecessary (pointers are exchanged at launch) and these
- * calls are accepted no-ops. */
+ * blob, all-gathers the blobs (caller's channel) and connects.  Registered
+ * buffers are used in place; unregistered ones go through the library staging
+ * buffer; collectives on a registered buffer must use the same byte offset
+ * into it on every rank.  No-ops (SUCCESS) on single-process comms.
+ *   cudaMalloc memory (incl. PyTorch's caching allocator): a CUDA IPC handle
+ *   of the allocation plus the offset.  VMM memory (e.g. PyTorch
+ *   expandable_segments): every physical chunk the buffer touches is exported
+ *   as a POSIX fd; peers duplicate the fds (pidfd_getfd: needs ptrace access
+ *   to the exporter, e.g. same user with ptrace_scope 0, or CAP_SYS_PTRACE)
+ *   and map the chunks back to back.  The exporter keeps the fds until
+ *   blink_destroy.
+ * blink_register_export with blob == NULL only reports the blob size in
+ * *blob_bytes.  Errors: UNSUPPORTED (neither kind of memory, or more than
+ * 128 VMM chunks), SYSTEM (pidfd failures), CUDA. */
 blink_result_t blink_register_export(blink_comm_t comm, void* buf, size_t bytes, void* blob,
                                      size_t* blob_bytes);
 blink_result_t blink_register_connect(blink_comm_t comm, void* buf, const void* all_blobs,

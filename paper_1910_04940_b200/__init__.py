@@ -332,8 +332,9 @@ class Comm:
     def register(self, buf, nbytes, exchange):
         """Symmetric registration (multi-process).  `exchange(bytes) -> list[bytes]`
         all-gathers one blob per rank in rank order."""
-        n = _sz(512)
-        blob = ctypes.create_string_buffer(512)
+        n = _sz(0)
+        _check(_lib.blink_register_export(self._h, _ptr(buf), nbytes, None, ctypes.byref(n)), self._h)
+        blob = ctypes.create_string_buffer(max(1, n.value))
         _check(_lib.blink_register_export(self._h, _ptr(buf), nbytes, blob, ctypes.byref(n)), self._h)
         blobs = exchange(blob.raw[:n.value])
         allb = b"".join(blobs)

@@ -261,6 +261,23 @@ bool nvls_add_device(NvlsMem* m, int dev, std::string* err);
 bool nvls_bind_map(NvlsMem* m, int dev, bool fabric, std::string* err);
 void nvls_release(NvlsMem* m);
 bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<NvlsMem>* out, std::string* err);
+// VMM (PyTorch expandable segments) registration: the physical chunks a
+// buffer touches, exported as POSIX fds, mapped back to back at a peer.
+struct VmmChunk {
+  int64_t off = 0;    // chunk start relative to the buffer (<= 0 for the first)
+  size_t size = 0;
+  int fd = -1;        // exporter's fd
+};
+struct VmmMapping {
+  unsigned long long va = 0;
+  size_t span = 0;
+  char* base = nullptr;  // where the peer's buffer starts in this process
+  std::vector<std::pair<unsigned long long, size_t>> mapped;
+};
+bool vmm_chunks(const void* buf, size_t bytes, std::vector<VmmChunk>* out, std::string* err);
+bool vmm_map_peer(const std::vector<VmmChunk>& chunks, const std::vector<int>& local_fds, int dev,
+                  VmmMapping* out, std::string* err);
+void vmm_unmap(VmmMapping* m);
 
 // exec.cu
 cudaError_t launch_ll(const LLArgs& a, int grid, void* stream, bool cooperative, bool pdl);

@@ -49,6 +49,8 @@ struct Drv {
   CUresult (*MemExportToShareableHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
                                          unsigned long long) = nullptr;
   CUresult (*MemImportFromShareableHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+  CUresult (*MemRetainAllocationHandle)(CUmemGenericAllocationHandle*, void*) = nullptr;
+  CUresult (*MemGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
 };
 
 template <class F>
@@ -79,7 +81,9 @@ const Drv& drv() {
            load("cuMemAddressFree", &x.MemAddressFree, &e) && load("cuMemMap", &x.MemMap, &e) &&
            load("cuMemUnmap", &x.MemUnmap, &e) && load("cuMemSetAccess", &x.MemSetAccess, &e) &&
            load("cuMemExportToShareableHandle", &x.MemExportToShareableHandle, &e) &&
-           load("cuMemImportFromShareableHandle", &x.MemImportFromShareableHandle, &e);
+           load("cuMemImportFromShareableHandle", &x.MemImportFromShareableHandle, &e) &&
+           load("cuMemRetainAllocationHandle", &x.MemRetainAllocationHandle, &e) &&
+           load("cuMemGetAddressRange", &x.MemGetAddressRange, &e);
     return x;
   }();
   return d;
@@ -258,6 +262,93 @@ bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<N
     if (!nvls_bind_map(&m, devs[i], false, err)) return false;
   }
   return true;
+}
+
+// ------------------------------------------------------------ VMM registration
+// PyTorch's expandable segments map fixed-size physical chunks (cuMemCreate,
+// POSIX-fd exportable) into one reserved range; a tensor can straddle chunks.
+// The legacy cudaIpcGetMemHandle rejects such memory, so registration exports
+// every chunk the buffer touches and the peers map them back to back.
+bool vmm_chunks(const void* buf, size_t bytes, std::vector<VmmChunk>* out, std::string* err) {
+  const Drv& d = drv();
+  if (!d.ok) {
+    *err = d.err;
+    return false;
+  }
+  out->clear();
+  const CUdeviceptr b = reinterpret_cast<CUdeviceptr>(buf);
+  CUdeviceptr a = b;
+  while (a < b + bytes) {
+    CUdeviceptr cb = 0;
+    size_t cs = 0;
+    DRV_TRY(d.MemGetAddressRange(&cb, &cs, a), "cuMemGetAddressRange");
+    CUmemGenericAllocationHandle h;
+    DRV_TRY(d.MemRetainAllocationHandle(&h, reinterpret_cast<void*>(cb)), "cuMemRetainAllocationHandle");
+    int fd = -1;
+    CUresult r = d.MemExportToShareableHandle(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+    d.MemRelease(h);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuMemExportToShareableHandle(POSIX fd) failed (CUresult " + std::to_string(int(r)) +
+             "): the allocation is not exportable";
+      return false;
+    }
+    VmmChunk c;
+    c.off = int64_t(cb) - int64_t(b);
+    c.size = cs;
+    c.fd = fd;
+    out->push_back(c);
+    a = cb + cs;
+  }
+  return true;
+}
+
+bool vmm_map_peer(const std::vector<VmmChunk>& chunks, const std::vector<int>& local_fds, int dev,
+                  VmmMapping* out, std::string* err) {
+  const Drv& d = drv();
+  if (!d.ok) {
+    *err = d.err;
+    return false;
+  }
+  if (chunks.empty()) {
+    *err = "no chunks";
+    return false;
+  }
+  const int64_t first = chunks.front().off;
+  const int64_t span = chunks.back().off + int64_t(chunks.back().size) - first;
+  CUdeviceptr va = 0;
+  DRV_TRY(d.MemAddressReserve(&va, size_t(span), size_t(2) << 20, 0, 0), "cuMemAddressReserve");
+  out->va = va;
+  out->span = size_t(span);
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof acc);
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    CUmemGenericAllocationHandle h;
+    DRV_TRY(d.MemImportFromShareableHandle(&h, reinterpret_cast<void*>(static_cast<intptr_t>(local_fds[i])),
+                                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+            "cuMemImportFromShareableHandle(POSIX fd)");
+    const CUdeviceptr at = va + CUdeviceptr(chunks[i].off - first);
+    CUresult r = d.MemMap(at, chunks[i].size, 0, h, 0);
+    d.MemRelease(h);  // the mapping keeps the memory alive
+    if (r != CUDA_SUCCESS) {
+      *err = "cuMemMap of a peer chunk failed (CUresult " + std::to_string(int(r)) + ")";
+      return false;
+    }
+    out->mapped.push_back({at, chunks[i].size});
+    DRV_TRY(d.MemSetAccess(at, chunks[i].size, &acc, 1), "cuMemSetAccess");
+  }
+  out->base = reinterpret_cast<char*>(va) - first;  // the peer's buf
+  return true;
+}
+
+void vmm_unmap(VmmMapping* m) {
+  const Drv& d = drv();
+  if (!d.ok) return;
+  for (auto& x : m->mapped) d.MemUnmap(x.first, x.second);
+  if (m->va) d.MemAddressFree(m->va, m->span);
+  *m = VmmMapping();
 }
 
 }  // namespace blink

@@ -29,6 +29,14 @@
 #include <tuple>
 #include <string>
 #include <unistd.h>
+#include <sys/syscall.h>
+#include <cerrno>
+#ifndef SYS_pidfd_open
+#define SYS_pidfd_open 434
+#endif
+#ifndef SYS_pidfd_getfd
+#define SYS_pidfd_getfd 438
+#endif
 #include <vector>
 
 #include "blink_internal.h"
@@ -125,6 +133,8 @@ struct blink_comm {
   NvlsMem nvls;
   bool nvls_on = false;
   std::string nvls_note = "off (cfg.nvls = 0)";
+  std::vector<int> exported_fds;      // VMM registration: fds peers duplicate (closed at destroy)
+  std::vector<VmmMapping> vmm_maps;   // VMM registration: peers' chunks mapped here
   Probe probe;                // topology probe result (graph == NULL at init)
   bool probe_at_connect = false;  // multi-process: graph == NULL, probed from the peers' bus ids
   char* scratch = nullptr;    // single-process Gather on link graphs: forwarding buffer of a
@@ -1398,11 +1408,18 @@ uint64_t chunking_fingerprint(blink_comm_t comm) {
   }
   return h;
 }
+constexpr int kMaxVmmChunks = 128;
 struct RegBlob {
   char magic[8];
-  int32_t rank, pad;
-  cudaIpcMemHandle_t h;
+  int32_t rank, kind;              // kind 0: cudaMalloc memory (legacy IPC handle)
+  cudaIpcMemHandle_t h;            // kind 1: VMM chunks (PyTorch expandable segments)
   uint64_t offset, bytes;
+  int32_t pid, nchunks;            // kind 1: exporter pid and its POSIX fds, one per chunk
+  struct {
+    int64_t off;
+    uint64_t size;
+    int32_t fd, pad;
+  } chunks[kMaxVmmChunks];
 };
 
 blink_result_t open_handle(blink_comm_t comm, const cudaIpcMemHandle_t& h, char** out) {
@@ -2301,8 +2318,8 @@ blink_result_t blink_register_export(blink_comm_t comm, void* buf, size_t bytes,
   if (!comm || !blob_bytes) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "NULL argument");
   size_t cap = *blob_bytes;
   *blob_bytes = sizeof(RegBlob);
-  if (!comm->multiprocess) return BLINK_SUCCESS;
-  if (!blob || cap < sizeof(RegBlob)) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "blob too small");
+  if (!comm->multiprocess || !blob) return BLINK_SUCCESS;  // blob == NULL: size query
+  if (cap < sizeof(RegBlob)) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "blob too small");
   if (!buf || bytes == 0) return fail(comm, BLINK_ERR_INVALID_ARGUMENT, "empty buffer");
   DeviceGuard g(comm->device);
   // allocation base of `buf` (IPC handles name whole allocations); the driver
@@ -2323,9 +2340,31 @@ blink_result_t blink_register_export(blink_comm_t comm, void* buf, size_t bytes,
   RegBlob rb{};
   memcpy(rb.magic, "BLINKrg", 8);
   rb.rank = comm->rank;
-  CUDA_TRY(comm, cudaIpcGetMemHandle(&rb.h, reinterpret_cast<void*>(base)));
-  rb.offset = uint64_t(reinterpret_cast<char*>(buf) - reinterpret_cast<char*>(base));
   rb.bytes = bytes;
+  if (cudaIpcGetMemHandle(&rb.h, reinterpret_cast<void*>(base)) == cudaSuccess) {
+    rb.kind = 0;
+    rb.offset = uint64_t(reinterpret_cast<char*>(buf) - reinterpret_cast<char*>(base));
+  } else {  // VMM memory (e.g. PyTorch expandable segments): export every chunk
+    cudaGetLastError();
+    std::vector<VmmChunk> ch;
+    std::string verr;
+    if (!vmm_chunks(buf, bytes, &ch, &verr))
+      return fail(comm, BLINK_ERR_UNSUPPORTED,
+                  "buffer is neither cudaMalloc memory nor an exportable VMM allocation: " + verr);
+    if (int(ch.size()) > kMaxVmmChunks) {
+      for (auto& c : ch) close(c.fd);
+      return fail(comm, BLINK_ERR_UNSUPPORTED, "buffer spans more than 128 VMM chunks");
+    }
+    rb.kind = 1;
+    rb.pid = int32_t(getpid());
+    rb.nchunks = int32_t(ch.size());
+    for (size_t i = 0; i < ch.size(); ++i) {
+      rb.chunks[i].off = ch[i].off;
+      rb.chunks[i].size = ch[i].size;
+      rb.chunks[i].fd = ch[i].fd;
+      comm->exported_fds.push_back(ch[i].fd);
+    }
+  }
   memcpy(blob, &rb, sizeof rb);
   return BLINK_SUCCESS;
 }
@@ -2350,6 +2389,42 @@ blink_result_t blink_register_connect(blink_comm_t comm, void* buf, const void* 
       return fail(comm, BLINK_ERR_INVALID_USAGE, "registered sizes differ across ranks (symmetric registration)");
     if (u == comm->rank) {
       reg.peer[u] = reg.buf;
+      continue;
+    }
+    if (rb.kind == 1) {  // VMM chunks: duplicate the exporter's fds, map them back to back
+      if (rb.nchunks <= 0 || rb.nchunks > kMaxVmmChunks)
+        return fail(comm, BLINK_ERR_INVALID_USAGE, "registration blob " + std::to_string(u) + " is invalid");
+      const int pidfd = int(syscall(SYS_pidfd_open, rb.pid, 0));
+      if (pidfd < 0)
+        return fail(comm, BLINK_ERR_SYSTEM, "pidfd_open(rank " + std::to_string(u) + "): " + strerror(errno));
+      std::vector<VmmChunk> ch(rb.nchunks);
+      std::vector<int> lfds;
+      for (int i = 0; i < rb.nchunks; ++i) {
+        ch[i].off = rb.chunks[i].off;
+        ch[i].size = rb.chunks[i].size;
+        ch[i].fd = rb.chunks[i].fd;
+        const int lfd = int(syscall(SYS_pidfd_getfd, pidfd, rb.chunks[i].fd, 0));
+        if (lfd < 0) {
+          const std::string why = strerror(errno);
+          for (int f : lfds) close(f);
+          close(pidfd);
+          return fail(comm, BLINK_ERR_SYSTEM,
+                      "pidfd_getfd(rank " + std::to_string(u) + "): " + why +
+                          " (VMM registration needs ptrace access to the peer process)");
+        }
+        lfds.push_back(lfd);
+      }
+      close(pidfd);
+      VmmMapping m;
+      std::string verr;
+      const bool ok = vmm_map_peer(ch, lfds, comm->device, &m, &verr);
+      for (int f : lfds) close(f);
+      if (!ok) {
+        vmm_unmap(&m);
+        return fail(comm, BLINK_ERR_CUDA, "mapping rank " + std::to_string(u) + "'s VMM chunks: " + verr);
+      }
+      reg.peer[u] = m.base;
+      comm->vmm_maps.push_back(m);
       continue;
     }
     char* p = nullptr;
@@ -2516,6 +2591,8 @@ blink_result_t blink_destroy(blink_comm_t comm) {
         cudaFree(kv.second.d_trees);
       }
       for (auto& kv : comm->opened) cudaIpcCloseMemHandle(kv.second);
+      for (auto& m : comm->vmm_maps) vmm_unmap(&m);
+      for (int f : comm->exported_fds) close(f);
       if (comm->staging) cudaFree(comm->staging);
       for (auto& kv : comm->mp_miad) {
         if (kv.second.ev0) cudaEventDestroy(kv.second.ev0);

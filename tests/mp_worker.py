@@ -422,6 +422,40 @@ def fuzz_mode(rank, world):
     print(f"rank {rank}: fuzz ok {done}")
 
 
+def vmm_mode(rank, world):
+    """Zero-copy registration of VMM memory (PyTorch expandable segments,
+    PYTORCH_CUDA_ALLOC_CONF=expandable_segments:True set by the launcher):
+    buffers straddling the allocator's physical chunks are exported chunk by
+    chunk and mapped by the peers; a registered call is ONE launch (the staged
+    path would take many with a 1 MiB staging buffer) and bit-exact."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    assert "expandable_segments:True" in os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "")
+    torch.cuda.set_device(0)
+    comm = BD.init(cfg=B.config(timeout_s=60.0, staging_bytes=1 << 20, ll_max_bytes=0), device=0)
+    ex = BD.exchange()
+    pad = torch.empty(7 << 20, dtype=torch.uint8, device="cuda")  # push the next tensors across chunk edges
+    count = (12 << 20) + 5                                       # 48 MiB of fp32: spans 3+ chunks
+    fs = synth.inputs(56, world, count, "f32")
+    x = torch.from_numpy(fs[rank]).cuda()
+    y = torch.empty_like(x)
+    comm.register(x, x.numel() * 4, ex)
+    comm.register(y, y.numel() * 4, ex)
+    l0 = comm.stats()["launches"]
+    comm.allreduce(x, y, op="sum")
+    torch.cuda.synchronize()
+    assert comm.stats()["launches"] - l0 == 1, "expected the zero-copy path"
+    if not np.array_equal(y.cpu().numpy().view(np.uint32), OC.naive_reduce(fs, "f32", "sum").view(np.uint32)):
+        raise SystemExit(f"rank {rank}: VMM registered allreduce mismatch")
+    comm.broadcast(x if rank == 1 else None, y, root=1)
+    torch.cuda.synchronize()
+    if not np.array_equal(y.cpu().numpy().view(np.uint32), fs[1].view(np.uint32)):
+        raise SystemExit(f"rank {rank}: VMM registered broadcast mismatch")
+    del pad
+    comm.destroy()
+    print(f"rank {rank}: vmm ok")
+
+
 def fingerprint_mode(rank, world):
     """Ranks whose chunk tables differ (here BLINK_CHUNKS_PER_CTA on rank 1)
     would consume each other's flags for different byte ranges: blink_connect
@@ -486,6 +520,8 @@ def main():
             nvls_mode(rank, world)
         elif mode == "fuzz":
             fuzz_mode(rank, world)
+        elif mode == "vmm":
+            vmm_mode(rank, world)
         else:
             gpu_mode(rank, world)
     finally:

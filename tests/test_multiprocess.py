@@ -103,3 +103,11 @@ def test_multiprocess_fuzz(n, base):
     protocol (processes time-sharing one GPU)."""
     out = launch(n, "fuzz", {"BLINK_SAME_GPU": "1", "MP_FUZZ_BASE": str(base)}, timeout=900)
     assert out.count("fuzz ok") == n
+
+
+@pytest.mark.gpu
+def test_vmm_expandable_segments_register_zero_copy():
+    """PyTorch expandable-segments buffers (VMM chunks) register zero-copy."""
+    out = launch(2, "vmm", {"BLINK_SAME_GPU": "1", "PYTORCH_CUDA_ALLOC_CONF": "expandable_segments:True"},
+                 timeout=600)
+    assert out.count("vmm ok") == 2
