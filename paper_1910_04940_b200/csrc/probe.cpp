@@ -225,7 +225,10 @@ std::string probe_to_json(const Probe& p) {
         o << (first ? "" : ",") << "[" << u << "," << v << "," << p.links[u][v] << "]";
         first = false;
       }
-  o << "],\"note\":\"" << p.note << "\"}";
+  std::string note = p.note;  // JSON-safe
+  for (char& c : note)
+    if (c == '"' || c == '\\' || static_cast<unsigned char>(c) < 0x20) c = '\'';
+  o << "],\"note\":\"" << note << "\"}";
   return o.str();
 }
 
