@@ -121,7 +121,9 @@ typedef struct {
  *                  decides for every rank.  One process per GPU: rank 0
  *                  decides and publishes each call's size in its flag words,
  *                  the other ranks read it before enqueueing the call (they
- *                  wait for rank 0 to get that far).  Must agree across ranks.
+ *                  wait for rank 0 to get that far).  Calls enqueued on a
+ *                  stream under CUDA-graph capture use the static table
+ *                  (no timing inside a capture).  Must agree across ranks.
  *                  0 = the static table (default)
  *   launch_per_rank  single-process comms only: 1 = every rank runs in its own
  *                  launch on a library-owned stream (forked from and joined

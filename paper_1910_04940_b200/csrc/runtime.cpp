@@ -148,7 +148,7 @@ struct blink_comm {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool pending = false;  // rank 0: ev0/ev1 bracket a launch not yet folded into st
     bool done = false;     // converged (phase 2) and published: no more slots
-    size_t chunk = 0;
+    size_t chunk = 0;      // chunk of the last autotuned call (identical on every rank)
     int calls = 0;
   };
   std::map<std::tuple<int, int, int, size_t>, MpMiad> mp_miad;  // (coll, root, dtype, count)
@@ -681,6 +681,15 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   return BLINK_SUCCESS;
 }
 
+// Switches this thread's stream-capture mode to relaxed for its lifetime:
+// allocations and uploads made on behalf of a call being captured into a CUDA
+// graph are not part of the graph and must not invalidate the capture.
+struct RelaxedCapture {
+  cudaStreamCaptureMode prev = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&prev); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&prev); }
+};
+
 blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* s) {
   DeviceGuard g(device);
   std::vector<DevTree> trees(s->ranges.size());
@@ -698,13 +707,21 @@ blink_result_t finalize_tables(blink_comm_t comm, int device, int esize, Sized* 
   for (auto& t : s->tasks)
     if (t.tree >= 0 && size_t(t.tree) < trees.size()) t.tr = trees[t.tree];
   s->htrees = trees;
+  // a call first seen while its stream is being captured into a CUDA graph
+  // builds its tables here too: allocate and upload outside the capture
+  // (relaxed mode, a private non-blocking stream) so the capture stays valid
+  RelaxedCapture rc;
   CUDA_TRY(comm, cudaMalloc(&s->d_tasks, sizeof(DevTask) * s->tasks.size()));
   CUDA_TRY(comm, cudaMalloc(&s->d_trees, sizeof(DevTree) * std::max<size_t>(1, trees.size())));
-  CUDA_TRY(comm, cudaMemcpy(s->d_tasks, s->tasks.data(), sizeof(DevTask) * s->tasks.size(),
-                            cudaMemcpyHostToDevice));
-  if (!trees.empty())
-    CUDA_TRY(comm, cudaMemcpy(s->d_trees, trees.data(), sizeof(DevTree) * trees.size(),
-                              cudaMemcpyHostToDevice));
+  cudaStream_t up = nullptr;
+  CUDA_TRY(comm, cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(s->d_tasks, s->tasks.data(), sizeof(DevTask) * s->tasks.size(),
+                                  cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess && !trees.empty())
+    e = cudaMemcpyAsync(s->d_trees, trees.data(), sizeof(DevTree) * trees.size(), cudaMemcpyHostToDevice, up);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(up);
+  cudaStreamDestroy(up);
+  CUDA_TRY(comm, e);
   return BLINK_SUCCESS;
 }
 
@@ -1021,7 +1038,21 @@ blink_result_t clique_launch(Clique* q) {
   const bool ll = lltree || ((q->groups.size() > 1 || bytes <= kLLOneLaunchMax) &&
                              ll_slices(c0, *plan, q->coll, q->count, es, ll_lo));
   if (q->nvls && !ll && nvls_call(q->coll, q->op)) return clique_nvls(q, bytes);
-  if (c0->cfg.autotune && !ll) {
+  // MIAD does not step while a stream is being captured into a CUDA graph:
+  // its event timing cannot run inside a capture
+  bool capturing = false;
+  for (int v = 0; v < n && !capturing; ++v) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(q->pending[v].stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      capturing = true;
+  }
+  if (c0->cfg.autotune && !ll && capturing) {
+    // freeze: a captured call takes the chunk the eager calls have tuned so
+    // far (the static table's if none ran), without timing it
+    auto mit = q->miad.find(std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count));
+    if (mit != q->miad.end()) chunk_override = mit->second.st.phase == 2 ? mit->second.st.best : mit->second.st.chunk;
+  }
+  if (c0->cfg.autotune && !ll && !capturing) {
     auto mk = std::make_tuple(q->coll, q->coll == kBroadcast ? q->root : -1, q->dtype, q->count);
     auto mit = q->miad.find(mk);
     if (mit == q->miad.end()) {
@@ -1198,6 +1229,7 @@ blink_result_t clique_launch(Clique* q) {
           const size_t need = size_t(n) * bytes;
           if (cv->scratch_bytes < need) {
             DeviceGuard gv(cv->device);
+            RelaxedCapture rc;
             if (cv->scratch) cudaFree(cv->scratch);
             cv->scratch = nullptr;
             cv->scratch_bytes = 0;
@@ -1215,6 +1247,7 @@ blink_result_t clique_launch(Clique* q) {
         const size_t need = size_t(n) * bytes;
         if (cv->scratch_bytes < need) {
           DeviceGuard gv(cv->device);
+          RelaxedCapture rc;
           if (cv->scratch) cudaFree(cv->scratch);
           cv->scratch = nullptr;
           cv->scratch_bytes = 0;
@@ -1517,10 +1550,8 @@ blink_result_t mp_miad_chunk(blink_comm_t comm, int coll, int root, blink_dtype_
     c = size_t(v[1] & ((uint64_t(1) << 56) - 1));
     conv = (v[1] >> 56) != 0;
   }
-  if (conv) {
-    m.done = true;
-    m.chunk = c;
-  }
+  m.done = conv;
+  m.chunk = c;  // the last chunk every rank used for this key (also a capture's)
   m.calls++;
   *chunk = c;
   return BLINK_SUCCESS;
@@ -1539,7 +1570,16 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   uint64_t mask = uint64_t(1) << comm->rank;
   size_t chunk_override = 0;
   blink_comm::MpMiad* mm = nullptr;
-  if (comm->cfg.autotune && (coll == kBroadcast || coll == kAllReduce)) {
+  cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+  const bool capturing = cudaStreamIsCapturing(stream, &cap_st) == cudaSuccess &&
+                         cap_st != cudaStreamCaptureStatusNone;
+  if (comm->cfg.autotune && capturing && (coll == kBroadcast || coll == kAllReduce)) {
+    // a captured call neither times nor reads a slot: it takes the chunk of
+    // the last eager autotuned call, which every rank used (static if none)
+    auto mit = comm->mp_miad.find(std::make_tuple(coll, coll == kBroadcast ? root : -1, int(dtype), count));
+    if (mit != comm->mp_miad.end()) chunk_override = mit->second.chunk;
+  }
+  if (comm->cfg.autotune && !capturing && (coll == kBroadcast || coll == kAllReduce)) {
     r = mp_miad_chunk(comm, coll, root, dtype, count, *plan, stream, &chunk_override, &mm);
     if (r != BLINK_SUCCESS) return r;
   }

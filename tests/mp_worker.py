@@ -289,8 +289,38 @@ def miad_mode(rank, world):
     dist.all_gather_object(allc, (chunks, bchunks))
     assert all(c == allc[0] for c in allc), allc
     assert len(set(chunks)) >= 2, chunks
+    # a call captured into a CUDA graph neither times nor reads a slot: it
+    # takes the last eager call's chunk on every rank; eager calls afterwards
+    # continue the same numbered sequence
+    torch.cuda.synchronize()
+    dist.barrier()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=st):
+        comm.allreduce(x, y, op="sum", stream=torch.cuda.current_stream())
+    cap_chunk = comm.stats()["last_chunk_bytes"]
+    for k in range(3):
+        y.fill_(float("nan"))
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        if not np.array_equal(y.cpu().numpy().view(np.uint32), want.view(np.uint32)):
+            raise SystemExit(f"rank {rank}: MIAD captured replay {k}: allreduce mismatch")
+    for k in range(2):
+        y.fill_(float("nan"))
+        comm.allreduce(x, y, op="sum")
+        torch.cuda.synchronize()
+        if not np.array_equal(y.cpu().numpy().view(np.uint32), want.view(np.uint32)):
+            raise SystemExit(f"rank {rank}: MIAD eager call after capture {k}: allreduce mismatch")
+    allcap = [None] * world
+    dist.all_gather_object(allcap, cap_chunk)
+    assert all(c == allcap[0] for c in allcap), allcap
+    assert cap_chunk == chunks[-1], (cap_chunk, chunks[-1])
+    del g
     comm.destroy()
-    print(f"rank {rank}: miad ok {chunks} {bchunks}")
+    print(f"rank {rank}: miad ok {chunks} {bchunks} captured {cap_chunk}")
 
 
 def nvls_mode(rank, world):

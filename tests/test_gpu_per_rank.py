@@ -276,3 +276,42 @@ def test_per_rank_link_graph_allgather_and_gather(B, dtype):
         assert_bitwise(to_host(outs[r], dtype), want[r])
     for c in comms:
         c.destroy()
+
+
+@pytest.mark.parametrize("warm", [1, 0])
+@pytest.mark.parametrize("per_rank", [0, 1])
+def test_miad_calls_inside_a_cuda_graph_capture(B, per_rank, warm):
+    """With cfg.autotune, a call captured into a CUDA graph takes the chunk
+    the eager calls tuned so far without timing it (the static table's when
+    the capture is the first call, whose tables are then built outside the
+    capture); replays are bit-exact, and eager calls afterwards still tune."""
+    m, count = 4, (1 << 20) + 3
+    comms = B.init_all([0] * m, cfg=B.config(timeout_s=20.0, autotune=1, launch_per_rank=per_rank))
+    sends = synth.inputs(122, m, count, "f32")
+    want = OC.naive_reduce(sends, "f32", "sum")
+    ds = [to_dev(s, "f32") for s in sends]
+    out = [torch.empty_like(d) for d in ds]
+    for _ in range(3 if warm else 0):  # eager warm-up (tuning)
+        for r, c in enumerate(comms):
+            c.allreduce(ds[r], out[r])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=s):
+        for r, c in enumerate(comms):
+            c.allreduce(ds[r], out[r], stream=torch.cuda.current_stream())
+    for _ in range(3):
+        for o in out:
+            o.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        for o in out:
+            assert_bitwise(o.cpu().numpy(), want)
+    for r, c in enumerate(comms):
+        c.allreduce(ds[r], out[r])
+    torch.cuda.synchronize()
+    for o in out:
+        assert_bitwise(o.cpu().numpy(), want)
+    for c in comms:
+        c.destroy()
