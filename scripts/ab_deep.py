@@ -35,7 +35,10 @@ cases = [("c1-bc", B.init_all([0]*3, graph=B.Graph.from_pairs(3, tri[1])), "bc")
          ("n4-44", B.init_all([0]*8, graph=B.Graph.multi_server(8, g[1], [[0,1,2,3],[4,5,6,7]])), "ar")]
 cases[2] = ("c2-ar", cases[1][1], "ar")
 line = []
+only = os.environ.get("CASES")  # e.g. CASES=c2-bc,c2-ar
 for name, comms, coll in cases:
+    if only and name not in only.split(","):
+        continue
     for S in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20):
         line.append(f"{name}/{S>>20}M:{run(comms, coll, S):.0f}")
-print(os.environ.get("BLINK_MIN_CHUNK_DEEP", "default"), " ".join(line), flush=True)
+print(os.environ.get("CFG_LABEL", os.environ.get("BLINK_MIN_CHUNK_DEEP", "default")), " ".join(line), flush=True)
