@@ -30,6 +30,23 @@ def _src_hash():
     return h.hexdigest()
 
 
+def _obj_hash(src):
+    """One object's inputs: its source, every header and the flags."""
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    for d in [os.path.join(CSRC, s) for s in [src] + HEADERS]:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def _obj_fresh(src, obj):
+    try:
+        with open(obj + ".srchash") as f:
+            return os.path.exists(obj) and f.read().strip() == _obj_hash(src)
+    except OSError:
+        return False
+
+
 def _stale():
     """The library is stale when the hash of its sources changed (content, not
     mtimes: snapshots copied to the GPU box keep a fresh build fresh)."""
@@ -47,15 +64,18 @@ def build(force=False, verbose=False):
         fcntl.flock(lk, fcntl.LOCK_EX)     # concurrent importers build once
         if not force and not _stale():
             return LIB
-        return _build(verbose)
+        return _build(verbose, force)
 
 
-def _build(verbose):
+def _build(verbose, force=False):
     objs = []
     procs = []
-    for src in SOURCES:          # the sources compile concurrently
+    for src in SOURCES:          # the stale sources compile concurrently
         obj = os.path.join(CSRC, "build", src + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
+        if not force and _obj_fresh(src, obj):
+            objs.append(obj)
+            continue
         cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                                  text=True)))
@@ -67,6 +87,8 @@ def _build(verbose):
             raise RuntimeError(f"nvcc failed on {src}")
         with open(obj + ".ptxas.txt", "w") as f:
             f.write(log)
+        with open(obj + ".srchash", "w") as f:
+            f.write(_obj_hash(src))
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",

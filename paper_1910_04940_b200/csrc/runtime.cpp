@@ -359,6 +359,9 @@ bool alloc_channels(const Plan& plan, const std::vector<std::vector<uint32_t>>& 
            std::to_string(budget) + " CTAs can be co-resident";
     return false;
   }
+  // Proportional split: CTAs in proportion to work, largest remainders get
+  // the CTAs the floors left over (every SM works); ties by channel order, so
+  // every launch group computes the same split.
   double tot = 0;
   for (auto& c : chans) tot += c.work;
   int used = 0;
@@ -370,8 +373,6 @@ bool alloc_channels(const Plan& plan, const std::vector<std::vector<uint32_t>>& 
     rem.push_back({share - std::floor(share), int(j)});
     used += c.ctas;
   }
-  // largest remainders get the CTAs the floors left over (every SM works);
-  // ties by channel order, so every launch group computes the same split
   std::stable_sort(rem.begin(), rem.end(),
                    [](const std::pair<double, int>& a, const std::pair<double, int>& b) { return a.first > b.first; });
   for (size_t j = 0; used < avail && j < rem.size(); ++j, ++used) ++chans[rem[j].second].ctas;
@@ -381,6 +382,40 @@ bool alloc_channels(const Plan& plan, const std::vector<std::vector<uint32_t>>& 
     --it->ctas;
     --used;
   }
+  // Makespan split: every channel starts with one CTA and each further CTA
+  // goes to the channel with the most work per CTA (ties: channel order).
+  // It minimises max(work / ctas), the slowest channel's time, over integer
+  // splits.  With dozens of channels on one device (multi-level trees of
+  // virtual ranks) the proportional split rounds shares of 1-2 CTAs to 1 or
+  // 2, up to 2x between the channels of one tree (DGX-1V AllReduce 256 MiB:
+  // 1-CTA channels ended at 1.85 ms, others at 0.61 ms).  It replaces the
+  // proportional split only when that rounding leaves the slowest channel
+  // >= 10% slower; with large shares the two differ by one CTA here and there
+  // and the proportional split measured as fast or faster.
+  // BLINK_ALLOC=prop|greedy forces one.
+  static const int mode = [] {
+    const char* e = getenv("BLINK_ALLOC");
+    if (!e) return 0;
+    return std::string(e) == "prop" ? 1 : (std::string(e) == "greedy" ? 2 : 0);
+  }();
+  if (mode == 1 || chans.empty()) return true;
+  std::vector<int> g(chans.size(), 1);
+  for (int u = int(chans.size()); u < avail; ++u) {
+    size_t best = 0;
+    for (size_t j = 1; j < chans.size(); ++j)
+      if (chans[j].work * g[best] > chans[best].work * g[j]) best = j;
+    ++g[best];
+  }
+  double mp = 0, mg = 0;
+  for (size_t j = 0; j < chans.size(); ++j) {
+    mp = std::max(mp, chans[j].work / chans[j].ctas);
+    mg = std::max(mg, chans[j].work / g[j]);
+  }
+  if (mode == 2 || mg < 0.9 * mp)
+    for (size_t j = 0; j < chans.size(); ++j) chans[j].ctas = g[j];
+  if (getenv("BLINK_DEBUG_TASKS"))
+    fprintf(stderr, "[blink] alloc: %zu channels, %d CTAs, makespan prop %.4g greedy %.4g -> %s\n",
+            chans.size(), avail, mp, mg, (mode == 2 || mg < 0.9 * mp) ? "greedy" : "prop");
   return true;
 }
 
@@ -1433,7 +1468,7 @@ uint64_t chunking_fingerprint(blink_comm_t comm) {
                                "BLINK_DEEP_CAP", "BLINK_CHUNKS_PER_CTA", "BLINK_SMEM_KB", "BLINK_TILE",
                                "BLINK_TMA", "BLINK_ONE_CHUNK", "BLINK_MERGE", "BLINK_DYNAMIC",
                                "BLINK_PACK", "BLINK_THREADS", "BLINK_MIAD", "BLINK_ILP_DIVES",
-                               "BLINK_LL_TREE"};
+                               "BLINK_LL_TREE", "BLINK_ALLOC"};
   for (const char* name : envs) {
     const char* e = getenv(name);
     mix(0x5eedull);
