@@ -346,6 +346,7 @@ typedef struct {
   int last_chunks;
   int last_trees;
   int64_t last_chunk_bytes;  /* chunk size of tree 0 in the last launch (MIAD trace) */
+  int last_steal_channels;   /* channels CTAs may join in the last launch (work stealing; 0 = off) */
 } blink_stats_t;
 blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* stats);
 /* Device-side trace of the last launch on this comm's device when the

@@ -65,7 +65,7 @@ class Miad(ctypes.Structure):
 class _Stats(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("last_ctas", ctypes.c_int),
                 ("last_chunks", ctypes.c_int), ("last_trees", ctypes.c_int),
-                ("last_chunk_bytes", ctypes.c_int64)]
+                ("last_chunk_bytes", ctypes.c_int64), ("last_steal_channels", ctypes.c_int)]
 
 
 _vp, _sz, _i, _cp = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_char_p
@@ -316,7 +316,8 @@ class Comm:
         s = _Stats()
         _check(_lib.blink_get_stats(self._h, ctypes.byref(s)), self._h)
         return dict(launches=s.launches, last_ctas=s.last_ctas, last_chunks=s.last_chunks,
-                    last_trees=s.last_trees, last_chunk_bytes=s.last_chunk_bytes)
+                    last_trees=s.last_trees, last_chunk_bytes=s.last_chunk_bytes,
+                    last_steal_channels=s.last_steal_channels)
 
     def trace(self):
         """Per-CTA %globaltimer stamps of the last launch (BLINK_TRACE=1), as a

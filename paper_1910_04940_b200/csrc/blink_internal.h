@@ -148,6 +148,8 @@ struct LaunchArgs {
   int nctr;                  // chunk counters ctrl[2 .. 2 + nctr) zeroed by the last CTA
   int split_ring;            // 1: signalling copies alternate chunks over two store threads
   int copy_stages;           // stage-ring depth of copies (0 = default 6; BLINK_COPY_STAGES)
+  int chan0, nchan;          // work stealing (a6): tasks[chan0 + ci] describes dynamic channel ci
+                             // of this launch (cta_idx = -1: a joining CTA); nchan = 0: off
   uint64_t epoch;            // set by the kernel from ctrl[0] + 1
   uint64_t* ctrl;            // device words: [0] epoch of the last completed launch,
                              // [1] CTAs finished in the current launch (graph-safe epochs)

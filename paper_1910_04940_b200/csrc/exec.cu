@@ -593,7 +593,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
     for (;;) {
       int c;
       if (ctr) {
-        if (first_chunk) {
+        if (first_chunk && t.cta_idx >= 0) {  // a joining CTA (cta_idx -1) only uses the counter
           c = t.cta_idx;
           first_chunk = false;
         } else if (nch <= t.cta_cnt) {
@@ -909,9 +909,55 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
 
   // segments: usually one; packed launches chain contiguous chunk ranges of
   // independent channels so that every SM carries the same number of bytes
-  for (int ti = blockIdx.x; ti >= 0;) {
-    const DevTask t = ti == int(blockIdx.x) ? t0 : a.tasks[ti];
-    ti = t.next;
+  // Then work stealing (a6, TMA path, dynamic channels): a CTA whose own
+  // channel has handed out every chunk joins the channel of this launch with
+  // the most chunks not yet taken and takes chunks from its counter,
+  // until no channel has any left.  Channels still hand out chunks in
+  // increasing order and a joined chunk's inputs come from chunks that other
+  // resident CTAs hold or will take, so DESIGN 2b's deadlock argument stands.
+  __shared__ int s_join;
+  bool stealing = false;
+  for (int ti = blockIdx.x;;) {
+    DevTask t;
+    if (!stealing) {
+      if (ti < 0) {
+        if (!(ws && a.nchan > 0)) break;
+        stealing = true;
+        continue;
+      }
+      t = ti == int(blockIdx.x) ? t0 : a.tasks[ti];
+      ti = t.next;
+    } else {
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const volatile unsigned int* ctrs = reinterpret_cast<const volatile unsigned int*>(a.ctrl + 2);
+        int best = -1, brem = 1;
+        for (int ci = lane; ci < a.nchan; ci += 32) {
+          const DevTask& r = a.tasks[a.chan0 + ci];
+          const int rem = r.tr.nchunks - r.cta_cnt - int(ctrs[r.ctr]);
+          // only where the channel's own CTAs still have > 2 rounds of
+          // chunks: a joiner's set-up costs about one chunk, and at the tail
+          // of small calls joiners only add pollers (A/B: 1 MiB 1 us slower)
+          if (rem > 2 * r.cta_cnt && rem > brem) {
+            brem = rem;
+            best = ci;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {  // most chunks left; ties: lowest channel
+          const int orem = __shfl_xor_sync(0xffffffffu, brem, o);
+          const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+          if (orem > brem || (orem == brem && ob >= 0 && (best < 0 || ob < best))) {
+            brem = orem;
+            best = ob;
+          }
+        }
+        if (lane == 0) s_join = best;
+      }
+      __syncthreads();
+      const int j = s_join;
+      if (j < 0) break;
+      t = a.tasks[a.chan0 + j];
+    }
     if (t.role != kRoleReduce && t.role != kRoleBcast) continue;
     const int w = t.rank;
     uint64_t* wflags = a.flags[w];

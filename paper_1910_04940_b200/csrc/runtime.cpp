@@ -87,6 +87,7 @@ struct Sized {
   int ctas = 0;
   int chunks = 0;
   int nctr = 0;  // dynamic chunk counters used by the launch
+  int chan0 = 0, nchan = 0;  // work stealing: channel descriptors after the CTAs' tasks
 };
 
 struct Reg {
@@ -306,6 +307,8 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
   comm->plans[k] = std::move(p);
   return BLINK_SUCCESS;
 }
+
+bool steal_on();
 
 struct Channel {
   int rank, tree, role, parent;
@@ -706,8 +709,34 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   }
   s->ctas = int(s->tasks.size());
   s->plan = &plan;
+  // work stealing (a6): one descriptor per dynamic channel after the CTAs'
+  // tasks.  A CTA whose own chunks are all taken joins the channel with the
+  // most chunks left; it takes chunks from that channel's counter only
+  // (cta_idx = -1), so a channel's chunks still go out in increasing order.
+  // Only when some channel has more than 3 rounds of chunks for its own CTAs
+  // (a CTA joins a channel with > 2 rounds left): otherwise nobody can join,
+  // and the exit-time scan would only delay the last CTA (about 1 us).
+  bool stealable = false;
+  for (auto& c : chans)
+    stealable = stealable || (((launch_mask >> c.rank) & 1) && s->ranges[c.tree].nchunks > 3 * c.ctas);
+  if (dynamic && steal_on() && stealable) {
+    s->chan0 = int(s->tasks.size());
+    for (size_t ci = 0; ci < chans.size(); ++ci) {
+      if (!((launch_mask >> chans[ci].rank) & 1)) continue;
+      for (int j = 0; j < s->chan0; ++j) {
+        if (s->tasks[j].ctr != int(ci)) continue;
+        DevTask t = s->tasks[j];
+        t.cta_idx = -1;
+        t.do_entry = 0;
+        t.next = -1;
+        s->tasks.push_back(t);
+        break;
+      }
+    }
+    s->nchan = int(s->tasks.size()) - s->chan0;
+  }
   if (getenv("BLINK_DEBUG_TASKS")) {  // CTA -> channel map (scripts/trace_tree.py)
-    for (size_t j = 0; j < s->tasks.size(); ++j) {
+    for (size_t j = 0; j < size_t(s->ctas); ++j) {
       const DevTask& t = s->tasks[j];
       fprintf(stderr, "[blink] cta %zu rank %d tree %d role %d parent %d children %x chunks %d\n", j,
               int(t.rank), int(t.tree), int(t.role), int(t.parent), t.children, t.c1);
@@ -809,6 +838,14 @@ int store_depth() {
   static int v = [] {
     const char* e = getenv("BLINK_STORE_DEPTH");
     return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+// Work stealing across a launch's channels (default on; BLINK_STEAL=0 off).
+bool steal_on() {
+  static bool v = [] {
+    const char* e = getenv("BLINK_STEAL");
+    return !(e && e[0] == '0');
   }();
   return v;
 }
@@ -1027,6 +1064,7 @@ blink_result_t clique_nvls(Clique* q, size_t bytes) {
       if (e != cudaSuccess) return fail(cv, BLINK_ERR_CUDA, std::string("NVLS launch: ") + cudaGetErrorString(e));
       cv->stats.launches++;
       cv->stats.last_ctas = cv->sms;
+      cv->stats.last_steal_channels = 0;
       cv->stats.last_chunks = 0;
       cv->stats.last_trees = n;
       cv->stats.last_chunk_bytes = int64_t(cnt);
@@ -1172,6 +1210,7 @@ blink_result_t clique_launch(Clique* q) {
         if (!((grp.mask >> v) & 1)) continue;
         q->comms[v]->stats.launches++;
         q->comms[v]->stats.last_ctas = grid;
+        q->comms[v]->stats.last_steal_channels = 0;
         q->comms[v]->stats.last_chunks = 0;
         q->comms[v]->stats.last_trees = int(plan->trees.size());
         q->comms[v]->stats.last_chunk_bytes = 0;
@@ -1240,6 +1279,8 @@ blink_result_t clique_launch(Clique* q) {
     a.store_depth = store_depth();
     a.split_ring = split_ring();
     a.copy_stages = copy_stages();
+    a.chan0 = s.chan0;
+    a.nchan = s.nchan;
     a.l2_hint = l2_hint();
     a.defer_signal = defer_signal();
     a.nctr = s.nctr;
@@ -1339,6 +1380,7 @@ blink_result_t clique_launch(Clique* q) {
       if (!((mask >> v) & 1)) continue;
       q->comms[v]->stats.launches++;
       q->comms[v]->stats.last_ctas = s.ctas;
+      q->comms[v]->stats.last_steal_channels = s.nchan;
       q->comms[v]->stats.last_chunks = s.chunks;
       q->comms[v]->stats.last_trees = int(plan->trees.size());
       q->comms[v]->stats.last_chunk_bytes = s.ranges.empty() ? 0 : s.ranges[0].chunk * es;
@@ -1656,6 +1698,8 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.store_depth = store_depth();
     a.split_ring = split_ring();
     a.copy_stages = copy_stages();
+    a.chan0 = s.chan0;
+    a.nchan = s.nchan;
   a.l2_hint = l2_hint();
   a.defer_signal = defer_signal();
   a.nctr = s.nctr;
@@ -1681,6 +1725,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   }
   comm->stats.launches++;
   comm->stats.last_ctas = s.ctas;
+  comm->stats.last_steal_channels = s.nchan;
   comm->stats.last_chunks = s.chunks;
   comm->stats.last_trees = int(plan->trees.size());
   comm->stats.last_chunk_bytes = s.ranges.empty() ? 0 : s.ranges[0].chunk * es;
@@ -1803,6 +1848,7 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
         return fail(comm, BLINK_ERR_CUDA, std::string("LL launch: ") + cudaGetErrorString(le));
       comm->stats.launches++;
       comm->stats.last_ctas = a.ctas_per_rank;
+      comm->stats.last_steal_channels = 0;
       comm->stats.last_chunks = 0;
       comm->stats.last_trees = int(plan->trees.size());
       comm->stats.last_chunk_bytes = 0;
@@ -1821,6 +1867,7 @@ blink_result_t mp_collective(blink_comm_t comm, int coll, const void* sendbuf, v
       if (e != cudaSuccess) return fail(comm, BLINK_ERR_CUDA, std::string("NVLS launch: ") + cudaGetErrorString(e));
       comm->stats.launches++;
       comm->stats.last_ctas = comm->sms;
+      comm->stats.last_steal_channels = 0;
       comm->stats.last_chunks = 0;
       comm->stats.last_trees = comm->nranks;
       comm->stats.last_chunk_bytes = int64_t(cnt);

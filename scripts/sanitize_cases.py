@@ -13,7 +13,7 @@ ReduceScatter / AllGather, DGX-1V packed Broadcast and multi-level AllReduce,
 the R#27 shallow tree on the tree executor, the shallow tree in the LL
 protocol, NEXT-3 on the DGX-1V link graph (AllGather, Gather with relays,
 ReduceScatter with relayed partials; batched and per-rank), switch LL (batched
-and per-rank launches), per-rank tree AllReduce.
+and per-rank launches), per-rank tree AllReduce, work stealing across channels.
 """
 import os
 import sys
@@ -132,6 +132,21 @@ def dgx1v_sections(n=20000 + 3):
     if comms[0].stats()["last_trees"] <= 1:
         raise SystemExit("dgx1v allreduce: expected packed trees")
     print("ok DGX-1V packed Broadcast + multi-level AllReduce", flush=True)
+    for c in comms:
+        c.destroy()
+    # work stealing: 4 KiB chunks give the 1-CTA channels > 3 rounds of chunks
+    steal = B.config(timeout_s=T, chunk_bytes=4096, shallow_max_bytes=0, ll_max_bytes=0)
+    comms = B.init_all([0] * 8, graph=G, cfg=steal)
+    ns = 60000 + 3
+    ssends = synth.inputs(204, 8, ns, "i32")
+    sx = [dev(s) for s in ssends]
+    sy = [torch.empty_like(x) for x in sx]
+    allreduce(comms, sx, sy)
+    for y in sy:
+        check(y, OC.naive_reduce(ssends, "i32", "sum"), "dgx1v allreduce (stealing)")
+    if comms[0].stats()["last_steal_channels"] <= 0:
+        raise SystemExit("dgx1v allreduce: expected work stealing on")
+    print("ok DGX-1V multi-level AllReduce with work stealing", flush=True)
     for c in comms:
         c.destroy()
     # R#27 shallow tree on the tree executor (LL off), 64 KiB
