@@ -350,10 +350,14 @@ typedef struct {
 } blink_stats_t;
 blink_result_t blink_get_stats(blink_comm_t comm, blink_stats_t* stats);
 /* Device-side trace of the last launch on this comm's device when the
- * environment variable BLINK_TRACE is set (single-process comms): 8 %globaltimer
+ * environment variable BLINK_TRACE is set (single-process comms): 16 %globaltimer
  * stamps (ns) per CTA -- start, epoch read, entry handshake done, first TMA
  * load, first bulk store, last stores complete, end of work, after the epoch
- * update (0 where a CTA has no such event).  *n_words in/out like
+ * update; then the hop's parts in the CTA's last segment: 8 producer has the
+ * first chunk's inputs (flags acquired), 9 store thread sees the first stage
+ * full, 10 store thread sees the end of the stream, 11 stores drained, 12
+ * chunk signals published, 13-15 spare (0 where a CTA has no such event).
+ * *n_words in/out like
  * blink_plan_json; synchronous copy.  *n_words = 0 when tracing is off. */
 blink_result_t blink_get_trace(blink_comm_t comm, uint64_t* out, size_t* n_words);
 blink_result_t blink_comm_info(blink_comm_t comm, int* nranks, int* rank, int* device);

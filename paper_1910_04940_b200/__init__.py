@@ -321,14 +321,15 @@ class Comm:
 
     def trace(self):
         """Per-CTA %globaltimer stamps of the last launch (BLINK_TRACE=1), as a
-        list of 8-tuples (ns); empty when tracing is off."""
+        list of 16-tuples (ns, include/blink.h blink_get_trace); empty when
+        tracing is off."""
         n = _sz(0)
         _check(_lib.blink_get_trace(self._h, None, ctypes.byref(n)), self._h)
         if n.value == 0:
             return []
         buf = (ctypes.c_uint64 * n.value)()
         _check(_lib.blink_get_trace(self._h, buf, ctypes.byref(n)), self._h)
-        return [tuple(buf[i:i + 8]) for i in range(0, n.value, 8)]
+        return [tuple(buf[i:i + 16]) for i in range(0, n.value, 16)]
 
     def register(self, buf, nbytes, exchange):
         """Symmetric registration (multi-process).  `exchange(bytes) -> list[bytes]`

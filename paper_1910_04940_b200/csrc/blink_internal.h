@@ -17,7 +17,7 @@ constexpr int kMaxRanks = 16;       // ranks per comm (one NVSwitch node; DGX-2 
 constexpr int kMaxTrees = 32;       // trees per plan
 constexpr int kMaxChunks = 512;     // chunks per tree per call
 constexpr int kGrain = 16;
-constexpr int kTraceSlots = 8;      // per-CTA trace stamps (BLINK_TRACE)
+constexpr int kTraceSlots = 16;     // per-CTA trace stamps (BLINK_TRACE)
 constexpr int kMaxCounters = 4096;  // dynamic chunk counters per launch (ctrl[2..])          // split grain in bytes (R#11) == one 128-bit vector
 
 // Flag region of one rank (uint64 words, monotonically increasing epochs,

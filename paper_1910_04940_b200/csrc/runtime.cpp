@@ -88,6 +88,7 @@ struct Sized {
   int chunks = 0;
   int nctr = 0;  // dynamic chunk counters used by the launch
   int chan0 = 0, nchan = 0;  // work stealing: channel descriptors after the CTAs' tasks
+  bool lsu = false;          // small chunks: the register (LSU) path, not the TMA pipeline
 };
 
 struct Reg {
@@ -309,6 +310,7 @@ blink_result_t get_plan(blink_comm_t comm, int coll, int root, size_t bytes, con
 }
 
 bool steal_on();
+int64_t lsu_chunk_max();
 
 struct Channel {
   int rank, tree, role, parent;
@@ -709,6 +711,18 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   }
   s->ctas = int(s->tasks.size());
   s->plan = &plan;
+  // Small chunks run the register path: one hop of a chunk through the TMA
+  // pipeline (flag -> producer warp -> bulk load -> mbarrier -> store warp ->
+  // bulk store -> drain -> flag) takes 3.5 us at 4 KiB, the all-threads LSU
+  // copy 1.6 us (scripts/hop_probe.py), and per-CTA throughput only matters
+  // once chunks are large (A/B per call, 1 MiB: DGX-1V Broadcast 23.6 -> 16.9
+  // us, 3-GPU chains 11.1 -> 8.0, switch two-level Broadcast 13.1 -> 10.4,
+  // DGX-1V AllReduce 37.9 -> 33.6; 4 MiB even; TMA wins from 16 MiB).
+  {
+    int64_t maxc = 0;
+    for (auto& r : s->ranges) maxc = std::max<int64_t>(maxc, r.chunk * int64_t(esize));
+    s->lsu = lsu_chunk_max() > 0 && maxc <= lsu_chunk_max();
+  }
   // work stealing (a6): one descriptor per dynamic channel after the CTAs'
   // tasks.  A CTA whose own chunks are all taken joins the channel with the
   // most chunks left; it takes chunks from that channel's counter only
@@ -719,7 +733,7 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   bool stealable = false;
   for (auto& c : chans)
     stealable = stealable || (((launch_mask >> c.rank) & 1) && s->ranges[c.tree].nchunks > 3 * c.ctas);
-  if (dynamic && steal_on() && stealable) {
+  if (dynamic && steal_on() && stealable && !s->lsu) {
     s->chan0 = int(s->tasks.size());
     for (size_t ci = 0; ci < chans.size(); ++ci) {
       if (!((launch_mask >> chans[ci].rank) & 1)) continue;
@@ -838,6 +852,15 @@ int store_depth() {
   static int v = [] {
     const char* e = getenv("BLINK_STORE_DEPTH");
     return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+// Largest chunk that runs the register path in a non-merged launch
+// (BLINK_LSU_CHUNK_MAX bytes; 0 = always the TMA pipeline).
+int64_t lsu_chunk_max() {
+  static int64_t v = [] {
+    const char* e = getenv("BLINK_LSU_CHUNK_MAX");
+    return e ? int64_t(atoll(e)) : int64_t(32 << 10);
   }();
   return v;
 }
@@ -1273,7 +1296,7 @@ blink_result_t clique_launch(Clique* q) {
     a.exit_wait = all_one_launch ? 0 : 1;
     a.scope_sys = q->devices.size() > 1 ? 1 : 0;
     a.bcast_root = (q->coll == kBroadcast || q->coll == kGather) ? q->root : -1;
-    a.use_tma = use_tma();
+    a.use_tma = use_tma() && !s.lsu;
     a.smem_bytes = smem_bytes();
     a.tile_bytes = tile_bytes();
     a.store_depth = store_depth();
@@ -1692,7 +1715,7 @@ blink_result_t mp_run(blink_comm_t comm, int coll, char* send[kMaxRanks], char* 
   a.exit_wait = 1;
   a.scope_sys = 1;
   a.bcast_root = (coll == kBroadcast || coll == kGather) ? root : -1;
-  a.use_tma = use_tma();
+  a.use_tma = use_tma() && !s.lsu;
   a.smem_bytes = smem_bytes();
   a.tile_bytes = tile_bytes();
   a.store_depth = store_depth();

@@ -15,7 +15,7 @@ import paper_1910_04940_b200 as B  # noqa: E402
 from oracle import graphs as OG  # noqa: E402  (topology presets only)
 from sweep import run_coll  # noqa: E402
 
-SIZES = [int(x) << 20 for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,16,64,256".split(","))]
+SIZES = [int(float(x) * (1 << 20)) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,16,64,256".split(","))]
 ONLY = os.environ.get("AB_ONLY", "")
 label = os.environ.get("CFG_LABEL", "")
 
@@ -29,7 +29,7 @@ def case(tag, comms, colls):
         parts = []
         for S in SIZES:
             r = run_coll(comms, coll, S, "f32", 0, tag)
-            parts.append(f"{S >> 20}M:{r['ms'] * 1e3:.1f}us/{r['plan_hbm_frac']:.2f}")
+            parts.append(f"{S / (1 << 20):g}M:{r['ms'] * 1e3:.1f}us/{r['plan_hbm_frac']:.2f}")
         print(f"{label:10s} {tag:22s} {coll:9s} " + " ".join(parts), flush=True)
     for c in comms:
         c.destroy()

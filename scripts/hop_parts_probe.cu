@@ -1,0 +1,322 @@
+// What one tree hop costs, part by part, on one B200 (scripts/hop_trace.py
+// measured ~3.5 us per hop for a 4 KB chunk: 1.1 us load-to-store, 1.4 us
+// store completion, 0.8 us signal-to-load).  Each test runs N times in one
+// thread (or warp) of one CTA on L2-resident data and reports the mean in ns
+// (%globaltimer) and SM cycles (clock64).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/hop_parts scripts/hop_parts_probe.cu
+//   /tmp/hop_parts
+//
+//   tma_load      cp.async.bulk global->smem of B bytes, wait on its mbarrier
+//   tma_store     cp.async.bulk smem->global of B bytes, commit, wait_group 0
+//   tma_store_rd  the same, wait_group.read 0 (smem reusable, writes not done)
+//   lsu_store     one warp stores B bytes (16 B per lane per step) + __syncwarp
+//                 + fence.acq_rel.gpu by lane 0
+//   fence_acqrel  fence.acq_rel.gpu alone
+//   fence_proxy   fence.proxy.async alone
+//   pingpong_*    two CTAs bounce a flag N times; one-way latency
+//                 relaxed: st.relaxed.gpu + fence / ld.relaxed.gpu poll + fence
+//                 relacq:  st.release.gpu / ld.acquire.gpu poll
+//                 volatile: st.volatile / ld.volatile poll (+ __threadfence)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+constexpr int N = 200;
+
+__global__ void parts(char* buf, int bytes, unsigned long long* out) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t bar;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // warm the lines into L2
+  for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16) *reinterpret_cast<uint4*>(buf + i) = make_uint4(i, 0, 0, 0);
+  __syncthreads();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (threadIdx.x >= 32) return;
+  uint64_t t0, t1;
+  long long c0, c1;
+  // tma_load
+  if (lane == 0) {
+    t0 = gtimer();
+    c0 = clock64();
+    for (int i = 0; i < N; ++i) {
+      mbar_expect_tx(&bar, bytes);
+      tma_load(sm, buf, bytes, &bar);
+      mbar_wait(&bar, i & 1);
+    }
+    c1 = clock64();
+    t1 = gtimer();
+    out[0] = (t1 - t0);
+    out[1] = (c1 - c0);
+  }
+  __syncwarp();
+  // tma_store + wait_group 0
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    t0 = gtimer();
+    c0 = clock64();
+    for (int i = 0; i < N; ++i) {
+      tma_store(buf + bytes, sm, bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    c1 = clock64();
+    t1 = gtimer();
+    out[2] = (t1 - t0);
+    out[3] = (c1 - c0);
+    t0 = gtimer();
+    c0 = clock64();
+    for (int i = 0; i < N; ++i) {
+      tma_store(buf + bytes, sm, bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    c1 = clock64();
+    t1 = gtimer();
+    out[4] = (t1 - t0);
+    out[5] = (c1 - c0);
+  }
+  __syncwarp();
+  // lsu_store: whole warp
+  {
+    const uint4* s4 = reinterpret_cast<const uint4*>(sm);
+    uint4* d4 = reinterpret_cast<uint4*>(buf + 2 * bytes);
+    t0 = gtimer();
+    c0 = clock64();
+    for (int i = 0; i < N; ++i) {
+      for (int k = lane; k < bytes / 16; k += 32) d4[k] = s4[k];
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      __syncwarp();
+    }
+    c1 = clock64();
+    t1 = gtimer();
+    if (lane == 0) {
+      out[6] = (t1 - t0);
+      out[7] = (c1 - c0);
+    }
+  }
+  if (lane == 0) {
+    t0 = gtimer();
+    c0 = clock64();
+    for (int i = 0; i < N; ++i) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    c1 = clock64();
+    t1 = gtimer();
+    out[8] = (t1 - t0);
+    out[9] = (c1 - c0);
+    t0 = gtimer();
+    c0 = clock64();
+    for (int i = 0; i < N; ++i) asm volatile("fence.proxy.async;" ::: "memory");
+    c1 = clock64();
+    t1 = gtimer();
+    out[10] = (t1 - t0);
+    out[11] = (c1 - c0);
+  }
+}
+
+template <int MODE>
+__global__ void pingpong(uint64_t* flags, unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  uint64_t* mine = flags + (blockIdx.x == 0 ? 0 : 32);
+  uint64_t* theirs = flags + (blockIdx.x == 0 ? 32 : 0);
+  const uint64_t t0 = gtimer();
+  for (uint64_t i = 1; i <= N; ++i) {
+    if (blockIdx.x == 1) {  // wait first
+      for (;;) {
+        uint64_t v;
+        if (MODE == 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+        else if (MODE == 1) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+        else v = *reinterpret_cast<volatile uint64_t*>(mine);
+        if (v >= i) break;
+      }
+      if (MODE != 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    if (MODE == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(theirs), "l"(i) : "memory");
+    } else if (MODE == 1) {
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(theirs), "l"(i) : "memory");
+    } else {
+      __threadfence();
+      *reinterpret_cast<volatile uint64_t*>(theirs) = i;
+    }
+    if (blockIdx.x == 0) {
+      for (;;) {
+        uint64_t v;
+        if (MODE == 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+        else if (MODE == 1) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+        else v = *reinterpret_cast<volatile uint64_t*>(mine);
+        if (v >= i) break;
+      }
+      if (MODE != 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+  }
+  if (blockIdx.x == 0) out[MODE] = gtimer() - t0;
+}
+
+
+// Two CTAs bounce a B-byte chunk with the executor's primitives: wait flag
+// (relaxed poll + fence.acq_rel) -> fence.proxy.async -> TMA load of the
+// chunk (written by the other CTA's bulk store) -> TMA store into the other
+// CTA's buffer -> wait_group 0 -> fence.proxy.async -> fence.acq_rel ->
+// relaxed flag store.  One-way time = one hop of a path.  VAR 1: the flag is
+// st.release / ld.acquire; VAR 2: the load / store are done by the warp
+// with LSU (ld.global.cg / st.global) instead of TMA.
+template <int VAR>
+__global__ void hop_pingpong(char* bufs, uint64_t* flags, int bytes, unsigned long long* out) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t bar;
+  const int lane = threadIdx.x;
+  const int me = blockIdx.x, other = 1 - me;
+  char* mybuf = bufs + size_t(me) * (1 << 20);
+  char* obuf = bufs + size_t(other) * (1 << 20);
+  uint64_t* myflag = flags + me * 32;
+  uint64_t* oflag = flags + other * 32;
+  if (lane == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t t0 = gtimer();
+  for (uint64_t i = 1; i <= N; ++i) {
+    if (!(me == 0 && i == 1)) {
+      if (lane == 0) {
+        for (;;) {
+          uint64_t v;
+          if (VAR == 1) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(myflag) : "memory");
+          else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(myflag) : "memory");
+          if (v >= i - (me == 0 ? 1 : 0)) break;
+        }
+        if (VAR != 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      __syncwarp();
+    }
+    if (VAR == 2) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(mybuf);
+      uint4* d4 = reinterpret_cast<uint4*>(obuf);
+      for (int k = lane; k < bytes / 16; k += 32) d4[k] = __ldcg(s4 + k);
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(oflag), "l"(i) : "memory");
+      }
+      __syncwarp();
+      continue;
+    }
+    if (lane == 0) {
+      asm volatile("fence.proxy.async;" ::: "memory");
+      mbar_expect_tx(&bar, bytes);
+      tma_load(sm, mybuf, bytes, &bar);
+      mbar_wait(&bar, (i - 1) & 1);
+      tma_store(obuf, sm, bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async;" ::: "memory");
+      if (VAR == 1) {
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(oflag), "l"(i) : "memory");
+      } else {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(oflag), "l"(i) : "memory");
+      }
+    }
+    __syncwarp();
+  }
+  if (me == 0 && lane == 0) out[VAR] = gtimer() - t0;
+}
+
+int main() {
+  char* buf;
+  unsigned long long *out, h[16];
+  uint64_t* flags;
+  cudaMalloc(&buf, 1 << 24);
+  cudaMalloc(&out, 16 * sizeof(unsigned long long));
+  cudaMalloc(&flags, 4096);
+  cudaFuncSetAttribute(parts, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10);
+  for (int bytes : {4096, 16384, 65536}) {
+    parts<<<1, 256, 65536 + 1024>>>(buf, bytes, out);
+    parts<<<1, 256, 65536 + 1024>>>(buf, bytes, out);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    const char* names[] = {"tma_load", "tma_store", "tma_store_rd", "lsu_store+fence", "fence_acqrel", "fence_proxy"};
+    printf("B = %d\n", bytes);
+    for (int k = 0; k < 6; ++k)
+      printf("  %-16s %8.1f ns %8.1f cyc\n", names[k], double(h[2 * k]) / N, double(h[2 * k + 1]) / N);
+  }
+  const char* pn[] = {"relaxed+fence", "release/acquire", "volatile+threadfence"};
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaMemset(flags, 0, 4096);
+    pingpong<0><<<2, 32>>>(flags, out);
+    cudaMemset(flags, 0, 4096);
+    pingpong<1><<<2, 32>>>(flags, out);
+    cudaMemset(flags, 0, 4096);
+    pingpong<2><<<2, 32>>>(flags, out);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+  }
+  for (int k = 0; k < 3; ++k) printf("pingpong %-22s one-way %8.1f ns\n", pn[k], double(h[k]) / N / 2);
+  char* hb;
+  cudaMalloc(&hb, 2 << 20);
+  cudaMemset(hb, 1, 2 << 20);
+  const char* hn[] = {"tma relaxed+fence", "tma release/acquire", "lsu relaxed+fence"};
+  cudaFuncSetAttribute(hop_pingpong<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(hop_pingpong<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(hop_pingpong<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaMemset(out, 0, 16 * sizeof(unsigned long long));
+  for (int kind : {0, 1}) {  // 0: both CTAs on nearby SMs; 1: grid of 148, CTAs 0 and 147 bounce
+    for (int bytes : {4096, 16384, 65536}) {
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(flags, 0, 4096);
+        hop_pingpong<0><<<2, 32, 65536>>>(hb, flags, bytes, out);
+        cudaMemset(flags, 0, 4096);
+        hop_pingpong<1><<<2, 32, 65536>>>(hb, flags, bytes, out);
+        cudaMemset(flags, 0, 4096);
+        hop_pingpong<2><<<2, 32, 65536>>>(hb, flags, bytes, out);
+      }
+      cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+      for (int k = 0; k < 3; ++k) printf("hop B=%6d %-22s one-way %8.1f ns\n", bytes, hn[k], double(h[k]) / N / 2);
+      printf("  (%s)\n", cudaGetErrorString(cudaGetLastError()));
+    }
+    break;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("%s\n", cudaGetErrorString(e));
+  return 0;
+}

@@ -134,10 +134,11 @@ def dgx1v_sections(n=20000 + 3):
     print("ok DGX-1V packed Broadcast + multi-level AllReduce", flush=True)
     for c in comms:
         c.destroy()
-    # work stealing: 4 KiB chunks give the 1-CTA channels > 3 rounds of chunks
-    steal = B.config(timeout_s=T, chunk_bytes=4096, shallow_max_bytes=0, ll_max_bytes=0)
+    # work stealing: 36 KiB chunks (TMA path, above the 32 KiB register-path
+    # cap) give the 1-CTA channels > 3 rounds of chunks
+    steal = B.config(timeout_s=T, chunk_bytes=36864, shallow_max_bytes=0, ll_max_bytes=0)
     comms = B.init_all([0] * 8, graph=G, cfg=steal)
-    ns = 60000 + 3
+    ns = 600000 + 3
     ssends = synth.inputs(204, 8, ns, "i32")
     sx = [dev(s) for s in ssends]
     sy = [torch.empty_like(x) for x in sx]

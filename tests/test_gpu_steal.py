@@ -1,9 +1,9 @@
 """GPU parity of work stealing (DESIGN 2b "Work stealing"): CTAs whose own
 channel has handed out every chunk join other channels of the launch.
 
-Small chunks (cfg.chunk_bytes) give every channel many more chunks than CTAs,
-so joins happen at test sizes; `last_steal_channels` proves the launch had
-stealing on.  Results must stay bit-exact against the oracle (a joined chunk
+Chunks of 36-40 KiB (above the register path's 32 KiB, so the TMA pipeline
+runs) give every channel many more chunks than CTAs, so joins happen at test
+sizes; `last_steal_channels` proves the launch had stealing on.  Results must stay bit-exact against the oracle (a joined chunk
 is combined by the same channel code in the same operand order).
 """
 import numpy as np
@@ -31,9 +31,9 @@ def B():
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_steal_dgx1v_allreduce_bitexact(B, dtype, per_rank):
     g = OG.dgx1v()
-    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=8192,
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=36864,
                        launch_per_rank=int(per_rank))
-    count = (3 << 18) + 7
+    count = (3 << 20) + 7
     sends = synth.inputs(77, 8, count, dtype)
     got = run_allreduce(B, comms, sends, dtype, "sum")
     assert comms[0].stats()["last_steal_channels"] > 0
@@ -51,8 +51,8 @@ def test_steal_dgx1v_allreduce_bitexact(B, dtype, per_rank):
 @pytest.mark.parametrize("root", [0, 7])
 def test_steal_dgx1v_broadcast_bitexact(B, root):
     g = OG.dgx1v()
-    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=16384)
-    count = (1 << 20) + 5
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=40960)
+    count = (4 << 20) + 5
     send = synth.rank_input(9, root, count, "f32")
     recv = [sentinel(count, "f32") for _ in range(8)]
     src = to_dev(send, "f32")
@@ -69,8 +69,8 @@ def test_steal_dgx1v_broadcast_bitexact(B, root):
 def test_steal_int_exact_under_any_join_order(B):
     """int32 SUM is exact: any chunk-to-CTA assignment gives the naive sum."""
     tri, _ = OG.induced(OG.dgx1v(), [0, 1, 3, 4, 5, 7])
-    comms = make_comms(B, 6, graph=B.Graph.from_pairs(6, tri[1]), chunk_bytes=4096)
-    count = 300017
+    comms = make_comms(B, 6, graph=B.Graph.from_pairs(6, tri[1]), chunk_bytes=36864)
+    count = (1 << 20) + 17
     sends = synth.inputs(5, 6, count, "i32")
     got = run_allreduce(B, comms, sends, "i32", "sum")
     assert comms[0].stats()["last_steal_channels"] > 0
@@ -87,7 +87,7 @@ def test_steal_off_same_bits(B, monkeypatch):
     g = OG.dgx1v()
     count = (1 << 19) + 3
     sends = synth.inputs(12, 8, count, "f32")
-    a = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=8192)
+    a = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=36864)
     got_a = run_allreduce(B, a, sends, "f32", "sum")
     assert a[0].stats()["last_steal_channels"] > 0
     plan_a = a[0].plan(True, 0, count, "f32")
