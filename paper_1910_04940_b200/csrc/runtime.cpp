@@ -718,10 +718,19 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
   // once chunks are large (A/B per call, 1 MiB: DGX-1V Broadcast 23.6 -> 16.9
   // us, 3-GPU chains 11.1 -> 8.0, switch two-level Broadcast 13.1 -> 10.4,
   // DGX-1V AllReduce 37.9 -> 33.6; 4 MiB even; TMA wins from 16 MiB).
+  // One-hop plans (stars: ReduceScatter / AllGather blocks, per-rank
+  // launches) keep 16 KiB chunks at every size, so there it also needs few
+  // chunks per CTA (<= 4, the latency regime): ReduceScatter 16 / 64 MiB ran
+  // 31 / 96 us on the TMA pipeline and 51 / 173 us on the register path.
   {
     int64_t maxc = 0;
+    int depth = 0, per = 0;
     for (auto& r : s->ranges) maxc = std::max<int64_t>(maxc, r.chunk * int64_t(esize));
-    s->lsu = lsu_chunk_max() > 0 && maxc <= lsu_chunk_max();
+    for (auto& t : plan.trees) depth = std::max(depth, t.depth);
+    for (auto& c : chans)
+      if ((launch_mask >> c.rank) & 1)
+        per = std::max(per, (s->ranges[c.tree].nchunks + c.ctas - 1) / c.ctas);
+    s->lsu = lsu_chunk_max() > 0 && maxc <= lsu_chunk_max() && (depth >= 2 || per <= 4);
   }
   // work stealing (a6): one descriptor per dynamic channel after the CTAs'
   // tasks.  A CTA whose own chunks are all taken joins the channel with the
