@@ -455,6 +455,12 @@ __device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
 __device__ __forceinline__ void trace(const LaunchArgs& a, int slot) {
   if (a.trace) a.trace[size_t(blockIdx.x) * kTraceSlots + slot] = globaltimer();
 }
+// Hop parts are stamped into registers and written after the last fence of
+// the role (a global store in front of a fence would delay the fence).
+__device__ __forceinline__ uint64_t stamp(const LaunchArgs& a) { return a.trace ? globaltimer() : 0; }
+__device__ __forceinline__ void trace_at(const LaunchArgs& a, int slot, uint64_t t) {
+  if (a.trace && t) a.trace[size_t(blockIdx.x) * kTraceSlots + slot] = t;
+}
 
 struct TileMeta {
   int64_t off;  // byte offset of the tile in every buffer
@@ -617,6 +623,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
   if (warp == 0) {
     // ------------------------------------------------ producer
     uint32_t gq[2] = {0u, 0u};  // tiles issued per sub-ring
+    uint64_t p_acq = 0, p_issue = 0;  // trace stamps (written at the end)
     uint32_t nord = 0;          // chunks taken so far (sub-ring = nord % R)
     int cs = t.c0;  // static sequence
     // dynamic tasks: the first chunk is the CTA's own index (no atomic round
@@ -651,7 +658,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         if (lane == 0) sh.abort = 1;
         break;
       }
-      if (lane == 0 && nord == 0) trace(a, 8);
+      if (lane == 0 && nord == 0) p_acq = stamp(a);
       int64_t b0, b1;
       if (t.merged) {  // one-hop roots over every rank: a chunk is a byte range
         b0 = int64_t(c) * a.mchunk;
@@ -676,7 +683,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
       if (lane == 0) {
         if (wmask) fence_proxy_async();  // acquired flags order the TMA reads below
-        if (c == t.c0 || (ctr && nord == 0)) trace(a, 3);
+        if (c == t.c0 || (ctr && nord == 0)) p_issue = stamp(a);
         const uint32_t r = nord % R;
         uint32_t& g = gq[r];
         const int ntiles = body > 0 ? int((body + tile - 1) / tile) : 1;
@@ -708,6 +715,10 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       __syncwarp();
       ++nord;
     }
+    if (lane == 0) {
+      trace_at(a, 8, p_acq);
+      trace_at(a, 3, p_issue);
+    }
     if (lane == 0)  // end of stream, in every sub-ring
       for (uint32_t r = 0; r < R; ++r) {
         const uint32_t s = r * H + gq[r] % H;
@@ -728,6 +739,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
         mbar_arrive(&sh.empty[r * H + gt % H]);
     };
     int kept = 0;
+    uint64_t s_full = 0, s_store = 0, s_eos = 0;  // trace stamps (written at the end)
     bool first = true;
     // Deferred chunk signals (a5): a finished chunk is published once its
     // bulk-store group has completed, without draining the stores behind it.
@@ -777,9 +789,9 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
       if (!mbar_wait_or_abort(fb, par, sh)) break;
       mt = reduce ? sh.ometa[g % K] : sh.smeta[r * H + g % H];
-      if (g == 0) trace(a, 9);
+      if (g == 0) s_full = stamp(a);
       if (mt.c < 0) {
-        trace(a, 10);
+        s_eos = stamp(a);
         break;
       }
       if (a.l2_hint) {
@@ -791,7 +803,7 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       tma_commit();
       ++groups;
       if (first) {
-        trace(a, 4);
+        s_store = stamp(a);
         first = false;
       }
       if (++kept > D) {
@@ -824,11 +836,18 @@ __device__ void run_ws(const LaunchArgs& a, const DevTask& t, const DevTree& tr,
       }
     }
     tma_wait_all();
-    trace(a, 11);
+    const uint64_t s_drained = stamp(a);
     fence_proxy_async();
     if (npend > 0) publish_upto(groups);
-    trace(a, 12);
-    trace(a, 5);
+    const uint64_t s_pub = stamp(a);
+    if (r == 0) {
+      trace_at(a, 4, s_store);
+      trace_at(a, 9, s_full);
+      trace_at(a, 10, s_eos);
+      trace_at(a, 11, s_drained);
+      trace_at(a, 12, s_pub);
+      trace_at(a, 5, s_pub);
+    }
   } else if (reduce && warp >= 2) {
     // ------------------------------------------------ consumers
     const int ct = threadIdx.x - 64, CT = ncons * 32;

@@ -264,6 +264,64 @@ __global__ void hop_pingpong(char* bufs, uint64_t* flags, int bytes, unsigned lo
   if (me == 0 && lane == 0) out[VAR] = gtimer() - t0;
 }
 
+
+// VAR 0: the hop split like the executor -- warp 0 lane 0 polls the flag and
+// issues the TMA load; warp 1 lane 0 waits on the stage mbarrier (try_wait,
+// or test_wait spin for VAR 1), bulk-stores, drains and signals.
+template <int VAR>
+__global__ void hop_split(char* bufs, uint64_t* flags, int bytes, unsigned long long* out) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t full;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int me = blockIdx.x, other = 1 - me;
+  char* mybuf = bufs + size_t(me) * (1 << 20);
+  char* obuf = bufs + size_t(other) * (1 << 20);
+  uint64_t* myflag = flags + me * 32;
+  uint64_t* oflag = flags + other * 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t t0 = gtimer();
+  for (uint64_t i = 1; i <= N; ++i) {
+    const uint64_t want = i - (me == 0 ? 1 : 0);
+    if (warp == 0 && lane == 0) {
+      if (!(me == 0 && i == 1)) {
+        for (;;) {
+          uint64_t v;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(myflag) : "memory");
+          if (v >= want) break;
+        }
+      }
+      asm volatile("fence.proxy.async;" ::: "memory");
+      mbar_expect_tx(&full, bytes);
+      tma_load(sm, mybuf, bytes, &full);
+    } else if (warp == 1 && lane == 0) {
+      if (VAR == 0) {
+        mbar_wait(&full, (i - 1) & 1);
+      } else {
+        for (;;) {
+          uint32_t done;
+          asm volatile(
+              "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(done)
+              : "r"(smem_u32(&full)), "r"(uint32_t((i - 1) & 1))
+              : "memory");
+          if (done) break;
+        }
+      }
+      tma_store(obuf, sm, bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async;" ::: "memory");
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(oflag), "l"(i) : "memory");
+    }
+    __syncthreads();
+  }
+  if (me == 0 && threadIdx.x == 0) out[8 + VAR] = gtimer() - t0;
+}
+
 int main() {
   char* buf;
   unsigned long long *out, h[16];
@@ -315,6 +373,19 @@ int main() {
       printf("  (%s)\n", cudaGetErrorString(cudaGetLastError()));
     }
     break;
+  }
+  cudaFuncSetAttribute(hop_split<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(hop_split<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  for (int bytes : {4096, 16384, 65536}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(flags, 0, 4096);
+      hop_split<0><<<2, 256, 65536>>>(hb, flags, bytes, out);
+      cudaMemset(flags, 0, 4096);
+      hop_split<1><<<2, 256, 65536>>>(hb, flags, bytes, out);
+    }
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("hop B=%6d split warps, try_wait      one-way %8.1f ns\n", bytes, double(h[8]) / N / 2);
+    printf("hop B=%6d split warps, test_wait spin one-way %8.1f ns\n", bytes, double(h[9]) / N / 2);
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
