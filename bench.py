@@ -228,7 +228,7 @@ def run_virtual(args):
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
 
     peaks, how = load_peaks()
-    workload = f"c3-onehop-allreduce-m{m}-virtual-1gpu-f32-{S >> 20}MiB"
+    workload = arm_config(m, S, 1)["workload"]
     alg_bytes = 2 * m * S        # HBM: read every rank's send once, write every rank's recv once
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     peak = float(peaks["hbm_gbs"])
@@ -237,11 +237,8 @@ def run_virtual(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded N(0,1)*1e-2 gradients, generated on device)",
-        "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
-                   "ranks_kind": "virtual (all on cuda:0)", "bytes_per_rank": S,
-                   "trees": m, "plan": "one-hop stars (P:440-442)",
-                   "bus_bw_gbs": round(algbw * 2 * (m - 1) / m, 3),
-                   "l2": "inputs 2 GiB/step > 126 MB L2 (no flush needed)"},
+        "config": arm_config(m, S, 1),
+        "bus_bw_gbs": round(algbw * 2 * (m - 1) / m, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(workload),
                      "peak_source": f"{how} hbm_gbs",
@@ -378,7 +375,7 @@ def multiprocess_line(args, m, S, ms, bc_ms, graph, e2e_ms, n_e2e, launches, clo
     AllReduce is the headline (`value` = algBW); busBW = algBW * 2(m-1)/m is
     measured against NVLink's 900 GB/s per direction; the
     Broadcast arm (busBW = algBW) and NCCL's numbers ride along."""
-    workload = f"c3-onehop-allreduce-m{m}-nvswitch-f32-{S >> 20}MiB"
+    workload = arm_config(m, S, m)["workload"]
     algbw = S / (ms * 1e-3) / 1e9
     bus = algbw * 2 * (m - 1) / m
     bc_alg = S / (bc_ms * 1e-3) / 1e9
@@ -387,11 +384,8 @@ def multiprocess_line(args, m, S, ms, bc_ms, graph, e2e_ms, n_e2e, launches, clo
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded N(0,1)*1e-2 gradients, generated on device)",
-        "config": {"workload": workload, "collective": "allreduce", "op": "sum", "ranks": m,
-                   "ranks_kind": "one process per GPU", "bytes_per_rank": S,
-                   "bus_bw_gbs": round(bus, 3),
-                   "l2": f"{2 * S >> 20} MiB send+recv per rank per step"
-                         + (" > 126 MB L2" if 2 * S > (126 << 20) else " (fits L2)")},
+        "config": arm_config(m, S, m),
+        "bus_bw_gbs": round(bus, 3),
         "roofline": {"bound": "nvlink", "achieved": round(bus, 2), "peak": NVLINK_GBS, "unit": "GB/s",
                      "frac": round(bus / NVLINK_GBS, 4),
                      "traffic": traffic_from_profiles(workload),
@@ -680,6 +674,22 @@ def nccl_compare(args, send, recv, count, stream, rank, world, same_gpu, tune_lo
     return out
 
 
+# --------------------------------------------------------------------------- config
+def arm_config(m, S, world):
+    """The workload both arms report (`config`): the Blink arm runs it, the
+    reference arm times a bounded sample of it (cpu_baseline.sample)."""
+    if world > 1:
+        return {"workload": f"c3-onehop-allreduce-m{m}-nvswitch-f32-{S >> 20}MiB", "collective": "allreduce",
+                "op": "sum", "ranks": m, "ranks_kind": "one process per GPU", "bytes_per_rank": S,
+                "l2": f"{2 * S >> 20} MiB send+recv per rank per step"
+                      + (" > 126 MB L2" if 2 * S > (126 << 20) else " (fits L2)")}
+    return {"workload": f"c3-onehop-allreduce-m{m}-virtual-1gpu-f32-{S >> 20}MiB", "collective": "allreduce",
+            "op": "sum", "ranks": m, "ranks_kind": "virtual (all on cuda:0)", "bytes_per_rank": S,
+            "trees": m, "plan": "one-hop stars (P:440-442)",
+            "l2": f"send+recv {2 * m * S >> 30} GiB/step > 126 MB L2 (no flush needed)"
+                  if 2 * m * S > (126 << 20) else "inputs fit L2"}
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     """The oracle as the reference arm (no reference implementation exists):
@@ -701,13 +711,14 @@ def run_reference(args):
         OC.allreduce(plan, sends, "f32", "sum")
     t = (time.perf_counter() - t0) / args.steps
     v = count * 4 / t / 1e9
-    sample = f"AllReduce of {count} fp32/rank ({count * 4 >> 20} MiB) over {m} one-hop trees per step"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sample = (f"bounded sample of the workload: AllReduce of {count} fp32/rank ({count * 4 >> 20} MiB of the "
+              f"{args.count * 4 >> 20} MiB per rank) over {m} one-hop trees per step, numpy single-thread")
     return {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "impl": "reference",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"c3-onehop-allreduce-m{m}-oracle-cpu-f32-{count * 4 >> 20}MiB",
-                       "collective": "allreduce", "ranks": m},
+            "config": arm_config(m, args.count * 4, world),
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": sample, "host_cpus": os.cpu_count()},
             "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
