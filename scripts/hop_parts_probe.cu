@@ -322,6 +322,77 @@ __global__ void hop_split(char* bufs, uint64_t* flags, int bytes, unsigned long 
   if (me == 0 && threadIdx.x == 0) out[8 + VAR] = gtimer() - t0;
 }
 
+
+// A chain over G CTAs, each used ONCE (like the executor's per-call hops):
+// CTA k waits for flag k, moves the B-byte chunk from buffer k to buffer k+1
+// (TMA: one thread loads + stores; VAR 1: the warp with 16-byte LSU copies)
+// and raises flag k+1.  Time per hop = (end - start) / (G - 1).
+template <int VAR>
+__global__ void hop_chain(char* bufs, uint64_t* flags, int bytes, unsigned long long* out) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t full;
+  const int k = blockIdx.x, lane = threadIdx.x;
+  char* src = bufs + size_t(k) * 65536;
+  char* dst = bufs + size_t(k + 1) * 65536;
+  if (lane == 0) {
+    mbar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (k == 0 && lane == 0) out[12 + VAR] = gtimer();
+  if (k > 0 && lane == 0) {
+    for (;;) {
+      uint64_t v;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + 32 * k) : "memory");
+      if (v) break;
+    }
+  }
+  __syncwarp();
+  if (VAR == 0) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async;" ::: "memory");
+      mbar_expect_tx(&full, bytes);
+      tma_load(sm, src, bytes, &full);
+      mbar_wait(&full, 0);
+      tma_store(dst, sm, bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async;" ::: "memory");
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + 32 * (k + 1)), "l"(1ull) : "memory");
+    }
+  } else {
+    for (int j = lane; j < bytes / 16; j += 32)
+      reinterpret_cast<uint4*>(dst)[j] = __ldcg(reinterpret_cast<const uint4*>(src) + j);
+    __syncwarp();
+    if (lane == 0) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + 32 * (k + 1)), "l"(1ull) : "memory");
+  }
+  if (k == gridDim.x - 1 && lane == 0) out[14 + VAR] = gtimer();
+}
+
+
+// Instruction fetch: one thread runs 4096 straight-line IADDs (64 KB of SASS)
+// twice; pass 1 fetches the code cold from L2, pass 2 runs from the
+// instruction caches.  Independent adds over 8 registers (no dependency
+// stalls beyond issue).
+#define MIX(r) "{ .reg .b32 t; mul.lo.u32 " r ", " r ", 0x9e3779b1; shr.b32 t, " r ", 13; xor.b32 " r ", " r ", t; }"
+#define ADD8 asm volatile(MIX("%0") MIX("%1") MIX("%2") MIX("%3") MIX("%4") MIX("%5") MIX("%6") MIX("%7") : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3), "+r"(r4), "+r"(r5), "+r"(r6), "+r"(r7));
+#define ADD64 ADD8 ADD8 ADD8 ADD8 ADD8 ADD8 ADD8 ADD8
+#define ADD512 ADD64 ADD64 ADD64 ADD64 ADD64 ADD64 ADD64 ADD64
+__global__ void icache_probe(unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  uint32_t r0 = clock(), r1 = r0 + 1, r2 = r0 + 2, r3 = r0 + 3, r4 = r0 + 4, r5 = r0 + 5, r6 = r0 + 6, r7 = r0 + 7;
+  long long c[3];
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c[pass]) :: "memory");
+    ADD512 ADD512 ADD512
+  }
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c[2]) :: "memory");
+  out[0] = c[1] - c[0];
+  out[1] = c[2] - c[1];
+  out[2] = r0 + r1 + r2 + r3 + r4 + r5 + r6 + r7;
+}
+
 int main() {
   char* buf;
   unsigned long long *out, h[16];
@@ -386,6 +457,33 @@ int main() {
     cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
     printf("hop B=%6d split warps, try_wait      one-way %8.1f ns\n", bytes, double(h[8]) / N / 2);
     printf("hop B=%6d split warps, test_wait spin one-way %8.1f ns\n", bytes, double(h[9]) / N / 2);
+  }
+  {
+    char* cb;
+    uint64_t* cf;
+    const int G = 100;
+    cudaMalloc(&cb, size_t(G + 1) * 65536);
+    cudaMalloc(&cf, size_t(G + 1) * 256);
+    cudaMemset(cb, 3, size_t(G + 1) * 65536);
+    cudaFuncSetAttribute(hop_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaFuncSetAttribute(hop_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    for (int bytes : {4096, 16384, 65536}) {
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(cf, 0, size_t(G + 1) * 256);
+        hop_chain<0><<<G, 32, 65536>>>(cb, cf, bytes, out);
+        cudaMemset(cf, 0, size_t(G + 1) * 256);
+        hop_chain<1><<<G, 32, 65536>>>(cb, cf, bytes, out);
+      }
+      cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("chain of %d CTAs (each once) B=%6d: TMA %7.1f ns/hop, LSU warp %7.1f ns/hop\n", G, bytes,
+             double(h[14] - h[12]) / (G - 1), double(h[15] - h[13]) / (G - 1));
+    }
+  }
+  for (int rep = 0; rep < 3; ++rep) {
+    icache_probe<<<1, 32>>>(out);
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("icache: 4608 ALU instructions (~74 KB SASS) pass 1 (cold) %lld cyc, pass 2 (warm) %lld cyc\n",
+           (long long)h[0], (long long)h[1]);
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
