@@ -162,8 +162,10 @@ typedef struct {
  *                  result to every rank; Broadcast = the root's multimem.st)
  *                  for AllReduce SUM (f32, bf16, int32) and Broadcast above
  *                  the LL sizes, 16-byte-aligned buffers.  Needs one rank per
- *                  device on >= 2 multicast-capable GPUs (multi-process: FABRIC
- *                  handles); otherwise the P2P stars run and blink_get_plan's
+ *                  device on >= 2 multicast-capable GPUs (multi-process: a
+ *                  FABRIC handle, or without FABRIC support a POSIX fd that the
+ *                  ranks duplicate from rank 0's process with pidfd_getfd, so
+ *                  one node and ptrace access); otherwise the P2P stars run and blink_get_plan's
  *                  "nvls" says why.  Float sums then follow the switch's
  *                  order, not ascending ranks (within the north_star
  *                  tolerance).  0 = off (default).  Must agree across ranks

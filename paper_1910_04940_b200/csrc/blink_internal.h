@@ -247,20 +247,30 @@ struct NvlsArgs {
 cudaError_t launch_nvls(const NvlsArgs& a, int grid, void* stream);
 
 // nvls_host.cpp: multicast objects (driver handles as 64-bit integers)
+// How a multicast object crosses processes: not at all (single process), a
+// FABRIC handle (IMEX / fabric manager), or a POSIX file descriptor the
+// peers duplicate with pidfd_getfd (single node without FABRIC support).
+enum NvlsShare { kNvlsLocal = 0, kNvlsFabric = 1, kNvlsPosixFd = 2 };
 struct NvlsMem {
   unsigned long long mc = 0, mem = 0;      // multicast object, bound physical memory
   unsigned long long uc_va = 0, mc_va = 0; // unicast / multicast mappings
   size_t size = 0;
   int dev = -1;
   bool owner = false, bound = false;
+  int share = kNvlsLocal;
+  int export_fd = -1;  // kNvlsPosixFd exporter: kept open until release (peers duplicate it)
 };
-bool nvls_supported(int dev, bool fabric, std::string* err);
+// multicast support on `dev`; `share` kNvlsFabric also needs FABRIC handles
+bool nvls_supported(int dev, int share, std::string* err);
+bool nvls_fabric_supported(int dev);
 size_t nvls_round(int ndev, size_t bytes);
-bool nvls_create(int ndev, size_t bytes, bool fabric, NvlsMem* m, std::string* err);
-bool nvls_export(const NvlsMem& m, void* fabric_handle, std::string* err);   // 64-byte FABRIC handle
-bool nvls_import(const void* fabric_handle, size_t bytes, NvlsMem* m, std::string* err);
+bool nvls_create(int ndev, size_t bytes, int share, NvlsMem* m, std::string* err);
+// 64 bytes: the FABRIC handle, or (kNvlsPosixFd) the exporter's fd as an int
+bool nvls_export(NvlsMem* m, void* handle, std::string* err);
+// kNvlsPosixFd: `handle` holds a fd valid in THIS process (duplicated by the caller)
+bool nvls_import(const void* handle, int share, size_t bytes, NvlsMem* m, std::string* err);
 bool nvls_add_device(NvlsMem* m, int dev, std::string* err);
-bool nvls_bind_map(NvlsMem* m, int dev, bool fabric, std::string* err);
+bool nvls_bind_map(NvlsMem* m, int dev, std::string* err);
 void nvls_release(NvlsMem* m);
 bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<NvlsMem>* out, std::string* err);
 // VMM (PyTorch expandable segments) registration: the physical chunks a

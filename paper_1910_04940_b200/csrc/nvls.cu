@@ -76,17 +76,37 @@ __device__ bool nv_wait(const uint64_t* p, uint64_t e, uint64_t timeout_ns, int*
   }
 }
 
-// grid-wide arrival on a device counter (CTAs are co-resident: grid <= SMs)
-__device__ void grid_sync(unsigned int* ctr, unsigned int target) {
+// grid-wide arrival on a device counter (CTAs are co-resident: grid <= SMs).
+// Bounded like every other wait: if another stream's kernels keep some of
+// this grid's CTAs off the SMs, the launch aborts with BLINK_ERR_TIMEOUT
+// through the host-mapped error word instead of spinning forever.  Returns
+// false (in every thread) on timeout or abort.
+__device__ bool grid_sync(unsigned int* ctr, unsigned int target, uint64_t timeout_ns, int* err) {
+  __shared__ int s_gs_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
-    while (atomicAdd(ctr, 0u) < target) {
+    const uint64_t t0 = gtimer();
+    int ok = 1;
+    for (int spin = 0; atomicAdd(ctr, 0u) < target; ++spin) {
+      if ((spin & 255) == 255) {
+        if (*reinterpret_cast<volatile int*>(err) != 0) {
+          ok = 0;
+          break;
+        }
+        if (gtimer() - t0 > timeout_ns) {
+          *reinterpret_cast<volatile int*>(err) = int(BLINK_ERR_TIMEOUT);
+          ok = 0;
+          break;
+        }
+      }
     }
     __threadfence();
+    s_gs_ok = ok;
   }
   __syncthreads();
+  return s_gs_ok != 0;
 }
 
 template <int DT>
@@ -172,7 +192,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   //    straight through the switch)
   if (!bcast)
     for (int64_t i = tid; i < nvec; i += T) uc[i] = user_vec(a.send, i, a.bytes, sal);
-  grid_sync(ctr, gridDim.x);
+  if (!grid_sync(ctr, gridDim.x, a.timeout_ns, a.err)) return;
   // 2. entry: my uc holds call e's input and call e - 1's copy-out is done
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     fence_alias();
@@ -207,7 +227,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
     else
       mm_st(mc + i, mm_ld_reduce<DT>(mc + i));
   }
-  grid_sync(ctr + 1, gridDim.x);
+  if (!grid_sync(ctr + 1, gridDim.x, a.timeout_ns, a.err)) return;
   // 5. publish my slice (bflag[v][0]) and wait for every root's
   if (threadIdx.x == 0 && blockIdx.x == 0 && hi > lo) {
     fence_alias();

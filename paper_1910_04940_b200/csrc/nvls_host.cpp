@@ -9,14 +9,20 @@
 //   single process (init_all, one rank per device): create, add every device,
 //     then bind + map per device;
 //   one process per GPU: rank 0 creates the object at blink_init and exports
-//     a FABRIC handle in its blob; at blink_connect every rank imports it and
-//     adds its device, the ranks meet at a barrier in each other's flag words,
-//     bind + map, and meet again; NVLS turns on only if every rank succeeded.
+//     it in its blob -- a FABRIC handle where the device supports them (IMEX
+//     / fabric manager), else a POSIX fd that the peers duplicate from rank
+//     0's process with pidfd_getfd (one node, same user); at blink_connect
+//     every rank imports it and adds its device, the ranks meet at a barrier
+//     in each other's flag words, bind + map, and meet again; NVLS turns on
+//     only if every rank succeeded.
 // Driver symbols come from cudaGetDriverEntryPoint (the library never links
 // libcuda).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
+#include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -109,7 +115,23 @@ CUmulticastObjectProp mc_prop(int ndev, size_t bytes, CUmemAllocationHandleType 
 
 }  // namespace
 
-bool nvls_supported(int dev, bool fabric, std::string* err) {
+CUmemAllocationHandleType handle_type(int share) {
+  return share == kNvlsFabric ? CU_MEM_HANDLE_TYPE_FABRIC
+                              : (share == kNvlsPosixFd ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+                                                       : CU_MEM_HANDLE_TYPE_NONE);
+}
+
+bool nvls_fabric_supported(int dev) {
+  const Drv& d = drv();
+  CUdevice cd;
+  int fab = 0;
+  if (!d.ok || d.DeviceGet(&cd, dev) != CUDA_SUCCESS) return false;
+  d.DeviceGetAttribute(&fab, CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_FABRIC_SUPPORTED, cd);
+  return fab != 0;
+}
+
+bool nvls_supported(int dev, int share, std::string* err) {
+  const bool fabric = share == kNvlsFabric;
   const Drv& d = drv();
   if (!d.ok) {
     *err = d.err;
@@ -145,33 +167,52 @@ size_t nvls_round(int ndev, size_t bytes) {
   return (bytes + g - 1) / g * g;
 }
 
-bool nvls_create(int ndev, size_t bytes, bool fabric, NvlsMem* m, std::string* err) {
+bool nvls_create(int ndev, size_t bytes, int share, NvlsMem* m, std::string* err) {
   const Drv& d = drv();
-  CUmulticastObjectProp p =
-      mc_prop(ndev, bytes, fabric ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_NONE);
+  CUmulticastObjectProp p = mc_prop(ndev, bytes, handle_type(share));
   CUmemGenericAllocationHandle h;
   DRV_TRY(d.MulticastCreate(&h, &p), "cuMulticastCreate");
   m->mc = h;
   m->size = bytes;
   m->owner = true;
+  m->share = share;
   return true;
 }
 
-bool nvls_export(const NvlsMem& m, void* fabric_handle, std::string* err) {
+bool nvls_export(NvlsMem* m, void* handle, std::string* err) {
   const Drv& d = drv();
-  DRV_TRY(d.MemExportToShareableHandle(fabric_handle, m.mc, CU_MEM_HANDLE_TYPE_FABRIC, 0),
+  if (m->share == kNvlsPosixFd) {
+    if (m->export_fd < 0) {
+      int fd = -1;
+      DRV_TRY(d.MemExportToShareableHandle(&fd, m->mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+              "cuMemExportToShareableHandle(POSIX_FD)");
+      m->export_fd = fd;  // stays open until release: peers duplicate it with pidfd_getfd
+    }
+    memcpy(handle, &m->export_fd, sizeof m->export_fd);
+    return true;
+  }
+  DRV_TRY(d.MemExportToShareableHandle(handle, m->mc, CU_MEM_HANDLE_TYPE_FABRIC, 0),
           "cuMemExportToShareableHandle(FABRIC)");
   return true;
 }
 
-bool nvls_import(const void* fabric_handle, size_t bytes, NvlsMem* m, std::string* err) {
+bool nvls_import(const void* handle, int share, size_t bytes, NvlsMem* m, std::string* err) {
   const Drv& d = drv();
   CUmemGenericAllocationHandle h;
-  DRV_TRY(d.MemImportFromShareableHandle(&h, const_cast<void*>(fabric_handle), CU_MEM_HANDLE_TYPE_FABRIC),
-          "cuMemImportFromShareableHandle(FABRIC)");
+  if (share == kNvlsPosixFd) {
+    int fd = -1;
+    memcpy(&fd, handle, sizeof fd);
+    DRV_TRY(d.MemImportFromShareableHandle(&h, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)),
+                                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+            "cuMemImportFromShareableHandle(POSIX_FD)");
+  } else {
+    DRV_TRY(d.MemImportFromShareableHandle(&h, const_cast<void*>(handle), CU_MEM_HANDLE_TYPE_FABRIC),
+            "cuMemImportFromShareableHandle(FABRIC)");
+  }
   m->mc = h;
   m->size = bytes;
   m->owner = true;  // this process's reference
+  m->share = share;
   return true;
 }
 
@@ -185,14 +226,14 @@ bool nvls_add_device(NvlsMem* m, int dev, std::string* err) {
 }
 
 // after every device joined: bind this device's memory and map uc + mc
-bool nvls_bind_map(NvlsMem* m, int dev, bool fabric, std::string* err) {
+bool nvls_bind_map(NvlsMem* m, int dev, std::string* err) {
   const Drv& d = drv();
   CUmemAllocationProp ap;
   memset(&ap, 0, sizeof ap);
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = dev;
-  ap.requestedHandleTypes = fabric ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_NONE;
+  ap.requestedHandleTypes = handle_type(m->share);
   DRV_TRY(d.MemCreate(&m->mem, m->size, &ap, 0), "cuMemCreate");
   DRV_TRY(d.MulticastBindMem(m->mc, 0, m->mem, 0, m->size, 0), "cuMulticastBindMem");
   m->bound = true;
@@ -228,6 +269,7 @@ void nvls_release(NvlsMem* m) {
   }
   if (m->mem) d.MemRelease(m->mem);
   if (m->mc && m->owner) d.MemRelease(m->mc);  // one reference per process
+  if (m->export_fd >= 0) close(m->export_fd);
   *m = NvlsMem();
 }
 
@@ -235,7 +277,7 @@ bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<N
                        std::string* err) {
   const int n = int(devs.size());
   for (int dv : devs)
-    if (!nvls_supported(dv, false, err)) return false;
+    if (!nvls_supported(dv, kNvlsLocal, err)) return false;
   int cur = 0;
   cudaGetDevice(&cur);
   struct Restore {
@@ -244,7 +286,7 @@ bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<N
   } restore{cur};
   const size_t size = nvls_round(n, bytes);
   NvlsMem base;
-  if (!nvls_create(n, size, false, &base, err)) return false;
+  if (!nvls_create(n, size, kNvlsLocal, &base, err)) return false;
   out->assign(n, NvlsMem());
   for (int i = 0; i < n; ++i) {
     if (!nvls_add_device(&base, devs[i], err)) {
@@ -259,7 +301,7 @@ bool nvls_setup_single(const std::vector<int>& devs, size_t bytes, std::vector<N
     m.dev = devs[i];
     m.owner = i == 0;
     cudaSetDevice(devs[i]);
-    if (!nvls_bind_map(&m, devs[i], false, err)) return false;
+    if (!nvls_bind_map(&m, devs[i], err)) return false;
   }
   return true;
 }

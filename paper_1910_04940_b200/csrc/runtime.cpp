@@ -1511,7 +1511,7 @@ struct Blob {
   uint64_t shallow_max_bytes;       // so must the plan choices by size (R#27,
   uint64_t onehop_bcast_max_bytes;  // the switch Broadcast star)
   uint64_t chunk_fp;                // and every input of the chunk table (a chunk's flags name bytes)
-  int32_t nvls_offer, pad2;         // rank 0: a multicast object for NEXT-1 (FABRIC handle below)
+  int32_t nvls_offer, pad2;         // rank 0: a multicast object for NEXT-1 (NvlsShare: FABRIC handle or POSIX fd below)
   uint64_t nvls_size;
   unsigned char nvls_handle[64];
 };
@@ -2289,7 +2289,8 @@ blink_result_t blink_init(blink_comm_t* comm, int nranks, int rank, int cuda_dev
   if (c->cfg.nvls && nranks >= 2 && rank == 0) {  // NEXT-1: the multicast object, shared at connect
     std::string nerr;
     const size_t size = nvls_round(nranks, c->cfg.nvls_bytes);
-    if (!nvls_supported(cuda_device, true, &nerr) || !nvls_create(nranks, size, true, &c->nvls, &nerr)) {
+    const int share = nvls_fabric_supported(cuda_device) ? kNvlsFabric : kNvlsPosixFd;
+    if (!nvls_supported(cuda_device, share, &nerr) || !nvls_create(nranks, size, share, &c->nvls, &nerr)) {
       c->nvls_note = "off: " + nerr;
       nvls_release(&c->nvls);
     }
@@ -2331,18 +2332,50 @@ blink_result_t setup_barrier(blink_comm_t comm, int round, bool ok, bool* all_ok
   return BLINK_SUCCESS;
 }
 
+// kNvlsPosixFd: duplicate rank 0's exported fd into this process (same node,
+// ptrace access to rank 0's process); -1 with *err on failure
+int dup_peer_fd(int pid, int fd, std::string* err) {
+  const int pidfd = int(syscall(SYS_pidfd_open, pid, 0));
+  if (pidfd < 0) {
+    *err = std::string("pidfd_open(rank 0): ") + strerror(errno);
+    return -1;
+  }
+  const int lfd = int(syscall(SYS_pidfd_getfd, pidfd, fd, 0));
+  if (lfd < 0)
+    *err = std::string("pidfd_getfd(rank 0): ") + strerror(errno) +
+           " (POSIX-fd NVLS needs ptrace access to rank 0's process)";
+  close(pidfd);
+  return lfd;
+}
+
 blink_result_t mp_nvls_connect(blink_comm_t comm, const Blob& b0) {
-  std::string nerr = "rank 0 offered no multicast object";
-  bool ok = b0.nvls_offer == 1;
+  // rank 0 keeps its own reason (set when creating / exporting the object)
+  std::string nerr = comm->rank == 0 && comm->nvls_note.rfind("off: ", 0) == 0
+                         ? comm->nvls_note.substr(5)
+                         : "rank 0 offered no multicast object";
+  bool ok = b0.nvls_offer == kNvlsFabric || b0.nvls_offer == kNvlsPosixFd;
   if (ok && comm->rank != 0) {
-    ok = nvls_supported(comm->device, true, &nerr) &&
-         nvls_import(b0.nvls_handle, size_t(b0.nvls_size), &comm->nvls, &nerr);
+    ok = nvls_supported(comm->device, b0.nvls_offer, &nerr);
+    if (ok && b0.nvls_offer == kNvlsPosixFd) {
+      int fd = -1;
+      memcpy(&fd, b0.nvls_handle, sizeof fd);
+      const int lfd = dup_peer_fd(b0.pid, fd, &nerr);
+      ok = lfd >= 0;
+      if (ok) {
+        unsigned char h[64] = {};
+        memcpy(h, &lfd, sizeof lfd);
+        ok = nvls_import(h, kNvlsPosixFd, size_t(b0.nvls_size), &comm->nvls, &nerr);
+        close(lfd);  // the imported handle holds its own reference
+      }
+    } else if (ok) {
+      ok = nvls_import(b0.nvls_handle, kNvlsFabric, size_t(b0.nvls_size), &comm->nvls, &nerr);
+    }
   }
   if (ok) ok = nvls_add_device(&comm->nvls, comm->device, &nerr);
   bool all = false;
   blink_result_t r = setup_barrier(comm, 0, ok, &all);
   if (r != BLINK_SUCCESS) return r;
-  bool ok2 = all && nvls_bind_map(&comm->nvls, comm->device, true, &nerr);
+  bool ok2 = all && nvls_bind_map(&comm->nvls, comm->device, &nerr);
   if (all && !ok2) nerr = "bind/map: " + nerr;
   if (!all && ok) nerr = "another rank failed to join the multicast object";
   bool all2 = false;
@@ -2383,8 +2416,8 @@ blink_result_t blink_export_handle(blink_comm_t comm, void* blob, size_t* blob_b
   b.chunk_fp = chunking_fingerprint(comm);
   if (comm->rank == 0 && comm->nvls.mc) {
     std::string nerr;
-    if (nvls_export(comm->nvls, b.nvls_handle, &nerr)) {
-      b.nvls_offer = 1;
+    if (nvls_export(&comm->nvls, b.nvls_handle, &nerr)) {
+      b.nvls_offer = comm->nvls.share;
       b.nvls_size = comm->nvls.size;
     } else {
       comm->nvls_note = "off: " + nerr;

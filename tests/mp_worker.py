@@ -358,6 +358,31 @@ def nvls_mode(rank, world):
     print(f"rank {rank}: nvls ok")
 
 
+def nvls_fallback_mode(rank, world):
+    """cfg.nvls = 1 with every process on ONE GPU: a multicast team needs
+    distinct devices, so the multi-process set-up (rank 0's object shared as
+    a FABRIC handle or, without FABRIC support, a POSIX fd duplicated with
+    pidfd_getfd) must end with NVLS off on EVERY rank, with the reason, and
+    the collectives must run on the P2P stars, bit-exact."""
+    import paper_1910_04940_b200 as B
+    from paper_1910_04940_b200 import dist as BD
+    torch.cuda.set_device(0)
+    comm = BD.init(cfg=B.config(timeout_s=60.0, nvls=1, nvls_bytes=4 << 20), device=0)
+    p = comm.plan(True, 0, 1 << 20, "f32")
+    assert p["nvls"]["active"] is False and p["nvls"]["note"].startswith("off"), p["nvls"]
+    count = (1 << 18) + 3
+    fs = synth.inputs(55, world, count, "f32")
+    x = torch.from_numpy(fs[rank]).cuda()
+    y = torch.empty_like(x)
+    comm.allreduce(x, y, op="sum")
+    torch.cuda.synchronize()
+    want = OC.allreduce(OP.plan_switch_allreduce(world), fs, "f32", "sum")
+    if not np.array_equal(y.cpu().numpy().view(np.uint32), want.view(np.uint32)):
+        raise SystemExit(f"rank {rank}: allreduce after the NVLS fallback mismatch")
+    comm.destroy()
+    print(f"rank {rank}: nvls fallback ok ({p['nvls']['note']})")
+
+
 def fuzz_mode(rank, world):
     """Randomized multi-process parity: every rank draws the same seeded
     sequence of graphs and collectives (switch or link graph, every
@@ -548,6 +573,8 @@ def main():
             miad_mode(rank, world)
         elif mode == "nvls":
             nvls_mode(rank, world)
+        elif mode == "nvls_fallback":
+            nvls_fallback_mode(rank, world)
         elif mode == "fuzz":
             fuzz_mode(rank, world)
         elif mode == "vmm":

@@ -49,6 +49,12 @@ def test_two_processes_share_one_gpu():
 
 
 @pytest.mark.gpu
+def test_multiprocess_nvls_falls_back_on_one_gpu():
+    out = launch(2, "nvls_fallback", {"BLINK_SAME_GPU": "1"}, timeout=900)
+    assert out.count("nvls fallback ok") == 2, out[-2000:]
+
+
+@pytest.mark.gpu
 def test_three_processes_shallow_tree_ll():
     out = launch(3, "chain", {"BLINK_SAME_GPU": "1"}, timeout=900)
     assert out.count("chain ok") == 3
