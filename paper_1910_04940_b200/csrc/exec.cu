@@ -1295,6 +1295,8 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LLArgs a) {
   const int v = a.ranks[blockIdx.x / a.ctas_per_rank];
   const int cta = blockIdx.x % a.ctas_per_rank;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: see exec_kernel
+  if (threadIdx.x == 0 && a.trace)  // slots this kernel does not stamp read 0
+    for (int k = 1; k < kTraceSlots; ++k) a.trace[size_t(blockIdx.x) * kTraceSlots + k] = 0;
   if (threadIdx.x == 0) ll_trace(a, 0);
   const int m = a.nranks;
   const int64_t T = int64_t(a.ctas_per_rank) * blockDim.x;
