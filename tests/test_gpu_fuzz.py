@@ -92,10 +92,13 @@ def test_random_configuration(B, seed):
                                                                  "reduce_scatter", "allgather", "gather"])
     dtype = rng.choice(["f32", "bf16", "i32"])
     op = rng.choice(["sum", "min", "max", "avg"] + (["prod"] if dtype == "i32" else []))
-    count = rng.choice([1, 7, 255, 4096, 65537, 300001, rng.randint(1, 200000)])
+    # 1000003 fp32 (4 MB, above the register path's 2 MiB size class) and
+    # 128 KiB chunks keep the TMA pipeline and work stealing in the mix;
+    # smaller calls / chunks run the register path (DESIGN 2)
+    count = rng.choice([1, 7, 255, 4096, 65537, 300001, 1000003, rng.randint(1, 200000)])
     inplace = rng.random() < 0.25 and coll in ("allreduce", "broadcast")
     misalign = rng.random() < 0.15 and not inplace
-    chunk = rng.choice([0, 4096, 65536])
+    chunk = rng.choice([0, 4096, 65536, 131072])
     per_rank = int(rng.random() < 0.2)
     autotune = int(coll in ("allreduce", "broadcast") and chunk == 0 and rng.random() < 0.2)  # NEXT-2
     comms = B.init_all([0] * m, graph=graph, cfg=B.config(timeout_s=30.0, chunk_bytes=chunk,
