@@ -421,7 +421,7 @@ def fuzz_mode(rank, world):
             coll = rng.choice(["allreduce", "allreduce", "broadcast", "reduce_scatter", "allgather", "gather"])
             dtype = rng.choice(["f32", "bf16", "i32"])
             op = rng.choice(["sum", "max", "min"] + (["avg"] if coll == "allreduce" else []))
-            count = rng.choice([1, 777, 65537, 300001])
+            count = rng.choice([1, 777, 65537, 300001, 1000003])  # 4 MB: TMA pipeline when registered
             reg = rng.random() < 0.4
             root = rng.randrange(world)
             n_in = world * count if coll == "reduce_scatter" else count
