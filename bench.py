@@ -252,10 +252,52 @@ def run_virtual(args):
         "clocks": clk.summary(),
     }
     out["protocol_path"] = per_rank_protocol(B, m, sends, recvs, S, stream, max(3, min(args.steps, 20)))
+    out["vs_size"] = size_profile(torch, comms, sends, recvs)
     if not args.no_cpu_baseline:   # the same sample as the reference arm: 16 MiB per rank
         out["cpu_baseline"] = cpu_oracle_baseline(m, min(count, REF_SAMPLE_COUNT))
     for c in comms:
         c.destroy()
+    return out
+
+
+def size_profile(torch, comms, sends, recvs, sizes=(1 << 10, 64 << 10, 1 << 20, 16 << 20, 64 << 20)):
+    """The metric is "algBW vs size": AllReduce and Broadcast (root 0) on the
+    same m virtual ranks at a few sizes per rank, device time per call of 10
+    back-to-back calls captured in one CUDA graph (a graph launch costs ~2 us
+    of its own), algBW = S / t.  Context for the headline, which is the
+    256 MiB AllReduce above; sizes up to 1 MiB stay in the 126 MB L2 across
+    replays (profiles/sweep_r02.json has every config)."""
+    out = {"note": "per-call device time, 10 calls per CUDA graph, m virtual ranks; sizes with 2*m*S <= 126 MB "
+                   "stay L2-resident across replays", "allreduce": {}, "broadcast": {}}
+    for coll in ("allreduce", "broadcast"):
+        for nb in sizes:
+            cnt = nb // 4
+
+            def call():
+                for r, c in enumerate(comms):
+                    if coll == "allreduce":
+                        c.allreduce(sends[r][:cnt], recvs[r][:cnt], op="sum")
+                    else:
+                        c.broadcast(sends[0][:cnt] if r == 0 else None, recvs[r][:cnt], root=0)
+            for _ in range(3):
+                call()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(10):
+                    call()
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / 50 * 1e3
+            key = f"{nb >> 20} MiB" if nb >= (1 << 20) else f"{nb >> 10} KiB"
+            out[coll][key] = {"us": round(us, 2), "alg_bw_gbs": round(nb / (us * 1e-6) / 1e9, 2)}
+            del g
     return out
 
 
