@@ -27,6 +27,11 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
+    # the reference arm reports the Blink arm's workload (a bounded sample of it)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.arm_config(bench.DEFAULT_M, 65536 * 4, 1)
+    assert "bounded sample" in d["cpu_baseline"]["sample"]
 
 
 def test_reference_arm_under_torchrun_prints_once():
