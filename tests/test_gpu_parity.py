@@ -120,6 +120,25 @@ def test_onehop_edge_values_f32(B):
             assert_bitwise(g, want)
 
 
+# Multi-level trees with the edge-case set (+-0, subnormals, +-1e30
+# cancellation pairs, NaN-free): the register path (8 KiB chunks), and the TMA
+# pipeline with work stealing (36 KiB chunks, 3 MiB calls), both bit-exact
+# against the oracle's evaluation of the library's own plan in tree order.
+@pytest.mark.parametrize("chunk,count", [(8192, 120003), (36864, (3 << 18) + 5)])
+def test_multilevel_edge_values_f32(B, chunk, count):
+    g = OG.dgx1v()
+    comms = make_comms(B, 8, graph=B.Graph.from_pairs(8, g[1]), chunk_bytes=chunk, shallow_max_bytes=0,
+                       ll_max_bytes=0)
+    sends = [synth.edge_case_f32(6, r, count) for r in range(8)]
+    for op in ("sum", "min", "max"):
+        got = run_allreduce(B, comms, sends, "f32", op)
+        want = OC.allreduce(oracle_plan_from_json(comms[0].plan(True, 0, count, "f32")), sends, "f32", op)
+        for x in got:
+            assert_bitwise(x, want)
+    for c in comms:
+        c.destroy()
+
+
 @pytest.mark.parametrize("count", [0, 1, 2, 3, 4, 5, 7, 8, 9, 31, 33, 1000])
 def test_tiny_and_ragged_counts(B, count):
     m = 8
