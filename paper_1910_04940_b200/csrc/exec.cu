@@ -414,7 +414,13 @@ __device__ __forceinline__ void tma_wait_group() {  // all but the N newest grou
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
+#ifdef BLINK_PROXY_FENCE_ALL
   asm volatile("fence.proxy.async;" ::: "memory");
+#else
+  // only global memory crosses proxies here (flags and user buffers; the
+  // stage ring has its own .shared::cta fence): the narrower fence
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ waits
