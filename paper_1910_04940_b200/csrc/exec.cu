@@ -50,8 +50,8 @@ namespace blink {
 namespace {
 
 // ------------------------------------------------------------------ PTX helpers
-// Flag accesses are relaxed; ordering comes from one fence per group of
-// waits (acquire pattern) or per group of signals (release pattern).  Scope is
+// Flag accesses are relaxed; ordering comes from one acquire fence per group
+// of waits or one release fence (or st.release) per group of signals.  Scope is
 // .gpu when every rank lives on this device (virtual ranks), else .sys.
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p, bool sys) {
   uint64_t v;
@@ -67,28 +67,29 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool sys) {
   else
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// Acquire / release forms for a single flag on the chunk hand-off path: a
-// polled ld.acquire replaces poll + fence.acq_rel, one st.release replaces
-// fence.acq_rel + st.relaxed (hop_parts_probe: ~110 ns less per flag).
-__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool sys) {
-  uint64_t v;
-  if (sys)
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  else
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
+// Release store for a single flag: one st.release (MEMBAR + strong store)
+// instead of a fence then a relaxed store.
 __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool sys) {
   if (sys)
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acqrel(bool sys) {
+// One-sided fences: on sm_100a fence.acq_rel is MEMBAR + CCTL.IVALL (L1
+// invalidate); fence.release is the MEMBAR alone and fence.acquire the
+// invalidate alone -- a release pattern (data, fence, flag) needs only the
+// former, an acquire pattern (flag, fence, data) only the latter.
+__device__ __forceinline__ void fence_release(bool sys) {
   if (sys)
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("fence.release.sys;" ::: "memory");
   else
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("fence.release.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void fence_acquire(bool sys) {
+  if (sys)
+    asm volatile("fence.acquire.sys;" ::: "memory");
+  else
+    asm volatile("fence.acquire.gpu;" ::: "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -431,16 +432,22 @@ struct Ctl {
   bool sys;
 };
 
-// Spin (one thread) until *p >= epoch.  Relaxed loads: the caller issues
-// fence_acqrel() after its group of waits; ACQ: acquire loads, no fence
-// needed.  Returns false on timeout / abort.
+// Spin (one thread) until *p >= epoch with relaxed loads.  Without ACQ the
+// caller issues one acquire fence after its group of waits; with ACQ this
+// thread does (an ld.acquire would invalidate L1 on every poll).  Returns
+// false on timeout / abort.
 template <bool ACQ = false>
 __device__ bool wait_ge(const uint64_t* p, const Ctl& c) {
-  auto ld = [&]() { return ACQ ? ld_acquire(p, c.sys) : ld_relaxed(p, c.sys); };
-  if (ld() >= c.epoch) return true;
+  if (ld_relaxed(p, c.sys) >= c.epoch) {
+    if (ACQ) fence_acquire(c.sys);
+    return true;
+  }
   uint64_t t0 = globaltimer();
   for (int spin = 0;; ++spin) {
-    if (ld() >= c.epoch) return true;
+    if (ld_relaxed(p, c.sys) >= c.epoch) {
+      if (ACQ) fence_acquire(c.sys);
+      return true;
+    }
     if ((spin & 255) == 255) {
       if (ld_volatile_int(c.err) != 0) return false;
       if (globaltimer() - t0 > c.timeout_ns) {
@@ -554,7 +561,7 @@ __device__ __forceinline__ void signal_chunk(const LaunchArgs& a, const DevTask&
     st_release(a.flags[__ffs(t.children) - 1] + bflag_idx(t.tree, c), ctl.epoch, sys);
     return;
   }
-  fence_acqrel(sys);
+  fence_release(sys);
   if (up) {
     st_relaxed(a.flags[t.parent] + pflag_idx(t.tree, t.rank, c), ctl.epoch, sys);
     // ReduceScatter on multi-level trees: this rank has consumed its
@@ -967,7 +974,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
       if (!tt.do_entry) continue;
       // earlier kernels' writes to send are ordered by the launch boundary;
       // across devices / processes publish with a release fence anyway
-      if (!fenced && ctl.sys) fence_acqrel(true);
+      if (!fenced && ctl.sys) fence_release(true);
       fenced = true;
       for (int u = 0; u < a.nranks; ++u)
         if (u != tt.rank) st_relaxed(a.flags[u] + entry_idx(tt.rank), ctl.epoch, ctl.sys);
@@ -1124,7 +1131,7 @@ __global__ void __launch_bounds__(256, 1) exec_kernel(const LaunchArgs a_in) {
       for (; k < base + tr.nchunks; k += G) wait_ge(myflags + bflag_idx(i, k - base), ctl);
       base += tr.nchunks;
     }
-    fence_acqrel(ctl.sys);
+    fence_acquire(ctl.sys);
   }
   // the last CTA to finish advances the device epoch for the next launch
   __syncthreads();
