@@ -22,6 +22,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -393,6 +394,51 @@ __global__ void icache_probe(unsigned long long* out) {
   out[2] = r0 + r1 + r2 + r3 + r4 + r5 + r6 + r7;
 }
 
+
+// The same one-shot chain, every CTA's buffer in its own allocation (distinct
+// 2 MB pages, like the executor's per-rank buffers and flag regions); VAR 1
+// first touches its source and destination with a 16-byte TMA prefetch /
+// generic load before waiting on its flag (translation warm-up).
+template <int VAR>
+__global__ void hop_chain_pages(char* const* bufs, uint64_t* const* flags, int bytes, unsigned long long* out) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t full;
+  const int k = blockIdx.x, lane = threadIdx.x;
+  char* src = bufs[k];
+  char* dst = bufs[k + 1];
+  if (lane == 0) {
+    mbar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (VAR == 1) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 16;" ::"l"(src) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 16;" ::"l"(dst) : "memory");
+    }
+  }
+  __syncwarp();
+  if (k == 0 && lane == 0) out[12 + VAR] = gtimer();
+  if (k > 0 && lane == 0) {
+    for (;;) {
+      uint64_t v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags[k]) : "memory");
+      if (v) break;
+    }
+    asm volatile("fence.acquire.gpu;" ::: "memory");
+  }
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_expect_tx(&full, bytes);
+    tma_load(sm, src, bytes, &full);
+    mbar_wait(&full, 0);
+    tma_store(dst, sm, bytes);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags[k + 1]), "l"(1ull) : "memory");
+  }
+  if (k == gridDim.x - 1 && lane == 0) out[14 + VAR] = gtimer();
+}
+
 int main() {
   char* buf;
   unsigned long long *out, h[16];
@@ -476,6 +522,35 @@ int main() {
       }
       cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
       printf("chain of %d CTAs (each once) B=%6d: TMA %7.1f ns/hop, LSU warp %7.1f ns/hop\n", G, bytes,
+             double(h[14] - h[12]) / (G - 1), double(h[15] - h[13]) / (G - 1));
+    }
+  }
+  {
+    const int G = 100;
+    std::vector<char*> hb2(G + 1);
+    std::vector<uint64_t*> hf(G + 1);
+    for (int i = 0; i <= G; ++i) {
+      cudaMalloc(&hb2[i], 4 << 20);
+      cudaMalloc(&hf[i], 4 << 20);
+      cudaMemset(hb2[i], 1, 65536);
+    }
+    char** db;
+    uint64_t** df;
+    cudaMalloc(&db, sizeof(char*) * (G + 1));
+    cudaMalloc(&df, sizeof(uint64_t*) * (G + 1));
+    cudaMemcpy(db, hb2.data(), sizeof(char*) * (G + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(df, hf.data(), sizeof(uint64_t*) * (G + 1), cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(hop_chain_pages<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    cudaFuncSetAttribute(hop_chain_pages<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    for (int bytes : {4096, 65536}) {
+      for (int rep = 0; rep < 3; ++rep) {
+        for (int i = 0; i <= G; ++i) cudaMemset(hf[i], 0, 64);
+        hop_chain_pages<0><<<G, 32, 65536>>>(db, df, bytes, out);
+        for (int i = 0; i <= G; ++i) cudaMemset(hf[i], 0, 64);
+        hop_chain_pages<1><<<G, 32, 65536>>>(db, df, bytes, out);
+      }
+      cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("chain, separate 4 MB allocations, B=%6d: TMA %7.1f ns/hop, with prefetch first %7.1f ns/hop\n", bytes,
              double(h[14] - h[12]) / (G - 1), double(h[15] - h[13]) / (G - 1));
     }
   }
