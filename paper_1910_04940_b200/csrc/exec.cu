@@ -29,9 +29,10 @@
 //   BCAST  (a2/a4) wait bflag[i][c] (non-root), read the chunk from the own
 //                recv (root: send), push it into the children's recv,
 //                release their bflag[i][c].
-// Readiness (a5): 64-bit epoch flags in the consumer's memory: one
-// fence.acq_rel then relaxed stores to signal, relaxed polls by the lanes of
-// one warp then a fence to wait; .gpu scope inside one device, .sys across.
+// Readiness (a5): 64-bit epoch flags in the consumer's memory: st.release
+// (or fence.release then relaxed stores) to signal, relaxed polls by the
+// lanes of one warp then fence.acquire to wait; .gpu scope inside one
+// device, .sys across.
 // Epochs live in device memory (CUDA-graph safe).  Misaligned buffers run a
 // 128-bit / scalar LSU path with ld.global.cg.  Timeouts (globaltimer) abort
 // the launch through a host-mapped error word instead of hanging.
