@@ -730,11 +730,16 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
     for (auto& c : chans)
       if ((launch_mask >> c.rank) & 1)
         per = std::max(per, (s->ranges[c.tree].nchunks + c.ctas - 1) / c.ctas);
-    // calls of <= 2 MiB per rank take it up to 3x the cap (96 KiB chunks):
-    // 1-2 MiB on multi-hop plans 5-15% faster; at 4 MiB mixed, from 8 MiB
-    // the pipeline wins by up to 1.5x (ab_lsu_small_r02.txt)
-    const int64_t cap = int64_t(count) * esize <= (int64_t(2) << 20) ? 3 * lsu_chunk_max() : lsu_chunk_max();
-    s->lsu = cap > 0 && maxc <= cap && (depth >= 2 || per <= 4);
+    // Only calls of <= 1.5 MiB per rank (BLINK_LSU_SMALL_CALL): since the
+    // pipeline's proxy fences were narrowed (3.6 -> 3.2 us per hop) it is as
+    // fast or faster from 2 MiB, while the register path still wins 5-20% at
+    // 0.25-1.5 MiB, chunks up to 96 KiB (ab_lsu_small_r02.txt)
+    static const int64_t small_call = [] {
+      const char* e = getenv("BLINK_LSU_SMALL_CALL");
+      return e ? int64_t(atoll(e)) : (int64_t(3) << 19);
+    }();
+    const int64_t cap = lsu_chunk_max();
+    s->lsu = cap > 0 && int64_t(count) * esize <= small_call && maxc <= cap && (depth >= 2 || per <= 4);
   }
   // work stealing (a6): one descriptor per dynamic channel after the CTAs'
   // tasks.  A CTA whose own chunks are all taken joins the channel with the
@@ -873,7 +878,7 @@ int store_depth() {
 int64_t lsu_chunk_max() {
   static int64_t v = [] {
     const char* e = getenv("BLINK_LSU_CHUNK_MAX");
-    return e ? int64_t(atoll(e)) : int64_t(32 << 10);
+    return e ? int64_t(atoll(e)) : int64_t(96 << 10);
   }();
   return v;
 }
