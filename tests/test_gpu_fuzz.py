@@ -92,7 +92,7 @@ def test_random_configuration(B, seed):
                                                                  "reduce_scatter", "allgather", "gather"])
     dtype = rng.choice(["f32", "bf16", "i32"])
     op = rng.choice(["sum", "min", "max", "avg"] + (["prod"] if dtype == "i32" else []))
-    # 1000003 fp32 (4 MB, above the register path's 2 MiB size class) and
+    # 1000003 fp32 (4 MB, above the register path's 1.5 MiB size class) and
     # 128 KiB chunks keep the TMA pipeline and work stealing in the mix;
     # smaller calls / chunks run the register path (DESIGN 2)
     count = rng.choice([1, 7, 255, 4096, 65537, 300001, 1000003, rng.randint(1, 200000)])
