@@ -539,6 +539,14 @@ blink_result_t build_sized(blink_comm_t comm, const Plan& plan, size_t count, in
       s->chunks = total;
       s->plan = &plan;
       s->merged_all = true;
+      // the merged one-hop AllReduce is latency-bound below a few MiB too: the
+      // register path (every thread loads all m operands, combines, stores)
+      // skips the pipeline's ramp (BLINK_LSU_MERGED_MAX bytes per rank)
+      static const int64_t merged_max = [] {
+        const char* e = getenv("BLINK_LSU_MERGED_MAX");
+        return e ? int64_t(atoll(e)) : (int64_t(4) << 20);
+      }();
+      s->lsu = lsu_chunk_max() > 0 && S <= merged_max;
       return BLINK_SUCCESS;
     }
   }
