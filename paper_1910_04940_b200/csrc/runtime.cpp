@@ -1154,10 +1154,17 @@ blink_result_t clique_launch(Clique* q) {
   Clique::MiadRun* mr = nullptr;
   size_t chunk_override = 0;
   // one launch holding every rank has no handshake for LL to save; there it
-  // pays only below kLLOneLaunchMax (A/B: scripts/per_rank_trace.py)
+  // pays only for Broadcast below kLLOneLaunchMax (A/B: scripts/per_rank_trace.py).
+  // A one-launch AllReduce runs the merged channel on the register path
+  // instead (scripts/ab_small.py, m = 8: 1 KiB 6.4 -> 4.1 us, 64 KiB 7.1 ->
+  // 4.5 us; Broadcast stays on LL: 3.3 vs 4.3 us at 1 KiB)
   int64_t ll_lo[kMaxRanks + 1] = {};
-  const bool lltree = ll_tree(c0, *plan, q->coll, bytes);
-  const bool ll = lltree || ((q->groups.size() > 1 || bytes <= kLLOneLaunchMax) &&
+  // the R#27 tree in LL: in one launch only up to kLLOneLaunchMax (128 KiB
+  // ran 10-70% slower than the register path, e.g. DGX-1V AllReduce 15.0 vs
+  // 12.5 us; 64 KiB mostly faster, 10.7 vs 12.4 us)
+  const bool lltree = ll_tree(c0, *plan, q->coll, bytes) && (q->groups.size() > 1 || bytes <= kLLOneLaunchMax);
+  const bool one_launch_ll = q->coll != kAllReduce && bytes <= kLLOneLaunchMax;
+  const bool ll = lltree || ((q->groups.size() > 1 || one_launch_ll) &&
                              ll_slices(c0, *plan, q->coll, q->count, es, ll_lo));
   if (q->nvls && !ll && nvls_call(q->coll, q->op)) return clique_nvls(q, bytes);
   // MIAD does not step while a stream is being captured into a CUDA graph:

@@ -234,7 +234,8 @@ def ll_and_per_rank_sections(sends, want):
             lx = [dev(s) for s in ls]
             ly = [torch.empty_like(x) for x in lx]
             allreduce(comms, lx, ly)
-            expect_path(comms[0], False, f"LL allreduce pr={per_rank}")
+            # one launch holding every rank: AllReduce runs the merged register path
+            expect_path(comms[0], per_rank == 0, f"LL allreduce pr={per_rank}")
             for r, c in enumerate(comms):
                 c.broadcast(lx[r] if r == 2 else None, lx[r], root=2)
             torch.cuda.synchronize()
