@@ -439,6 +439,74 @@ __global__ void hop_chain_pages(char* const* bufs, uint64_t* const* flags, int b
   if (k == gridDim.x - 1 && lane == 0) out[14 + VAR] = gtimer();
 }
 
+
+// The one-shot chain with the executor's CTA shape: 256 threads, 200 KB of
+// dynamic shared memory, warp 0 = producer (lane 0 polls, fence, TMA load
+// into stage 0 with an mbarrier, then posts an end-of-stream meta into stage
+// 1), warp 1 lane 0 = store thread (waits stage 0, bulk-stores, waits the
+// end-of-stream, drains, publishes); the other warps wait at __syncthreads.
+struct PMeta { int c, tb; };
+__global__ void __launch_bounds__(256, 1) hop_chain_exec(char* const* bufs, uint64_t* const* flags, int bytes,
+                                                          unsigned long long* out, unsigned long long* cyc) {
+  extern __shared__ __align__(128) char ring[];
+  __shared__ uint64_t full[2];
+  __shared__ PMeta meta[2];
+  const int k = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* src = bufs[k];
+  char* dst = bufs[k + 1];
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (k == 0 && threadIdx.x == 0) out[12] = gtimer();
+  if (warp == 0) {
+    if (k > 0 && lane == 0) {
+      for (;;) {
+        uint64_t v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags[k]) : "memory");
+        if (v) break;
+      }
+      asm volatile("fence.acquire.gpu;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0 && k == 3) cyc[1] = gtimer();
+    if (lane == 0 && k == 4) cyc[8] = gtimer();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (k == 3) cyc[2] = gtimer();
+      meta[0].c = 0;
+      meta[0].tb = bytes;
+      mbar_expect_tx(&full[0], bytes);
+      tma_load(ring, src, bytes, &full[0]);
+      meta[1].c = -1;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[1])) : "memory");
+    }
+  } else if (warp == 1 && lane == 0) {
+    mbar_wait(&full[0], 0);
+    const uint64_t t_full = gtimer();
+    tma_store(dst, ring, uint32_t(meta[0].tb));
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    const uint64_t t_store = gtimer();
+    mbar_wait(&full[1], 0);
+    const uint64_t t_eos = gtimer();
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    const uint64_t t_drained = gtimer();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const long long c0 = clock64();
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags[k + 1]), "l"(1ull) : "memory");
+    const long long c1 = clock64();
+    const uint64_t t_pub = gtimer();
+    if (k == 3) {
+      cyc[0] = c1 - c0;
+      cyc[3] = t_full; cyc[4] = t_store; cyc[5] = t_eos; cyc[6] = t_drained; cyc[7] = t_pub;
+    }
+  }
+  __syncthreads();
+  if (k == gridDim.x - 1 && threadIdx.x == 0) out[14] = gtimer();
+}
+
 int main() {
   char* buf;
   unsigned long long *out, h[16];
@@ -552,6 +620,43 @@ int main() {
       cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
       printf("chain, separate 4 MB allocations, B=%6d: TMA %7.1f ns/hop, with prefetch first %7.1f ns/hop\n", bytes,
              double(h[14] - h[12]) / (G - 1), double(h[15] - h[13]) / (G - 1));
+    }
+  }
+  {
+    const int G = 100;
+    std::vector<char*> hb3(G + 1);
+    std::vector<uint64_t*> hf3(G + 1);
+    for (int i = 0; i <= G; ++i) {
+      cudaMalloc(&hb3[i], 4 << 20);
+      cudaMalloc(&hf3[i], 4 << 20);
+      cudaMemset(hb3[i], 1, 65536);
+    }
+    char** db;
+    uint64_t** df;
+    unsigned long long* dc;
+    cudaMalloc(&db, sizeof(char*) * (G + 1));
+    cudaMalloc(&df, sizeof(uint64_t*) * (G + 1));
+    cudaMalloc(&dc, 256);
+    cudaMemcpy(db, hb3.data(), sizeof(char*) * (G + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(df, hf3.data(), sizeof(uint64_t*) * (G + 1), cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(hop_chain_exec, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    for (int bytes : {4096, 65536}) {
+      unsigned long long hc = 0;
+      for (int rep = 0; rep < 3; ++rep) {
+        for (int i = 0; i <= G; ++i) cudaMemset(hf3[i], 0, 64);
+        hop_chain_exec<<<G, 256, 200 << 10>>>(db, df, bytes, out, dc);
+      }
+      cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+      printf("chain, executor CTA shape (256 thr, 200 KB smem, producer/store warps), B=%6d: %7.1f ns/hop, publish %llu cyc (%s)\n",
+             bytes, double(h[14] - h[12]) / (G - 1), hc, cudaGetErrorString(cudaGetLastError()));
+      unsigned long long hs[8 + 1];
+      cudaMemcpy(hs, dc, sizeof(hs), cudaMemcpyDeviceToHost);
+      const double b0 = double(hs[9]);
+      printf("  CTA 3 (ns from acquire): issue %.0f full %.0f store %.0f eos %.0f drained %.0f published %.0f; CTA 4 acquired %.0f\n",
+             double(hs[2]) - double(hs[1]), double(hs[3]) - double(hs[1]), double(hs[4]) - double(hs[1]),
+             double(hs[5]) - double(hs[1]), double(hs[6]) - double(hs[1]), double(hs[7]) - double(hs[1]),
+             double(hs[8]) - double(hs[1]));
     }
   }
   for (int rep = 0; rep < 3; ++rep) {
